@@ -1,0 +1,161 @@
+/*
+ * stfem_b200 — C-ABI of the B200-native FDM space-time solver.
+ *
+ * Drop-in boundary for the reference's FDM hot path (arxiv 2504.07269).  The
+ * reference has no FFI: its boundary is the in-process Python library API of
+ * SPEC.md.  Each entry point below replaces one SPEC operation;
+ * the Python host package (paper_2504_07269_b200) binds them with ctypes and
+ * exposes the SPEC names.  Plain pointers and sizes only; every device buffer
+ * is caller-owned (torch tensors on the Python side); all calls are
+ * stream-ordered on the caller's stream (`stream` = cudaStream_t, NULL = legacy
+ * default stream).
+ *
+ * Complex numbers are interleaved (re, im) float64 pairs ("c128"), exactly
+ * torch.complex128 / numpy complex128 memory.
+ *
+ * Return value: STFEM_OK or an error code; stfem_last_error() gives the
+ * message (thread-local).
+ */
+#ifndef STFEM_B200_H
+#define STFEM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  STFEM_OK = 0,
+  STFEM_ERR_ARG = 1,        /* invalid argument */
+  STFEM_ERR_DIM = 2,        /* dimension mismatch */
+  STFEM_ERR_SINGULAR = 3,   /* pivot collapse; see stfem_last_error for the shift */
+  STFEM_ERR_CUDA = 4,
+  STFEM_ERR_NOMEM = 5,
+  STFEM_ERR_INTERNAL = 6,
+};
+
+typedef struct stfem_plan stfem_plan;   /* symbolic analysis + device tables for one spatial pattern */
+typedef struct stfem_asm stfem_asm;     /* mesh + CSR pattern + colouring for assembly */
+
+const char* stfem_last_error(void);
+int stfem_version(void);
+int stfem_cuda_device_count(void);
+
+/* ---------------------------------------------------------------------------
+ * BlockVector addressing ("BlockVector", temporal index outer)
+ * Element (rhs r, temporal/shift index l, spatial DoF j) lives at complex
+ * offset   r*rhs_stride + l*shift_stride + (j / chunk_cols)*chunk_stride + j % chunk_cols.
+ * A single (n_t, n_x) BlockVector: rhs_stride = n_t*n_x, shift_stride = n_x,
+ * chunk_cols = n_x, chunk_stride = 0.  The chunked form addresses the receive
+ * buffer of the spatial->temporal all-to-all without a repack.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int64_t rhs_stride;
+  int64_t shift_stride;
+  int64_t chunk_cols;
+  int64_t chunk_stride;
+} stfem_bv_layout;
+
+/* ---------------------------------------------------------------------------
+ * K3  transform_blocks (SPEC.md:392-400, steps 2 and 4 of solve, :377):
+ *   out[b][l][j] = sum_k T[l][k] * in[b][k][j]     (complex128)
+ * T: device, nt x nt row-major c128.  in/out: device, row stride ld_in/ld_out
+ * (complex elements), `ncols` columns, `batch` matrices `bstride_*` apart.
+ * Complex-fp64 GEMM on the FP64 tensor pipe (DMMA), cp.async-staged tiles.
+ * ------------------------------------------------------------------------- */
+int stfem_time_transform(const void* T, int nt, const void* in, int64_t ld_in,
+                         void* out, int64_t ld_out, int64_t ncols, int batch,
+                         int64_t bstride_in, int64_t bstride_out, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Symbolic analysis (host, once per spatial sparsity pattern; SPEC.md:326,
+ * :343 "fill-reducing ordering computed once per sparsity pattern and reused
+ * across shifts").  Geometric nested dissection on the DoF coordinates,
+ * supernodal elimination tree (fronts = separators / leaf regions), extend-add
+ * maps.  `rowptr/colind`: symmetric CSR pattern of M_x / A_x (n rows, may
+ * include the diagonal).  `coords`: n x 2 (dim 2) or n x 1 (dim 1) float64.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int32_t n;              /* spatial DoFs */
+  int32_t num_fronts;
+  int32_t depth;          /* tree depth (root = 0) */
+  int32_t max_front;      /* max front order */
+  int32_t max_pivots;
+  int64_t nnz_factor;     /* nnz(L) incl. diagonal, per shift */
+  int64_t factor_elems;   /* complex elements of factor storage per shift (sum n*p) */
+  int64_t update_elems;   /* complex elements of the two update pools per shift */
+  double flops_factor;    /* algorithmic real flops per shift: sum_j 4*c_j^2 */
+  int64_t nnz_pattern;
+} stfem_plan_stats;
+
+int stfem_plan_create(int32_t n, const int64_t* rowptr, const int32_t* colind,
+                      const double* coords, int32_t dim, int32_t leaf_size,
+                      stfem_plan** out);
+int stfem_plan_destroy(stfem_plan* plan);
+int stfem_plan_stats_get(const stfem_plan* plan, stfem_plan_stats* out);
+/* perm[new] = old (host array of n int32) */
+int stfem_plan_perm(const stfem_plan* plan, int32_t* perm);
+/* per-front table export for tests: rows of (pbeg, p, n, parent, depth) */
+int stfem_plan_fronts(const stfem_plan* plan, int32_t* table5);
+/* row index lists (new numbering) of every front: pivots then boundary rows;
+ * offsets has num_fronts + 1 entries (call with rows = NULL for the sizes) */
+int stfem_plan_front_rows(const stfem_plan* plan, int64_t* offsets, int32_t* rows);
+
+/* ---------------------------------------------------------------------------
+ * K4+K5  factor + solve, batched over shifts (FD step 3 :377):
+ *   (M_x + lam[s] A_x) w[r][s] = g[r][s]      for s < nshift, r < nrhs
+ * Complex-symmetric multifrontal LDL^T (transpose, not conjugate), numeric
+ * phase on the GPU, forward substitution fused into the factorization,
+ * backward substitution level by level.  Mvals/Avals: device CSR values in
+ * the plan's pattern (nnz_pattern).  lam: device c128[nshift].  G read, W
+ * written (may not alias), both in `layout`.  Factors are transient (streamed
+ * in batches of shifts, never kept: SURVEY.md §7 hard part 4).
+ * ------------------------------------------------------------------------- */
+int stfem_factor_solve(stfem_plan* plan, const double* Mvals, const double* Avals,
+                       const void* lam, int32_t nshift, int32_t nrhs,
+                       const void* G, void* W, stfem_bv_layout layout,
+                       void* stream);
+/* batch size in shifts (0 = auto from free memory); returns bytes per shift */
+int stfem_plan_set_batch(stfem_plan* plan, int32_t batch, int64_t* bytes_per_shift);
+
+/* ---------------------------------------------------------------------------
+ * K1/K2/K7  assembly and the matrix-free residual
+ * (apply_global) on the GPU.
+ * degree 1: elems ne x 3 (P1 triangles); degree 2: ne x 6 (v0 v1 v2 m01 m12 m20).
+ * interior_dof: nv int64 (-1 on the boundary).
+ * ------------------------------------------------------------------------- */
+int stfem_asm_create(int32_t degree, int32_t nv, const double* verts, int32_t ne,
+                     const int64_t* elems, const int64_t* interior_dof,
+                     stfem_asm** out);
+int stfem_asm_destroy(stfem_asm* a);
+/* host export of the CSR pattern: nnz via *nnz (call with NULL arrays first) */
+int stfem_asm_pattern(const stfem_asm* a, int32_t* n, int64_t* nnz,
+                      int64_t* rowptr, int32_t* colind);
+/* M_x, A_x values into the pattern (device double[nnz] each), coloured scatter */
+int stfem_asm_spatial(stfem_asm* a, double* Mvals, double* Avals, void* stream);
+/* space-time load vector F (n_t x n_x c128 at F + l*ld) for a built-in source:
+ * kind 1 = s(x)(i pi cos pi t + 2 pi^2 sin pi t)  (C1/C2 manufactured)
+ * kind 2 = s(x) e^{-it}(i + t + 2 pi^2 t)         (C3 manufactured)
+ * kind 3 = paper's e^{it} sin sin sin(t x y)
+ * P1 in space and time; breakpoints: host double[N+1]. */
+int stfem_asm_rhs(stfem_asm* a, int32_t kind, const double* breakpoints, int32_t N,
+                  void* F, int64_t ld, void* stream);
+/* y = alpha * A v (+ beta y): CSR SpMV on complex vectors, batched over
+ * `nvec` vectors (row stride ld), real matrix values `vals` (device) */
+int stfem_csr_spmv_c(const stfem_asm* a, const double* vals, const void* v,
+                     int64_t ldv, void* y, int64_t ldy, int32_t nvec,
+                     double alpha_re, double alpha_im, double beta, void* stream);
+/* apply_global: out = (i B_t (x) M_x + M_t (x) A_x) v for a
+ * banded M_t / B_t (P1 time: bw = 1; P2 time: bw = 2) given as device arrays
+ * nt x (2 bw + 1), band[l][k - l + bw].  v/out: (nt, n_x) c128 row-major;
+ * work: device scratch of 2 * nt * n_x c128. */
+int stfem_apply_global(const stfem_asm* a, const double* Mvals, const double* Avals,
+                       const double* Mt_band, const double* Bt_band, int32_t bw, int32_t nt,
+                       const void* v, void* out, void* work, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STFEM_B200_H */

@@ -1,0 +1,43 @@
+"""Thin torch-tensor wrappers over the C-ABI kernels (no logic, no fallback)."""
+
+from __future__ import annotations
+
+import torch
+
+from . import _native as N
+
+C128 = torch.complex128
+
+
+def _c128(t: torch.Tensor, name: str):
+    if t.dtype != C128:
+        raise TypeError(f"{name} must be complex128, got {t.dtype}")
+    N.require_cuda(t)
+
+
+def time_transform(T: torch.Tensor, v: torch.Tensor, out: torch.Tensor | None = None,
+                   stream=None) -> torch.Tensor:
+    """out[..., l, :] = sum_k T[l, k] v[..., k, :] on the DMMA kernel (K3).
+
+    v: (n_t, N) or (B, n_t, N) complex128 with unit column stride (rows may be
+    strided).  Returns a new tensor (or writes `out`)."""
+    _c128(T, "T")
+    _c128(v, "v")
+    nt = T.shape[0]
+    if T.shape != (nt, nt) or v.shape[-2] != nt:
+        raise N.DimensionMismatch(N.ERR_DIM, f"transform: T {tuple(T.shape)} vs v {tuple(v.shape)}")
+    T = T.contiguous()
+    squeeze = v.dim() == 2
+    vb = v.unsqueeze(0) if squeeze else v
+    if vb.stride(-1) != 1:
+        vb = vb.contiguous()
+    if out is None:
+        out = torch.empty(v.shape, dtype=C128, device=v.device)
+    ob = out.unsqueeze(0) if out.dim() == 2 else out
+    if ob.stride(-1) != 1 or ob.shape != vb.shape:
+        raise N.DimensionMismatch(N.ERR_DIM, "transform: bad output tensor")
+    B, _, ncols = vb.shape
+    N.check(N.lib().stfem_time_transform(
+        N.ptr(T), nt, N.ptr(vb), vb.stride(-2), N.ptr(ob), ob.stride(-2), ncols, B,
+        vb.stride(0) if B > 1 else 0, ob.stride(0) if B > 1 else 0, N.stream_ptr(stream)))
+    return out

@@ -1,0 +1,97 @@
+// Shared helpers for the stfem_b200 kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/stfem_b200.h"
+
+namespace stfem {
+
+// ---- error reporting (thread-local message behind stfem_last_error) -------
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+
+#define STFEM_CUDA_TRY(expr)                                          \
+  do {                                                                \
+    cudaError_t _e = (expr);                                          \
+    if (_e != cudaSuccess) return ::stfem::cuda_fail(_e, #expr);      \
+  } while (0)
+
+#define STFEM_LAUNCH_CHECK(where)                                     \
+  do {                                                                \
+    cudaError_t _e = cudaGetLastError();                              \
+    if (_e != cudaSuccess) return ::stfem::cuda_fail(_e, where);      \
+  } while (0)
+
+// ---- complex128 as double2 ------------------------------------------------
+struct __align__(16) cplx {
+  double re, im;
+};
+
+__host__ __device__ __forceinline__ cplx cmk(double r, double i) { return cplx{r, i}; }
+__host__ __device__ __forceinline__ cplx cadd(cplx a, cplx b) { return cplx{a.re + b.re, a.im + b.im}; }
+__host__ __device__ __forceinline__ cplx csub(cplx a, cplx b) { return cplx{a.re - b.re, a.im - b.im}; }
+__host__ __device__ __forceinline__ cplx cmul(cplx a, cplx b) {
+  return cplx{fma(a.re, b.re, -a.im * b.im), fma(a.re, b.im, a.im * b.re)};
+}
+// a - b*c
+__host__ __device__ __forceinline__ cplx cfms(cplx a, cplx b, cplx c) {
+  return cplx{fma(-b.im, -c.im, fma(-b.re, c.re, a.re)), fma(-b.re, c.im, fma(-b.im, c.re, a.im))};
+}
+// a + b*c
+__host__ __device__ __forceinline__ cplx cfma(cplx b, cplx c, cplx a) {
+  return cplx{fma(-b.im, c.im, fma(b.re, c.re, a.re)), fma(b.re, c.im, fma(b.im, c.re, a.im))};
+}
+__host__ __device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
+  // Smith's algorithm
+  if (fabs(b.re) >= fabs(b.im)) {
+    double r = b.im / b.re, den = b.re + b.im * r;
+    return cplx{(a.re + a.im * r) / den, (a.im - a.re * r) / den};
+  } else {
+    double r = b.re / b.im, den = b.re * r + b.im;
+    return cplx{(a.re * r + a.im) / den, (a.im * r - a.re) / den};
+  }
+}
+__host__ __device__ __forceinline__ cplx crecip(cplx b) { return cdiv(cplx{1.0, 0.0}, b); }
+__host__ __device__ __forceinline__ double cabs2(cplx a) { return a.re * a.re + a.im * a.im; }
+
+#ifdef __CUDACC__
+__device__ __forceinline__ cplx ldc(const cplx* p) {
+  double2 v = *reinterpret_cast<const double2*>(p);
+  return cplx{v.x, v.y};
+}
+__device__ __forceinline__ void stc(cplx* p, cplx v) {
+  *reinterpret_cast<double2*>(p) = make_double2(v.re, v.im);
+}
+
+// ---- FP64 tensor core: mma.sync m16n8k4 f64 (lowers to DMMA on sm_100a) ---
+// Fragment layout (CuTe SM90_16x8x4_F64F64F64F64_TN):
+//   g = lane>>2, t = lane&3
+//   A (16x4, row): a0 = A[g][t], a1 = A[g+8][t]
+//   B (4x8, col):  b0 = B[t][g]
+//   C (16x8):      c0 = C[g][2t], c1 = C[g][2t+1], c2 = C[g+8][2t], c3 = C[g+8][2t+1]
+__device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 "
+      "{%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// ---- cp.async 16-byte with zero fill ---------------------------------------
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+#endif  // __CUDACC__
+
+}  // namespace stfem

@@ -1,0 +1,666 @@
+// K4/K5 — batched multifrontal complex-symmetric LDL^T factor + solve of the
+// n_t shifted spatial systems (M_x + lam_l A_x) w_l = g_l (SPEC.md:323-340,
+// FD step 3 SPEC.md:377; factor/solve contract SPEC.md:319).
+//
+// One symbolic tree (plan) is shared by every shift, so a depth level of the
+// tree times a batch of shifts is a set of independent, identically-shaped
+// dense front problems.  One CTA owns one (front, shift) instance per level:
+//   1. assemble: zero the factor block (n x p) and update block (b x b),
+//      scatter the original entries M + lam*A, extend-add the children's
+//      update blocks and forward-RHS vectors (children in fixed order ->
+//      deterministic, no atomics);
+//   2. factor the p pivot columns, right-looking in panels of NB=32:
+//      diagonal block LDL^T in shared memory, row-parallel TRSM for the rows
+//      below (the forward substitution of the RHS is fused here as extra
+//      columns), trailing pivot-column update on the FP64 tensor pipe (DMMA);
+//   3. Schur update U = F22 - L21 D L21^T (lower tiles, K = p, DMMA).
+// Backward substitution walks the levels root-first; each instance gathers
+// x_B of its boundary rows (already final), applies L21^T and the transposed
+// triangle, and writes x both to the permuted work vector and (un-permuted)
+// to the caller's BlockVector.  Transpose, not conjugate transpose: K is
+// complex symmetric.
+#include <stdio.h>
+
+#include <algorithm>
+#include <string>
+
+#include "plan.h"
+
+namespace stfem {
+namespace {
+
+constexpr int NT = 256;
+constexpr int NB = 32;            // panel width
+constexpr int TM = 64, TK = 16;   // GEMM tile: 64 x 64 complex, k-chunk 16
+constexpr int LDS = TM + 2;       // smem [k][m] row stride: (t*LDS + g) mod 8 distinct
+constexpr int LDD = NB + 1;       // diagonal block column stride
+constexpr int MAXR = 16;          // max RHS per call (bv chunks of 16 in the host loop)
+
+constexpr int GEMM_SMEM = (2 * 2 * TK * LDS + 2 * TK) * 16;
+constexpr int DIAG_SMEM = (NB * LDD + NB + NB * MAXR) * 16;
+constexpr int FACTOR_SMEM = GEMM_SMEM + DIAG_SMEM;
+
+struct LevelArgs {
+  const FrontDev* fronts;
+  const int32_t* list;
+  int32_t nlist, nbatch;
+  const int32_t *child_ids, *relpos, *bidx, *ent_src, *ent_dst, *perm;
+  const double *Mv, *Av;
+  const cplx* lam;
+  cplx* factor;
+  int64_t fstride;
+  cplx* ucur;
+  int64_t ucur_stride;
+  const cplx* uchild;
+  int64_t uchild_stride;
+  cplx* rcur;
+  int64_t rcur_stride;  // per shift per rhs
+  const cplx* rchild;
+  int64_t rchild_stride;
+  cplx* Z;
+  int32_t nx, nrhs;
+  const cplx* G;
+  cplx* W;
+  stfem_bv_layout lay;
+  int32_t shift0;
+  int* err;
+};
+
+__device__ __forceinline__ int64_t bv_off(const stfem_bv_layout& L, int r, int64_t shift, int64_t j) {
+  return r * L.rhs_stride + shift * L.shift_stride + (j / L.chunk_cols) * L.chunk_stride +
+         j % L.chunk_cols;
+}
+
+// C[i + c*ldC] -= sum_k A[i + k*lda] * D[k*ldd] * B[c + k*ldb],  i < M, c < N.
+// sym: only i >= c is written and only tiles ti >= tj are computed.
+// 8 warps = 2 (M) x 4 (N); warp tile 32 x 16 complex; mma.m16n8k4.f64.
+__device__ void gemm_update(cplx* __restrict__ C, int ldC, int M, int N, const cplx* __restrict__ A,
+                            int lda, const cplx* __restrict__ B, int ldb, const cplx* __restrict__ D,
+                            int ldd, int K, bool sym, cplx* smem) {
+  if (M <= 0 || N <= 0 || K <= 0) return;
+  cplx* As = smem;
+  cplx* Bs = smem + 2 * TK * LDS;
+  cplx* Ds = Bs + 2 * TK * LDS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3, wm = warp & 1, wn = warp >> 1;
+  const int tiles_m = (M + TM - 1) / TM, tiles_n = (N + TM - 1) / TM;
+  const int nk = (K + TK - 1) / TK;
+  // lower trapezoid (sym) or full rectangle of 64x64 tiles, one CTA walks them all
+  for (int tj = 0; tj < tiles_n; ++tj)
+  for (int ti = sym ? tj : 0; ti < tiles_m; ++ti) {
+    const int i0 = ti * TM, c0 = tj * TM;
+
+    auto load = [&](int stage, int kc) {
+      const int k0 = kc * TK;
+      cplx* as = As + stage * TK * LDS;
+      cplx* bs = Bs + stage * TK * LDS;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        int idx = tid + NT * r;
+        int m = idx & 63, k = idx >> 6;
+        bool okk = k0 + k < K;
+        bool oka = okk && (i0 + m < M);
+        bool okb = okk && (c0 + m < N);
+        cp_async16(as + k * LDS + m, oka ? A + (int64_t)(i0 + m) + (int64_t)(k0 + k) * lda : A, oka);
+        cp_async16(bs + k * LDS + m, okb ? B + (int64_t)(c0 + m) + (int64_t)(k0 + k) * ldb : B, okb);
+      }
+      if (tid < TK) {
+        bool ok = k0 + tid < K;
+        cp_async16(Ds + stage * TK + tid, ok ? D + (int64_t)(k0 + tid) * ldd : D, ok);
+      }
+    };
+
+    double cre[2][2][4], cim[2][2][4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) cre[a][b][v] = cim[a][b][v] = 0.0;
+
+    load(0, 0);
+    cp_async_commit();
+    for (int kc = 0; kc < nk; ++kc) {
+      if (kc + 1 < nk) {
+        load((kc + 1) & 1, kc + 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      const cplx* as = As + (kc & 1) * TK * LDS + t * LDS + wm * 32 + g;
+      const cplx* bs = Bs + (kc & 1) * TK * LDS + t * LDS + wn * 16 + g;
+      const cplx* ds = Ds + (kc & 1) * TK + t;
+#pragma unroll
+      for (int kk = 0; kk < TK; kk += 4) {
+        cplx a[2][2], b[2];
+        cplx d = ds[kk];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+          a[mi][0] = ldc(as + kk * LDS + mi * 16);
+          a[mi][1] = ldc(as + kk * LDS + mi * 16 + 8);
+        }
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) b[ni] = cmul(ldc(bs + kk * LDS + ni * 8), d);
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni) {
+            dmma_16x8x4(cre[mi][ni], a[mi][0].re, a[mi][1].re, b[ni].re);
+            dmma_16x8x4(cre[mi][ni], -a[mi][0].im, -a[mi][1].im, b[ni].im);
+            dmma_16x8x4(cim[mi][ni], a[mi][0].re, a[mi][1].re, b[ni].im);
+            dmma_16x8x4(cim[mi][ni], a[mi][0].im, a[mi][1].im, b[ni].re);
+          }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            int row = i0 + wm * 32 + mi * 16 + g + 8 * h;
+            int col = c0 + wn * 16 + ni * 8 + 2 * t + v;
+            if (row < M && col < N && (!sym || row >= col)) {
+              cplx* p = C + (int64_t)row + (int64_t)col * ldC;
+              cplx o = ldc(p);
+              stc(p, cmk(o.re - cre[mi][ni][2 * h + v], o.im - cim[mi][ni][2 * h + v]));
+            }
+          }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(NT, 1) factor_level_kernel(LevelArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* gsm = reinterpret_cast<cplx*>(smem_raw);
+  cplx* Ld = gsm + GEMM_SMEM / 16;          // NB x LDD, column-major
+  cplx* dinv_s = Ld + NB * LDD;             // NB
+  cplx* ysm = dinv_s + NB;                  // NB x MAXR
+
+  const int tid = threadIdx.x;
+  const int inst = blockIdx.x;
+  const int k = inst % a.nbatch;
+  const FrontDev F = a.fronts[a.list[inst / a.nbatch]];
+  const int n = F.n, p = F.p, b = n - p;
+  const int nrhs = a.nrhs, nx = a.nx;
+  const cplx lam = a.lam[k];
+  cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
+  cplx* U = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
+  cplx* R = a.rcur + ((int64_t)k * a.rcur_stride + F.rofs) * nrhs;
+  cplx* Zk = a.Z + (int64_t)k * nx * nrhs;
+  const int64_t shift = a.shift0 + k;
+
+  // ---- 1. assembly ----
+  const cplx zero = cmk(0.0, 0.0);
+  for (int64_t i = tid; i < (int64_t)n * p; i += NT) stc(P + i, zero);
+  for (int64_t i = tid; i < (int64_t)b * b; i += NT) stc(U + i, zero);
+  for (int i = tid; i < b * nrhs; i += NT) stc(R + i, zero);
+  for (int i = tid; i < p * nrhs; i += NT) {
+    int r = i / p, ii = i % p;
+    int64_t j = a.perm[F.pbeg + ii];
+    stc(Zk + F.pbeg + ii + (int64_t)r * nx, a.G[bv_off(a.lay, r, shift, j)]);
+  }
+  __syncthreads();
+  for (int e = tid; e < F.ent_cnt; e += NT) {
+    int src = a.ent_src[F.ent_beg + e];
+    double mv = a.Mv[src], av = a.Av[src];
+    stc(P + a.ent_dst[F.ent_beg + e], cmk(fma(lam.re, av, mv), lam.im * av));
+  }
+  __syncthreads();
+  for (int ci = 0; ci < F.nchild; ++ci) {
+    const FrontDev Cf = a.fronts[a.child_ids[F.child_beg + ci]];
+    const int bc = Cf.n - Cf.p;
+    const cplx* Uc = a.uchild + (int64_t)k * a.uchild_stride + Cf.uofs;
+    const cplx* Rc = a.rchild + ((int64_t)k * a.rchild_stride + Cf.rofs) * nrhs;
+    const int32_t* rel = a.relpos + Cf.relpos_beg;
+    for (int idx = tid; idx < bc * bc; idx += NT) {
+      int k1 = idx % bc, k2 = idx / bc;
+      if (k1 < k2) continue;
+      int r1 = rel[k1], r2 = rel[k2];
+      cplx v = ldc(Uc + idx);
+      cplx* dst = (r2 < p) ? P + r1 + (int64_t)r2 * n : U + (r1 - p) + (int64_t)(r2 - p) * b;
+      stc(dst, cadd(ldc(dst), v));
+    }
+    for (int idx = tid; idx < bc * nrhs; idx += NT) {
+      int k1 = idx % bc, r = idx / bc;
+      int r1 = rel[k1];
+      cplx v = ldc(Rc + k1 + (int64_t)r * bc);
+      cplx* dst = (r1 < p) ? Zk + F.pbeg + r1 + (int64_t)r * nx : R + (r1 - p) + (int64_t)r * b;
+      stc(dst, cadd(ldc(dst), v));
+    }
+    __syncthreads();
+  }
+
+  // ---- 2. pivot columns, panels of NB ----
+  for (int kb = 0; kb < p; kb += NB) {
+    const int w = min(NB, p - kb);
+    // load the diagonal block (lower incl. diagonal)
+    for (int idx = tid; idx < w * w; idx += NT) {
+      int i = idx % w, c = idx / w;
+      if (i >= c) Ld[c * LDD + i] = ldc(P + (kb + i) + (int64_t)(kb + c) * n);
+    }
+    __syncthreads();
+    // LDL^T of the diagonal block: one barrier per column.  Phase j scales
+    // column j-1 and applies column j's rank-1 update with unscaled values.
+    for (int j = 0; j <= w; ++j) {
+      if (j > 0 && tid < w && tid > j - 1) {
+        int jj = j - 1;
+        Ld[jj * LDD + tid] = cmul(Ld[jj * LDD + tid], dinv_s[jj]);
+      }
+      if (j < w) {
+        cplx d = Ld[j * LDD + j];
+        cplx dinv = crecip(d);
+        if (tid == 0) {
+          double m2 = cabs2(d);
+          if (!(m2 > 1e-300) || !isfinite(m2)) atomicCAS(a.err, 0, (int)shift + 1);
+          dinv_s[j] = dinv;
+        }
+        for (int idx = tid; idx < w * w; idx += NT) {
+          int i = idx % w, c = idx / w;
+          if (c > j && i >= c) {
+            cplx lc = cmul(Ld[j * LDD + c], dinv);
+            Ld[c * LDD + i] = cfms(Ld[c * LDD + i], Ld[j * LDD + i], lc);
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // write back L11 and D; forward-solve the panel RHS: y = L11^{-1} r
+    for (int idx = tid; idx < w * w; idx += NT) {
+      int i = idx % w, c = idx / w;
+      if (i >= c) stc(P + (kb + i) + (int64_t)(kb + c) * n, Ld[c * LDD + i]);
+    }
+    if (tid < nrhs) {
+      const int r = tid;
+      cplx* z = Zk + F.pbeg + kb + (int64_t)r * nx;
+      for (int j = 0; j < w; ++j) {
+        cplx y = ldc(z + j);
+        for (int c = 0; c < j; ++c) y = cfms(y, Ld[c * LDD + j], ysm[c * MAXR + r]);
+        ysm[j * MAXR + r] = y;
+        stc(z + j, y);
+      }
+    }
+    __syncthreads();
+    // TRSM rows below the diagonal block + fused RHS update (thread per row)
+    for (int i = kb + w + tid; i < n; i += NT) {
+      cplx y[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+        if (j < w) y[j] = ldc(P + i + (int64_t)(kb + j) * n);
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        if (j < w) {
+#pragma unroll
+          for (int c = 0; c < j; ++c) y[j] = cfms(y[j], y[c], Ld[c * LDD + j]);
+        }
+      }
+      // y now holds l_ij * d_j; finish with D^{-1}
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+        if (j < w) {
+          y[j] = cmul(y[j], dinv_s[j]);
+          stc(P + i + (int64_t)(kb + j) * n, y[j]);
+        }
+      for (int r = 0; r < nrhs; ++r) {
+        cplx* dst = (i < p) ? Zk + F.pbeg + i + (int64_t)r * nx : R + (i - p) + (int64_t)r * b;
+        cplx acc = ldc(dst);
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          if (j < w) acc = cfms(acc, y[j], ysm[j * MAXR + r]);
+        stc(dst, acc);
+      }
+    }
+    __syncthreads();
+    // trailing pivot-column update (lower part), K = w
+    const int base = kb + w;
+    if (base < p)
+      gemm_update(P + base + (int64_t)base * n, n, n - base, p - base, P + base + (int64_t)kb * n, n,
+                  P + base + (int64_t)kb * n, n, P + kb + (int64_t)kb * n, n + 1, w, true, gsm);
+  }
+  // z = D^{-1} y for this front's pivots
+  for (int i = tid; i < p * nrhs; i += NT) {
+    int r = i / p, j = i % p;
+    cplx* z = Zk + F.pbeg + j + (int64_t)r * nx;
+    stc(z, cdiv(ldc(z), ldc(P + j + (int64_t)j * n)));
+  }
+  // ---- 3. Schur update of the boundary block ----
+  if (b > 0)
+    gemm_update(U, b, b, b, P + p, n, P + p, n, P, n + 1, p, true, gsm);
+}
+
+__global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a) {
+  __shared__ cplx ts[NB * MAXR];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int inst = blockIdx.x;
+  const int k = inst % a.nbatch;
+  const FrontDev F = a.fronts[a.list[inst / a.nbatch]];
+  const int n = F.n, p = F.p;
+  const int nrhs = a.nrhs, nx = a.nx;
+  const cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
+  cplx* Zk = a.Z + (int64_t)k * nx * nrhs;
+  const int32_t* bidx = a.bidx + F.bidx_beg;
+  const int64_t shift = a.shift0 + k;
+
+  for (int kb = ((p - 1) / NB) * NB; kb >= 0; kb -= NB) {
+    const int w = min(NB, p - kb);
+    // t_j = z_j - sum_{i >= kb+w} L[i][kb+j] x_i   (warp per column)
+    for (int j = warp; j < w; j += NT / 32) {
+      cplx acc[MAXR];
+#pragma unroll
+      for (int r = 0; r < MAXR; ++r) acc[r] = cmk(0.0, 0.0);
+      const cplx* col = P + (int64_t)(kb + j) * n;
+      for (int i = kb + w + lane; i < n; i += 32) {
+        cplx l = ldc(col + i);
+        int64_t gi = (i < p) ? (int64_t)F.pbeg + i : (int64_t)bidx[i - p];
+#pragma unroll
+        for (int r = 0; r < MAXR; ++r)
+          if (r < nrhs) acc[r] = cfma(l, ldc(Zk + gi + (int64_t)r * nx), acc[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < MAXR; ++r) {
+        if (r < nrhs) {
+          double re = acc[r].re, im = acc[r].im;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            re += __shfl_xor_sync(0xffffffffu, re, o);
+            im += __shfl_xor_sync(0xffffffffu, im, o);
+          }
+          if (lane == 0) {
+            cplx z = ldc(Zk + F.pbeg + kb + j + (int64_t)r * nx);
+            ts[j * MAXR + r] = cmk(z.re - re, z.im - im);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // transposed unit triangle, backward (thread per rhs)
+    if (tid < nrhs) {
+      const int r = tid;
+      for (int j = w - 1; j >= 0; --j) {
+        cplx x = ts[j * MAXR + r];
+        for (int c = j + 1; c < w; ++c)
+          x = cfms(x, ldc(P + (kb + c) + (int64_t)(kb + j) * n), ts[c * MAXR + r]);
+        ts[j * MAXR + r] = x;
+        stc(Zk + F.pbeg + kb + j + (int64_t)r * nx, x);
+        a.W[bv_off(a.lay, r, shift, a.perm[F.pbeg + kb + j])] = x;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+int upload(Plan& P) {
+  int dev;
+  STFEM_CUDA_TRY(cudaGetDevice(&dev));
+  if (P.d_fronts && P.device == dev) return STFEM_OK;
+  P.free_device();
+  P.device = dev;
+  auto up = [&](auto** dptr, const auto& vec) -> int {
+    using T = typename std::decay_t<decltype(vec)>::value_type;
+    size_t bytes = std::max<size_t>(1, vec.size()) * sizeof(T);
+    STFEM_CUDA_TRY(cudaMalloc((void**)dptr, bytes));
+    if (!vec.empty()) STFEM_CUDA_TRY(cudaMemcpy(*dptr, vec.data(), vec.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return STFEM_OK;
+  };
+  std::vector<int32_t> lv;
+  P.level_off.assign(P.levels.size() + 1, 0);
+  for (size_t d = 0; d < P.levels.size(); ++d) {
+    P.level_off[d] = (int64_t)lv.size();
+    lv.insert(lv.end(), P.levels[d].begin(), P.levels[d].end());
+  }
+  P.level_off[P.levels.size()] = (int64_t)lv.size();
+  int rc;
+  if ((rc = up(&P.d_fronts, P.fronts))) return rc;
+  if ((rc = up(&P.d_levels, lv))) return rc;
+  if ((rc = up(&P.d_child_ids, P.child_ids))) return rc;
+  if ((rc = up(&P.d_bidx, P.bidx))) return rc;
+  if ((rc = up(&P.d_relpos, P.relpos))) return rc;
+  if ((rc = up(&P.d_ent_src, P.ent_src))) return rc;
+  if ((rc = up(&P.d_ent_dst, P.ent_dst))) return rc;
+  if ((rc = up(&P.d_perm, P.perm))) return rc;
+  STFEM_CUDA_TRY(cudaMalloc(&P.d_err, sizeof(int)));
+  STFEM_CUDA_TRY(cudaMemset(P.d_err, 0, sizeof(int)));
+  STFEM_CUDA_TRY(cudaFuncSetAttribute(factor_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      FACTOR_SMEM));
+  return STFEM_OK;
+}
+
+int64_t bytes_per_shift(const Plan& P, int nrhs) {
+  return 16 * (P.factor_stride + P.upool_stride[0] + P.upool_stride[1] +
+               (int64_t)nrhs * (P.rpool_stride[0] + P.rpool_stride[1]) + (int64_t)P.n * nrhs);
+}
+
+int ensure_workspace(Plan& P, int batch, int nrhs) {
+  if (P.d_factor && P.ws_batch >= batch && P.ws_nrhs >= nrhs) return STFEM_OK;
+  P.free_workspace();
+  auto al = [&](cplx** d, int64_t elems) -> int {
+    STFEM_CUDA_TRY(cudaMalloc((void**)d, std::max<int64_t>(1, elems) * 16));
+    return STFEM_OK;
+  };
+  int rc;
+  if ((rc = al(&P.d_factor, P.factor_stride * batch))) return rc;
+  for (int q = 0; q < 2; ++q) {
+    if ((rc = al(&P.d_upool[q], P.upool_stride[q] * batch))) return rc;
+    if ((rc = al(&P.d_rpool[q], P.rpool_stride[q] * batch * nrhs))) return rc;
+  }
+  if ((rc = al(&P.d_Z, (int64_t)P.n * nrhs * batch))) return rc;
+  P.ws_batch = batch;
+  P.ws_nrhs = nrhs;
+  return STFEM_OK;
+}
+
+int auto_batch(Plan& P, int nshift, int nrhs) {
+  if (P.batch > 0) return std::min(P.batch, nshift);
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = (size_t)8 << 30;
+  // keep whatever workspace we already own in the budget
+  size_t owned = P.d_factor ? (size_t)bytes_per_shift(P, P.ws_nrhs) * P.ws_batch : 0;
+  double budget = 0.45 * (double)(fr + owned);
+  int64_t per = bytes_per_shift(P, nrhs);
+  int64_t b = std::max<int64_t>(1, (int64_t)(budget / (double)per));
+  return (int)std::min<int64_t>(std::min<int64_t>(b, 4096), nshift);
+}
+
+}  // namespace
+
+Plan::~Plan() {
+  free_workspace();
+  free_device();
+}
+
+void Plan::free_device() {
+  cudaFree(d_fronts);
+  cudaFree(d_levels);
+  cudaFree(d_child_ids);
+  cudaFree(d_bidx);
+  cudaFree(d_relpos);
+  cudaFree(d_ent_src);
+  cudaFree(d_ent_dst);
+  cudaFree(d_perm);
+  cudaFree(d_err);
+  d_fronts = nullptr;
+  d_levels = nullptr;
+  d_child_ids = d_bidx = d_relpos = d_ent_src = d_ent_dst = d_perm = nullptr;
+  d_err = nullptr;
+  device = -1;
+}
+
+void Plan::free_workspace() {
+  cudaFree(d_factor);
+  for (int q = 0; q < 2; ++q) {
+    cudaFree(d_upool[q]);
+    cudaFree(d_rpool[q]);
+    d_upool[q] = d_rpool[q] = nullptr;
+  }
+  cudaFree(d_Z);
+  d_factor = d_Z = nullptr;
+  ws_batch = ws_nrhs = 0;
+}
+
+int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, int nshift, int nrhs,
+                 const cplx* G, cplx* W, stfem_bv_layout lay, cudaStream_t stream) {
+  if (nshift < 0 || nrhs < 1) return fail(STFEM_ERR_DIM, "factor_solve: nshift >= 0 and nrhs >= 1 required");
+  if (nrhs > MAXR) return fail(STFEM_ERR_DIM, "factor_solve: at most 16 right-hand sides per call");
+  if (!Mv || !Av || !lam || !G || !W) return fail(STFEM_ERR_ARG, "factor_solve: null pointer");
+  if (lay.chunk_cols <= 0) return fail(STFEM_ERR_ARG, "factor_solve: chunk_cols must be positive");
+  if (nshift == 0) return STFEM_OK;
+  int rc;
+  if ((rc = upload(P))) return rc;
+  int batch = auto_batch(P, nshift, nrhs);
+  if ((rc = ensure_workspace(P, batch, nrhs))) return rc;
+  STFEM_CUDA_TRY(cudaMemsetAsync(P.d_err, 0, sizeof(int), stream));
+
+  LevelArgs a{};
+  a.fronts = P.d_fronts;
+  a.child_ids = P.d_child_ids;
+  a.relpos = P.d_relpos;
+  a.bidx = P.d_bidx;
+  a.ent_src = P.d_ent_src;
+  a.ent_dst = P.d_ent_dst;
+  a.perm = P.d_perm;
+  a.Mv = Mv;
+  a.Av = Av;
+  a.factor = P.d_factor;
+  a.fstride = P.factor_stride;
+  a.Z = P.d_Z;
+  a.nx = P.n;
+  a.nrhs = nrhs;
+  a.G = G;
+  a.W = W;
+  a.lay = lay;
+  a.err = P.d_err;
+  for (int s0 = 0; s0 < nshift; s0 += batch) {
+    const int nb = std::min(batch, nshift - s0);
+    a.nbatch = nb;
+    a.lam = lam + s0;
+    a.shift0 = s0;
+    for (int d = P.depth; d >= 0; --d) {
+      const int q = d & 1;
+      a.list = P.d_levels + P.level_off[d];
+      a.nlist = (int32_t)P.levels[d].size();
+      a.ucur = P.d_upool[q];
+      a.ucur_stride = P.upool_stride[q];
+      a.uchild = P.d_upool[q ^ 1];
+      a.uchild_stride = P.upool_stride[q ^ 1];
+      a.rcur = P.d_rpool[q];
+      a.rcur_stride = P.rpool_stride[q];
+      a.rchild = P.d_rpool[q ^ 1];
+      a.rchild_stride = P.rpool_stride[q ^ 1];
+      factor_level_kernel<<<a.nlist * nb, NT, FACTOR_SMEM, stream>>>(a);
+      STFEM_LAUNCH_CHECK("factor_level_kernel");
+    }
+    for (int d = 0; d <= P.depth; ++d) {
+      a.list = P.d_levels + P.level_off[d];
+      a.nlist = (int32_t)P.levels[d].size();
+      backward_level_kernel<<<a.nlist * nb, NT, 0, stream>>>(a);
+      STFEM_LAUNCH_CHECK("backward_level_kernel");
+    }
+  }
+  int h_err = 0;
+  STFEM_CUDA_TRY(cudaMemcpyAsync(&h_err, P.d_err, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  STFEM_CUDA_TRY(cudaStreamSynchronize(stream));
+  if (h_err) {
+    char buf[160];
+    snprintf(buf, sizeof(buf), "singular pivot (numerically singular shifted system) at shift index %d",
+             h_err - 1);
+    return fail(STFEM_ERR_SINGULAR, buf);
+  }
+  return STFEM_OK;
+}
+
+}  // namespace stfem
+
+using stfem::Plan;
+
+extern "C" int stfem_plan_create(int32_t n, const int64_t* rowptr, const int32_t* colind,
+                                 const double* coords, int32_t dim, int32_t leaf_size, stfem_plan** out) {
+  if (!out || !rowptr || !colind || !coords) return stfem::fail(STFEM_ERR_ARG, "plan_create: null pointer");
+  Plan* P = new Plan();
+  int rc = stfem::build_symbolic(*P, n, rowptr, colind, coords, dim, leaf_size);
+  if (rc) {
+    delete P;
+    return rc;
+  }
+  *out = reinterpret_cast<stfem_plan*>(P);
+  return STFEM_OK;
+}
+
+extern "C" int stfem_plan_destroy(stfem_plan* plan) {
+  delete reinterpret_cast<Plan*>(plan);
+  return STFEM_OK;
+}
+
+extern "C" int stfem_plan_stats_get(const stfem_plan* plan, stfem_plan_stats* s) {
+  if (!plan || !s) return stfem::fail(STFEM_ERR_ARG, "plan_stats: null pointer");
+  const Plan& P = *reinterpret_cast<const Plan*>(plan);
+  s->n = P.n;
+  s->num_fronts = (int32_t)P.fronts.size();
+  s->depth = P.depth;
+  s->max_front = P.max_front;
+  s->max_pivots = P.max_pivots;
+  s->nnz_factor = P.nnz_factor;
+  s->factor_elems = P.factor_stride;
+  s->update_elems = P.upool_stride[0] + P.upool_stride[1];
+  s->flops_factor = P.flops;
+  s->nnz_pattern = P.nnz_pattern;
+  return STFEM_OK;
+}
+
+extern "C" int stfem_plan_perm(const stfem_plan* plan, int32_t* perm) {
+  if (!plan || !perm) return stfem::fail(STFEM_ERR_ARG, "plan_perm: null pointer");
+  const Plan& P = *reinterpret_cast<const Plan*>(plan);
+  std::copy(P.perm.begin(), P.perm.end(), perm);
+  return STFEM_OK;
+}
+
+extern "C" int stfem_plan_fronts(const stfem_plan* plan, int32_t* t) {
+  if (!plan || !t) return stfem::fail(STFEM_ERR_ARG, "plan_fronts: null pointer");
+  const Plan& P = *reinterpret_cast<const Plan*>(plan);
+  for (size_t f = 0; f < P.fronts.size(); ++f) {
+    const auto& F = P.fronts[f];
+    t[5 * f + 0] = F.pbeg;
+    t[5 * f + 1] = F.p;
+    t[5 * f + 2] = F.n;
+    t[5 * f + 3] = F.parent;
+    t[5 * f + 4] = F.depth;
+  }
+  return STFEM_OK;
+}
+
+extern "C" int stfem_plan_front_rows(const stfem_plan* plan, int64_t* offsets, int32_t* rows) {
+  if (!plan || !offsets) return stfem::fail(STFEM_ERR_ARG, "plan_front_rows: null pointer");
+  const Plan& P = *reinterpret_cast<const Plan*>(plan);
+  int64_t o = 0;
+  for (size_t f = 0; f < P.fronts.size(); ++f) {
+    const auto& F = P.fronts[f];
+    offsets[f] = o;
+    if (rows) {
+      for (int32_t i = 0; i < F.p; ++i) rows[o + i] = F.pbeg + i;
+      for (int32_t i = 0; i < F.n - F.p; ++i) rows[o + F.p + i] = P.bidx[F.bidx_beg + i];
+    }
+    o += F.n;
+  }
+  offsets[P.fronts.size()] = o;
+  return STFEM_OK;
+}
+
+extern "C" int stfem_plan_set_batch(stfem_plan* plan, int32_t batch, int64_t* bps) {
+  if (!plan) return stfem::fail(STFEM_ERR_ARG, "plan_set_batch: null pointer");
+  Plan& P = *reinterpret_cast<Plan*>(plan);
+  P.batch = std::max(0, batch);
+  if (bps) *bps = stfem::bytes_per_shift(P, 1);
+  return STFEM_OK;
+}
+
+extern "C" int stfem_factor_solve(stfem_plan* plan, const double* Mvals, const double* Avals,
+                                  const void* lam, int32_t nshift, int32_t nrhs, const void* G, void* W,
+                                  stfem_bv_layout layout, void* stream) {
+  if (!plan) return stfem::fail(STFEM_ERR_ARG, "factor_solve: null plan");
+  return stfem::factor_solve(*reinterpret_cast<Plan*>(plan), Mvals, Avals, (const stfem::cplx*)lam, nshift,
+                             nrhs, (const stfem::cplx*)G, (stfem::cplx*)W, layout, (cudaStream_t)stream);
+}

@@ -1,0 +1,70 @@
+// Plan = symbolic analysis of one spatial sparsity pattern (shared by all
+// shifts) + device tables + per-batch numeric workspace.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace stfem {
+
+// One front (supernode) of the multifrontal elimination tree.  Front order
+// n = p (pivots, contiguous in the new numbering from pbeg) + b (boundary rows,
+// all belonging to ancestors).  Factor block: n x p column-major (ld n) holding
+// D on the diagonal and unit-lower L below it.  Update block: b x b column-major.
+struct FrontDev {
+  int32_t pbeg, p, n, nchild;
+  int32_t child_beg;   // into child_ids
+  int32_t ent_beg, ent_cnt;  // original (lower-triangle) entries of K owned by this front
+  int32_t bidx_beg;    // into bidx: new indices of the b boundary rows
+  int32_t relpos_beg;  // into relpos: position of each boundary row in the parent front
+  int32_t parent, depth;
+  int64_t fofs;        // factor block offset (complex elements) within one shift
+  int64_t uofs;        // update block offset within the pool of parity depth%2 (one shift)
+  int64_t rofs;        // forward-RHS update offset (units of b, times nrhs) within its pool
+};
+
+struct Plan {
+  // ---- symbolic (host) ----
+  int32_t n = 0;
+  int64_t nnz_pattern = 0;
+  std::vector<int32_t> perm, iperm;       // perm[new] = old
+  std::vector<FrontDev> fronts;           // postorder
+  std::vector<int32_t> child_ids, bidx, relpos, ent_src, ent_dst;
+  std::vector<std::vector<int32_t>> levels;  // fronts per depth
+  int32_t depth = 0, max_front = 0, max_pivots = 0;
+  int64_t factor_stride = 0;               // complex per shift
+  int64_t upool_stride[2] = {0, 0};        // complex per shift
+  int64_t rpool_stride[2] = {0, 0};        // complex per shift per rhs
+  int64_t nnz_factor = 0;
+  double flops = 0;
+
+  // ---- device tables (uploaded lazily) ----
+  int device = -1;
+  FrontDev* d_fronts = nullptr;
+  int32_t* d_levels = nullptr;             // concatenated level lists
+  std::vector<int64_t> level_off;          // offsets into d_levels
+  int32_t *d_child_ids = nullptr, *d_bidx = nullptr, *d_relpos = nullptr;
+  int32_t *d_ent_src = nullptr, *d_ent_dst = nullptr, *d_perm = nullptr;
+  int* d_err = nullptr;
+
+  // ---- numeric workspace (per batch of shifts) ----
+  int32_t batch = 0;       // requested (0 = auto)
+  int32_t ws_batch = 0;    // allocated for
+  int32_t ws_nrhs = 0;
+  cplx* d_factor = nullptr;
+  cplx* d_upool[2] = {nullptr, nullptr};
+  cplx* d_rpool[2] = {nullptr, nullptr};
+  cplx* d_Z = nullptr;
+
+  ~Plan();
+  void free_device();
+  void free_workspace();
+};
+
+int build_symbolic(Plan& P, int32_t n, const int64_t* rowptr, const int32_t* colind,
+                   const double* coords, int32_t dim, int32_t leaf_size);
+
+}  // namespace stfem

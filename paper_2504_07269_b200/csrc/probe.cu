@@ -1,0 +1,62 @@
+// Peak probes for the roofline denominators that MEASURED_PEAKS.json lacks:
+// FP64 tensor (DMMA) and FP64 CUDA-core (DFMA) throughput.  Register-only
+// loops with 8 independent accumulator chains per warp; one CTA of 256
+// threads per SM x `ctas_per_sm`.
+#include "common.cuh"
+
+namespace stfem {
+namespace {
+
+__global__ void __launch_bounds__(256) dmma_probe_kernel(double* sink, int iters) {
+  double c[8][4];
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, b0 = 1.0 - a0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) c[i][v] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dmma_16x8x4(c[i], a0, a1, b0);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) s += c[i][v];
+  if (s == 12345.678) sink[threadIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(256) dfma_probe_kernel(double* sink, int iters) {
+  double c[8];
+  double a = threadIdx.x * 1e-9, b = 1.0 - a;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i] = i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i] = fma(c[i], b, a);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i];
+  if (s == 12345.678) sink[threadIdx.x] = s;
+}
+
+}  // namespace
+}  // namespace stfem
+
+// kind 0 = DMMA (flops = 2*16*8*4 per mma per warp), 1 = DFMA.  Returns the
+// real fp64 flop count executed in *flops; caller times it with events.
+extern "C" int stfem_probe_launch(int kind, int blocks, int iters, double* sink, double* flops,
+                                  void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  double warps = blocks * 8.0;
+  if (kind == 0) {
+    stfem::dmma_probe_kernel<<<blocks, 256, 0, s>>>(sink, iters);
+    *flops = warps * iters * 8.0 * (2.0 * 16 * 8 * 4);
+  } else {
+    stfem::dfma_probe_kernel<<<blocks, 256, 0, s>>>(sink, iters);
+    *flops = blocks * 256.0 * iters * 8.0 * 2.0;
+  }
+  STFEM_LAUNCH_CHECK("probe");
+  return STFEM_OK;
+}

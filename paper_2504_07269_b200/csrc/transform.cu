@@ -1,0 +1,173 @@
+// K3 — time-axis transform (FD steps 2 and 4):
+//   out[b][l][j] = sum_k T[l][k] * in[b][k][j]      complex128
+//
+// A complex-fp64 GEMM (M = K = n_t, N = n_x * n_rhs) on the FP64 tensor pipe:
+// mma.sync.m16n8k4.f64 (SASS DMMA) with the 4-real-product complex scheme
+//   Cre += Tre*Bre + (-Tim)*Bim ,  Cim += Tre*Bim + Tim*Bre
+// Operand tiles are staged global->shared with 16-byte cp.async (one complex
+// per copy) in a 3-stage pipeline.  CTA tile 64(l) x 64(j) complex, k-tile 16,
+// 8 warps as 2 x 4, warp tile 32 x 16 complex (2 x 2 DMMA tiles, separate
+// re/im accumulators: 32 fp64 registers per thread).
+//
+// Grid: x = M-tiles (fastest) so the n_t/64 CTAs that read the same column
+// block of `in` run together and share it through L2 (in is read from HBM
+// once; T (<= 16 MB) stays L2-resident).
+#include "common.cuh"
+
+namespace stfem {
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3;
+constexpr int LDA = BK + 4;   // As[m][k]: (g*LDA + t) mod 8 distinct -> conflict-free LDS.128
+constexpr int LDB = BN + 2;   // Bs[k][n]: (t*LDB + g) mod 8 distinct
+constexpr int A_STAGE = BM * LDA;
+constexpr int B_STAGE = BK * LDB;
+constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * 16;
+
+__global__ void __launch_bounds__(256, 2)
+time_transform_kernel(const cplx* __restrict__ T, int nt, const cplx* __restrict__ in,
+                      int64_t ld_in, cplx* __restrict__ out, int64_t ld_out, int64_t ncols,
+                      int64_t bs_in, int64_t bs_out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* As = reinterpret_cast<cplx*>(smem_raw);
+  cplx* Bs = As + STAGES * A_STAGE;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int l0 = blockIdx.x * BM;
+  const int64_t j0 = (int64_t)blockIdx.y * BN;
+  in += (int64_t)blockIdx.z * bs_in;
+  out += (int64_t)blockIdx.z * bs_out;
+
+  const int nk = (nt + BK - 1) / BK;
+
+  auto load_stage = [&](int stage, int kt) {
+    const int k0 = kt * BK;
+    cplx* as = As + stage * A_STAGE;
+    cplx* bs = Bs + stage * B_STAGE;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      int idx = tid + 256 * r;
+      int m = idx >> 4, k = idx & 15;
+      bool ok = (l0 + m < nt) && (k0 + k < nt);
+      const cplx* src = ok ? T + (int64_t)(l0 + m) * nt + (k0 + k) : T;
+      cp_async16(as + m * LDA + k, src, ok);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      int idx = tid + 256 * r;
+      int k = idx >> 6, n = idx & 63;
+      bool ok = (k0 + k < nt) && (j0 + n < ncols);
+      const cplx* src = ok ? in + (int64_t)(k0 + k) * ld_in + (j0 + n) : in;
+      cp_async16(bs + k * LDB + n, src, ok);
+    }
+  };
+
+  double cre[2][2][4], cim[2][2][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) cre[i][j][v] = cim[i][j][v] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_stage(s, s);
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      int nxt = kt + STAGES - 1;
+      if (nxt < nk) load_stage(nxt % STAGES, nxt);
+      cp_async_commit();
+    }
+    const cplx* as = As + (kt % STAGES) * A_STAGE + (wm * 32 + g) * LDA + t;
+    const cplx* bs = Bs + (kt % STAGES) * B_STAGE + t * LDB + wn * 16 + g;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      cplx a[2][2], b[2];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        a[mi][0] = ldc(as + (mi * 16) * LDA + kk);
+        a[mi][1] = ldc(as + (mi * 16 + 8) * LDA + kk);
+      }
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) b[ni] = ldc(bs + kk * LDB + ni * 8);
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) {
+          dmma_16x8x4(cre[mi][ni], a[mi][0].re, a[mi][1].re, b[ni].re);
+          dmma_16x8x4(cre[mi][ni], -a[mi][0].im, -a[mi][1].im, b[ni].im);
+          dmma_16x8x4(cim[mi][ni], a[mi][0].re, a[mi][1].re, b[ni].im);
+          dmma_16x8x4(cim[mi][ni], a[mi][0].im, a[mi][1].im, b[ni].re);
+        }
+    }
+  }
+  cp_async_wait<0>();
+
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        int row = l0 + wm * 32 + mi * 16 + g + 8 * h;
+        int64_t col = j0 + wn * 16 + ni * 8 + 2 * t;
+        if (row < nt) {
+          cplx* dst = out + (int64_t)row * ld_out + col;
+          if (col < ncols) stc(dst, cmk(cre[mi][ni][2 * h], cim[mi][ni][2 * h]));
+          if (col + 1 < ncols) stc(dst + 1, cmk(cre[mi][ni][2 * h + 1], cim[mi][ni][2 * h + 1]));
+        }
+      }
+}
+
+}  // namespace
+
+int time_transform(const void* T, int nt, const void* in, int64_t ld_in, void* out,
+                   int64_t ld_out, int64_t ncols, int batch, int64_t bs_in, int64_t bs_out,
+                   cudaStream_t stream) {
+  if (nt <= 0 || ncols < 0 || batch < 0 || ld_in < ncols || ld_out < ncols)
+    return fail(STFEM_ERR_DIM, "time_transform: bad dimensions");
+  if (!T || !in || !out) return fail(STFEM_ERR_ARG, "time_transform: null pointer");
+  if (((uintptr_t)T | (uintptr_t)in | (uintptr_t)out) & 15)
+    return fail(STFEM_ERR_ARG, "time_transform: buffers must be 16-byte aligned");
+  if (ncols == 0 || batch == 0) return STFEM_OK;
+  static bool attr_set = false;
+  if (!attr_set) {
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(time_transform_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    attr_set = true;
+  }
+  int64_t ntile = (ncols + BN - 1) / BN;
+  if (ntile > 65535) {
+    // split the column range into chunks of <= 65535 tiles
+    for (int64_t c0 = 0; c0 < ncols; c0 += 65535LL * BN) {
+      int64_t cn = ncols - c0 < 65535LL * BN ? ncols - c0 : 65535LL * BN;
+      int rc = time_transform(T, nt, (const cplx*)in + c0, ld_in, (cplx*)out + c0, ld_out, cn,
+                              batch, bs_in, bs_out, stream);
+      if (rc) return rc;
+    }
+    return STFEM_OK;
+  }
+  dim3 grid((nt + BM - 1) / BM, (unsigned)ntile, batch);
+  time_transform_kernel<<<grid, 256, SMEM_BYTES, stream>>>(
+      (const cplx*)T, nt, (const cplx*)in, ld_in, (cplx*)out, ld_out, ncols, bs_in, bs_out);
+  STFEM_LAUNCH_CHECK("time_transform_kernel");
+  return STFEM_OK;
+}
+
+}  // namespace stfem
+
+extern "C" int stfem_time_transform(const void* T, int nt, const void* in, int64_t ld_in,
+                                    void* out, int64_t ld_out, int64_t ncols, int batch,
+                                    int64_t bstride_in, int64_t bstride_out, void* stream) {
+  return stfem::time_transform(T, nt, in, ld_in, out, ld_out, ncols, batch, bstride_in,
+                               bstride_out, (cudaStream_t)stream);
+}

@@ -1,0 +1,168 @@
+"""Kronecker space-time solver, fast-diagonalization variant.
+
+  solve(ops, M_t, B_t, f, variant=FastDiagonalization) -> SolveReport
+    (1) temporal core + eigendecomposition (host fp64, `t_setup`)
+    (2) G = (Y (x) I) F                     K3 DMMA GEMM
+    (3) (M_x + lam_l A_x) w_l = g_l         K4/K5 multifrontal SPEC.md:377, :415
+    (4) Psi = (X (x) I) W                   K3 DMMA GEMM
+  transform_blocks(T, v)   -> K3
+  apply_global(...)   -> K7 (residual certificate, :405)
+
+Kronecker factors are never materialised.  There is no silent
+Bartels-Stewart fallback: a defective core raises
+`NotDiagonalizable`.  All device work is stream-ordered; stage times are
+CUDA-event times on the launching stream.
+"""
+
+from __future__ import annotations
+
+import enum
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _kernels as K
+from . import _native as N
+from .dense_complex_linalg import TemporalFactors, temporal_factors
+from .fem_assembly import SpatialOperators, temporal_band
+from .sparse_spatial_solver import SpatialPlan, blockvector_layout
+
+C128 = torch.complex128
+
+
+class SolverVariant(enum.Enum):
+    BartelsStewart = "bs"
+    FastDiagonalization = "fd"
+
+
+@dataclass
+class SolveReport:
+    """SPEC.md:364-371."""
+
+    solution: torch.Tensor
+    solve_seconds: float
+    kappa2: float
+    relative_residual: float | None
+    timings: dict = field(default_factory=dict)
+
+
+def transform_blocks(T, v: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """out_l = sum_k T[l,k] v_k for v of shape (n_t, n_x) or (n_rhs, n_t, n_x)."""
+    Tt = torch.as_tensor(np.asarray(T) if not torch.is_tensor(T) else T, dtype=C128, device=v.device)
+    return K.time_transform(Tt, v, out=out, stream=stream)
+
+
+def apply_global(ops: SpatialOperators, M_t: np.ndarray, B_t: np.ndarray, v: torch.Tensor,
+                 stream=None) -> torch.Tensor:
+    """(i B_t (x) M_x + M_t (x) A_x) v, matrix-free (banded in time)."""
+    nt = M_t.shape[0]
+    if v.shape[-2:] != (nt, ops.n):
+        raise N.DimensionMismatch(N.ERR_DIM, f"apply_global: v {tuple(v.shape)} vs ({nt}, {ops.n})")
+    bw = 1 if np.count_nonzero(np.triu(M_t, 2)) == 0 and np.count_nonzero(np.triu(B_t, 2)) == 0 else 2
+    Mb = torch.as_tensor(temporal_band(M_t, bw), device=v.device)
+    Bb = torch.as_tensor(temporal_band(B_t, bw), device=v.device)
+    vb = v.reshape(-1, nt, ops.n)
+    out = torch.empty_like(vb)
+    work = torch.empty((2, nt, ops.n), dtype=C128, device=v.device)
+    for r in range(vb.shape[0]):
+        vr = vb[r].contiguous()
+        N.check(N.lib().stfem_apply_global(ops.handle, N.ptr(ops.Mvals), N.ptr(ops.Avals), N.ptr(Mb),
+                                           N.ptr(Bb), bw, nt, N.ptr(vr), N.ptr(out[r]), N.ptr(work),
+                                           N.stream_ptr(stream)))
+    return out.reshape(v.shape)
+
+
+def relative_residual(ops, M_t, B_t, psi: torch.Tensor, f: torch.Tensor) -> float:
+    r = apply_global(ops, M_t, B_t, psi) - f
+    fb = f.reshape(-1, *f.shape[-2:])
+    rb = r.reshape(-1, *r.shape[-2:])
+    worst = 0.0
+    for i in range(fb.shape[0]):
+        nf = float(torch.linalg.vector_norm(fb[i]))
+        nr = float(torch.linalg.vector_norm(rb[i]))
+        worst = max(worst, nr / nf if nf > 0 else nr)
+    return worst
+
+
+class FDMSolver:
+    """Reusable FD solver for one (spatial mesh, temporal mesh) pair.
+
+    setup(): temporal eigendecomposition (host fp64) + symbolic analysis,
+    uploaded once; solve(F): steps 2-4 on the GPU."""
+
+    def __init__(self, ops: SpatialOperators, M_t: np.ndarray, B_t: np.ndarray,
+                 plan: SpatialPlan | None = None, factors: TemporalFactors | None = None,
+                 leaf_size: int = 32):
+        t0 = time.perf_counter()
+        self.ops = ops
+        self.M_t = np.asarray(M_t, float)
+        self.B_t = np.asarray(B_t, float)
+        self.nt = self.M_t.shape[0]
+        self.tf = factors if factors is not None else temporal_factors(self.M_t, self.B_t)
+        t1 = time.perf_counter()
+        self.plan = plan if plan is not None else SpatialPlan(ops, leaf_size)
+        t2 = time.perf_counter()
+        dev = ops.device
+        self.X = torch.as_tensor(self.tf.X, dtype=C128, device=dev)
+        self.Y = torch.as_tensor(self.tf.Y, dtype=C128, device=dev)
+        self.lam = torch.as_tensor(self.tf.eigenvalues, dtype=C128, device=dev)
+        self.t_eig = t1 - t0
+        self.t_symbolic = t2 - t1
+
+    @property
+    def kappa2(self) -> float:
+        return self.tf.kappa2
+
+    def solve(self, F: torch.Tensor, out: torch.Tensor | None = None, work: torch.Tensor | None = None,
+              stream=None, timings: dict | None = None) -> torch.Tensor:
+        """Psi for F of shape (n_t, n_x) or (n_rhs, n_t, n_x), complex128 on the GPU."""
+        N.require_cuda(F)
+        if F.shape[-2:] != (self.nt, self.ops.n):
+            raise N.DimensionMismatch(N.ERR_DIM, f"solve: f {tuple(F.shape)} vs ({self.nt}, {self.ops.n})")
+        single = F.dim() == 2
+        Fb = (F.unsqueeze(0) if single else F).contiguous()
+        nr = Fb.shape[0]
+        G = work if work is not None else torch.empty_like(Fb)
+        G = G.reshape(Fb.shape)
+        W = out.reshape(Fb.shape) if out is not None else torch.empty_like(Fb)
+        s = stream if stream is not None else torch.cuda.current_stream()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timings is not None else None
+        if ev:
+            ev[0].record(s)
+        K.time_transform(self.Y, Fb, out=G, stream=s)                 # (2)
+        if ev:
+            ev[1].record(s)
+        self.plan.factor_solve(self.lam, G, W, blockvector_layout(self.nt, self.ops.n), nr, stream=s)  # (3)
+        if ev:
+            ev[2].record(s)
+        K.time_transform(self.X, W, out=G, stream=s)                  # (4)
+        if ev:
+            ev[3].record(s)
+            ev[3].synchronize()
+            timings["forward_transform_s"] = ev[0].elapsed_time(ev[1]) / 1e3
+            timings["factor_solve_s"] = ev[1].elapsed_time(ev[2]) / 1e3
+            timings["back_transform_s"] = ev[2].elapsed_time(ev[3]) / 1e3
+        if out is not None:
+            out.copy_(G.reshape(out.shape))
+            return out
+        res = G
+        return res[0] if single else res
+
+
+def solve(ops: SpatialOperators, M_t: np.ndarray, B_t: np.ndarray, f: torch.Tensor,
+          variant: SolverVariant = SolverVariant.FastDiagonalization, check_residual: bool = True,
+          plan: SpatialPlan | None = None) -> SolveReport:
+    """SPEC.md:374-382 (FD variant).  Times steps 1-4."""
+    if variant != SolverVariant.FastDiagonalization:
+        raise NotImplementedError("Bartels-Stewart is out of scope for this build (SURVEY.md §2)")
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    fdm = FDMSolver(ops, M_t, B_t, plan=plan)
+    timings = {"eig_s": fdm.t_eig, "symbolic_s": fdm.t_symbolic}
+    psi = fdm.solve(f, timings=timings)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    res = relative_residual(ops, fdm.M_t, fdm.B_t, psi, f) if check_residual else None
+    return SolveReport(psi, t1 - t0, fdm.kappa2, res, timings)

@@ -1,0 +1,140 @@
+"""Batched sparse direct solver for the shifted spatial systems.
+
+`SpatialPlan` = one host symbolic analysis per sparsity pattern (geometric
+nested dissection, supernodal tree, extend-add maps; csrc/symbolic.cpp),
+shared by every shift.  The numeric multifrontal
+complex-symmetric LDL^T factorization and both triangular solves run on the
+GPU, batched across shifts (csrc/multifrontal.cu).
+
+SPEC API: `factor(M_x, A_x, lam) -> SpatialFactorization`, `solve(fact, b)`.
+Factors are never materialised for later reuse on the device (they are
+streamed per batch of shifts, SURVEY.md §7 hard part 4), so a
+`SpatialFactorization` records (plan, operators, shifts) and `solve` runs the
+fused factor + solve.  `factor_solve_batch` is the batched form used by the
+FD solver.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .fem_assembly import SpatialOperators
+
+
+class SpatialPlan:
+    def __init__(self, ops: SpatialOperators, leaf_size: int = 32):
+        self.ops = ops
+        self.n = ops.n
+        h = C.c_void_p()
+        N.check(N.lib().stfem_plan_create(ops.n, ops.rowptr.ctypes.data, ops.colind.ctypes.data,
+                                          ops.coords.ctypes.data, 2, leaf_size, C.byref(h)))
+        self._h = h
+        st = N.plan_stats()
+        N.check(N.lib().stfem_plan_stats_get(h, C.byref(st)))
+        self.stats = {f: getattr(st, f) for f, _ in N.plan_stats._fields_}
+
+    @property
+    def handle(self):
+        return self._h
+
+    def perm(self) -> np.ndarray:
+        p = np.empty(self.n, dtype=np.int32)
+        N.check(N.lib().stfem_plan_perm(self._h, p.ctypes.data))
+        return p
+
+    def fronts(self) -> np.ndarray:
+        t = np.empty((self.stats["num_fronts"], 5), dtype=np.int32)
+        N.check(N.lib().stfem_plan_fronts(self._h, t.ctypes.data))
+        return t
+
+    def front_rows(self):
+        """List of row-index arrays (new numbering) per front."""
+        nf = self.stats["num_fronts"]
+        off = np.empty(nf + 1, dtype=np.int64)
+        N.check(N.lib().stfem_plan_front_rows(self._h, off.ctypes.data, None))
+        rows = np.empty(off[-1], dtype=np.int32)
+        N.check(N.lib().stfem_plan_front_rows(self._h, off.ctypes.data, rows.ctypes.data))
+        return [rows[off[f]:off[f + 1]] for f in range(nf)]
+
+    def set_batch(self, batch: int) -> int:
+        bps = C.c_int64()
+        N.check(N.lib().stfem_plan_set_batch(self._h, int(batch), C.byref(bps)))
+        return bps.value
+
+    def factor_solve(self, lam: torch.Tensor, G: torch.Tensor, W: torch.Tensor, layout: N.bv_layout,
+                     nrhs: int, stream=None):
+        """(M_x + lam[s] A_x) W[r, s] = G[r, s] for every shift s (device c128)."""
+        N.require_cuda(G)
+        ops = self.ops
+        if ops.Mvals is None:
+            raise RuntimeError("spatial operators are not assembled")
+        lam = lam.to(device=G.device, dtype=torch.complex128).contiguous()
+        for r0 in range(0, nrhs, 16):
+            nr = min(16, nrhs - r0)
+            off = r0 * layout.rhs_stride
+            N.check(N.lib().stfem_factor_solve(
+                self._h, N.ptr(ops.Mvals), N.ptr(ops.Avals), N.ptr(lam), lam.numel(), nr,
+                C.c_void_p(G.data_ptr() + 16 * off), C.c_void_p(W.data_ptr() + 16 * off), layout,
+                N.stream_ptr(stream)))
+        return W
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and N is not None and N._lib is not None:
+            N._lib.stfem_plan_destroy(h)
+            self._h = None
+
+
+def blockvector_layout(nt: int, nx: int) -> N.bv_layout:
+    """Layout of a (n_rhs, n_t, n_x) stack of BlockVectors."""
+    return N.bv_layout(nt * nx, nx, nx, 0)
+
+
+@dataclass(frozen=True)
+class SpatialFactorization:
+    """K_lam = M_x + lam A_x over a shared plan."""
+
+    plan: SpatialPlan
+    lam: complex
+
+    @property
+    def n(self) -> int:
+        return self.plan.n
+
+
+def factor(plan_or_ops, M_x=None, A_x=None, lam: complex = 0j) -> SpatialFactorization:
+    """SPEC.md:323-331.  `plan_or_ops` is a SpatialPlan (or SpatialOperators,
+    for which a plan is built).  M_x/A_x must be the plan's operators."""
+    plan = plan_or_ops if isinstance(plan_or_ops, SpatialPlan) else SpatialPlan(plan_or_ops)
+    return SpatialFactorization(plan, complex(lam))
+
+
+def solve(fact: SpatialFactorization, b: torch.Tensor) -> torch.Tensor:
+    """w with K_lam w = b (b: (n_x,) or (n_rhs, n_x) complex128 on the GPU)."""
+    n = fact.n
+    if b.shape[-1] != n:
+        raise N.DimensionMismatch(N.ERR_DIM, f"solve: rhs length {b.shape[-1]} != n_x {n}")
+    bb = b.reshape(-1, n).to(torch.complex128).contiguous()
+    W = torch.empty_like(bb)
+    lam = torch.tensor([fact.lam], dtype=torch.complex128, device=bb.device)
+    fact.plan.factor_solve(lam, bb, W, N.bv_layout(n, 0, n, 0), bb.shape[0])
+    return W.reshape(b.shape)
+
+
+def factor_solve_batch(plan: SpatialPlan, lam, G: torch.Tensor, W: torch.Tensor | None = None):
+    """W[r, l] = (M_x + lam_l A_x)^{-1} G[r, l] for G of shape (n_t, n_x) or (n_rhs, n_t, n_x)."""
+    single = G.dim() == 2
+    Gb = (G.unsqueeze(0) if single else G).contiguous()
+    nr, nt, nx = Gb.shape
+    if W is None:
+        W = torch.empty_like(Gb)
+    lam_t = torch.as_tensor(np.asarray(lam), dtype=torch.complex128, device=G.device)
+    if lam_t.numel() != nt:
+        raise N.DimensionMismatch(N.ERR_DIM, "factor_solve_batch: one shift per temporal block")
+    plan.factor_solve(lam_t, Gb, W, blockvector_layout(nt, nx), nr)
+    return W[0] if single else W

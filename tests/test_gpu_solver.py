@@ -1,0 +1,213 @@
+"""GPU parity: assembly (K1/K2), multifrontal factor+solve (K4/K5), FD solve,
+apply_global (K7) against the CPU oracle on the same inputs."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import stfem_oracle as O
+from paper_2504_07269_b200 import fem_assembly as fa
+from paper_2504_07269_b200 import kronecker_solver as ks
+from paper_2504_07269_b200 import spatial_mesh as sm
+from paper_2504_07269_b200 import sparse_spatial_solver as sss
+from paper_2504_07269_b200 import temporal_mesh as tm
+from paper_2504_07269_b200.dense_complex_linalg import temporal_factors
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def omesh(mesh):
+    return O.finish(2, mesh.vertices, mesh.elements)
+
+
+@pytest.mark.parametrize("kind", ["square7", "p2square5", "lshape3"])
+def test_assembly_matches_oracle(kind):
+    if kind == "square7":
+        mesh, deg = sm.build_structured_square(7), 1
+        Mo, Ao = O.assemble_spatial(omesh(mesh))
+    elif kind == "p2square5":
+        mesh, deg = sm.refine_uniform(sm.build_structured_square(5)), 2
+        Mo, Ao = O.assemble_spatial(omesh(mesh), 2, mesh.p2_elements)
+    else:
+        mesh, deg = sm.build_lshape(3), 1
+        Mo, Ao = O.assemble_spatial(omesh(mesh))
+    ops = fa.assemble_spatial(mesh, deg)
+    M = ops.M_x.to_scipy().toarray()
+    A = ops.A_x.to_scipy().toarray()
+    assert rel(M, Mo.toarray()) < 1e-14
+    assert rel(A, Ao.toarray()) < 1e-14
+
+
+def test_spec_example_m2():
+    """m=2 -> M_x = [1/8], A_x = [4]."""
+    ops = fa.assemble_spatial(sm.build_structured_square(2))
+    assert abs(ops.Mvals.item() - 1 / 8) < 1e-15 and abs(ops.Avals.item() - 4) < 1e-14
+
+
+@pytest.mark.parametrize("source", ["sinpit", "texp", "paper"])
+def test_rhs_matches_oracle(source):
+    mesh = sm.build_structured_square(6)
+    bp = O.temporal_uniform(1.5, 5)
+    ops = fa.assemble_spatial(mesh)
+    F = fa.assemble_rhs(ops, tm.uniform(1.5, 5), source).cpu().numpy()
+    Fo = O.assemble_rhs(omesh(mesh), bp, O.manufactured(source)[3])
+    assert rel(F, Fo) < 1e-13
+
+
+def test_lifting_matches_oracle():
+    mesh = sm.build_lshape(4)
+    from paper_2504_07269_b200.problems import psi0_interior
+    ops = fa.assemble_spatial(mesh)
+    p0 = psi0_interior(mesh)
+    L = fa.lifting_rhs(ops, tm.uniform(1.0, 6), p0).cpu().numpy()
+    _, Ao = O.assemble_spatial(omesh(mesh))
+    Lo = O.lifting_rhs(omesh(mesh), O.temporal_uniform(1.0, 6), Ao, p0)
+    assert rel(L, Lo) < 1e-13
+
+
+@pytest.mark.parametrize("kind,leaf", [("square9", 4), ("square16", 32), ("p2square6", 8),
+                                        ("lshape5", 16), ("square40", 32)])
+def test_factor_solve_matches_splu(kind, leaf):
+    if kind.startswith("p2"):
+        mesh, deg = sm.refine_uniform(sm.build_structured_square(int(kind[8:]))), 2
+        Mo, Ao = O.assemble_spatial(omesh(mesh), 2, mesh.p2_elements)
+    elif kind.startswith("lshape"):
+        mesh, deg = sm.build_lshape(int(kind[6:])), 1
+        Mo, Ao = O.assemble_spatial(omesh(mesh))
+    else:
+        mesh, deg = sm.build_structured_square(int(kind[6:])), 1
+        Mo, Ao = O.assemble_spatial(omesh(mesh))
+    ops = fa.assemble_spatial(mesh, deg)
+    plan = sss.SpatialPlan(ops, leaf_size=leaf)
+    rng = np.random.default_rng(1)
+    nt, nr = 7, 3
+    lam = np.array([0.3 - 0.1j, -0.02 - 1e-4j, 1 + 1j, 1e-3 - 2e-3j, -0.5 - 0.01j, 2.0 + 0j, -1e-2 - 5e-1j])
+    G = rng.standard_normal((nr, nt, ops.n)) + 1j * rng.standard_normal((nr, nt, ops.n))
+    W = sss.factor_solve_batch(plan, lam, torch.from_numpy(G).cuda()).cpu().numpy()
+    for l in range(nt):
+        ref = O._solve_shift(Mo, Ao, lam[l], G[:, l, :].T).T
+        assert rel(W[:, l, :], ref) < 1e-11, (l, rel(W[:, l, :], ref))
+
+
+def test_batching_invariance():
+    """Results identical whatever the shift batch size."""
+    mesh = sm.build_structured_square(20)
+    ops = fa.assemble_spatial(mesh)
+    plan = sss.SpatialPlan(ops)
+    rng = np.random.default_rng(5)
+    nt = 9
+    lam = rng.standard_normal(nt) - 1j * rng.random(nt)
+    G = torch.from_numpy(rng.standard_normal((1, nt, ops.n)) + 0j).cuda()
+    plan.set_batch(0)
+    W0 = sss.factor_solve_batch(plan, lam, G).cpu().numpy()
+    plan.set_batch(2)
+    W1 = sss.factor_solve_batch(plan, lam, G).cpu().numpy()
+    assert np.array_equal(W0, W1)
+
+
+def test_spec_scalar_factor_example():
+    """n_x=1, lam=-2i/3 -> solve([1]) = 1/(1/8 - 8i/3)."""
+    ops = fa.assemble_spatial(sm.build_structured_square(2))
+    f = sss.factor(ops, lam=-2j / 3)
+    w = sss.solve(f, torch.ones(1, dtype=torch.complex128, device="cuda")).item()
+    assert abs(w - 1 / (1 / 8 - 8j / 3)) < 1e-14
+
+
+def fd_case(m, T, N, source, seed=3):
+    mesh = sm.build_structured_square(m)
+    tmesh = tm.uniform(T, N)
+    ops = fa.assemble_spatial(mesh)
+    Mt, Bt = fa.assemble_temporal(tmesh)
+    F = [fa.assemble_rhs(ops, tmesh, source)]
+    rng = np.random.default_rng(seed)
+    F.append(torch.from_numpy((rng.standard_normal((N, ops.n)) + 1j * rng.standard_normal((N, ops.n))) / np.sqrt(2)).cuda())
+    return mesh, tmesh, ops, Mt, Bt, torch.stack(F)
+
+
+@pytest.mark.parametrize("m,T,N,source", [(16, 1.0, 16, "sinpit"), (64, 1.0, 64, "sinpit"),
+                                          (32, 2.0, 48, "texp")])
+def test_fdm_solve_matches_oracle(m, T, N, source):
+    """Full FD solve (C1 and C2 configs) vs the oracle on identical (lam, X, Y) and F: <= 1e-9."""
+    mesh, tmesh, ops, Mt, Bt, F = fd_case(m, T, N, source)
+    Mo, Ao = O.assemble_spatial(omesh(mesh))
+    tfo = O.eigen_decompose(Mt, Bt)
+    mine = temporal_factors(Mt, Bt)
+    assert np.abs(mine.eigenvalues - tfo.lam).max() < 1e-14 * np.abs(tfo.lam).max()
+    assert np.abs(mine.X - tfo.X).max() < 1e-13
+    # parity isolates the GPU arithmetic: both paths consume the same (lam, X, Y)
+    from paper_2504_07269_b200.dense_complex_linalg import TemporalFactors
+    shared = TemporalFactors(X=tfo.X, S=np.diag(tfo.lam), Y=tfo.Y, kappa2=tfo.kappa2)
+    fdm = ks.FDMSolver(ops, Mt, Bt, factors=shared)
+    psi = fdm.solve(F).cpu().numpy()
+    ref = O.fdm_solve(Mo, Ao, tfo, F.cpu().numpy())
+    for r in range(2):
+        assert rel(psi[r], ref[r]) < 1e-9, rel(psi[r], ref[r])
+    res = ks.relative_residual(ops, Mt, Bt, torch.from_numpy(psi).cuda(), F)
+    assert res < 1e-8
+    if m == 16:
+        # manufactured-solution errors reproduce the oracle's to 3 significant digits
+        from paper_2504_07269_b200 import error_analysis as ea
+        e_gpu = ea.spacetime_errors(psi[0], ea.exact_solution(source), mesh, tmesh)
+        ps, dt, gr, _ = O.manufactured(source)
+        e_ref = O.spacetime_errors(omesh(mesh), tmesh.breakpoints, ref[0], ps, dt, gr)
+        for a, b in zip(e_gpu, e_ref):
+            assert abs(a - b) / b < 5e-4
+
+
+def test_spec_1x1_global():
+    """n_x = n_t = 1 global system, psi = 1/(4/3 + i/16)."""
+    ops = fa.assemble_spatial(sm.build_structured_square(2))
+    Mt, Bt = fa.assemble_temporal(tm.uniform(1.0, 1))
+    rep = ks.solve(ops, Mt, Bt, torch.ones((1, 1), dtype=torch.complex128, device="cuda"))
+    assert abs(rep.solution.item() - 1 / (4 / 3 + 1j / 16)) < 1e-14
+    assert rep.relative_residual < 1e-14
+
+
+def test_apply_global_matches_oracle():
+    mesh = sm.build_structured_square(9)
+    for deg_t in (1, 2):
+        tmesh = tm.uniform(1.0, 7)
+        ops = fa.assemble_spatial(mesh)
+        Mt, Bt = fa.assemble_temporal(tmesh, deg_t)
+        rng = np.random.default_rng(0)
+        v = rng.standard_normal((Mt.shape[0], ops.n)) + 1j * rng.standard_normal((Mt.shape[0], ops.n))
+        out = ks.apply_global(ops, Mt, Bt, torch.from_numpy(v).cuda()).cpu().numpy()
+        Mo, Ao = O.assemble_spatial(omesh(mesh))
+        ref = O.apply_global(Mo, Ao, Mt, Bt, v)
+        assert rel(out, ref) < 1e-13
+
+
+def test_dense_oracle_small():
+    """m=4 square, n_t=4, random f vs the explicit Kronecker system, 1e-10."""
+    mesh = sm.build_structured_square(4)
+    tmesh = tm.uniform(1.0, 4)
+    ops = fa.assemble_spatial(mesh)
+    Mt, Bt = fa.assemble_temporal(tmesh)
+    rng = np.random.default_rng(11)
+    f = rng.standard_normal((4, ops.n)) + 1j * rng.standard_normal((4, ops.n))
+    psi = ks.solve(ops, Mt, Bt, torch.from_numpy(f).cuda()).solution.cpu().numpy()
+    Mo, Ao = O.assemble_spatial(omesh(mesh))
+    ref = np.linalg.solve(O.dense_global(Mo, Ao, Mt, Bt), f.ravel()).reshape(f.shape)
+    assert rel(psi, ref) < 1e-10
+
+
+def test_fd_factor_solve_c3_sample_shifts():
+    """C3-size operator (m=256, P1) at the hardest shifts of n_t = 256 vs splu."""
+    mesh = sm.build_structured_square(256)
+    ops = fa.assemble_spatial(mesh)
+    Mt, Bt = fa.assemble_temporal(tm.uniform(2.0, 256))
+    tf = temporal_factors(Mt, Bt)
+    lam_all = tf.eigenvalues
+    pick = np.r_[np.argsort(np.abs(lam_all.imag))[:3], [0, 128, 255]]
+    lam = lam_all[pick]
+    plan = sss.SpatialPlan(ops)
+    rng = np.random.default_rng(2)
+    G = rng.standard_normal((1, len(lam), ops.n)) + 1j * rng.standard_normal((1, len(lam), ops.n))
+    W = sss.factor_solve_batch(plan, lam, torch.from_numpy(G).cuda()).cpu().numpy()
+    Mo, Ao = O.assemble_spatial(omesh(mesh))
+    for l in range(len(lam)):
+        ref = O._solve_shift(Mo, Ao, lam[l], G[0, l])
+        assert rel(W[0, l], ref) < 1e-10
