@@ -20,6 +20,7 @@
 // to the caller's BlockVector.  Transpose, not conjugate transpose: K is
 // complex symmetric.
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <string>
@@ -394,6 +395,8 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a) {
   }
 }
 
+#include "multifrontal_small.cuh"
+
 int upload(Plan& P) {
   int dev;
   STFEM_CUDA_TRY(cudaGetDevice(&dev));
@@ -427,6 +430,17 @@ int upload(Plan& P) {
   STFEM_CUDA_TRY(cudaMemset(P.d_err, 0, sizeof(int)));
   STFEM_CUDA_TRY(cudaFuncSetAttribute(factor_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       FACTOR_SMEM));
+  STFEM_CUDA_TRY(cudaFuncSetAttribute(factor_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      small_smem_bytes(SMALL_N, MAXR)));
+  STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      200 * 1024));
+  P.level_nmax.assign(P.levels.size(), 0);
+  P.level_pmax.assign(P.levels.size(), 0);
+  for (size_t d = 0; d < P.levels.size(); ++d)
+    for (int32_t f : P.levels[d]) {
+      P.level_nmax[d] = std::max(P.level_nmax[d], P.fronts[f].n);
+      P.level_pmax[d] = std::max(P.level_pmax[d], P.fronts[f].p);
+    }
   return STFEM_OK;
 }
 
@@ -534,6 +548,17 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
   a.W = W;
   a.lay = lay;
   a.err = P.d_err;
+  // STFEM_LEVEL_TIMING=1: per-launch CUDA-event times to stderr (diagnostics only)
+  static const bool level_timing = getenv("STFEM_LEVEL_TIMING") != nullptr;
+  std::vector<cudaEvent_t> evs;
+  auto mark = [&]() {
+    if (!level_timing) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, stream);
+    evs.push_back(e);
+  };
+  mark();
   for (int s0 = 0; s0 < nshift; s0 += batch) {
     const int nb = std::min(batch, nshift - s0);
     a.nbatch = nb;
@@ -551,15 +576,43 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
       a.rcur_stride = P.rpool_stride[q];
       a.rchild = P.d_rpool[q ^ 1];
       a.rchild_stride = P.rpool_stride[q ^ 1];
-      factor_level_kernel<<<a.nlist * nb, NT, FACTOR_SMEM, stream>>>(a);
-      STFEM_LAUNCH_CHECK("factor_level_kernel");
+      const int nmax = P.level_nmax[d];
+      if (nmax <= SMALL_N && !P.force_big) {
+        factor_small_kernel<<<a.nlist * nb, (nmax + 31) / 32 * 32, small_smem_bytes(nmax, nrhs), stream>>>(a, nmax);
+        STFEM_LAUNCH_CHECK("factor_small_kernel");
+      } else {
+        factor_level_kernel<<<a.nlist * nb, NT, FACTOR_SMEM, stream>>>(a);
+        STFEM_LAUNCH_CHECK("factor_level_kernel");
+      }
+      mark();
     }
     for (int d = 0; d <= P.depth; ++d) {
       a.list = P.d_levels + P.level_off[d];
       a.nlist = (int32_t)P.levels[d].size();
-      backward_level_kernel<<<a.nlist * nb, NT, 0, stream>>>(a);
-      STFEM_LAUNCH_CHECK("backward_level_kernel");
+      const int nmax = P.level_nmax[d], pmax = P.level_pmax[d];
+      const int bsm = small_bwd_smem_bytes(nmax, pmax, nrhs);
+      if (nmax <= SMALL_N && bsm <= 200 * 1024 && !P.force_big) {
+        backward_small_kernel<<<a.nlist * nb, (nmax + 31) / 32 * 32, bsm, stream>>>(a, nmax, pmax);
+        STFEM_LAUNCH_CHECK("backward_small_kernel");
+      } else {
+        backward_level_kernel<<<a.nlist * nb, NT, 0, stream>>>(a);
+        STFEM_LAUNCH_CHECK("backward_level_kernel");
+      }
+      mark();
     }
+  }
+  P.last_batch = batch;
+  if (level_timing) {
+    cudaStreamSynchronize(stream);
+    int L = P.depth + 1;
+    for (size_t i = 1; i < evs.size(); ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, evs[i - 1], evs[i]);
+      int j = (int)((i - 1) % (2 * L));
+      fprintf(stderr, "[stfem] batch %d %s depth %d: %.3f ms\n", (int)((i - 1) / (2 * L)),
+              j < L ? "factor" : "backward", j < L ? P.depth - j : j - L, ms);
+    }
+    for (auto e : evs) cudaEventDestroy(e);
   }
   int h_err = 0;
   STFEM_CUDA_TRY(cudaMemcpyAsync(&h_err, P.d_err, sizeof(int), cudaMemcpyDeviceToHost, stream));

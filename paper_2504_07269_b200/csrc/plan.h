@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdlib.h>
+
 #include <vector>
 
 #include "common.cuh"
@@ -46,6 +48,8 @@ struct Plan {
   FrontDev* d_fronts = nullptr;
   int32_t* d_levels = nullptr;             // concatenated level lists
   std::vector<int64_t> level_off;          // offsets into d_levels
+  std::vector<int32_t> level_nmax, level_pmax;  // per depth: max front order / pivots
+  bool force_big = getenv("STFEM_FORCE_BIG") != nullptr;  // diagnostics: disable the small-front path
   int32_t *d_child_ids = nullptr, *d_bidx = nullptr, *d_relpos = nullptr;
   int32_t *d_ent_src = nullptr, *d_ent_dst = nullptr, *d_perm = nullptr;
   int* d_err = nullptr;
@@ -54,6 +58,7 @@ struct Plan {
   int32_t batch = 0;       // requested (0 = auto)
   int32_t ws_batch = 0;    // allocated for
   int32_t ws_nrhs = 0;
+  int32_t last_batch = 0;  // batch size used by the last factor_solve
   cplx* d_factor = nullptr;
   cplx* d_upool[2] = {nullptr, nullptr};
   cplx* d_rpool[2] = {nullptr, nullptr};

@@ -1,0 +1,210 @@
+"""Multi-GPU FD solve: one process per GPU, NCCL all-to-all over NVLink.
+
+Partitioning (north_star):
+  * every rank holds the plan, M_x/A_x, X, Y, lam (replicated; X/Y/lam are
+    computed once on rank 0 and broadcast so every rank uses identical bits);
+  * spatial shard: rank p owns columns [p c, (p+1) c) of every temporal block,
+    c = ceil(n_x / P) (the last shard is zero-padded);
+  * local layout of a shard is (n_t, n_rhs, c): the forward transform is ONE
+    GEMM G_p = Y F_p with N = n_rhs c, and the all-to-all send block for rank
+    q (its n_t/P shifts) is one contiguous (n_t/P, n_rhs, c) slab;
+  * all-to-all #1 -> rank q holds (P, n_t/P, n_rhs, c) = all columns of its
+    n_t/P shifts; the multifrontal factor+solve reads/writes that buffer in
+    place through the chunked BlockVector layout (no repack);
+  * all-to-all #2 returns (n_t, n_rhs, c) shards; back transform Psi_p = X W_p.
+The compute backend is injectable so the orchestration (sharding, layouts,
+exchange) is testable on CPU with gloo; the product backend is the CUDA one.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _native as N
+
+C128 = torch.complex128
+
+
+class CudaBackend:
+    """K3 transforms + K4/K5 factor/solve through the C-ABI."""
+
+    def __init__(self, plan):
+        self.plan = plan
+
+    def transform(self, T, x, out):
+        from . import _kernels as K
+        K.time_transform(T, x, out=out)
+
+    def factor_solve(self, lam, G, W, layout, nrhs):
+        self.plan.factor_solve(lam, G, W, layout, nrhs)
+
+
+def shard_cols(nx: int, P: int) -> int:
+    return -(-nx // P)
+
+
+def chunked_layout(nt_loc: int, nrhs: int, c: int) -> N.bv_layout:
+    """Element (rhs r, local shift l, column j) of a (P, nt_loc, nrhs, c) buffer."""
+    return N.bv_layout(c, nrhs * c, c, nt_loc * nrhs * c)
+
+
+def shard_rhs(F: torch.Tensor, rank: int, P: int) -> torch.Tensor:
+    """(n_rhs, n_t, n_x) full stack -> this rank's (n_t, n_rhs, c) shard (zero padded)."""
+    nr, nt, nx = F.shape
+    c = shard_cols(nx, P)
+    lo, hi = rank * c, min(nx, (rank + 1) * c)
+    out = torch.zeros((nt, nr, c), dtype=F.dtype, device=F.device)
+    if hi > lo:
+        out[:, :, :hi - lo] = F[:, :, lo:hi].permute(1, 0, 2)
+    return out
+
+
+def unshard(Psi_p: torch.Tensor, nx: int, rank: int, P: int) -> torch.Tensor:
+    """(n_t, n_rhs, c) shard -> (n_rhs, n_t, cols) of the real columns it owns."""
+    c = Psi_p.shape[-1]
+    lo, hi = rank * c, min(nx, (rank + 1) * c)
+    return Psi_p[:, :, :max(0, hi - lo)].permute(1, 0, 2)
+
+
+class DistributedFDM:
+    """FD solve of a replicated problem with spatially sharded inputs/outputs."""
+
+    def __init__(self, nx: int, nt: int, nrhs: int, X: torch.Tensor, Y: torch.Tensor, lam: torch.Tensor,
+                 backend, group=None):
+        self.group = group
+        self.P = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if nt % self.P:
+            raise N.DimensionMismatch(N.ERR_DIM, f"n_t={nt} must be divisible by the world size {self.P}")
+        self.nx, self.nt, self.nrhs = nx, nt, nrhs
+        self.c = shard_cols(nx, self.P)
+        self.ntl = nt // self.P
+        self.X, self.Y = X, Y
+        self.lam_local = lam[self.rank * self.ntl:(self.rank + 1) * self.ntl].contiguous()
+        self.backend = backend
+        dev = X.device
+        shape = (nt, nrhs, self.c)
+        self.G = torch.empty(shape, dtype=C128, device=dev)
+        self.R = torch.empty(shape, dtype=C128, device=dev)   # receive buffer (P, ntl, nrhs, c)
+        self.W = torch.zeros(shape, dtype=C128, device=dev)
+        self.layout = chunked_layout(self.ntl, nrhs, self.c)
+
+    def _a2a(self, out, inp):
+        if self.P == 1:
+            out.copy_(inp)
+        else:
+            dist.all_to_all_single(out, inp, group=self.group)
+
+    def solve(self, F_p: torch.Tensor, out: torch.Tensor | None = None, timings: dict | None = None):
+        """F_p: (n_t, n_rhs, c) shard.  Returns Psi_p in the same layout."""
+        nt, nr, c = self.nt, self.nrhs, self.c
+        if F_p.shape != (nt, nr, c):
+            raise N.DimensionMismatch(N.ERR_DIM, f"shard {tuple(F_p.shape)} != {(nt, nr, c)}")
+        out = out if out is not None else torch.empty_like(F_p)
+        t = [time.perf_counter()]
+        self.backend.transform(self.Y, F_p.view(nt, nr * c), self.G.view(nt, nr * c))      # (2)
+        self._a2a(self.R, self.G)                                                           # a2a #1
+        self.backend.factor_solve(self.lam_local, self.R, self.W, self.layout, nr)         # (3)
+        self._a2a(self.G, self.W)                                                           # a2a #2
+        self.backend.transform(self.X, self.G.view(nt, nr * c), out.view(nt, nr * c))      # (4)
+        return out
+
+
+def broadcast_factors(X, Y, lam, device):
+    """Rank 0's (X, Y, lam) on every rank (identical bits everywhere)."""
+    out = []
+    for a in (X, Y, lam):
+        t = torch.tensor(np.ascontiguousarray(a), dtype=C128).to(device)
+        if dist.is_initialized() and dist.get_world_size() > 1:
+            dist.broadcast(torch.view_as_real(t), 0)   # collectives on the real view
+        out.append(t)
+    return tuple(out)
+
+
+def bench_main(args):
+    """bench.py --gpus N under torchrun: strong scaling of one config."""
+    import json
+
+    from . import kronecker_solver as ks  # noqa: F401
+    from .dense_complex_linalg import temporal_factors
+    from .problems import Problem
+    from .sparse_spatial_solver import SpatialPlan
+
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    t0 = time.perf_counter()
+    prob = Problem(args.workload, device=dev, with_rhs=False)
+    prob.assemble()
+    torch.cuda.synchronize()
+    t_asm = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    tf = temporal_factors(prob.M_t, prob.B_t) if rank == 0 else None
+    nt = prob.nt
+    X = tf.X if rank == 0 else np.zeros((nt, nt), complex)
+    Y = tf.Y if rank == 0 else np.zeros((nt, nt), complex)
+    lam = tf.eigenvalues if rank == 0 else np.zeros(nt, complex)
+    Xt, Yt, lt = broadcast_factors(X, Y, lam, dev)
+    plan = SpatialPlan(prob.ops)
+    t_setup = time.perf_counter() - t1
+    solver = DistributedFDM(prob.nx, nt, prob.n_rhs, Xt, Yt, lt, CudaBackend(plan))
+    # this rank's RHS shard: deterministic part on device + Gaussian columns from the shared streams
+    Fp = _local_rhs(prob, rank, world, dev)
+    out = torch.empty_like(Fp)
+    for _ in range(args.warmup):
+        solver.solve(Fp, out)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(args.steps):
+        solver.solve(Fp, out)
+    e.record()
+    torch.cuda.synchronize()
+    t_local = s.elapsed_time(e) / 1e3 / args.steps
+    tt = torch.tensor([t_local], dtype=torch.float64, device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    dist.barrier()
+    t_step = float(tt.item())
+    dofs = prob.nx * nt * prob.n_rhs
+    if rank == 0:
+        line = {"metric": "space-time DoF/s (complex fp64) of the FDM direct solve", "value": dofs / t_step,
+                "unit": "DoF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "c128", "data": "synthetic (seeded Gaussian RHS; BASELINE.json configs)",
+                "config": {"workload": args.workload, "n_x": prob.nx, "n_t": nt, "n_rhs": prob.n_rhs,
+                           "parallelism": f"space-sharded transforms + time-sharded shifts, a2a x2 over {world} GPUs"},
+                "setup_s": t_setup, "asm_s": t_asm, "gpu_launches": None}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
+def _local_rhs(prob, rank, world, dev):
+    """(n_t, n_rhs, c) shard of the config's RHS stack, generated locally."""
+    from . import fem_assembly as fa
+    from .problems import gaussian_rhs
+    nx, nt = prob.nx, prob.nt
+    c = shard_cols(nx, world)
+    lo, hi = rank * c, min(nx, (rank + 1) * c)
+    parts = []
+    if prob.cfg.source:
+        parts.append(fa.assemble_rhs(prob.ops, prob.tmesh, prob.cfg.source)[:, lo:hi])
+    if prob.cfg.psi0:
+        parts.append(fa.lifting_rhs(prob.ops, prob.tmesh, prob.psi0)[:, lo:hi])
+    Fp = torch.zeros((nt, prob.n_rhs, c), dtype=C128, device=dev)
+    for i, part in enumerate(parts):
+        Fp[:, i, :hi - lo] = part
+    if prob.cfg.n_gauss:
+        g = gaussian_rhs(prob.seed, prob.cfg.n_gauss, nt, nx)
+        Fp[:, len(parts):, :hi - lo] = torch.from_numpy(np.ascontiguousarray(g[:, :, lo:hi].transpose(1, 0, 2))).to(dev)
+    return Fp

@@ -68,9 +68,12 @@ def test_lifting_matches_oracle():
     assert rel(L, Lo) < 1e-13
 
 
+@pytest.mark.parametrize("force_big", [False, True])
 @pytest.mark.parametrize("kind,leaf", [("square9", 4), ("square16", 32), ("p2square6", 8),
                                         ("lshape5", 16), ("square40", 32)])
-def test_factor_solve_matches_splu(kind, leaf):
+def test_factor_solve_matches_splu(kind, leaf, force_big, monkeypatch):
+    if force_big:  # exercise the global-memory (large-front) kernels on small meshes too
+        monkeypatch.setenv("STFEM_FORCE_BIG", "1")
     if kind.startswith("p2"):
         mesh, deg = sm.refine_uniform(sm.build_structured_square(int(kind[8:]))), 2
         Mo, Ao = O.assemble_spatial(omesh(mesh), 2, mesh.p2_elements)
