@@ -111,16 +111,26 @@ __device__ void gemm_update(cplx* __restrict__ C, int ldC, int M, int N, const c
       }
     };
 
+    // accumulators start as C (loads issued together with the first cp.async
+    // stage so their latency overlaps); the MMAs subtract A D B^T in place
     double cre[2][2][4], cim[2][2][4];
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int b = 0; b < 2; ++b)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) cre[a][b][v] = cim[a][b][v] = 0.0;
-
     load(0, 0);
     cp_async_commit();
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int row = i0 + wm * 32 + mi * 16 + g + 8 * h;
+            const int col = c0 + wn * 16 + ni * 8 + 2 * t + v;
+            cplx o = cmk(0.0, 0.0);
+            if (row < M && col < N && (!sym || row >= col)) o = ldc(C + (int64_t)row + (int64_t)col * ldC);
+            cre[mi][ni][2 * h + v] = o.re;
+            cim[mi][ni][2 * h + v] = o.im;
+          }
     for (int kc = 0; kc < nk; ++kc) {
       if (kc + 1 < nk) {
         load((kc + 1) & 1, kc + 1);
@@ -148,10 +158,11 @@ __device__ void gemm_update(cplx* __restrict__ C, int ldC, int M, int N, const c
         for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
           for (int ni = 0; ni < 2; ++ni) {
-            dmma_16x8x4(cre[mi][ni], a[mi][0].re, a[mi][1].re, b[ni].re);
-            dmma_16x8x4(cre[mi][ni], -a[mi][0].im, -a[mi][1].im, b[ni].im);
-            dmma_16x8x4(cim[mi][ni], a[mi][0].re, a[mi][1].re, b[ni].im);
-            dmma_16x8x4(cim[mi][ni], a[mi][0].im, a[mi][1].im, b[ni].re);
+            // C -= A B:  Cre += (-Are) Bre + Aim Bim ;  Cim += (-Are) Bim + (-Aim) Bre
+            dmma_16x8x4(cre[mi][ni], -a[mi][0].re, -a[mi][1].re, b[ni].re);
+            dmma_16x8x4(cre[mi][ni], a[mi][0].im, a[mi][1].im, b[ni].im);
+            dmma_16x8x4(cim[mi][ni], -a[mi][0].re, -a[mi][1].re, b[ni].im);
+            dmma_16x8x4(cim[mi][ni], -a[mi][0].im, -a[mi][1].im, b[ni].re);
           }
       }
       __syncthreads();
@@ -164,13 +175,10 @@ __device__ void gemm_update(cplx* __restrict__ C, int ldC, int M, int N, const c
         for (int h = 0; h < 2; ++h)
 #pragma unroll
           for (int v = 0; v < 2; ++v) {
-            int row = i0 + wm * 32 + mi * 16 + g + 8 * h;
-            int col = c0 + wn * 16 + ni * 8 + 2 * t + v;
-            if (row < M && col < N && (!sym || row >= col)) {
-              cplx* p = C + (int64_t)row + (int64_t)col * ldC;
-              cplx o = ldc(p);
-              stc(p, cmk(o.re - cre[mi][ni][2 * h + v], o.im - cim[mi][ni][2 * h + v]));
-            }
+            const int row = i0 + wm * 32 + mi * 16 + g + 8 * h;
+            const int col = c0 + wn * 16 + ni * 8 + 2 * t + v;
+            if (row < M && col < N && (!sym || row >= col))
+              stc(C + (int64_t)row + (int64_t)col * ldC, cmk(cre[mi][ni][2 * h + v], cim[mi][ni][2 * h + v]));
           }
   }
   __syncthreads();
@@ -219,13 +227,30 @@ __global__ void __launch_bounds__(NT, 1) factor_level_kernel(LevelArgs a) {
     const cplx* Uc = a.uchild + (int64_t)k * a.uchild_stride + Cf.uofs;
     const cplx* Rc = a.rchild + ((int64_t)k * a.rchild_stride + Cf.rofs) * nrhs;
     const int32_t* rel = a.relpos + Cf.relpos_beg;
-    for (int idx = tid; idx < bc * bc; idx += NT) {
-      int k1 = idx % bc, k2 = idx / bc;
-      if (k1 < k2) continue;
-      int r1 = rel[k1], r2 = rel[k2];
-      cplx v = ldc(Uc + idx);
-      cplx* dst = (r2 < p) ? P + r1 + (int64_t)r2 * n : U + (r1 - p) + (int64_t)(r2 - p) * b;
-      stc(dst, cadd(ldc(dst), v));
+    // warp per child column, lanes over rows: coalesced reads of U_c, nearly
+    // contiguous destination (relpos is monotone), 4 independent RMWs in flight
+    {
+      const int lane = tid & 31, warp = tid >> 5;
+      for (int k2 = warp; k2 < bc; k2 += NT / 32) {
+        const int r2 = rel[k2];
+        cplx* dcol = (r2 < p) ? P + (int64_t)r2 * n : U + (int64_t)(r2 - p) * b - p;
+        const cplx* scol = Uc + (int64_t)k2 * bc;
+        int k1 = k2 + lane;
+        for (; k1 + 96 < bc; k1 += 128) {
+          const int q0 = rel[k1], q1 = rel[k1 + 32], q2 = rel[k1 + 64], q3 = rel[k1 + 96];
+          const cplx v0 = ldc(scol + k1), v1 = ldc(scol + k1 + 32), v2 = ldc(scol + k1 + 64),
+                     v3 = ldc(scol + k1 + 96);
+          const cplx d0 = ldc(dcol + q0), d1 = ldc(dcol + q1), d2 = ldc(dcol + q2), d3 = ldc(dcol + q3);
+          stc(dcol + q0, cadd(d0, v0));
+          stc(dcol + q1, cadd(d1, v1));
+          stc(dcol + q2, cadd(d2, v2));
+          stc(dcol + q3, cadd(d3, v3));
+        }
+        for (; k1 < bc; k1 += 32) {
+          const int q0 = rel[k1];
+          stc(dcol + q0, cadd(ldc(dcol + q0), ldc(scol + k1)));
+        }
+      }
     }
     for (int idx = tid; idx < bc * nrhs; idx += NT) {
       int k1 = idx % bc, r = idx / bc;
@@ -430,10 +455,6 @@ int upload(Plan& P) {
   STFEM_CUDA_TRY(cudaMemset(P.d_err, 0, sizeof(int)));
   STFEM_CUDA_TRY(cudaFuncSetAttribute(factor_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       FACTOR_SMEM));
-  STFEM_CUDA_TRY(cudaFuncSetAttribute(factor_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      small_smem_bytes(SMALL_N, MAXR)));
-  STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      200 * 1024));
   P.level_nmax.assign(P.levels.size(), 0);
   P.level_pmax.assign(P.levels.size(), 0);
   for (size_t d = 0; d < P.levels.size(); ++d)
@@ -578,8 +599,7 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
       a.rchild_stride = P.rpool_stride[q ^ 1];
       const int nmax = P.level_nmax[d];
       if (nmax <= SMALL_N && !P.force_big) {
-        factor_small_kernel<<<a.nlist * nb, (nmax + 31) / 32 * 32, small_smem_bytes(nmax, nrhs), stream>>>(a, nmax);
-        STFEM_LAUNCH_CHECK("factor_small_kernel");
+        if ((rc = launch_small_factor_any(a, a.nlist * nb, nmax, stream))) return rc;
       } else {
         factor_level_kernel<<<a.nlist * nb, NT, FACTOR_SMEM, stream>>>(a);
         STFEM_LAUNCH_CHECK("factor_level_kernel");
@@ -590,10 +610,9 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
       a.list = P.d_levels + P.level_off[d];
       a.nlist = (int32_t)P.levels[d].size();
       const int nmax = P.level_nmax[d], pmax = P.level_pmax[d];
-      const int bsm = small_bwd_smem_bytes(nmax, pmax, nrhs);
+      const int bsm = small_bwd_smem_bytes(nmax, pmax, small_nr(nrhs));
       if (nmax <= SMALL_N && bsm <= 200 * 1024 && !P.force_big) {
-        backward_small_kernel<<<a.nlist * nb, (nmax + 31) / 32 * 32, bsm, stream>>>(a, nmax, pmax);
-        STFEM_LAUNCH_CHECK("backward_small_kernel");
+        if ((rc = launch_small_backward_any(a, a.nlist * nb, nmax, pmax, stream))) return rc;
       } else {
         backward_level_kernel<<<a.nlist * nb, NT, 0, stream>>>(a);
         STFEM_LAUNCH_CHECK("backward_level_kernel");

@@ -4,57 +4,56 @@
 // Fronts of order n <= SMALL_N live entirely in shared memory (packed lower
 // triangle, column-major) for the whole factorization: one CTA per
 // (front, shift) instance, one thread per front row, CTA width = the level's
-// max n rounded up to a warp.  Right-looking LDL^T in register panels of
-// KB = 8 pivots: each thread keeps its row's panel entries in registers, the
-// scaled panel rows d_j l_cj are published to shared memory, and the trailing
-// update F[i][c] -= sum_j l_ij d_j l_cj runs as 8 complex FMAs per shared
-// load/store (broadcast reads of the panel row c).  The forward substitution
-// of the RHS rides along with the pivot steps (thread i keeps r_i).  Only the
-// initial gather (original entries, children's update blocks) and the final
-// write-out of L/D, U and the forward vectors touch global memory.
+// max n rounded up to a warp.  Right-looking LDL^T in panels of KB = 8 pivots
+// with four barriers per panel:
+//   1. the panel rows publish their forward-RHS values;
+//   2. warp 0 factors the 8x8 diagonal block in place (warp-synchronous) and
+//      forward-solves the panel RHS;
+//   3. every row below the panel runs its TRSM in registers (L11 read as
+//      shared-memory broadcasts), publishes d_j l_cj, updates its RHS;
+//   4. trailing update F[i][c] -= sum_j l_ij d_j l_cj, 8 complex FMAs per
+//      shared load/store, two columns per iteration (independent chains).
+// Only the initial gather (original entries, children's update blocks) and
+// the final write-out of L/D, U and the forward vectors touch global memory.
 #pragma once
 
 constexpr int SMALL_N = 128;   // max front order on the shared-memory path
-constexpr int KB = 8;          // register panel width
+constexpr int KB = 8;          // panel width
 
 __device__ __forceinline__ int pk(int i, int c, int n) { return c * n - ((c * (c - 1)) >> 1) + (i - c); }
 
-__host__ __device__ constexpr int small_smem_bytes(int nmax, int nrhs) {
-  return ((nmax * (nmax + 1)) / 2 + nmax * KB + KB + KB * MAXR + KB * KB + nmax * nrhs) * 16;
+__host__ __device__ constexpr int small_smem_bytes(int nmax, int nr) {
+  return ((nmax * (nmax + 1)) / 2 + nmax * KB + nmax * nr + 2 * KB) * 16;
 }
 
+template <int NR>
 __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int nmax) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* F = reinterpret_cast<cplx*>(smem_raw);
-  cplx* PB = F + (nmax * (nmax + 1)) / 2;   // nmax x KB : d_j * l_cj for the current panel
-  cplx* dsm = PB + nmax * KB;               // KB pivots of the panel
-  cplx* ysm = dsm + KB;                     // KB x MAXR forward values y_j of the panel pivots
-  cplx* plsm = ysm + KB * MAXR;             // KB x KB: l_{kb+cc, kb+jj} inside the panel
-  cplx* Rsm = plsm + KB * KB;               // nmax x nrhs RHS gather
+  cplx* PB = F + (nmax * (nmax + 1)) / 2;   // nmax x KB : d_j l_cj of the current panel
+  cplx* Rsm = PB + nmax * KB;               // nmax x NR  : forward RHS
+  cplx* dsm = Rsm + nmax * NR;              // KB pivots
+  cplx* dinvs = dsm + KB;                   // KB reciprocal pivots
 
-  const int i = threadIdx.x;
+  const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
+  const int nt = blockDim.x, nwarp = nt >> 5;
   const int inst = blockIdx.x;
   const int k = inst % a.nbatch;
   const FrontDev Fr = a.fronts[a.list[inst / a.nbatch]];
   const int n = Fr.n, p = Fr.p, b = n - p;
   const int nrhs = a.nrhs, nx = a.nx;
   const cplx lam = a.lam[k];
-  cplx* Pg = a.factor + (int64_t)k * a.fstride + Fr.fofs;
-  cplx* Ug = a.ucur + (int64_t)k * a.ucur_stride + Fr.uofs;
-  cplx* Rg = a.rcur + ((int64_t)k * a.rcur_stride + Fr.rofs) * nrhs;
-  cplx* Zk = a.Z + (int64_t)k * nx * nrhs;
   const int64_t shift = a.shift0 + k;
-  const int nt = blockDim.x;
   const cplx zero = cmk(0.0, 0.0);
 
   // ---- gather ----
   const int tri = (n * (n + 1)) / 2;
   for (int q = i; q < tri; q += nt) F[q] = zero;
-  for (int q = i; q < n * nrhs; q += nt) {
-    int row = q % n, r = q / n;
-    cplx v = zero;
-    if (row < p) v = a.G[bv_off(a.lay, r, shift, a.perm[Fr.pbeg + row])];
-    Rsm[row * nrhs + r] = v;
+  for (int row = i; row < n; row += nt) {
+    int64_t j = row < p ? a.perm[Fr.pbeg + row] : 0;
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+      Rsm[row * NR + r] = (row < p && r < nrhs) ? a.G[bv_off(a.lay, r, shift, j)] : zero;
   }
   __syncthreads();
   for (int e = i; e < Fr.ent_cnt; e += nt) {
@@ -70,119 +69,181 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
     const cplx* Uc = a.uchild + (int64_t)k * a.uchild_stride + Cf.uofs;
     const cplx* Rc = a.rchild + ((int64_t)k * a.rchild_stride + Cf.rofs) * nrhs;
     const int32_t* rel = a.relpos + Cf.relpos_beg;
-    for (int q = i; q < bc * bc; q += nt) {
-      int k1 = q % bc, k2 = q / bc;
-      if (k1 < k2) continue;
-      int r1 = rel[k1], r2 = rel[k2];
-      int pq = pk(r1, r2, n);
-      F[pq] = cadd(F[pq], ldc(Uc + q));
+    for (int k2 = warp; k2 < bc; k2 += nwarp) {      // warp per child column, lanes over rows
+      const int r2 = rel[k2];
+      const cplx* col = Uc + (int64_t)k2 * bc;
+      for (int k1 = k2 + lane; k1 < bc; k1 += 32) {
+        const int q = pk(rel[k1], r2, n);
+        F[q] = cadd(F[q], ldc(col + k1));
+      }
     }
-    for (int q = i; q < bc * nrhs; q += nt) {
-      int k1 = q % bc, r = q / bc;
-      int row = rel[k1];
-      Rsm[row * nrhs + r] = cadd(Rsm[row * nrhs + r], ldc(Rc + k1 + (int64_t)r * bc));
+    for (int q = i; q < bc; q += nt) {
+      const int row = rel[q];
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        if (r < nrhs) Rsm[row * NR + r] = cadd(Rsm[row * NR + r], ldc(Rc + q + (int64_t)r * bc));
     }
     __syncthreads();
   }
-  cplx rv[MAXR];
+  cplx rv[NR];
 #pragma unroll
-  for (int r = 0; r < MAXR; ++r) rv[r] = (r < nrhs && i < n) ? Rsm[i * nrhs + r] : zero;
+  for (int r = 0; r < NR; ++r) rv[r] = i < n ? Rsm[i * NR + r] : zero;
 
-  // ---- factor p pivots in register panels of KB ----
+  // ---- factor the p pivots, panels of KB ----
   for (int kb = 0; kb < p; kb += KB) {
     const int w = min(KB, p - kb);
-    cplx av[KB];
+    if (i >= kb && i < kb + w) {
 #pragma unroll
-    for (int jj = 0; jj < KB; ++jj)
-      av[jj] = (jj < w && i < n && kb + jj <= i) ? F[pk(i, kb + jj, n)] : zero;
-#pragma unroll
-    for (int jj = 0; jj < KB; ++jj) {
-      if (jj < w) {
-        const int j = kb + jj;
-        if (i == j) {
-          dsm[jj] = av[jj];
-#pragma unroll
-          for (int r = 0; r < MAXR; ++r)
-            if (r < nrhs) ysm[jj * MAXR + r] = rv[r];
-          double m2 = cabs2(av[jj]);
+      for (int r = 0; r < NR; ++r) Rsm[i * NR + r] = rv[r];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      // diagonal block LDL^T, lane = row within the panel
+      const int ri = kb + lane;
+      for (int jj = 0; jj < w; ++jj) {
+        const cplx d = F[pk(kb + jj, kb + jj, n)];
+        const cplx dinv = crecip(d);
+        if (lane == 0) {
+          dsm[jj] = d;
+          dinvs[jj] = dinv;
+          double m2 = cabs2(d);
           if (!(m2 > 1e-300) || !isfinite(m2)) atomicCAS(a.err, 0, (int)shift + 1);
         }
-        __syncthreads();
-        const cplx d = dsm[jj];
-        if (i > j && i < n) {
-          cplx l = cdiv(av[jj], d);
-          av[jj] = l;
-          if (i < kb + w) plsm[jj * KB + (i - kb)] = l;
-#pragma unroll
-          for (int r = 0; r < MAXR; ++r)
-            if (r < nrhs) rv[r] = cfms(rv[r], l, ysm[jj * MAXR + r]);
+        cplx aij = zero;
+        if (lane > jj && lane < w) {
+          aij = F[pk(ri, kb + jj, n)];
+          for (int cc = jj + 1; cc <= lane; ++cc) {
+            const int q = pk(ri, kb + cc, n);
+            F[q] = cfms(F[q], aij, cmul(F[pk(kb + cc, kb + jj, n)], dinv));
+          }
         }
-        __syncthreads();
-        if (i > j && i < n) {
-          const cplx ld = cmul(av[jj], d);
-#pragma unroll
-          for (int cc = jj + 1; cc < KB; ++cc)
-            if (cc < w && kb + cc <= i) av[cc] = cfms(av[cc], ld, plsm[jj * KB + cc]);
+        __syncwarp();
+        if (lane > jj && lane < w) F[pk(ri, kb + jj, n)] = cmul(aij, dinv);
+        __syncwarp();
+      }
+      // forward-solve the panel RHS: y = L11^{-1} r  (lane = rhs)
+      if (lane < nrhs && lane < NR) {
+        for (int jj = 0; jj < w; ++jj) {
+          cplx y = Rsm[(kb + jj) * NR + lane];
+          for (int cc = 0; cc < jj; ++cc) y = cfms(y, F[pk(kb + jj, kb + cc, n)], Rsm[(kb + cc) * NR + lane]);
+          Rsm[(kb + jj) * NR + lane] = y;
         }
       }
     }
-    // write the panel back; publish d_j l_cj for the trailing update
-    if (i < n) {
+    __syncthreads();
+    cplx av[KB];
+#pragma unroll
+    for (int jj = 0; jj < KB; ++jj) av[jj] = zero;
+    if (i >= kb && i < kb + w) {
+#pragma unroll
+      for (int r = 0; r < NR; ++r) rv[r] = Rsm[i * NR + r];
+    } else if (i >= kb + w && i < n) {
 #pragma unroll
       for (int jj = 0; jj < KB; ++jj)
-        if (jj < w && kb + jj <= i) {
-          F[pk(i, kb + jj, n)] = av[jj];
-          if (i >= kb + w) PB[i * KB + jj] = cmul(dsm[jj], av[jj]);
+        if (jj < w) av[jj] = F[pk(i, kb + jj, n)];
+      // row TRSM: y_jj = a_jj - sum_{cc<jj} y_cc L11[jj][cc];  l = y / d
+#pragma unroll
+      for (int jj = 1; jj < KB; ++jj) {
+        if (jj < w) {
+#pragma unroll
+          for (int cc = 0; cc < jj; ++cc) av[jj] = cfms(av[jj], av[cc], F[pk(kb + jj, kb + cc, n)]);
         }
+      }
+#pragma unroll
+      for (int jj = 0; jj < KB; ++jj) {
+        if (jj < w) {
+          av[jj] = cmul(av[jj], dinvs[jj]);
+          F[pk(i, kb + jj, n)] = av[jj];
+          PB[i * KB + jj] = cmul(dsm[jj], av[jj]);
+        } else {
+          PB[i * KB + jj] = zero;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        if (r < nrhs) {
+#pragma unroll
+          for (int jj = 0; jj < KB; ++jj)
+            if (jj < w) rv[r] = cfms(rv[r], av[jj], Rsm[(kb + jj) * NR + r]);
+        }
+      }
     }
     __syncthreads();
     if (i >= kb + w && i < n) {
-      for (int c = kb + w; c <= i; ++c) {
-        const int q = pk(i, c, n);
-        cplx acc = F[q];
+      int c = kb + w;
+      int q = pk(i, c, n);
+      const cplx* pb = PB + c * KB;
+      for (; c + 1 <= i; c += 2) {
+        const int q1 = q + (n - c - 1);
+        cplx x0 = F[q], x1 = F[q1];
 #pragma unroll
-        for (int jj = 0; jj < KB; ++jj)
-          if (jj < w) acc = cfms(acc, av[jj], PB[c * KB + jj]);
-        F[q] = acc;
+        for (int jj = 0; jj < KB; ++jj) {
+          x0 = cfms(x0, av[jj], pb[jj]);
+          x1 = cfms(x1, av[jj], pb[KB + jj]);
+        }
+        F[q] = x0;
+        F[q1] = x1;
+        q = q1 + (n - c - 2);
+        pb += 2 * KB;
+      }
+      if (c <= i) {
+        cplx x0 = F[q];
+#pragma unroll
+        for (int jj = 0; jj < KB; ++jj) x0 = cfms(x0, av[jj], pb[jj]);
+        F[q] = x0;
       }
     }
     __syncthreads();
   }
 
   // ---- write out: L/D (n x p), U (b x b), z = D^{-1} y, forward RHS update ----
+  cplx* Pg = a.factor + (int64_t)k * a.fstride + Fr.fofs;
+  cplx* Ug = a.ucur + (int64_t)k * a.ucur_stride + Fr.uofs;
+  cplx* Rg = a.rcur + ((int64_t)k * a.rcur_stride + Fr.rofs) * nrhs;
+  cplx* Zk = a.Z + (int64_t)k * nx * nrhs;
   if (i < n) {
     const int cmax = min(i, p - 1);
-    for (int c = 0; c <= cmax; ++c) stc(Pg + i + (int64_t)c * n, F[pk(i, c, n)]);
-    if (i >= p)
-      for (int c = p; c <= i; ++c) stc(Ug + (i - p) + (int64_t)(c - p) * b, F[pk(i, c, n)]);
-    if (i < p) {
-      cplx d = F[pk(i, i, n)];
+    int q = i;  // pk(i, 0, n)
+    for (int c = 0; c <= cmax; ++c) {
+      stc(Pg + i + (int64_t)c * n, F[q]);
+      q += n - c - 1;
+    }
+    if (i >= p) {
+      q = pk(i, p, n);
+      for (int c = p; c <= i; ++c) {
+        stc(Ug + (i - p) + (int64_t)(c - p) * b, F[q]);
+        q += n - c - 1;
+      }
 #pragma unroll
-      for (int r = 0; r < MAXR; ++r)
-        if (r < nrhs) stc(Zk + Fr.pbeg + i + (int64_t)r * nx, cdiv(rv[r], d));
-    } else {
-#pragma unroll
-      for (int r = 0; r < MAXR; ++r)
+      for (int r = 0; r < NR; ++r)
         if (r < nrhs) stc(Rg + (i - p) + (int64_t)r * b, rv[r]);
+    } else {
+      const cplx dinv = crecip(F[pk(i, i, n)]);
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        if (r < nrhs) stc(Zk + Fr.pbeg + i + (int64_t)r * nx, cmul(rv[r], dinv));
     }
   }
 }
 
-__host__ __device__ constexpr int small_bwd_smem_bytes(int nmax, int pmax, int nrhs) {
-  return ((nmax | 1) * pmax + nmax * nrhs + nrhs) * 16;
+__host__ __device__ constexpr int small_bwd_smem_bytes(int nmax, int pmax, int nr) {
+  return ((nmax | 1) * pmax + nmax * nr + KB * nr) * 16;
 }
 
-// Backward substitution for fronts with n * p small: the n x p factor block is
-// staged in shared memory (odd leading dimension: conflict-free column reads),
-// one thread per pivot column.
+// Backward substitution for fronts with small n * p: the factor block is
+// staged in shared memory (odd leading dimension: conflict-free column reads);
+// one thread per pivot column applies the boundary part, then the transposed
+// unit triangle is solved in blocks of KB (warp 0 solves the block, all
+// threads apply it): three barriers per block.
+template <int NR>
 __global__ void __launch_bounds__(SMALL_N) backward_small_kernel(LevelArgs a, int nmax, int pmax) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int ldl = nmax | 1;
   cplx* Ls = reinterpret_cast<cplx*>(smem_raw);   // Ls[c * ldl + i]
-  cplx* xs = Ls + ldl * pmax;                      // nmax x nrhs : x of boundary rows / solved pivots
-  cplx* xj = xs + nmax * a.nrhs;                   // nrhs: value published at each step
+  cplx* xs = Ls + ldl * pmax;                      // nmax x NR : x of boundary rows
+  cplx* Tsm = xs + nmax * NR;                      // KB x NR : current block
 
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
   const int inst = blockIdx.x;
   const int k = inst % a.nbatch;
   const FrontDev Fr = a.fronts[a.list[inst / a.nbatch]];
@@ -193,47 +254,109 @@ __global__ void __launch_bounds__(SMALL_N) backward_small_kernel(LevelArgs a, in
   const int32_t* bidx = a.bidx + Fr.bidx_beg;
   const int64_t shift = a.shift0 + k;
 
-  for (int q = tid; q < n * p; q += nt) {
-    int i = q % n, c = q / n;
-    Ls[c * ldl + i] = ldc(Pg + q);
-  }
-  for (int q = tid; q < (n - p) * nrhs; q += nt) {
-    int i = q % (n - p), r = q / (n - p);
-    xs[(p + i) * nrhs + r] = ldc(Zk + bidx[i] + (int64_t)r * nx);
+  for (int c = 0; c < p; ++c)
+    for (int i = c + tid; i < n; i += nt) Ls[c * ldl + i] = ldc(Pg + i + (int64_t)c * n);
+  for (int i = p + tid; i < n; i += nt) {
+    const int64_t g = bidx[i - p];
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+      if (r < nrhs) xs[i * NR + r] = ldc(Zk + g + (int64_t)r * nx);
   }
   __syncthreads();
   const int j = tid;
-  cplx t[MAXR];
+  cplx t[NR];
 #pragma unroll
-  for (int r = 0; r < MAXR; ++r) t[r] = cmk(0.0, 0.0);
+  for (int r = 0; r < NR; ++r) t[r] = cmk(0.0, 0.0);
   if (j < p) {
 #pragma unroll
-    for (int r = 0; r < MAXR; ++r)
+    for (int r = 0; r < NR; ++r)
       if (r < nrhs) t[r] = ldc(Zk + Fr.pbeg + j + (int64_t)r * nx);
     for (int i = p; i < n; ++i) {
-      cplx l = Ls[j * ldl + i];
+      const cplx l = Ls[j * ldl + i];
 #pragma unroll
-      for (int r = 0; r < MAXR; ++r)
-        if (r < nrhs) t[r] = cfms(t[r], l, xs[i * nrhs + r]);
+      for (int r = 0; r < NR; ++r)
+        if (r < nrhs) t[r] = cfms(t[r], l, xs[i * NR + r]);
     }
   }
-  for (int jj = p - 1; jj >= 0; --jj) {
-    if (j == jj) {
+  for (int kb = ((p - 1) / KB) * KB; kb >= 0; kb -= KB) {
+    const int w = min(KB, p - kb);
+    if (j >= kb && j < kb + w) {
 #pragma unroll
-      for (int r = 0; r < MAXR; ++r)
-        if (r < nrhs) {
-          xj[r] = t[r];
-          stc(Zk + Fr.pbeg + j + (int64_t)r * nx, t[r]);
-          a.W[bv_off(a.lay, r, shift, a.perm[Fr.pbeg + j])] = t[r];
+      for (int r = 0; r < NR; ++r) Tsm[(j - kb) * NR + r] = t[r];
+    }
+    __syncthreads();
+    if (tid < 32 && lane < nrhs && lane < NR) {
+      for (int jj = w - 1; jj >= 0; --jj) {
+        cplx x = Tsm[jj * NR + lane];
+        for (int cc = jj + 1; cc < w; ++cc) x = cfms(x, Ls[(kb + jj) * ldl + kb + cc], Tsm[cc * NR + lane]);
+        Tsm[jj * NR + lane] = x;
+        const int col = Fr.pbeg + kb + jj;
+        stc(Zk + col + (int64_t)lane * nx, x);
+        a.W[bv_off(a.lay, lane, shift, a.perm[col])] = x;
+      }
+    }
+    __syncthreads();
+    if (j < kb) {
+#pragma unroll
+      for (int jj = 0; jj < KB; ++jj) {
+        if (jj < w) {
+          const cplx l = Ls[j * ldl + kb + jj];
+#pragma unroll
+          for (int r = 0; r < NR; ++r)
+            if (r < nrhs) t[r] = cfms(t[r], l, Tsm[jj * NR + r]);
         }
+      }
     }
     __syncthreads();
-    if (j < jj) {
-      cplx l = Ls[j * ldl + jj];
-#pragma unroll
-      for (int r = 0; r < MAXR; ++r)
-        if (r < nrhs) t[r] = cfms(t[r], l, xj[r]);
-    }
-    __syncthreads();
+  }
+}
+
+template <int NR>
+int launch_small_factor(const LevelArgs& a, int grid, int nmax, cudaStream_t s) {
+  const int smem = small_smem_bytes(nmax, NR);
+  static bool attr = false;
+  if (!attr) {
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(factor_small_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        small_smem_bytes(SMALL_N, NR)));
+    attr = true;
+  }
+  factor_small_kernel<NR><<<grid, (nmax + 31) / 32 * 32, smem, s>>>(a, nmax);
+  STFEM_LAUNCH_CHECK("factor_small_kernel");
+  return STFEM_OK;
+}
+
+template <int NR>
+int launch_small_backward(const LevelArgs& a, int grid, int nmax, int pmax, cudaStream_t s) {
+  const int smem = small_bwd_smem_bytes(nmax, pmax, NR);
+  static bool attr = false;
+  if (!attr) {
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_small_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        200 * 1024));
+    attr = true;
+  }
+  backward_small_kernel<NR><<<grid, (nmax + 31) / 32 * 32, smem, s>>>(a, nmax, pmax);
+  STFEM_LAUNCH_CHECK("backward_small_kernel");
+  return STFEM_OK;
+}
+
+inline int small_nr(int nrhs) { return nrhs <= 1 ? 1 : nrhs <= 2 ? 2 : nrhs <= 4 ? 4 : nrhs <= 8 ? 8 : 16; }
+
+int launch_small_factor_any(const LevelArgs& a, int grid, int nmax, cudaStream_t s) {
+  switch (small_nr(a.nrhs)) {
+    case 1: return launch_small_factor<1>(a, grid, nmax, s);
+    case 2: return launch_small_factor<2>(a, grid, nmax, s);
+    case 4: return launch_small_factor<4>(a, grid, nmax, s);
+    case 8: return launch_small_factor<8>(a, grid, nmax, s);
+    default: return launch_small_factor<16>(a, grid, nmax, s);
+  }
+}
+
+int launch_small_backward_any(const LevelArgs& a, int grid, int nmax, int pmax, cudaStream_t s) {
+  switch (small_nr(a.nrhs)) {
+    case 1: return launch_small_backward<1>(a, grid, nmax, pmax, s);
+    case 2: return launch_small_backward<2>(a, grid, nmax, pmax, s);
+    case 4: return launch_small_backward<4>(a, grid, nmax, pmax, s);
+    case 8: return launch_small_backward<8>(a, grid, nmax, pmax, s);
+    default: return launch_small_backward<16>(a, grid, nmax, pmax, s);
   }
 }
