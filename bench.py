@@ -289,8 +289,7 @@ def run_ours(args):
             "algorithmic": f"{fdm.plan.stats['flops_factor']:.4e} real flops per shift (sum_j 4 c_j^2) x {prob.nt} shifts"}
     roof_tr = {"bound": "tensor", "kernel": "time_transform_kernel (K3)", "achieved": flops_tr / t_tr / 1e12,
                "peak": peak, "unit": "TFLOP/s", "frac": flops_tr / t_tr / 1e12 / peak}
-    nb = -(-prob.nt // max(1, getattr(fdm.plan, "last_batch", prob.nt)))
-    launches = 2 + 2 * (fdm.plan.stats["depth"] + 1) * nb
+    launches = 2 + fdm.plan.last_launches()   # two K3 transforms + the multifrontal level launches
 
     cpu = None
     if not args.no_cpu_baseline:

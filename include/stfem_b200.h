@@ -119,6 +119,8 @@ int stfem_factor_solve(stfem_plan* plan, const double* Mvals, const double* Aval
                        void* stream);
 /* batch size in shifts (0 = auto from free memory); returns bytes per shift */
 int stfem_plan_set_batch(stfem_plan* plan, int32_t batch, int64_t* bytes_per_shift);
+/* kernel launches of the last stfem_factor_solve call (for launch accounting) */
+int stfem_plan_last_launches(const stfem_plan* plan, int64_t* launches);
 
 /* ---------------------------------------------------------------------------
  * K1/K2/K7  assembly and the matrix-free residual

@@ -55,6 +55,11 @@ __host__ __device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
   }
 }
 __host__ __device__ __forceinline__ cplx crecip(cplx b) { return cdiv(cplx{1.0, 0.0}, b); }
+// 1/b with one division: conj(b)/|b|^2 (pivots here are far from over/underflow)
+__host__ __device__ __forceinline__ cplx crecip_fast(cplx b) {
+  double s = 1.0 / fma(b.re, b.re, b.im * b.im);
+  return cplx{b.re * s, -b.im * s};
+}
 __host__ __device__ __forceinline__ double cabs2(cplx a) { return a.re * a.re + a.im * a.im; }
 
 #ifdef __CUDACC__

@@ -229,26 +229,34 @@ __global__ void __launch_bounds__(NT, 1) factor_level_kernel(LevelArgs a) {
     const int32_t* rel = a.relpos + Cf.relpos_beg;
     // warp per child column, lanes over rows: coalesced reads of U_c, nearly
     // contiguous destination (relpos is monotone), 4 independent RMWs in flight
+    // each warp owns 8 child columns at a time, lanes run over child rows:
+    // per lane one relpos load + 8 U_c loads + 8 destination loads in flight
     {
+      constexpr int CU = 8, NW = NT / 32;
       const int lane = tid & 31, warp = tid >> 5;
-      for (int k2 = warp; k2 < bc; k2 += NT / 32) {
-        const int r2 = rel[k2];
-        cplx* dcol = (r2 < p) ? P + (int64_t)r2 * n : U + (int64_t)(r2 - p) * b - p;
-        const cplx* scol = Uc + (int64_t)k2 * bc;
-        int k1 = k2 + lane;
-        for (; k1 + 96 < bc; k1 += 128) {
-          const int q0 = rel[k1], q1 = rel[k1 + 32], q2 = rel[k1 + 64], q3 = rel[k1 + 96];
-          const cplx v0 = ldc(scol + k1), v1 = ldc(scol + k1 + 32), v2 = ldc(scol + k1 + 64),
-                     v3 = ldc(scol + k1 + 96);
-          const cplx d0 = ldc(dcol + q0), d1 = ldc(dcol + q1), d2 = ldc(dcol + q2), d3 = ldc(dcol + q3);
-          stc(dcol + q0, cadd(d0, v0));
-          stc(dcol + q1, cadd(d1, v1));
-          stc(dcol + q2, cadd(d2, v2));
-          stc(dcol + q3, cadd(d3, v3));
+      for (int k2b = warp; k2b < bc; k2b += CU * NW) {
+        cplx* dcol[CU];
+#pragma unroll
+        for (int u = 0; u < CU; ++u) {
+          const int k2 = k2b + u * NW;
+          const int r2 = k2 < bc ? rel[k2] : 0;
+          dcol[u] = (r2 < p) ? P + (int64_t)r2 * n : U + (int64_t)(r2 - p) * b - p;
         }
-        for (; k1 < bc; k1 += 32) {
-          const int q0 = rel[k1];
-          stc(dcol + q0, cadd(ldc(dcol + q0), ldc(scol + k1)));
+        for (int k1 = k2b + lane; k1 < bc; k1 += 32) {
+          const int r1 = rel[k1];
+          cplx v[CU], d[CU];
+#pragma unroll
+          for (int u = 0; u < CU; ++u) {
+            const int k2 = k2b + u * NW;
+            const bool ok = k2 < bc && k1 >= k2;
+            v[u] = ok ? ldc(Uc + (int64_t)k2 * bc + k1) : cmk(0.0, 0.0);
+            d[u] = ok ? ldc(dcol[u] + r1) : cmk(0.0, 0.0);
+          }
+#pragma unroll
+          for (int u = 0; u < CU; ++u) {
+            const int k2 = k2b + u * NW;
+            if (k2 < bc && k1 >= k2) stc(dcol[u] + r1, cadd(d[u], v[u]));
+          }
         }
       }
     }
@@ -621,6 +629,7 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
     }
   }
   P.last_batch = batch;
+  P.last_launches = (int64_t)((nshift + batch - 1) / batch) * 2 * (P.depth + 1);
   if (level_timing) {
     cudaStreamSynchronize(stream);
     int L = P.depth + 1;
@@ -718,6 +727,12 @@ extern "C" int stfem_plan_front_rows(const stfem_plan* plan, int64_t* offsets, i
     o += F.n;
   }
   offsets[P.fronts.size()] = o;
+  return STFEM_OK;
+}
+
+extern "C" int stfem_plan_last_launches(const stfem_plan* plan, int64_t* launches) {
+  if (!plan || !launches) return stfem::fail(STFEM_ERR_ARG, "plan_last_launches: null pointer");
+  *launches = reinterpret_cast<const Plan*>(plan)->last_launches;
   return STFEM_OK;
 }
 

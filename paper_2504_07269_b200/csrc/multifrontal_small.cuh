@@ -22,8 +22,43 @@ constexpr int KB = 8;          // panel width
 
 __device__ __forceinline__ int pk(int i, int c, int n) { return c * n - ((c * (c - 1)) >> 1) + (i - c); }
 
+// per-warp scratch (complex): L11 (KB x KB), y (KB x nr), d, 1/d
+__host__ __device__ constexpr int scr_size(int nr) { return KB * KB + KB * nr + 2 * KB; }
+
 __host__ __device__ constexpr int small_smem_bytes(int nmax, int nr) {
-  return ((nmax * (nmax + 1)) / 2 + nmax * KB + nmax * nr + 2 * KB) * 16;
+  return ((nmax * (nmax + 1)) / 2 + nmax * KB + nmax * nr + ((nmax + 31) / 32) * scr_size(nr)) * 16;
+}
+
+__device__ __forceinline__ cplx shfl_c(cplx v, int src) {
+  return cmk(__shfl_sync(0xffffffffu, v.re, src), __shfl_sync(0xffffffffu, v.im, src));
+}
+
+// trailing update of row i: F[i][c] -= sum_jj av[jj] * PB[c][jj] for c in [c0, i]
+__device__ __forceinline__ void trailing_row(cplx* __restrict__ F, const cplx* __restrict__ PB, const cplx (&av)[KB],
+                                             int i, int c0, int n) {
+  int c = c0;
+  int q = pk(i, c, n);
+  const cplx* __restrict__ pb = PB + c * KB;
+#pragma unroll 2
+  for (; c + 1 <= i; c += 2) {
+    const int q1 = q + (n - c - 1);
+    cplx x0 = F[q], x1 = F[q1];
+#pragma unroll
+    for (int jj = 0; jj < KB; ++jj) {
+      x0 = cfms(x0, av[jj], pb[jj]);
+      x1 = cfms(x1, av[jj], pb[KB + jj]);
+    }
+    F[q] = x0;
+    F[q1] = x1;
+    q = q1 + (n - c - 2);
+    pb += 2 * KB;
+  }
+  if (c <= i) {
+    cplx x0 = F[q];
+#pragma unroll
+    for (int jj = 0; jj < KB; ++jj) x0 = cfms(x0, av[jj], pb[jj]);
+    F[q] = x0;
+  }
 }
 
 template <int NR>
@@ -32,8 +67,7 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
   cplx* F = reinterpret_cast<cplx*>(smem_raw);
   cplx* PB = F + (nmax * (nmax + 1)) / 2;   // nmax x KB : d_j l_cj of the current panel
   cplx* Rsm = PB + nmax * KB;               // nmax x NR  : forward RHS
-  cplx* dsm = Rsm + nmax * NR;              // KB pivots
-  cplx* dinvs = dsm + KB;                   // KB reciprocal pivots
+  cplx* scratch = Rsm + nmax * NR;          // per warp: L11 (KB x KB), y (KB x NR), d, 1/d
 
   const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
   const int nt = blockDim.x, nwarp = nt >> 5;
@@ -45,6 +79,10 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
   const cplx lam = a.lam[k];
   const int64_t shift = a.shift0 + k;
   const cplx zero = cmk(0.0, 0.0);
+  cplx* W8 = scratch + warp * scr_size(NR);
+  cplx* Y8 = W8 + KB * KB;
+  cplx* Dv = Y8 + KB * NR;
+  cplx* Dinv = Dv + KB;
 
   // ---- gather ----
   const int tri = (n * (n + 1)) / 2;
@@ -69,12 +107,32 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
     const cplx* Uc = a.uchild + (int64_t)k * a.uchild_stride + Cf.uofs;
     const cplx* Rc = a.rchild + ((int64_t)k * a.rchild_stride + Cf.rofs) * nrhs;
     const int32_t* rel = a.relpos + Cf.relpos_beg;
-    for (int k2 = warp; k2 < bc; k2 += nwarp) {      // warp per child column, lanes over rows
-      const int r2 = rel[k2];
-      const cplx* col = Uc + (int64_t)k2 * bc;
-      for (int k1 = k2 + lane; k1 < bc; k1 += 32) {
-        const int q = pk(rel[k1], r2, n);
-        F[q] = cadd(F[q], ldc(col + k1));
+    // each warp owns 8 child columns at a time (k2 = k2b + u*nwarp), lanes run
+    // over child rows: one relpos load + 8 independent U_c loads in flight per lane
+    constexpr int CU = 8;
+    for (int k2b = warp; k2b < bc; k2b += CU * nwarp) {
+      int r2[CU];
+#pragma unroll
+      for (int u = 0; u < CU; ++u) {
+        const int k2 = k2b + u * nwarp;
+        r2[u] = k2 < bc ? rel[k2] : 0;
+      }
+      for (int k1 = k2b + lane; k1 < bc; k1 += 32) {
+        const int r1 = rel[k1];
+        cplx v[CU];
+#pragma unroll
+        for (int u = 0; u < CU; ++u) {
+          const int k2 = k2b + u * nwarp;
+          v[u] = (k2 < bc && k1 >= k2) ? ldc(Uc + (int64_t)k2 * bc + k1) : zero;
+        }
+#pragma unroll
+        for (int u = 0; u < CU; ++u) {
+          const int k2 = k2b + u * nwarp;
+          if (k2 < bc && k1 >= k2) {
+            const int q = pk(r1, r2[u], n);
+            F[q] = cadd(F[q], v[u]);
+          }
+        }
       }
     }
     for (int q = i; q < bc; q += nt) {
@@ -89,72 +147,83 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
 #pragma unroll
   for (int r = 0; r < NR; ++r) rv[r] = i < n ? Rsm[i * NR + r] : zero;
 
-  // ---- factor the p pivots, panels of KB ----
+  // ---- factor the p pivots, panels of KB, two barriers per panel ----
   for (int kb = 0; kb < p; kb += KB) {
     const int w = min(KB, p - kb);
-    if (i >= kb && i < kb + w) {
+    // (A) every warp factors the w x w diagonal block redundantly in registers
+    //     (lane = panel row) and forward-solves the panel RHS; warp-private results
+    {
+      cplx ar[KB], yr[NR];
 #pragma unroll
-      for (int r = 0; r < NR; ++r) Rsm[i * NR + r] = rv[r];
-    }
-    __syncthreads();
-    if (warp == 0) {
-      // diagonal block LDL^T, lane = row within the panel
-      const int ri = kb + lane;
-      for (int jj = 0; jj < w; ++jj) {
-        const cplx d = F[pk(kb + jj, kb + jj, n)];
-        const cplx dinv = crecip(d);
-        if (lane == 0) {
-          dsm[jj] = d;
-          dinvs[jj] = dinv;
-          double m2 = cabs2(d);
-          if (!(m2 > 1e-300) || !isfinite(m2)) atomicCAS(a.err, 0, (int)shift + 1);
-        }
-        cplx aij = zero;
-        if (lane > jj && lane < w) {
-          aij = F[pk(ri, kb + jj, n)];
-          for (int cc = jj + 1; cc <= lane; ++cc) {
-            const int q = pk(ri, kb + cc, n);
-            F[q] = cfms(F[q], aij, cmul(F[pk(kb + cc, kb + jj, n)], dinv));
+      for (int cc = 0; cc < KB; ++cc) ar[cc] = (lane < w && cc <= lane) ? F[pk(kb + lane, kb + cc, n)] : zero;
+#pragma unroll
+      for (int r = 0; r < NR; ++r) yr[r] = lane < w ? Rsm[(kb + lane) * NR + r] : zero;
+#pragma unroll
+      for (int jj = 0; jj < KB; ++jj) {
+        if (jj < w) {
+          const cplx d = shfl_c(ar[jj], jj);
+          const cplx dinv = crecip_fast(d);
+          const cplx l = lane > jj ? cmul(ar[jj], dinv) : zero;
+#pragma unroll
+          for (int r = 0; r < NR; ++r) {
+            const cplx ys = shfl_c(yr[r], jj);
+            if (lane > jj) yr[r] = cfms(yr[r], l, ys);
+          }
+          const cplx ld = cmul(l, d);
+#pragma unroll
+          for (int cc = jj + 1; cc < KB; ++cc) {
+            if (cc < w) {
+              const cplx lc = shfl_c(l, cc);
+              if (lane >= cc) ar[cc] = cfms(ar[cc], ld, lc);
+            }
+          }
+          if (lane > jj) ar[jj] = l;
+          if (lane == 0) {
+            Dv[jj] = d;
+            Dinv[jj] = dinv;
+            if (warp == 0) {
+              double m2 = cabs2(d);
+              if (!(m2 > 1e-300) || !isfinite(m2)) atomicCAS(a.err, 0, (int)shift + 1);
+            }
           }
         }
-        __syncwarp();
-        if (lane > jj && lane < w) F[pk(ri, kb + jj, n)] = cmul(aij, dinv);
-        __syncwarp();
       }
-      // forward-solve the panel RHS: y = L11^{-1} r  (lane = rhs)
-      if (lane < nrhs && lane < NR) {
-        for (int jj = 0; jj < w; ++jj) {
-          cplx y = Rsm[(kb + jj) * NR + lane];
-          for (int cc = 0; cc < jj; ++cc) y = cfms(y, F[pk(kb + jj, kb + cc, n)], Rsm[(kb + cc) * NR + lane]);
-          Rsm[(kb + jj) * NR + lane] = y;
-        }
+      if (lane < w) {
+#pragma unroll
+        for (int cc = 0; cc < KB; ++cc) W8[lane * KB + cc] = ar[cc];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) Y8[lane * NR + r] = yr[r];
       }
+      __syncwarp();
     }
-    __syncthreads();
+    // (B) rows: panel rows take their factored row; rows below run the TRSM
     cplx av[KB];
 #pragma unroll
     for (int jj = 0; jj < KB; ++jj) av[jj] = zero;
     if (i >= kb && i < kb + w) {
+      const int row = i - kb;
 #pragma unroll
-      for (int r = 0; r < NR; ++r) rv[r] = Rsm[i * NR + r];
+      for (int cc = 0; cc < KB; ++cc)
+        if (cc <= row) F[pk(i, kb + cc, n)] = W8[row * KB + cc];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) rv[r] = Y8[row * NR + r];
     } else if (i >= kb + w && i < n) {
 #pragma unroll
       for (int jj = 0; jj < KB; ++jj)
         if (jj < w) av[jj] = F[pk(i, kb + jj, n)];
-      // row TRSM: y_jj = a_jj - sum_{cc<jj} y_cc L11[jj][cc];  l = y / d
 #pragma unroll
       for (int jj = 1; jj < KB; ++jj) {
         if (jj < w) {
 #pragma unroll
-          for (int cc = 0; cc < jj; ++cc) av[jj] = cfms(av[jj], av[cc], F[pk(kb + jj, kb + cc, n)]);
+          for (int cc = 0; cc < jj; ++cc) av[jj] = cfms(av[jj], av[cc], W8[jj * KB + cc]);
         }
       }
 #pragma unroll
       for (int jj = 0; jj < KB; ++jj) {
         if (jj < w) {
-          av[jj] = cmul(av[jj], dinvs[jj]);
+          av[jj] = cmul(av[jj], Dinv[jj]);
           F[pk(i, kb + jj, n)] = av[jj];
-          PB[i * KB + jj] = cmul(dsm[jj], av[jj]);
+          PB[i * KB + jj] = cmul(Dv[jj], av[jj]);
         } else {
           PB[i * KB + jj] = zero;
         }
@@ -164,35 +233,16 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
         if (r < nrhs) {
 #pragma unroll
           for (int jj = 0; jj < KB; ++jj)
-            if (jj < w) rv[r] = cfms(rv[r], av[jj], Rsm[(kb + jj) * NR + r]);
+            if (jj < w) rv[r] = cfms(rv[r], av[jj], Y8[jj * NR + r]);
         }
+      }
+      if (i < kb + w + KB) {   // the next panel's rows publish their forward values
+#pragma unroll
+        for (int r = 0; r < NR; ++r) Rsm[i * NR + r] = rv[r];
       }
     }
     __syncthreads();
-    if (i >= kb + w && i < n) {
-      int c = kb + w;
-      int q = pk(i, c, n);
-      const cplx* pb = PB + c * KB;
-      for (; c + 1 <= i; c += 2) {
-        const int q1 = q + (n - c - 1);
-        cplx x0 = F[q], x1 = F[q1];
-#pragma unroll
-        for (int jj = 0; jj < KB; ++jj) {
-          x0 = cfms(x0, av[jj], pb[jj]);
-          x1 = cfms(x1, av[jj], pb[KB + jj]);
-        }
-        F[q] = x0;
-        F[q1] = x1;
-        q = q1 + (n - c - 2);
-        pb += 2 * KB;
-      }
-      if (c <= i) {
-        cplx x0 = F[q];
-#pragma unroll
-        for (int jj = 0; jj < KB; ++jj) x0 = cfms(x0, av[jj], pb[jj]);
-        F[q] = x0;
-      }
-    }
+    if (i >= kb + w && i < n) trailing_row(F, PB, av, i, kb + w, n);
     __syncthreads();
   }
 
@@ -218,7 +268,7 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
       for (int r = 0; r < NR; ++r)
         if (r < nrhs) stc(Rg + (i - p) + (int64_t)r * b, rv[r]);
     } else {
-      const cplx dinv = crecip(F[pk(i, i, n)]);
+      const cplx dinv = crecip_fast(F[pk(i, i, n)]);
 #pragma unroll
       for (int r = 0; r < NR; ++r)
         if (r < nrhs) stc(Zk + Fr.pbeg + i + (int64_t)r * nx, cmul(rv[r], dinv));
@@ -254,8 +304,19 @@ __global__ void __launch_bounds__(SMALL_N) backward_small_kernel(LevelArgs a, in
   const int32_t* bidx = a.bidx + Fr.bidx_beg;
   const int64_t shift = a.shift0 + k;
 
-  for (int c = 0; c < p; ++c)
-    for (int i = c + tid; i < n; i += nt) Ls[c * ldl + i] = ldc(Pg + i + (int64_t)c * n);
+  // stage the n x p factor block (full columns; 4 loads in flight per thread)
+  {
+    const int tot = n * p;
+    int q = tid;
+    for (; q + 3 * nt < tot; q += 4 * nt) {
+      const cplx v0 = ldc(Pg + q), v1 = ldc(Pg + q + nt), v2 = ldc(Pg + q + 2 * nt), v3 = ldc(Pg + q + 3 * nt);
+      Ls[(q / n) * ldl + q % n] = v0;
+      Ls[((q + nt) / n) * ldl + (q + nt) % n] = v1;
+      Ls[((q + 2 * nt) / n) * ldl + (q + 2 * nt) % n] = v2;
+      Ls[((q + 3 * nt) / n) * ldl + (q + 3 * nt) % n] = v3;
+    }
+    for (; q < tot; q += nt) Ls[(q / n) * ldl + q % n] = ldc(Pg + q);
+  }
   for (int i = p + tid; i < n; i += nt) {
     const int64_t g = bidx[i - p];
 #pragma unroll
@@ -318,6 +379,9 @@ int launch_small_factor(const LevelArgs& a, int grid, int nmax, cudaStream_t s) 
   if (!attr) {
     STFEM_CUDA_TRY(cudaFuncSetAttribute(factor_small_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         small_smem_bytes(SMALL_N, NR)));
+    // occupancy here is shared-memory bound: ask for the full 228 KB carveout
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(factor_small_kernel<NR>,
+                                        cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     attr = true;
   }
   factor_small_kernel<NR><<<grid, (nmax + 31) / 32 * 32, smem, s>>>(a, nmax);
@@ -332,6 +396,8 @@ int launch_small_backward(const LevelArgs& a, int grid, int nmax, int pmax, cuda
   if (!attr) {
     STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_small_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         200 * 1024));
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_small_kernel<NR>,
+                                        cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     attr = true;
   }
   backward_small_kernel<NR><<<grid, (nmax + 31) / 32 * 32, smem, s>>>(a, nmax, pmax);

@@ -59,6 +59,7 @@ struct Plan {
   int32_t ws_batch = 0;    // allocated for
   int32_t ws_nrhs = 0;
   int32_t last_batch = 0;  // batch size used by the last factor_solve
+  int64_t last_launches = 0;  // kernel launches issued by the last factor_solve
   cplx* d_factor = nullptr;
   cplx* d_upool[2] = {nullptr, nullptr};
   cplx* d_rpool[2] = {nullptr, nullptr};

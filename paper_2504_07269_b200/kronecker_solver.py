@@ -94,7 +94,7 @@ class FDMSolver:
 
     def __init__(self, ops: SpatialOperators, M_t: np.ndarray, B_t: np.ndarray,
                  plan: SpatialPlan | None = None, factors: TemporalFactors | None = None,
-                 leaf_size: int = 32):
+                 leaf_size: int = 16):
         t0 = time.perf_counter()
         self.ops = ops
         self.M_t = np.asarray(M_t, float)
@@ -124,9 +124,9 @@ class FDMSolver:
         single = F.dim() == 2
         Fb = (F.unsqueeze(0) if single else F).contiguous()
         nr = Fb.shape[0]
-        G = work if work is not None else torch.empty_like(Fb)
-        G = G.reshape(Fb.shape)
-        W = out.reshape(Fb.shape) if out is not None else torch.empty_like(Fb)
+        # buffer rotation without copies: F -> G (=out) -> W (=work) -> out
+        G = out.reshape(Fb.shape) if out is not None else torch.empty_like(Fb)
+        W = work.reshape(Fb.shape) if work is not None else torch.empty_like(Fb)
         s = stream if stream is not None else torch.cuda.current_stream()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timings is not None else None
         if ev:
@@ -145,10 +145,8 @@ class FDMSolver:
             timings["factor_solve_s"] = ev[1].elapsed_time(ev[2]) / 1e3
             timings["back_transform_s"] = ev[2].elapsed_time(ev[3]) / 1e3
         if out is not None:
-            out.copy_(G.reshape(out.shape))
             return out
-        res = G
-        return res[0] if single else res
+        return G[0] if single else G
 
 
 def solve(ops: SpatialOperators, M_t: np.ndarray, B_t: np.ndarray, f: torch.Tensor,

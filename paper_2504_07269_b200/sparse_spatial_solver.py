@@ -27,7 +27,7 @@ from .fem_assembly import SpatialOperators
 
 
 class SpatialPlan:
-    def __init__(self, ops: SpatialOperators, leaf_size: int = 32):
+    def __init__(self, ops: SpatialOperators, leaf_size: int = 16):
         self.ops = ops
         self.n = ops.n
         h = C.c_void_p()
@@ -60,6 +60,11 @@ class SpatialPlan:
         rows = np.empty(off[-1], dtype=np.int32)
         N.check(N.lib().stfem_plan_front_rows(self._h, off.ctypes.data, rows.ctypes.data))
         return [rows[off[f]:off[f + 1]] for f in range(nf)]
+
+    def last_launches(self) -> int:
+        v = C.c_int64()
+        N.check(N.lib().stfem_plan_last_launches(self._h, C.byref(v)))
+        return v.value
 
     def set_batch(self, batch: int) -> int:
         bps = C.c_int64()

@@ -21,7 +21,7 @@ def main():
     ap.add_argument("--workload", default="C3")
     ap.add_argument("--shifts", type=int, default=64)
     ap.add_argument("--reps", type=int, default=2)
-    ap.add_argument("--leaf", type=int, default=32)
+    ap.add_argument("--leaf", type=int, default=16)
     a = ap.parse_args()
     prob = Problem(a.workload, device="cuda")
     tf = temporal_factors(prob.M_t, prob.B_t)
