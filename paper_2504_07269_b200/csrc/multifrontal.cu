@@ -38,14 +38,14 @@ constexpr int LDD = NB + 1;       // diagonal block column stride
 constexpr int MAXR = 16;          // max RHS per call (bv chunks of 16 in the host loop)
 
 constexpr int GEMM_SMEM = (2 * 2 * TK * LDS + 2 * TK) * 16;
-constexpr int DIAG_SMEM = (NB * LDD + NB + NB * MAXR) * 16;
+constexpr int DIAG_SMEM = (2 * NB * LDD + NB + NB * MAXR) * 16;
 constexpr int FACTOR_SMEM = GEMM_SMEM + DIAG_SMEM;
 
 struct LevelArgs {
   const FrontDev* fronts;
   const int32_t* list;
   int32_t nlist, nbatch;
-  const int32_t *child_ids, *relpos, *bidx, *ent_src, *ent_dst, *perm;
+  const int32_t *child_ids, *relpos, *bidx, *ent_src, *ent_dst, *perm, *inv;
   const double *Mv, *Av;
   const cplx* lam;
   cplx* factor;
@@ -184,12 +184,13 @@ __device__ void gemm_update(cplx* __restrict__ C, int ldC, int M, int N, const c
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(NT, 1) factor_level_kernel(LevelArgs a) {
+__global__ void __launch_bounds__(NT, 2) factor_level_kernel(LevelArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* gsm = reinterpret_cast<cplx*>(smem_raw);
   cplx* Ld = gsm + GEMM_SMEM / 16;          // NB x LDD, column-major
   cplx* dinv_s = Ld + NB * LDD;             // NB
   cplx* ysm = dinv_s + NB;                  // NB x MAXR
+  cplx* LDs = ysm + NB * MAXR;              // NB x LDD: d_c * L11[i][c]
 
   const int tid = threadIdx.x;
   const int inst = blockIdx.x;
@@ -204,71 +205,80 @@ __global__ void __launch_bounds__(NT, 1) factor_level_kernel(LevelArgs a) {
   cplx* Zk = a.Z + (int64_t)k * nx * nrhs;
   const int64_t shift = a.shift0 + k;
 
-  // ---- 1. assembly ----
+  // ---- 1. assembly: gather once (each front entry written exactly once) ----
+  // parent entry (r1, c2) = sum over children s of U_s[inv_s[r1], inv_s[c2]]
+  // (inverse relpos maps staged in shared memory), then the original entries
+  // M + lam A are added at their unique positions.  No zero fill, no RMW.
   const cplx zero = cmk(0.0, 0.0);
-  for (int64_t i = tid; i < (int64_t)n * p; i += NT) stc(P + i, zero);
-  for (int64_t i = tid; i < (int64_t)b * b; i += NT) stc(U + i, zero);
-  for (int i = tid; i < b * nrhs; i += NT) stc(R + i, zero);
-  for (int i = tid; i < p * nrhs; i += NT) {
-    int r = i / p, ii = i % p;
-    int64_t j = a.perm[F.pbeg + ii];
-    stc(Zk + F.pbeg + ii + (int64_t)r * nx, a.G[bv_off(a.lay, r, shift, j)]);
-  }
-  __syncthreads();
-  for (int e = tid; e < F.ent_cnt; e += NT) {
-    int src = a.ent_src[F.ent_beg + e];
-    double mv = a.Mv[src], av = a.Av[src];
-    stc(P + a.ent_dst[F.ent_beg + e], cmk(fma(lam.re, av, mv), lam.im * av));
-  }
-  __syncthreads();
-  for (int ci = 0; ci < F.nchild; ++ci) {
-    const FrontDev Cf = a.fronts[a.child_ids[F.child_beg + ci]];
-    const int bc = Cf.n - Cf.p;
-    const cplx* Uc = a.uchild + (int64_t)k * a.uchild_stride + Cf.uofs;
-    const cplx* Rc = a.rchild + ((int64_t)k * a.rchild_stride + Cf.rofs) * nrhs;
-    const int32_t* rel = a.relpos + Cf.relpos_beg;
-    // warp per child column, lanes over rows: coalesced reads of U_c, nearly
-    // contiguous destination (relpos is monotone), 4 independent RMWs in flight
-    // each warp owns 8 child columns at a time, lanes run over child rows:
-    // per lane one relpos load + 8 U_c loads + 8 destination loads in flight
-    {
-      constexpr int CU = 8, NW = NT / 32;
-      const int lane = tid & 31, warp = tid >> 5;
-      for (int k2b = warp; k2b < bc; k2b += CU * NW) {
-        cplx* dcol[CU];
+  {
+    constexpr int CU = 4, NW = NT / 32;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int nc = min(F.nchild, 2);
+    int* inv_s = reinterpret_cast<int*>(gsm);   // nc x n (aliases the GEMM staging buffers)
+    for (int q = tid; q < nc * n; q += NT) inv_s[q] = a.inv[F.inv_beg + q];
+    const cplx* Ucs[2] = {nullptr, nullptr};
+    const cplx* Rcs[2] = {nullptr, nullptr};
+    int bcs[2] = {0, 0};
+    for (int s = 0; s < nc; ++s) {
+      const FrontDev Cf = a.fronts[a.child_ids[F.child_beg + s]];
+      bcs[s] = Cf.n - Cf.p;
+      Ucs[s] = a.uchild + (int64_t)k * a.uchild_stride + Cf.uofs;
+      Rcs[s] = a.rchild + ((int64_t)k * a.rchild_stride + Cf.rofs) * nrhs;
+    }
+    __syncthreads();
+    for (int c2b = warp; c2b < n; c2b += CU * NW) {
+      int k2[2][CU];
+      cplx* dst[CU];
+#pragma unroll
+      for (int u = 0; u < CU; ++u) {
+        const int c2 = min(c2b + u * NW, n - 1);
+#pragma unroll
+        for (int s = 0; s < 2; ++s) k2[s][u] = s < nc ? inv_s[s * n + c2] : -1;
+        dst[u] = (c2 < p) ? P + (int64_t)c2 * n : U + (int64_t)(c2 - p) * b - p;
+      }
+      for (int r1 = c2b + lane; r1 < n; r1 += 32) {
+        int k1[2];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) k1[s] = s < nc ? inv_s[s * n + r1] : -1;
+        cplx v[CU];
 #pragma unroll
         for (int u = 0; u < CU; ++u) {
-          const int k2 = k2b + u * NW;
-          const int r2 = k2 < bc ? rel[k2] : 0;
-          dcol[u] = (r2 < p) ? P + (int64_t)r2 * n : U + (int64_t)(r2 - p) * b - p;
+          v[u] = zero;
+#pragma unroll
+          for (int s = 0; s < 2; ++s)
+            if (k1[s] >= 0 && k2[s][u] >= 0)
+              v[u] = cadd(v[u], ldc(Ucs[s] + (int64_t)k2[s][u] * bcs[s] + k1[s]));
         }
-        for (int k1 = k2b + lane; k1 < bc; k1 += 32) {
-          const int r1 = rel[k1];
-          cplx v[CU], d[CU];
 #pragma unroll
-          for (int u = 0; u < CU; ++u) {
-            const int k2 = k2b + u * NW;
-            const bool ok = k2 < bc && k1 >= k2;
-            v[u] = ok ? ldc(Uc + (int64_t)k2 * bc + k1) : cmk(0.0, 0.0);
-            d[u] = ok ? ldc(dcol[u] + r1) : cmk(0.0, 0.0);
-          }
-#pragma unroll
-          for (int u = 0; u < CU; ++u) {
-            const int k2 = k2b + u * NW;
-            if (k2 < bc && k1 >= k2) stc(dcol[u] + r1, cadd(d[u], v[u]));
-          }
+        for (int u = 0; u < CU; ++u) {
+          const int c2 = c2b + u * NW;
+          if (c2 < n && r1 >= c2) stc(dst[u] + r1, v[u]);
         }
       }
     }
-    for (int idx = tid; idx < bc * nrhs; idx += NT) {
-      int k1 = idx % bc, r = idx / bc;
-      int r1 = rel[k1];
-      cplx v = ldc(Rc + k1 + (int64_t)r * bc);
-      cplx* dst = (r1 < p) ? Zk + F.pbeg + r1 + (int64_t)r * nx : R + (r1 - p) + (int64_t)r * b;
-      stc(dst, cadd(ldc(dst), v));
+    // forward RHS: pivot rows get G (gathered through perm) + children, boundary rows children only
+    for (int q = tid; q < n * nrhs; q += NT) {
+      const int r1 = q % n, r = q / n;
+      cplx v = zero;
+      if (r1 < p) v = a.G[bv_off(a.lay, r, shift, a.perm[F.pbeg + r1])];
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int kk = s < nc ? inv_s[s * n + r1] : -1;
+        if (kk >= 0) v = cadd(v, ldc(Rcs[s] + kk + (int64_t)r * bcs[s]));
+      }
+      if (r1 < p) stc(Zk + F.pbeg + r1 + (int64_t)r * nx, v);
+      else stc(R + (r1 - p) + (int64_t)r * b, v);
     }
-    __syncthreads();
   }
+  __syncthreads();
+  for (int e = tid; e < F.ent_cnt; e += NT) {
+    const int src = a.ent_src[F.ent_beg + e];
+    const double mv = a.Mv[src], av = a.Av[src];
+    cplx* dst = P + a.ent_dst[F.ent_beg + e];
+    const cplx o = ldc(dst);
+    stc(dst, cmk(o.re + fma(lam.re, av, mv), o.im + lam.im * av));
+  }
+  __syncthreads();
 
   // ---- 2. pivot columns, panels of NB ----
   for (int kb = 0; kb < p; kb += NB) {
@@ -304,10 +314,11 @@ __global__ void __launch_bounds__(NT, 1) factor_level_kernel(LevelArgs a) {
       }
       __syncthreads();
     }
-    // write back L11 and D; forward-solve the panel RHS: y = L11^{-1} r
+    // write back L11 and D; stage LDs[c][i] = d_c L11[i][c]; forward-solve the panel RHS
     for (int idx = tid; idx < w * w; idx += NT) {
       int i = idx % w, c = idx / w;
       if (i >= c) stc(P + (kb + i) + (int64_t)(kb + c) * n, Ld[c * LDD + i]);
+      if (i > c) LDs[c * LDD + i] = cmul(Ld[c * LDD + c], Ld[c * LDD + i]);
     }
     if (tid < nrhs) {
       const int r = tid;
@@ -320,33 +331,42 @@ __global__ void __launch_bounds__(NT, 1) factor_level_kernel(LevelArgs a) {
       }
     }
     __syncthreads();
-    // TRSM rows below the diagonal block + fused RHS update (thread per row)
+    // TRSM rows below the diagonal block + fused RHS update (thread per row),
+    // 8 columns at a time in registers; earlier columns of the row are re-read
+    // (L1) as scaled l and applied through LDs[c][j] = d_c L11[j][c]
     for (int i = kb + w + tid; i < n; i += NT) {
-      cplx y[NB];
+      cplx* prow = P + i + (int64_t)kb * n;
+      for (int jb = 0; jb < w; jb += 8) {
+        cplx y[8];
 #pragma unroll
-      for (int j = 0; j < NB; ++j)
-        if (j < w) y[j] = ldc(P + i + (int64_t)(kb + j) * n);
+        for (int jj = 0; jj < 8; ++jj) y[jj] = (jb + jj < w) ? ldc(prow + (int64_t)(jb + jj) * n) : zero;
+        for (int c = 0; c < jb; ++c) {
+          const cplx lc = ldc(prow + (int64_t)c * n);
 #pragma unroll
-      for (int j = 0; j < NB; ++j) {
-        if (j < w) {
-#pragma unroll
-          for (int c = 0; c < j; ++c) y[j] = cfms(y[j], y[c], Ld[c * LDD + j]);
+          for (int jj = 0; jj < 8; ++jj)
+            if (jb + jj < w) y[jj] = cfms(y[jj], lc, LDs[c * LDD + jb + jj]);
         }
-      }
-      // y now holds l_ij * d_j; finish with D^{-1}
 #pragma unroll
-      for (int j = 0; j < NB; ++j)
-        if (j < w) {
-          y[j] = cmul(y[j], dinv_s[j]);
-          stc(P + i + (int64_t)(kb + j) * n, y[j]);
+        for (int jj = 1; jj < 8; ++jj) {
+          if (jb + jj < w) {
+#pragma unroll
+            for (int cc = 0; cc < jj; ++cc) y[jj] = cfms(y[jj], y[cc], Ld[(jb + cc) * LDD + jb + jj]);
+          }
         }
-      for (int r = 0; r < nrhs; ++r) {
-        cplx* dst = (i < p) ? Zk + F.pbeg + i + (int64_t)r * nx : R + (i - p) + (int64_t)r * b;
-        cplx acc = ldc(dst);
 #pragma unroll
-        for (int j = 0; j < NB; ++j)
-          if (j < w) acc = cfms(acc, y[j], ysm[j * MAXR + r]);
-        stc(dst, acc);
+        for (int jj = 0; jj < 8; ++jj)
+          if (jb + jj < w) {
+            y[jj] = cmul(y[jj], dinv_s[jb + jj]);
+            stc(prow + (int64_t)(jb + jj) * n, y[jj]);
+          }
+        for (int r = 0; r < nrhs; ++r) {
+          cplx* dst = (i < p) ? Zk + F.pbeg + i + (int64_t)r * nx : R + (i - p) + (int64_t)r * b;
+          cplx acc = ldc(dst);
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj)
+            if (jb + jj < w) acc = cfms(acc, y[jj], ysm[(jb + jj) * MAXR + r]);
+          stc(dst, acc);
+        }
       }
     }
     __syncthreads();
@@ -369,6 +389,7 @@ __global__ void __launch_bounds__(NT, 1) factor_level_kernel(LevelArgs a) {
 
 __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a) {
   __shared__ cplx ts[NB * MAXR];
+  __shared__ cplx l11[NB * LDD];   // l11[c * LDD + i] = L[kb+i][kb+c], i > c
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int inst = blockIdx.x;
   const int k = inst % a.nbatch;
@@ -412,13 +433,17 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a) {
       }
     }
     __syncthreads();
-    // transposed unit triangle, backward (thread per rhs)
+    // stage the diagonal block, then the transposed unit triangle (thread per rhs)
+    for (int idx = tid; idx < w * w; idx += NT) {
+      const int i = idx % w, c = idx / w;
+      if (i > c) l11[c * LDD + i] = ldc(P + (kb + i) + (int64_t)(kb + c) * n);
+    }
+    __syncthreads();
     if (tid < nrhs) {
       const int r = tid;
       for (int j = w - 1; j >= 0; --j) {
         cplx x = ts[j * MAXR + r];
-        for (int c = j + 1; c < w; ++c)
-          x = cfms(x, ldc(P + (kb + c) + (int64_t)(kb + j) * n), ts[c * MAXR + r]);
+        for (int c = j + 1; c < w; ++c) x = cfms(x, l11[j * LDD + c], ts[c * MAXR + r]);
         ts[j * MAXR + r] = x;
         stc(Zk + F.pbeg + kb + j + (int64_t)r * nx, x);
         a.W[bv_off(a.lay, r, shift, a.perm[F.pbeg + kb + j])] = x;
@@ -456,6 +481,7 @@ int upload(Plan& P) {
   if ((rc = up(&P.d_child_ids, P.child_ids))) return rc;
   if ((rc = up(&P.d_bidx, P.bidx))) return rc;
   if ((rc = up(&P.d_relpos, P.relpos))) return rc;
+  if ((rc = up(&P.d_inv, P.inv))) return rc;
   if ((rc = up(&P.d_ent_src, P.ent_src))) return rc;
   if ((rc = up(&P.d_ent_dst, P.ent_dst))) return rc;
   if ((rc = up(&P.d_perm, P.perm))) return rc;
@@ -463,6 +489,7 @@ int upload(Plan& P) {
   STFEM_CUDA_TRY(cudaMemset(P.d_err, 0, sizeof(int)));
   STFEM_CUDA_TRY(cudaFuncSetAttribute(factor_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       FACTOR_SMEM));
+  STFEM_CUDA_TRY(cudaFuncSetAttribute(factor_level_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   P.level_nmax.assign(P.levels.size(), 0);
   P.level_pmax.assign(P.levels.size(), 0);
   for (size_t d = 0; d < P.levels.size(); ++d)
@@ -522,13 +549,14 @@ void Plan::free_device() {
   cudaFree(d_child_ids);
   cudaFree(d_bidx);
   cudaFree(d_relpos);
+  cudaFree(d_inv);
   cudaFree(d_ent_src);
   cudaFree(d_ent_dst);
   cudaFree(d_perm);
   cudaFree(d_err);
   d_fronts = nullptr;
   d_levels = nullptr;
-  d_child_ids = d_bidx = d_relpos = d_ent_src = d_ent_dst = d_perm = nullptr;
+  d_child_ids = d_bidx = d_relpos = d_inv = d_ent_src = d_ent_dst = d_perm = nullptr;
   d_err = nullptr;
   device = -1;
 }
@@ -562,6 +590,7 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
   a.fronts = P.d_fronts;
   a.child_ids = P.d_child_ids;
   a.relpos = P.d_relpos;
+  a.inv = P.d_inv;
   a.bidx = P.d_bidx;
   a.ent_src = P.d_ent_src;
   a.ent_dst = P.d_ent_dst;

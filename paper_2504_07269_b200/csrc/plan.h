@@ -23,6 +23,8 @@ struct FrontDev {
   int32_t bidx_beg;    // into bidx: new indices of the b boundary rows
   int32_t relpos_beg;  // into relpos: position of each boundary row in the parent front
   int32_t parent, depth;
+  int32_t inv_beg;     // into inv: nchild x n map parent row -> child boundary row (-1 if none)
+  int32_t pad_;
   int64_t fofs;        // factor block offset (complex elements) within one shift
   int64_t uofs;        // update block offset within the pool of parity depth%2 (one shift)
   int64_t rofs;        // forward-RHS update offset (units of b, times nrhs) within its pool
@@ -34,7 +36,7 @@ struct Plan {
   int64_t nnz_pattern = 0;
   std::vector<int32_t> perm, iperm;       // perm[new] = old
   std::vector<FrontDev> fronts;           // postorder
-  std::vector<int32_t> child_ids, bidx, relpos, ent_src, ent_dst;
+  std::vector<int32_t> child_ids, bidx, relpos, ent_src, ent_dst, inv;
   std::vector<std::vector<int32_t>> levels;  // fronts per depth
   int32_t depth = 0, max_front = 0, max_pivots = 0;
   int64_t factor_stride = 0;               // complex per shift
@@ -50,7 +52,7 @@ struct Plan {
   std::vector<int64_t> level_off;          // offsets into d_levels
   std::vector<int32_t> level_nmax, level_pmax;  // per depth: max front order / pivots
   bool force_big = getenv("STFEM_FORCE_BIG") != nullptr;  // diagnostics: disable the small-front path
-  int32_t *d_child_ids = nullptr, *d_bidx = nullptr, *d_relpos = nullptr;
+  int32_t *d_child_ids = nullptr, *d_bidx = nullptr, *d_relpos = nullptr, *d_inv = nullptr;
   int32_t *d_ent_src = nullptr, *d_ent_dst = nullptr, *d_perm = nullptr;
   int* d_err = nullptr;
 

@@ -248,11 +248,18 @@ int build_symbolic(Plan& P, int32_t n, const int64_t* rowptr, const int32_t* col
     for (size_t k = 0; k < B[f].size(); ++k) pos[B[f][k]] = F.p + (int32_t)k;
     F.child_beg = (int32_t)P.child_ids.size();
     F.nchild = (int32_t)kids[f].size();
-    for (int32_t c : kids[f]) {
+    if (kids[f].size() > 2) return fail(STFEM_ERR_INTERNAL, "plan: front with more than two children");
+    F.inv_beg = (int32_t)P.inv.size();
+    for (size_t s = 0; s < kids[f].size(); ++s) {
+      const int32_t c = kids[f][s];
       P.child_ids.push_back(c);
       FrontDev& Cf = P.fronts[c];
       Cf.relpos_beg = (int32_t)P.relpos.size();
       for (int32_t w : B[c]) P.relpos.push_back(pos[w]);
+      // inverse map (parent row -> child boundary row) for the gather assembly
+      const size_t base = P.inv.size();
+      P.inv.resize(base + F.n, -1);
+      for (size_t k = 0; k < B[c].size(); ++k) P.inv[base + pos[B[c][k]]] = (int32_t)k;
     }
     F.bidx_beg = (int32_t)P.bidx.size();
     P.bidx.insert(P.bidx.end(), B[f].begin(), B[f].end());
