@@ -119,6 +119,13 @@ int stfem_factor_solve(stfem_plan* plan, const double* Mvals, const double* Aval
                        void* stream);
 /* batch size in shifts (0 = auto from free memory); returns bytes per shift */
 int stfem_plan_set_batch(stfem_plan* plan, int32_t batch, int64_t* bytes_per_shift);
+/* per-level accounting: record CUDA-event times of every level launch on the
+ * next calls (on != 0); report ms[2*(depth+1)] (factor launches by depth, then
+ * backward launches by depth, summed over shift batches), the algorithmic
+ * flops per shift of each depth (flops[depth+1]) and whether the depth runs
+ * on the shared-memory small-front kernels (small[depth+1]) */
+int stfem_plan_record_levels(stfem_plan* plan, int32_t on);
+int stfem_plan_level_report(const stfem_plan* plan, double* ms, double* flops, int32_t* small);
 /* kernel launches of the last stfem_factor_solve call (for launch accounting) */
 int stfem_plan_last_launches(const stfem_plan* plan, int64_t* launches);
 

@@ -607,7 +607,8 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
   a.lay = lay;
   a.err = P.d_err;
   // STFEM_LEVEL_TIMING=1: per-launch CUDA-event times to stderr (diagnostics only)
-  static const bool level_timing = getenv("STFEM_LEVEL_TIMING") != nullptr;
+  static const bool level_print = getenv("STFEM_LEVEL_TIMING") != nullptr;
+  const bool level_timing = level_print || P.record_levels;
   std::vector<cudaEvent_t> evs;
   auto mark = [&]() {
     if (!level_timing) return;
@@ -662,12 +663,17 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
   if (level_timing) {
     cudaStreamSynchronize(stream);
     int L = P.depth + 1;
+    // level_ms[0..L): factor launches by depth, [L..2L): backward launches by depth (summed over batches)
+    P.level_ms.assign(2 * L, 0.0);
     for (size_t i = 1; i < evs.size(); ++i) {
       float ms = 0;
       cudaEventElapsedTime(&ms, evs[i - 1], evs[i]);
       int j = (int)((i - 1) % (2 * L));
-      fprintf(stderr, "[stfem] batch %d %s depth %d: %.3f ms\n", (int)((i - 1) / (2 * L)),
-              j < L ? "factor" : "backward", j < L ? P.depth - j : j - L, ms);
+      int d = j < L ? P.depth - j : j - L;
+      P.level_ms[(j < L ? 0 : L) + d] += ms;
+      if (level_print)
+        fprintf(stderr, "[stfem] batch %d %s depth %d: %.3f ms\n", (int)((i - 1) / (2 * L)),
+                j < L ? "factor" : "backward", d, ms);
     }
     for (auto e : evs) cudaEventDestroy(e);
   }
@@ -756,6 +762,32 @@ extern "C" int stfem_plan_front_rows(const stfem_plan* plan, int64_t* offsets, i
     o += F.n;
   }
   offsets[P.fronts.size()] = o;
+  return STFEM_OK;
+}
+
+extern "C" int stfem_plan_record_levels(stfem_plan* plan, int32_t on) {
+  if (!plan) return stfem::fail(STFEM_ERR_ARG, "plan_record_levels: null pointer");
+  reinterpret_cast<Plan*>(plan)->record_levels = on != 0;
+  return STFEM_OK;
+}
+
+extern "C" int stfem_plan_level_report(const stfem_plan* plan, double* ms, double* flops, int32_t* small) {
+  if (!plan) return stfem::fail(STFEM_ERR_ARG, "plan_level_report: null pointer");
+  const Plan& P = *reinterpret_cast<const Plan*>(plan);
+  const int L = P.depth + 1;
+  for (int i = 0; i < 2 * L; ++i)
+    if (ms) ms[i] = i < (int)P.level_ms.size() ? P.level_ms[i] : 0.0;
+  if (flops) {
+    for (int d = 0; d < L; ++d) flops[d] = 0.0;
+    for (const auto& F : P.fronts)
+      for (int32_t j = 0; j < F.p; ++j) {
+        const double c = (double)(F.n - 1 - j);
+        flops[F.depth] += 4.0 * c * c;
+      }
+  }
+  if (small)
+    for (int d = 0; d < L; ++d)
+      small[d] = (d < (int)P.level_nmax.size() && P.level_nmax[d] <= stfem::SMALL_N && !P.force_big) ? 1 : 0;
   return STFEM_OK;
 }
 

@@ -62,6 +62,8 @@ struct Plan {
   int32_t ws_nrhs = 0;
   int32_t last_batch = 0;  // batch size used by the last factor_solve
   int64_t last_launches = 0;  // kernel launches issued by the last factor_solve
+  bool record_levels = false;   // record per-level CUDA-event times into level_ms
+  std::vector<double> level_ms;
   cplx* d_factor = nullptr;
   cplx* d_upool[2] = {nullptr, nullptr};
   cplx* d_rpool[2] = {nullptr, nullptr};

@@ -75,13 +75,17 @@ def apply_global(ops: SpatialOperators, M_t: np.ndarray, B_t: np.ndarray, v: tor
 
 
 def relative_residual(ops, M_t, B_t, psi: torch.Tensor, f: torch.Tensor) -> float:
-    r = apply_global(ops, M_t, B_t, psi) - f
+    """max over RHS of ||A psi - f|| / ||f||, one RHS at a time
+    so the temporaries stay O(n_t n_x)."""
     fb = f.reshape(-1, *f.shape[-2:])
-    rb = r.reshape(-1, *r.shape[-2:])
+    pb = psi.reshape(-1, *psi.shape[-2:])
     worst = 0.0
     for i in range(fb.shape[0]):
+        r = apply_global(ops, M_t, B_t, pb[i])
+        r.sub_(fb[i])
         nf = float(torch.linalg.vector_norm(fb[i]))
-        nr = float(torch.linalg.vector_norm(rb[i]))
+        nr = float(torch.linalg.vector_norm(r))
+        del r
         worst = max(worst, nr / nf if nf > 0 else nr)
     return worst
 

@@ -61,6 +61,22 @@ class SpatialPlan:
         N.check(N.lib().stfem_plan_front_rows(self._h, off.ctypes.data, rows.ctypes.data))
         return [rows[off[f]:off[f + 1]] for f in range(nf)]
 
+    def record_levels(self, on: bool = True):
+        N.check(N.lib().stfem_plan_record_levels(self._h, 1 if on else 0))
+
+    def level_report(self):
+        """(factor_ms[d], backward_ms[d], flops_per_shift[d], small[d]) of the last recorded call."""
+        L = self.stats["depth"] + 1
+        ms = np.zeros(2 * L)
+        fl = np.zeros(L)
+        sm = np.zeros(L, dtype=np.int32)
+        N.check(N.lib().stfem_plan_level_report(self._h, ms.ctypes.data, fl.ctypes.data, sm.ctypes.data))
+        return ms[:L], ms[L:], fl, sm.astype(bool)
+
+    def last_num_batches(self) -> int:
+        """Shift batches used by the last factor_solve call."""
+        return max(1, self.last_launches() // (2 * (self.stats["depth"] + 1)))
+
     def last_launches(self) -> int:
         v = C.c_int64()
         N.check(N.lib().stfem_plan_last_launches(self._h, C.byref(v)))
