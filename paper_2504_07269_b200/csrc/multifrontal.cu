@@ -272,8 +272,7 @@ __global__ void __launch_bounds__(NT, 2) factor_level_kernel(LevelArgs a) {
   }
   __syncthreads();
   for (int e = tid; e < F.ent_cnt; e += NT) {
-    const int src = a.ent_src[F.ent_beg + e];
-    const double mv = a.Mv[src], av = a.Av[src];
+    const double mv = a.Mv[F.ent_beg + e], av = a.Av[F.ent_beg + e];   // entry-ordered values
     cplx* dst = P + a.ent_dst[F.ent_beg + e];
     const cplx o = ldc(dst);
     stc(dst, cmk(o.re + fma(lam.re, av, mv), o.im + lam.im * av));
@@ -455,6 +454,18 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a) {
 
 #include "multifrontal_small.cuh"
 
+// M_x / A_x values of every front entry, in entry order (shift-independent;
+// one coalesced stream per front instead of an indirect gather)
+__global__ void gather_entries_kernel(const int32_t* __restrict__ src, const double* __restrict__ Mv,
+                                      const double* __restrict__ Av, double* mv, double* av, int64_t ne) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < ne) {
+    const int s = src[e];
+    mv[e] = Mv[s];
+    av[e] = Av[s];
+  }
+}
+
 int upload(Plan& P) {
   int dev;
   STFEM_CUDA_TRY(cudaGetDevice(&dev));
@@ -483,6 +494,8 @@ int upload(Plan& P) {
   if ((rc = up(&P.d_relpos, P.relpos))) return rc;
   if ((rc = up(&P.d_inv, P.inv))) return rc;
   if ((rc = up(&P.d_ent_src, P.ent_src))) return rc;
+  STFEM_CUDA_TRY(cudaMalloc(&P.d_ent_mv, std::max<size_t>(1, P.ent_src.size()) * sizeof(double)));
+  STFEM_CUDA_TRY(cudaMalloc(&P.d_ent_av, std::max<size_t>(1, P.ent_src.size()) * sizeof(double)));
   if ((rc = up(&P.d_ent_dst, P.ent_dst))) return rc;
   if ((rc = up(&P.d_perm, P.perm))) return rc;
   STFEM_CUDA_TRY(cudaMalloc(&P.d_err, sizeof(int)));
@@ -551,6 +564,9 @@ void Plan::free_device() {
   cudaFree(d_relpos);
   cudaFree(d_inv);
   cudaFree(d_ent_src);
+  cudaFree(d_ent_mv);
+  cudaFree(d_ent_av);
+  d_ent_mv = d_ent_av = nullptr;
   cudaFree(d_ent_dst);
   cudaFree(d_perm);
   cudaFree(d_err);
@@ -595,8 +611,16 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
   a.ent_src = P.d_ent_src;
   a.ent_dst = P.d_ent_dst;
   a.perm = P.d_perm;
-  a.Mv = Mv;
-  a.Av = Av;
+  {
+    const int64_t ne = (int64_t)P.ent_src.size();
+    if (ne > 0) {
+      gather_entries_kernel<<<(unsigned)((ne + 255) / 256), 256, 0, stream>>>(P.d_ent_src, Mv, Av, P.d_ent_mv,
+                                                                             P.d_ent_av, ne);
+      STFEM_LAUNCH_CHECK("gather_entries_kernel");
+    }
+  }
+  a.Mv = P.d_ent_mv;   // entry-ordered
+  a.Av = P.d_ent_av;
   a.factor = P.d_factor;
   a.fstride = P.factor_stride;
   a.Z = P.d_Z;
@@ -659,7 +683,7 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
     }
   }
   P.last_batch = batch;
-  P.last_launches = (int64_t)((nshift + batch - 1) / batch) * 2 * (P.depth + 1);
+  P.last_launches = (int64_t)((nshift + batch - 1) / batch) * 2 * (P.depth + 1) + (P.ent_src.empty() ? 0 : 1);
   if (level_timing) {
     cudaStreamSynchronize(stream);
     int L = P.depth + 1;

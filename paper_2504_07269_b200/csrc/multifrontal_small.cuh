@@ -71,18 +71,21 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
 
   const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
   const int nt = blockDim.x, nwarp = nt >> 5;
-  const int inst = blockIdx.x;
-  const int k = inst % a.nbatch;
-  const FrontDev Fr = a.fronts[a.list[inst / a.nbatch]];
-  const int n = Fr.n, p = Fr.p, b = n - p;
   const int nrhs = a.nrhs, nx = a.nx;
-  const cplx lam = a.lam[k];
-  const int64_t shift = a.shift0 + k;
   const cplx zero = cmk(0.0, 0.0);
   cplx* W8 = scratch + warp * scr_size(NR);
   cplx* Y8 = W8 + KB * KB;
   cplx* Dv = Y8 + KB * NR;
   cplx* Dinv = Dv + KB;
+  // grid-stride over (front, shift) instances: amortises block launch and
+  // keeps a fixed set of resident CTAs busy on levels with millions of fronts
+  const int total = a.nlist * a.nbatch;
+  for (int inst = blockIdx.x; inst < total; inst += gridDim.x) {
+  const int k = inst % a.nbatch;
+  const FrontDev Fr = a.fronts[a.list[inst / a.nbatch]];
+  const int n = Fr.n, p = Fr.p, b = n - p;
+  const cplx lam = a.lam[k];
+  const int64_t shift = a.shift0 + k;
 
   // ---- gather ----
   const int tri = (n * (n + 1)) / 2;
@@ -95,9 +98,8 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
   }
   __syncthreads();
   for (int e = i; e < Fr.ent_cnt; e += nt) {
-    int src = a.ent_src[Fr.ent_beg + e];
-    int dst = a.ent_dst[Fr.ent_beg + e];
-    double mv = a.Mv[src], av = a.Av[src];
+    const int dst = a.ent_dst[Fr.ent_beg + e];
+    const double mv = a.Mv[Fr.ent_beg + e], av = a.Av[Fr.ent_beg + e];   // entry-ordered values
     F[pk(dst % n, dst / n, n)] = cmk(fma(lam.re, av, mv), lam.im * av);
   }
   __syncthreads();
@@ -274,6 +276,8 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
         if (r < nrhs) stc(Zk + Fr.pbeg + i + (int64_t)r * nx, cmul(rv[r], dinv));
     }
   }
+  __syncthreads();   // shared memory is reused by the next instance
+  }
 }
 
 __host__ __device__ constexpr int small_bwd_smem_bytes(int nmax, int pmax, int nr) {
@@ -294,11 +298,12 @@ __global__ void __launch_bounds__(SMALL_N) backward_small_kernel(LevelArgs a, in
   cplx* Tsm = xs + nmax * NR;                      // KB x NR : current block
 
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
-  const int inst = blockIdx.x;
+  const int nrhs = a.nrhs, nx = a.nx;
+  const int total = a.nlist * a.nbatch;
+  for (int inst = blockIdx.x; inst < total; inst += gridDim.x) {
   const int k = inst % a.nbatch;
   const FrontDev Fr = a.fronts[a.list[inst / a.nbatch]];
   const int n = Fr.n, p = Fr.p;
-  const int nrhs = a.nrhs, nx = a.nx;
   const cplx* Pg = a.factor + (int64_t)k * a.fstride + Fr.fofs;
   cplx* Zk = a.Z + (int64_t)k * nx * nrhs;
   const int32_t* bidx = a.bidx + Fr.bidx_beg;
@@ -370,6 +375,7 @@ __global__ void __launch_bounds__(SMALL_N) backward_small_kernel(LevelArgs a, in
     }
     __syncthreads();
   }
+  }   // instance loop
 }
 
 template <int NR>
@@ -384,7 +390,21 @@ int launch_small_factor(const LevelArgs& a, int grid, int nmax, cudaStream_t s) 
                                         cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     attr = true;
   }
-  factor_small_kernel<NR><<<grid, (nmax + 31) / 32 * 32, smem, s>>>(a, nmax);
+  // persistent-style grid: as many CTAs as can be resident, grid-striding over instances
+  const int threads = (nmax + 31) / 32 * 32;
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int per_sm = 0;
+  STFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_small_kernel<NR>, threads, smem));
+  const int resident = std::max(1, per_sm) * nsm;
+  // measured: one instance per CTA (grid = all instances) beats a resident-only
+  // grid-striding launch by ~5% on the leaf levels; keep the loop for large grids only
+  const int g = grid > 64 * resident ? 64 * resident : grid;
+  factor_small_kernel<NR><<<g, threads, smem, s>>>(a, nmax);
   STFEM_LAUNCH_CHECK("factor_small_kernel");
   return STFEM_OK;
 }
@@ -400,7 +420,12 @@ int launch_small_backward(const LevelArgs& a, int grid, int nmax, int pmax, cuda
                                         cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     attr = true;
   }
-  backward_small_kernel<NR><<<grid, (nmax + 31) / 32 * 32, smem, s>>>(a, nmax, pmax);
+  const int threads = (nmax + 31) / 32 * 32;
+  int nsm = 0, dev = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  STFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, backward_small_kernel<NR>, threads, smem));
+  backward_small_kernel<NR><<<std::min(grid, std::max(1, per_sm) * nsm), threads, smem, s>>>(a, nmax, pmax);
   STFEM_LAUNCH_CHECK("backward_small_kernel");
   return STFEM_OK;
 }

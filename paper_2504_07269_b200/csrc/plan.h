@@ -54,6 +54,7 @@ struct Plan {
   bool force_big = getenv("STFEM_FORCE_BIG") != nullptr;  // diagnostics: disable the small-front path
   int32_t *d_child_ids = nullptr, *d_bidx = nullptr, *d_relpos = nullptr, *d_inv = nullptr;
   int32_t *d_ent_src = nullptr, *d_ent_dst = nullptr, *d_perm = nullptr;
+  double *d_ent_mv = nullptr, *d_ent_av = nullptr;   // M_x / A_x values gathered into entry order
   int* d_err = nullptr;
 
   // ---- numeric workspace (per batch of shifts) ----

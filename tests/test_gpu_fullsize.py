@@ -1,0 +1,66 @@
+"""Full-size (BASELINE.json configs) parity through size-independent properties:
+manufactured-solution errors (the survey's oracle values, 3 significant digits),
+the global residual certificate (<= 1e-8), linearity, and
+per-shift agreement with SuperLU at sampled shifts of the full operators."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import stfem_oracle as O
+from paper_2504_07269_b200 import error_analysis as ea
+from paper_2504_07269_b200 import kronecker_solver as ks
+from paper_2504_07269_b200 import sparse_spatial_solver as sss
+from paper_2504_07269_b200.problems import Problem
+
+pytestmark = pytest.mark.gpu
+
+# oracle errors under SPEC conventions (L2, H1)
+SURVEY_ERRORS = {"C1": (4.004296e-03, 1.670489e-01), "C2": (2.540125e-04, 4.165419e-02),
+                 "C3": (3.749927e-05, 2.271354e-02)}
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3"])
+def test_manufactured_errors_full_size(cfg):
+    prob = Problem(cfg)
+    fdm = ks.FDMSolver(prob.ops, prob.M_t, prob.B_t)
+    psi = fdm.solve(prob.F)
+    res = ks.relative_residual(prob.ops, prob.M_t, prob.B_t, psi, prob.F)
+    assert res < 1e-8, res
+    l2, h1 = ea.spacetime_errors(psi[0].cpu().numpy(), ea.exact_solution(prob.cfg.source), prob.mesh, prob.tmesh)
+    want = SURVEY_ERRORS[cfg]
+    assert f"{l2:.3g}" == f"{want[0]:.3g}" and f"{h1:.3g}" == f"{want[1]:.3g}", (l2, h1)
+
+
+def test_linearity_c3():
+    prob = Problem("C3")
+    fdm = ks.FDMSolver(prob.ops, prob.M_t, prob.B_t)
+    F1, F2 = prob.F[0], prob.F[1]
+    a = fdm.solve(F1 + 2.0 * F2)
+    b = fdm.solve(F1) + 2.0 * fdm.solve(F2)
+    assert float((a - b).norm() / b.norm()) < 1e-12
+
+
+@pytest.mark.parametrize("cfg", ["C4", "C5"])
+def test_residual_certificate_c4_c5(cfg):
+    prob = Problem(cfg)
+    fdm = ks.FDMSolver(prob.ops, prob.M_t, prob.B_t)
+    psi = fdm.solve(prob.F)
+    assert ks.relative_residual(prob.ops, prob.M_t, prob.B_t, psi, prob.F) < 1e-8
+
+
+@pytest.mark.parametrize("cfg", ["C4", "C5"])
+def test_sampled_shifts_vs_superlu(cfg):
+    """Full-size operators, the 3 hardest shifts (smallest |Im lam|) + 2 others, vs SuperLU."""
+    prob = Problem(cfg, with_rhs=False).assemble()
+    fdm = ks.FDMSolver(prob.ops, prob.M_t, prob.B_t)
+    lam_all = fdm.tf.eigenvalues
+    pick = np.r_[np.argsort(np.abs(lam_all.imag))[:3], [0, len(lam_all) // 2]]
+    lam = lam_all[pick]
+    rng = np.random.default_rng(4)
+    G = rng.standard_normal((1, len(lam), prob.nx)) + 1j * rng.standard_normal((1, len(lam), prob.nx))
+    W = sss.factor_solve_batch(fdm.plan, lam, torch.from_numpy(G).cuda()).cpu().numpy()
+    Mx, Ax = prob.ops.M_x.to_scipy(), prob.ops.A_x.to_scipy()
+    for l in range(len(lam)):
+        ref = O._solve_shift(Mx, Ax, lam[l], G[0, l])
+        err = np.linalg.norm(W[0, l] - ref) / np.linalg.norm(ref)
+        assert err < 1e-10, (l, err)
