@@ -56,6 +56,17 @@ __host__ __device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
 }
 __host__ __device__ __forceinline__ cplx crecip(cplx b) { return cdiv(cplx{1.0, 0.0}, b); }
 // 1/b with one division: conj(b)/|b|^2 (pivots here are far from over/underflow)
+// principal square root (branch cut on the negative real axis)
+__host__ __device__ __forceinline__ cplx csqrt_(cplx z) {
+  const double r = hypot(z.re, z.im);
+  if (r == 0.0) return cplx{0.0, 0.0};
+  if (z.re >= 0.0) {
+    const double t = sqrt(0.5 * (r + z.re));
+    return cplx{t, z.im / (2.0 * t)};
+  }
+  const double t = sqrt(0.5 * (r - z.re));
+  return cplx{fabs(z.im) / (2.0 * t), z.im >= 0.0 ? t : -t};
+}
 __host__ __device__ __forceinline__ cplx crecip_fast(cplx b) {
   double s = 1.0 / fma(b.re, b.re, b.im * b.im);
   return cplx{b.re * s, -b.im * s};

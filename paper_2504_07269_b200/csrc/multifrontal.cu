@@ -38,7 +38,7 @@ constexpr int LDD = NB + 1;       // diagonal block column stride
 constexpr int MAXR = 16;          // max RHS per call (bv chunks of 16 in the host loop)
 
 constexpr int GEMM_SMEM = (2 * 2 * TK * LDS + 2 * TK) * 16;
-constexpr int DIAG_SMEM = (2 * NB * LDD + NB + NB * MAXR) * 16;
+constexpr int DIAG_SMEM = (NB * LDD + 2 * NB + NB * MAXR) * 16;
 constexpr int FACTOR_SMEM = GEMM_SMEM + DIAG_SMEM;
 
 struct LevelArgs {
@@ -72,16 +72,14 @@ __device__ __forceinline__ int64_t bv_off(const stfem_bv_layout& L, int r, int64
          j % L.chunk_cols;
 }
 
-// C[i + c*ldC] -= sum_k A[i + k*lda] * D[k*ldd] * B[c + k*ldb],  i < M, c < N.
+// C[i + c*ldC] -= sum_k A[i + k*lda] * B[c + k*ldb],  i < M, c < N.
 // sym: only i >= c is written and only tiles ti >= tj are computed.
 // 8 warps = 2 (M) x 4 (N); warp tile 32 x 16 complex; mma.m16n8k4.f64.
 __device__ void gemm_update(cplx* __restrict__ C, int ldC, int M, int N, const cplx* __restrict__ A,
-                            int lda, const cplx* __restrict__ B, int ldb, const cplx* __restrict__ D,
-                            int ldd, int K, bool sym, cplx* smem) {
+                            int lda, const cplx* __restrict__ B, int ldb, int K, bool sym, cplx* smem) {
   if (M <= 0 || N <= 0 || K <= 0) return;
   cplx* As = smem;
   cplx* Bs = smem + 2 * TK * LDS;
-  cplx* Ds = Bs + 2 * TK * LDS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3, wm = warp & 1, wn = warp >> 1;
   const int tiles_m = (M + TM - 1) / TM, tiles_n = (N + TM - 1) / TM;
@@ -104,10 +102,6 @@ __device__ void gemm_update(cplx* __restrict__ C, int ldC, int M, int N, const c
         bool okb = okk && (c0 + m < N);
         cp_async16(as + k * LDS + m, oka ? A + (int64_t)(i0 + m) + (int64_t)(k0 + k) * lda : A, oka);
         cp_async16(bs + k * LDS + m, okb ? B + (int64_t)(c0 + m) + (int64_t)(k0 + k) * ldb : B, okb);
-      }
-      if (tid < TK) {
-        bool ok = k0 + tid < K;
-        cp_async16(Ds + stage * TK + tid, ok ? D + (int64_t)(k0 + tid) * ldd : D, ok);
       }
     };
 
@@ -142,18 +136,16 @@ __device__ void gemm_update(cplx* __restrict__ C, int ldC, int M, int N, const c
       __syncthreads();
       const cplx* as = As + (kc & 1) * TK * LDS + t * LDS + wm * 32 + g;
       const cplx* bs = Bs + (kc & 1) * TK * LDS + t * LDS + wn * 16 + g;
-      const cplx* ds = Ds + (kc & 1) * TK + t;
 #pragma unroll
       for (int kk = 0; kk < TK; kk += 4) {
         cplx a[2][2], b[2];
-        cplx d = ds[kk];
 #pragma unroll
         for (int mi = 0; mi < 2; ++mi) {
           a[mi][0] = ldc(as + kk * LDS + mi * 16);
           a[mi][1] = ldc(as + kk * LDS + mi * 16 + 8);
         }
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) b[ni] = cmul(ldc(bs + kk * LDS + ni * 8), d);
+        for (int ni = 0; ni < 2; ++ni) b[ni] = ldc(bs + kk * LDS + ni * 8);
 #pragma unroll
         for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
@@ -190,7 +182,7 @@ __global__ void __launch_bounds__(NT, 2) factor_level_kernel(LevelArgs a) {
   cplx* Ld = gsm + GEMM_SMEM / 16;          // NB x LDD, column-major
   cplx* dinv_s = Ld + NB * LDD;             // NB
   cplx* ysm = dinv_s + NB;                  // NB x MAXR
-  cplx* LDs = ysm + NB * MAXR;              // NB x LDD: d_c * L11[i][c]
+  cplx* cdg = ysm + NB * MAXR;              // NB: diagonal c_jj of the panel
 
   const int tid = threadIdx.x;
   const int inst = blockIdx.x;
@@ -279,45 +271,45 @@ __global__ void __launch_bounds__(NT, 2) factor_level_kernel(LevelArgs a) {
   }
   __syncthreads();
 
-  // ---- 2. pivot columns, panels of NB ----
+  // ---- 2. pivot columns, panels of NB: complex-symmetric Cholesky K = C C^T ----
+  // c_jj = sqrt(d_j) (principal branch), so no diagonal scaling ever enters the
+  // DMMA updates (the D-scaled operand used to compete with DMMA for the FP64 pipe)
   for (int kb = 0; kb < p; kb += NB) {
     const int w = min(NB, p - kb);
-    // load the diagonal block (lower incl. diagonal)
     for (int idx = tid; idx < w * w; idx += NT) {
       int i = idx % w, c = idx / w;
       if (i >= c) Ld[c * LDD + i] = ldc(P + (kb + i) + (int64_t)(kb + c) * n);
     }
     __syncthreads();
-    // LDL^T of the diagonal block: one barrier per column.  Phase j scales
-    // column j-1 and applies column j's rank-1 update with unscaled values.
+    // diagonal block: one barrier per column.  Phase j finalises column j-1
+    // (scale by 1/c, write c on the diagonal) and applies column j's rank-1
+    // update with unscaled values: a_ic -= a_ij a_cj / d_j.
     for (int j = 0; j <= w; ++j) {
-      if (j > 0 && tid < w && tid > j - 1) {
-        int jj = j - 1;
-        Ld[jj * LDD + tid] = cmul(Ld[jj * LDD + tid], dinv_s[jj]);
+      if (j > 0 && tid < w && tid >= j - 1) {
+        const int jj = j - 1;
+        Ld[jj * LDD + tid] = (tid == jj) ? cdg[jj] : cmul(Ld[jj * LDD + tid], dinv_s[jj]);
       }
       if (j < w) {
-        cplx d = Ld[j * LDD + j];
-        cplx dinv = crecip(d);
+        const cplx d = Ld[j * LDD + j];
+        const cplx dinv = crecip(d);
         if (tid == 0) {
           double m2 = cabs2(d);
           if (!(m2 > 1e-300) || !isfinite(m2)) atomicCAS(a.err, 0, (int)shift + 1);
-          dinv_s[j] = dinv;
+          const cplx c = csqrt_(d);
+          cdg[j] = c;
+          dinv_s[j] = crecip(c);
         }
         for (int idx = tid; idx < w * w; idx += NT) {
           int i = idx % w, c = idx / w;
-          if (c > j && i >= c) {
-            cplx lc = cmul(Ld[j * LDD + c], dinv);
-            Ld[c * LDD + i] = cfms(Ld[c * LDD + i], Ld[j * LDD + i], lc);
-          }
+          if (c > j && i >= c) Ld[c * LDD + i] = cfms(Ld[c * LDD + i], Ld[j * LDD + i], cmul(Ld[j * LDD + c], dinv));
         }
       }
       __syncthreads();
     }
-    // write back L11 and D; stage LDs[c][i] = d_c L11[i][c]; forward-solve the panel RHS
+    // write back C11; forward-solve the panel RHS: y = C11^{-1} r
     for (int idx = tid; idx < w * w; idx += NT) {
       int i = idx % w, c = idx / w;
       if (i >= c) stc(P + (kb + i) + (int64_t)(kb + c) * n, Ld[c * LDD + i]);
-      if (i > c) LDs[c * LDD + i] = cmul(Ld[c * LDD + c], Ld[c * LDD + i]);
     }
     if (tid < nrhs) {
       const int r = tid;
@@ -325,14 +317,14 @@ __global__ void __launch_bounds__(NT, 2) factor_level_kernel(LevelArgs a) {
       for (int j = 0; j < w; ++j) {
         cplx y = ldc(z + j);
         for (int c = 0; c < j; ++c) y = cfms(y, Ld[c * LDD + j], ysm[c * MAXR + r]);
+        y = cmul(y, dinv_s[j]);
         ysm[j * MAXR + r] = y;
         stc(z + j, y);
       }
     }
     __syncthreads();
     // TRSM rows below the diagonal block + fused RHS update (thread per row),
-    // 8 columns at a time in registers; earlier columns of the row are re-read
-    // (L1) as scaled l and applied through LDs[c][j] = d_c L11[j][c]
+    // 8 columns at a time in registers; earlier columns of the row are re-read (L1)
     for (int i = kb + w + tid; i < n; i += NT) {
       cplx* prow = P + i + (int64_t)kb * n;
       for (int jb = 0; jb < w; jb += 8) {
@@ -343,21 +335,17 @@ __global__ void __launch_bounds__(NT, 2) factor_level_kernel(LevelArgs a) {
           const cplx lc = ldc(prow + (int64_t)c * n);
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj)
-            if (jb + jj < w) y[jj] = cfms(y[jj], lc, LDs[c * LDD + jb + jj]);
+            if (jb + jj < w) y[jj] = cfms(y[jj], lc, Ld[c * LDD + jb + jj]);
         }
 #pragma unroll
-        for (int jj = 1; jj < 8; ++jj) {
+        for (int jj = 0; jj < 8; ++jj) {
           if (jb + jj < w) {
 #pragma unroll
             for (int cc = 0; cc < jj; ++cc) y[jj] = cfms(y[jj], y[cc], Ld[(jb + cc) * LDD + jb + jj]);
-          }
-        }
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj)
-          if (jb + jj < w) {
             y[jj] = cmul(y[jj], dinv_s[jb + jj]);
             stc(prow + (int64_t)(jb + jj) * n, y[jj]);
           }
+        }
         for (int r = 0; r < nrhs; ++r) {
           cplx* dst = (i < p) ? Zk + F.pbeg + i + (int64_t)r * nx : R + (i - p) + (int64_t)r * b;
           cplx acc = ldc(dst);
@@ -373,22 +361,15 @@ __global__ void __launch_bounds__(NT, 2) factor_level_kernel(LevelArgs a) {
     const int base = kb + w;
     if (base < p)
       gemm_update(P + base + (int64_t)base * n, n, n - base, p - base, P + base + (int64_t)kb * n, n,
-                  P + base + (int64_t)kb * n, n, P + kb + (int64_t)kb * n, n + 1, w, true, gsm);
-  }
-  // z = D^{-1} y for this front's pivots
-  for (int i = tid; i < p * nrhs; i += NT) {
-    int r = i / p, j = i % p;
-    cplx* z = Zk + F.pbeg + j + (int64_t)r * nx;
-    stc(z, cdiv(ldc(z), ldc(P + j + (int64_t)j * n)));
+                  P + base + (int64_t)kb * n, n, w, true, gsm);
   }
   // ---- 3. Schur update of the boundary block ----
-  if (b > 0)
-    gemm_update(U, b, b, b, P + p, n, P + p, n, P, n + 1, p, true, gsm);
+  if (b > 0) gemm_update(U, b, b, b, P + p, n, P + p, n, p, true, gsm);
 }
 
-__global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a) {
+__global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int unit) {
   __shared__ cplx ts[NB * MAXR];
-  __shared__ cplx l11[NB * LDD];   // l11[c * LDD + i] = L[kb+i][kb+c], i > c
+  __shared__ cplx l11[NB * LDD];   // l11[c * LDD + i] = L[kb+i][kb+c], i > c; diagonal: 1/L[c][c] (or 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int inst = blockIdx.x;
   const int k = inst % a.nbatch;
@@ -432,10 +413,12 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a) {
       }
     }
     __syncthreads();
-    // stage the diagonal block, then the transposed unit triangle (thread per rhs)
+    // stage the diagonal block, then the transposed triangle (thread per rhs);
+    // unit = LDL^T fronts (unit L, z already D^{-1}-scaled), else C C^T fronts
     for (int idx = tid; idx < w * w; idx += NT) {
       const int i = idx % w, c = idx / w;
       if (i > c) l11[c * LDD + i] = ldc(P + (kb + i) + (int64_t)(kb + c) * n);
+      else if (i == c) l11[c * LDD + c] = unit ? cmk(1.0, 0.0) : crecip(ldc(P + (kb + c) + (int64_t)(kb + c) * n));
     }
     __syncthreads();
     if (tid < nrhs) {
@@ -443,6 +426,7 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a) {
       for (int j = w - 1; j >= 0; --j) {
         cplx x = ts[j * MAXR + r];
         for (int c = j + 1; c < w; ++c) x = cfms(x, l11[j * LDD + c], ts[c * MAXR + r]);
+        x = cmul(x, l11[j * LDD + j]);
         ts[j * MAXR + r] = x;
         stc(Zk + F.pbeg + kb + j + (int64_t)r * nx, x);
         a.W[bv_off(a.lay, r, shift, a.perm[F.pbeg + kb + j])] = x;
@@ -543,10 +527,14 @@ int auto_batch(Plan& P, int nshift, int nrhs) {
   if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = (size_t)8 << 30;
   // keep whatever workspace we already own in the budget
   size_t owned = P.d_factor ? (size_t)bytes_per_shift(P, P.ws_nrhs) * P.ws_batch : 0;
-  double budget = 0.45 * (double)(fr + owned);
+  // 70% of what is free leaves room for the caller's temporaries (residual checks)
+  const double frac = getenv("STFEM_WS_FRACTION") ? atof(getenv("STFEM_WS_FRACTION")) : 0.70;
+  double budget = frac * (double)(fr + owned);
   int64_t per = bytes_per_shift(P, nrhs);
-  int64_t b = std::max<int64_t>(1, (int64_t)(budget / (double)per));
-  return (int)std::min<int64_t>(std::min<int64_t>(b, 4096), nshift);
+  int64_t bmax = std::min<int64_t>(std::max<int64_t>(1, (int64_t)(budget / (double)per)), 4096);
+  // equal-sized batches: fewer, evenly filled waves at the top levels of the tree
+  const int64_t nb = (nshift + bmax - 1) / bmax;
+  return (int)((nshift + nb - 1) / nb);
 }
 
 }  // namespace
@@ -673,10 +661,12 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
       a.nlist = (int32_t)P.levels[d].size();
       const int nmax = P.level_nmax[d], pmax = P.level_pmax[d];
       const int bsm = small_bwd_smem_bytes(nmax, pmax, small_nr(nrhs));
-      if (nmax <= SMALL_N && bsm <= 200 * 1024 && !P.force_big) {
+      // factor format of this level: small-front kernel = unit-L LDL^T, large = C C^T
+      const bool ldlt = nmax <= SMALL_N && !P.force_big;
+      if (ldlt && bsm <= 200 * 1024) {
         if ((rc = launch_small_backward_any(a, a.nlist * nb, nmax, pmax, stream))) return rc;
       } else {
-        backward_level_kernel<<<a.nlist * nb, NT, 0, stream>>>(a);
+        backward_level_kernel<<<a.nlist * nb, NT, 0, stream>>>(a, ldlt ? 1 : 0);
         STFEM_LAUNCH_CHECK("backward_level_kernel");
       }
       mark();
