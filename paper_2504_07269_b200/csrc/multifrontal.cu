@@ -65,6 +65,7 @@ struct LevelArgs {
   stfem_bv_layout lay;
   int32_t shift0;
   int* err;
+  unsigned long long* prof;   // optional per-phase cycle counters (STFEM_PHASE_PROF)
 };
 
 __device__ __forceinline__ int64_t bv_off(const stfem_bv_layout& L, int r, int64_t shift, int64_t j) {
@@ -176,7 +177,17 @@ __device__ void gemm_update(cplx* __restrict__ C, int ldC, int M, int N, const c
   __syncthreads();
 }
 
+#define STFEM_PROF_MARK(slot)                                                            \
+  do {                                                                                   \
+    if (a.prof && threadIdx.x == 0) {                                                    \
+      const long long t_now = clock64();                                                 \
+      atomicAdd(a.prof + (slot), (unsigned long long)(t_now - t_prev));                  \
+      t_prev = t_now;                                                                    \
+    }                                                                                    \
+  } while (0)
+
 __global__ void __launch_bounds__(NT, 2) factor_level_kernel(LevelArgs a) {
+  long long t_prev = clock64();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* gsm = reinterpret_cast<cplx*>(smem_raw);
   cplx* Ld = gsm + GEMM_SMEM / 16;          // NB x LDD, column-major
@@ -271,6 +282,7 @@ __global__ void __launch_bounds__(NT, 2) factor_level_kernel(LevelArgs a) {
   }
   __syncthreads();
 
+  STFEM_PROF_MARK(0);
   // ---- 2. pivot columns, panels of NB: complex-symmetric Cholesky K = C C^T ----
   // c_jj = sqrt(d_j) (principal branch), so no diagonal scaling ever enters the
   // DMMA updates (the D-scaled operand used to compete with DMMA for the FP64 pipe)
@@ -281,48 +293,77 @@ __global__ void __launch_bounds__(NT, 2) factor_level_kernel(LevelArgs a) {
       if (i >= c) Ld[c * LDD + i] = ldc(P + (kb + i) + (int64_t)(kb + c) * n);
     }
     __syncthreads();
-    // diagonal block: one barrier per column.  Phase j finalises column j-1
-    // (scale by 1/c, write c on the diagonal) and applies column j's rank-1
-    // update with unscaled values: a_ic -= a_ij a_cj / d_j.
-    for (int j = 0; j <= w; ++j) {
-      if (j > 0 && tid < w && tid >= j - 1) {
-        const int jj = j - 1;
-        Ld[jj * LDD + tid] = (tid == jj) ? cdg[jj] : cmul(Ld[jj * LDD + tid], dinv_s[jj]);
-      }
-      if (j < w) {
+    // diagonal block by warp 0 alone (lane = row, warp-synchronous): step j
+    // applies column j's rank-1 update with unscaled values,
+    // a_ic -= (a_ij / d_j) a_cj, then all columns are scaled by 1/c_j = d_j^{-1/2}.
+    if ((tid >> 5) == 0) {
+      const int lane = tid & 31;
+      for (int j = 0; j < w; ++j) {
         const cplx d = Ld[j * LDD + j];
-        const cplx dinv = crecip(d);
-        if (tid == 0) {
-          double m2 = cabs2(d);
-          if (!(m2 > 1e-300) || !isfinite(m2)) atomicCAS(a.err, 0, (int)shift + 1);
-          const cplx c = csqrt_(d);
-          cdg[j] = c;
-          dinv_s[j] = crecip(c);
+        if (lane > j && lane < w) {
+          // row `lane`, columns c in (j, lane]: 4 independent RMWs in flight
+          const cplx f = cmul(Ld[j * LDD + lane], crecip_fast(d));
+          cplx* __restrict__ rowp = Ld + lane;             // (lane, c) at rowp[c * LDD]
+          const cplx* __restrict__ colj = Ld + j * LDD;    // (c, j)    at colj[c]
+          int c = j + 1;
+          for (; c + 3 <= lane; c += 4) {
+            const cplx x0 = rowp[c * LDD], x1 = rowp[(c + 1) * LDD], x2 = rowp[(c + 2) * LDD],
+                       x3 = rowp[(c + 3) * LDD];
+            const cplx y0 = colj[c], y1 = colj[c + 1], y2 = colj[c + 2], y3 = colj[c + 3];
+            rowp[c * LDD] = cfms(x0, f, y0);
+            rowp[(c + 1) * LDD] = cfms(x1, f, y1);
+            rowp[(c + 2) * LDD] = cfms(x2, f, y2);
+            rowp[(c + 3) * LDD] = cfms(x3, f, y3);
+          }
+          for (; c <= lane; ++c) rowp[c * LDD] = cfms(rowp[c * LDD], f, colj[c]);
         }
-        for (int idx = tid; idx < w * w; idx += NT) {
-          int i = idx % w, c = idx / w;
-          if (c > j && i >= c) Ld[c * LDD + i] = cfms(Ld[c * LDD + i], Ld[j * LDD + i], cmul(Ld[j * LDD + c], dinv));
-        }
+        __syncwarp();
       }
-      __syncthreads();
+      // off the critical path: pivots d_j -> c_j = sqrt(d_j), 1/c_j (lane j), checks
+      if (lane < w) {
+        const cplx d = Ld[lane * LDD + lane];
+        const double m2 = cabs2(d);
+        if (!(m2 > 1e-300) || !isfinite(m2)) atomicCAS(a.err, 0, (int)shift + 1);
+        const cplx c = csqrt_(d);
+        cdg[lane] = c;
+        dinv_s[lane] = crecip(c);
+      }
+      __syncwarp();
+      for (int j = 0; j < w; ++j) {
+        if (lane == j) Ld[j * LDD + j] = cdg[j];
+        else if (lane > j && lane < w) Ld[j * LDD + lane] = cmul(Ld[j * LDD + lane], dinv_s[j]);
+      }
     }
+    __syncthreads();
+    STFEM_PROF_MARK(1);
     // write back C11; forward-solve the panel RHS: y = C11^{-1} r
     for (int idx = tid; idx < w * w; idx += NT) {
       int i = idx % w, c = idx / w;
       if (i >= c) stc(P + (kb + i) + (int64_t)(kb + c) * n, Ld[c * LDD + i]);
     }
-    if (tid < nrhs) {
-      const int r = tid;
-      cplx* z = Zk + F.pbeg + kb + (int64_t)r * nx;
-      for (int j = 0; j < w; ++j) {
-        cplx y = ldc(z + j);
-        for (int c = 0; c < j; ++c) y = cfms(y, Ld[c * LDD + j], ysm[c * MAXR + r]);
-        y = cmul(y, dinv_s[j]);
-        ysm[j * MAXR + r] = y;
-        stc(z + j, y);
+    if ((tid >> 5) == 0) {
+      // warp 0: y = C11^{-1} r with lane c holding y_c; each step is a warp reduction
+      const int lane = tid & 31;
+      for (int r = 0; r < nrhs; ++r) {
+        cplx* z = Zk + F.pbeg + kb + (int64_t)r * nx;
+        cplx yl = lane < w ? ldc(z + lane) : zero;
+        for (int j = 0; j < w; ++j) {
+          cplx s = lane < j ? cmul(Ld[lane * LDD + j], yl) : zero;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            s.re += __shfl_xor_sync(0xffffffffu, s.re, o);
+            s.im += __shfl_xor_sync(0xffffffffu, s.im, o);
+          }
+          if (lane == j) yl = cmul(csub(yl, s), dinv_s[j]);
+        }
+        if (lane < w) {
+          ysm[lane * MAXR + r] = yl;
+          stc(z + lane, yl);
+        }
       }
     }
     __syncthreads();
+    STFEM_PROF_MARK(2);
     // TRSM rows below the diagonal block + fused RHS update (thread per row),
     // 8 columns at a time in registers; earlier columns of the row are re-read (L1)
     for (int i = kb + w + tid; i < n; i += NT) {
@@ -357,14 +398,17 @@ __global__ void __launch_bounds__(NT, 2) factor_level_kernel(LevelArgs a) {
       }
     }
     __syncthreads();
+    STFEM_PROF_MARK(3);
     // trailing pivot-column update (lower part), K = w
     const int base = kb + w;
     if (base < p)
       gemm_update(P + base + (int64_t)base * n, n, n - base, p - base, P + base + (int64_t)kb * n, n,
                   P + base + (int64_t)kb * n, n, w, true, gsm);
+    STFEM_PROF_MARK(4);
   }
   // ---- 3. Schur update of the boundary block ----
   if (b > 0) gemm_update(U, b, b, b, P + p, n, P + p, n, p, true, gsm);
+  STFEM_PROF_MARK(5);
 }
 
 __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int unit) {
@@ -618,6 +662,13 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
   a.W = W;
   a.lay = lay;
   a.err = P.d_err;
+  static const bool phase_prof = getenv("STFEM_PHASE_PROF") != nullptr;
+  static unsigned long long* d_prof = nullptr;
+  if (phase_prof) {
+    if (!d_prof) STFEM_CUDA_TRY(cudaMalloc(&d_prof, 8 * sizeof(unsigned long long)));
+    STFEM_CUDA_TRY(cudaMemsetAsync(d_prof, 0, 8 * sizeof(unsigned long long), stream));
+  }
+  a.prof = phase_prof ? d_prof : nullptr;
   // STFEM_LEVEL_TIMING=1: per-launch CUDA-event times to stderr (diagnostics only)
   static const bool level_print = getenv("STFEM_LEVEL_TIMING") != nullptr;
   const bool level_timing = level_print || P.record_levels;
@@ -690,6 +741,16 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
                 j < L ? "factor" : "backward", d, ms);
     }
     for (auto e : evs) cudaEventDestroy(e);
+  }
+  if (phase_prof) {
+    unsigned long long h[8];
+    cudaMemcpyAsync(h, d_prof, sizeof(h), cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    const char* names[6] = {"assembly", "diag", "writeback+fwd", "trsm", "panel_gemm", "syrk"};
+    double tot = 0;
+    for (int i = 0; i < 6; ++i) tot += (double)h[i];
+    for (int i = 0; i < 6; ++i)
+      fprintf(stderr, "[stfem phase] %-14s %5.1f%%  (%.3e cycles)\n", names[i], 100.0 * h[i] / tot, (double)h[i]);
   }
   int h_err = 0;
   STFEM_CUDA_TRY(cudaMemcpyAsync(&h_err, P.d_err, sizeof(int), cudaMemcpyDeviceToHost, stream));

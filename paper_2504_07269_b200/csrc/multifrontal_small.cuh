@@ -33,9 +33,11 @@ __device__ __forceinline__ cplx shfl_c(cplx v, int src) {
   return cmk(__shfl_sync(0xffffffffu, v.re, src), __shfl_sync(0xffffffffu, v.im, src));
 }
 
-// trailing update of row i: F[i][c] -= sum_jj av[jj] * PB[c][jj] for c in [c0, i]
-__device__ __forceinline__ void trailing_row(cplx* __restrict__ F, const cplx* __restrict__ PB, const cplx (&av)[KB],
-                                             int i, int c0, int n) {
+// trailing update of row i: F[i][c] -= sum_{jj<W} av[jj] * PB[c][jj] for c in [c0, i]
+// (W = panel width, compile-time: narrow last panels do no padded work)
+template <int W>
+__device__ __forceinline__ void trailing_row_w(cplx* __restrict__ F, const cplx* __restrict__ PB,
+                                               const cplx (&av)[KB], int i, int c0, int n) {
   int c = c0;
   int q = pk(i, c, n);
   const cplx* __restrict__ pb = PB + c * KB;
@@ -44,7 +46,7 @@ __device__ __forceinline__ void trailing_row(cplx* __restrict__ F, const cplx* _
     const int q1 = q + (n - c - 1);
     cplx x0 = F[q], x1 = F[q1];
 #pragma unroll
-    for (int jj = 0; jj < KB; ++jj) {
+    for (int jj = 0; jj < W; ++jj) {
       x0 = cfms(x0, av[jj], pb[jj]);
       x1 = cfms(x1, av[jj], pb[KB + jj]);
     }
@@ -56,8 +58,22 @@ __device__ __forceinline__ void trailing_row(cplx* __restrict__ F, const cplx* _
   if (c <= i) {
     cplx x0 = F[q];
 #pragma unroll
-    for (int jj = 0; jj < KB; ++jj) x0 = cfms(x0, av[jj], pb[jj]);
+    for (int jj = 0; jj < W; ++jj) x0 = cfms(x0, av[jj], pb[jj]);
     F[q] = x0;
+  }
+}
+
+__device__ __forceinline__ void trailing_row(cplx* F, const cplx* PB, const cplx (&av)[KB], int i, int c0,
+                                             int n, int w) {
+  switch (w) {
+    case 8: trailing_row_w<8>(F, PB, av, i, c0, n); break;
+    case 7: trailing_row_w<7>(F, PB, av, i, c0, n); break;
+    case 6: trailing_row_w<6>(F, PB, av, i, c0, n); break;
+    case 5: trailing_row_w<5>(F, PB, av, i, c0, n); break;
+    case 4: trailing_row_w<4>(F, PB, av, i, c0, n); break;
+    case 3: trailing_row_w<3>(F, PB, av, i, c0, n); break;
+    case 2: trailing_row_w<2>(F, PB, av, i, c0, n); break;
+    default: trailing_row_w<1>(F, PB, av, i, c0, n); break;
   }
 }
 
@@ -244,7 +260,7 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
       }
     }
     __syncthreads();
-    if (i >= kb + w && i < n) trailing_row(F, PB, av, i, kb + w, n);
+    if (i >= kb + w && i < n) trailing_row(F, PB, av, i, kb + w, n, w);
     __syncthreads();
   }
 
