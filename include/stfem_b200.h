@@ -160,6 +160,14 @@ int stfem_csr_spmv_c(const stfem_asm* a, const double* vals, const void* v,
  * banded M_t / B_t (P1 time: bw = 1; P2 time: bw = 2) given as device arrays
  * nt x (2 bw + 1), band[l][k - l + bw].  v/out: (nt, n_x) c128 row-major;
  * work: device scratch of 2 * nt * n_x c128. */
+/* K8 spacetime_errors: (||psi - psi_h||_{L2(Q)},
+ * |psi - psi_h|_{H1(Q)}) into host out2[2] for P1 x P1 coefficients
+ * (N x n_x c128 at coeffs + l*ld, device) against a built-in exact solution
+ * (kind as in stfem_asm_rhs), psi_h = sum coeff phi_j phi_l + psi0 (psi0:
+ * device nv c128 nodal values or NULL).  7-point x 5-point quadrature per
+ * prism, deterministic reduction. */
+int stfem_spacetime_errors(const stfem_asm* a, int32_t kind, const double* breakpoints, int32_t N,
+                           const void* coeffs, int64_t ld, const void* psi0, double* out2, void* stream);
 int stfem_apply_global(const stfem_asm* a, const double* Mvals, const double* Avals,
                        const double* Mt_band, const double* Bt_band, int32_t bw, int32_t nt,
                        const void* v, void* out, void* work, void* stream);

@@ -287,6 +287,128 @@ __global__ void combine_kernel(int nt, int nx, int bw, const double* __restrict_
   stc(out + gid, cmk(re, im));
 }
 
+// ---- K8: space-time error norms ---------------------------
+// psi, d_t psi, grad_x psi of the built-in manufactured solutions
+__device__ void exact_fn(int kind, double x, double y, double t, cplx& psi, cplx& dt, cplx& gx, cplx& gy) {
+  const double PI = 3.141592653589793;
+  const double sx = sin(PI * x), sy = sin(PI * y), cx = cos(PI * x), cy = cos(PI * y);
+  const double s = sx * sy, dsx = PI * cx * sy, dsy = PI * sx * cy;
+  if (kind == 1) {  // s sin(pi t)
+    const double st = sin(PI * t), ct = cos(PI * t);
+    psi = cmk(s * st, 0);
+    dt = cmk(s * PI * ct, 0);
+    gx = cmk(dsx * st, 0);
+    gy = cmk(dsy * st, 0);
+  } else if (kind == 2) {  // s t e^{-it}
+    const cplx e = cmk(cos(t), -sin(t));
+    psi = cmul(cmk(s * t, 0), e);
+    dt = cmul(cmk(s, -s * t), e);  // s e^{-it} (1 - i t)
+    gx = cmul(cmk(dsx * t, 0), e);
+    gy = cmul(cmk(dsy * t, 0), e);
+  } else {  // e^{it} s sin(t x y)
+    const cplx e = cmk(cos(t), sin(t));
+    const double q = sin(t * x * y), cq = cos(t * x * y);
+    psi = cmul(cmk(s * q, 0), e);
+    dt = cmul(cmk(s * x * y * cq, s * q), e);  // e^{it} s (i q + x y cq)
+    gx = cmul(cmk(dsx * q + s * cq * t * y, 0), e);
+    gy = cmul(cmk(dsy * q + s * cq * t * x, 0), e);
+  }
+}
+
+// one thread per (triangle, time interval); 7-point x 5-point quadrature;
+// deterministic two-level reduction (block tree, then a fixed-order pass)
+__global__ void __launch_bounds__(256) errors_kernel(int kind, const double* __restrict__ V,
+                                                     const int32_t* __restrict__ E, const int32_t* __restrict__ dof,
+                                                     int ne, const double* __restrict__ bp, int N,
+                                                     const cplx* __restrict__ C, int64_t ld,
+                                                     const cplx* __restrict__ psi0, double* partial) {
+  __shared__ double s1[256], s2[256];
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double l2 = 0, h1 = 0;
+  if (gid < (int64_t)ne * N) {
+    const int e = (int)(gid % ne), k = (int)(gid / ne);
+    const int32_t* el = E + (int64_t)e * 3;
+    double px[3], py[3];
+    cplx u0[3], u1[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      px[a] = V[2 * el[a]];
+      py[a] = V[2 * el[a] + 1];
+      const int j = dof[el[a]];
+      const cplx p0 = psi0 ? psi0[el[a]] : cmk(0, 0);
+      u0[a] = (k > 0 && j >= 0) ? cadd(C[(int64_t)(k - 1) * ld + j], p0) : p0;
+      u1[a] = (j >= 0) ? cadd(C[(int64_t)k * ld + j], p0) : p0;
+    }
+    const double area = 0.5 * ((px[1] - px[0]) * (py[2] - py[0]) - (px[2] - px[0]) * (py[1] - py[0]));
+    const double bx[3] = {py[1] - py[2], py[2] - py[0], py[0] - py[1]};
+    const double cy[3] = {px[2] - px[1], px[0] - px[2], px[1] - px[0]};
+    const double t0 = bp[k], ht = bp[k + 1] - bp[k];
+    for (int g = 0; g < 5; ++g) {
+      const double s = c_gl_x[g], t = t0 + ht * s;
+      cplx ut[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        ut[a] = cmk((1 - s) * u0[a].re + s * u1[a].re, (1 - s) * u0[a].im + s * u1[a].im);
+      cplx gxh = cmk(0, 0), gyh = cmk(0, 0), dth[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        gxh = cadd(gxh, cmk(ut[a].re * bx[a] / (2 * area), ut[a].im * bx[a] / (2 * area)));
+        gyh = cadd(gyh, cmk(ut[a].re * cy[a] / (2 * area), ut[a].im * cy[a] / (2 * area)));
+        dth[a] = cmk((u1[a].re - u0[a].re) / ht, (u1[a].im - u0[a].im) / ht);
+      }
+      for (int q = 0; q < 7; ++q) {
+        const double l1 = c_tri_a[q], l2q = c_tri_b[q], l0 = 1 - l1 - l2q;
+        const double x = l0 * px[0] + l1 * px[1] + l2q * px[2], y = l0 * py[0] + l1 * py[1] + l2q * py[2];
+        cplx ps, dt, gx, gy;
+        exact_fn(kind, x, y, t, ps, dt, gx, gy);
+        const cplx uh = cmk(l0 * ut[0].re + l1 * ut[1].re + l2q * ut[2].re, l0 * ut[0].im + l1 * ut[1].im + l2q * ut[2].im);
+        const cplx duh = cmk(l0 * dth[0].re + l1 * dth[1].re + l2q * dth[2].re,
+                             l0 * dth[0].im + l1 * dth[1].im + l2q * dth[2].im);
+        const double w = 2 * area * c_tri_w[q] * ht * c_gl_w[g];
+        l2 += w * cabs2(csub(ps, uh));
+        h1 += w * (cabs2(csub(dt, duh)) + cabs2(csub(gx, gxh)) + cabs2(csub(gy, gyh)));
+      }
+    }
+  }
+  s1[threadIdx.x] = l2;
+  s2[threadIdx.x] = h1;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      s1[threadIdx.x] += s1[threadIdx.x + o];
+      s2[threadIdx.x] += s2[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    partial[2 * blockIdx.x] = s1[0];
+    partial[2 * blockIdx.x + 1] = s2[0];
+  }
+}
+
+__global__ void sum_partials_kernel(const double* partial, int nb, double* out) {
+  __shared__ double s1[256], s2[256];
+  double a = 0, b = 0;
+  for (int i = threadIdx.x; i < nb; i += 256) {
+    a += partial[2 * i];
+    b += partial[2 * i + 1];
+  }
+  s1[threadIdx.x] = a;
+  s2[threadIdx.x] = b;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      s1[threadIdx.x] += s1[threadIdx.x + o];
+      s2[threadIdx.x] += s2[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = s1[0];
+    out[1] = s2[0];
+  }
+}
+
 int upload(Asm& A) {
   int dev;
   STFEM_CUDA_TRY(cudaGetDevice(&dev));
@@ -522,5 +644,36 @@ extern "C" int stfem_apply_global(const stfem_asm* a, const double* Mvals, const
   stfem::combine_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       nt, nx, bw, Mt_band, Bt_band, MV, AV, (stfem::cplx*)out);
   STFEM_LAUNCH_CHECK("combine_kernel");
+  return STFEM_OK;
+}
+
+extern "C" int stfem_spacetime_errors(const stfem_asm* a, int32_t kind, const double* breakpoints, int32_t N,
+                                      const void* coeffs, int64_t ld, const void* psi0, double* out2,
+                                      void* stream) {
+  if (!a || !breakpoints || !coeffs || !out2) return stfem::fail(STFEM_ERR_ARG, "spacetime_errors: null");
+  Asm& A = *reinterpret_cast<Asm*>(const_cast<stfem_asm*>(a));
+  if (A.degree != 1) return stfem::fail(STFEM_ERR_ARG, "spacetime_errors: P1 space only");
+  if (kind < 1 || kind > 3) return stfem::fail(STFEM_ERR_ARG, "spacetime_errors: unknown exact solution");
+  if (N < 1 || ld < A.n) return stfem::fail(STFEM_ERR_DIM, "spacetime_errors: bad N / ld");
+  int rc;
+  if ((rc = stfem::upload(A))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t tot = (int64_t)A.ne * N;
+  const int nb = (int)((tot + 255) / 256);
+  double *d_bp = nullptr, *d_part = nullptr;
+  STFEM_CUDA_TRY(cudaMallocAsync((void**)&d_bp, (N + 1) * 8, s));
+  STFEM_CUDA_TRY(cudaMallocAsync((void**)&d_part, (2 * (size_t)nb + 2) * 8, s));
+  STFEM_CUDA_TRY(cudaMemcpyAsync(d_bp, breakpoints, (N + 1) * 8, cudaMemcpyHostToDevice, s));
+  stfem::errors_kernel<<<nb, 256, 0, s>>>(kind, A.d_verts, A.d_elems, A.d_dof, A.ne, d_bp, N,
+                                          (const stfem::cplx*)coeffs, ld, (const stfem::cplx*)psi0, d_part);
+  STFEM_LAUNCH_CHECK("errors_kernel");
+  stfem::sum_partials_kernel<<<1, 256, 0, s>>>(d_part, nb, d_part + 2 * (size_t)nb);
+  STFEM_LAUNCH_CHECK("sum_partials_kernel");
+  STFEM_CUDA_TRY(cudaMemcpyAsync(out2, d_part + 2 * (size_t)nb, 2 * 8, cudaMemcpyDeviceToHost, s));
+  STFEM_CUDA_TRY(cudaFreeAsync(d_bp, s));
+  STFEM_CUDA_TRY(cudaFreeAsync(d_part, s));
+  STFEM_CUDA_TRY(cudaStreamSynchronize(s));
+  out2[0] = sqrt(out2[0]);
+  out2[1] = sqrt(out2[1]);
   return STFEM_OK;
 }

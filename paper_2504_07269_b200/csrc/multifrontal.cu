@@ -4,16 +4,19 @@
 //
 // One symbolic tree (plan) is shared by every shift, so a depth level of the
 // tree times a batch of shifts is a set of independent, identically-shaped
-// dense front problems.  One CTA owns one (front, shift) instance per level:
-//   1. assemble: zero the factor block (n x p) and update block (b x b),
-//      scatter the original entries M + lam*A, extend-add the children's
-//      update blocks and forward-RHS vectors (children in fixed order ->
-//      deterministic, no atomics);
-//   2. factor the p pivot columns, right-looking in panels of NB=32:
-//      diagonal block LDL^T in shared memory, row-parallel TRSM for the rows
-//      below (the forward substitution of the RHS is fused here as extra
-//      columns), trailing pivot-column update on the FP64 tensor pipe (DMMA);
-//   3. Schur update U = F22 - L21 D L21^T (lower tiles, K = p, DMMA).
+// dense front problems.  One CTA owns one (front, shift) instance per level.
+// Fronts of order <= SMALL_N take the shared-memory path of
+// multifrontal_small.cuh (unit-L LDL^T).  Larger fronts (this file) live in
+// HBM/L2 and use the complex-symmetric Cholesky form K = C C^T, c_jj = d_j^{1/2}:
+//   1. assemble by gathering: every front entry is written once as the sum of
+//      at most two children's update entries (inverse relpos maps in shared
+//      memory), then the original entries M + lam*A are added (deterministic,
+//      no atomics, no zero fill);
+//   2. factor the p pivot columns, right-looking in panels of NB=32: diagonal
+//      block by one warp in shared memory, row-parallel TRSM (8-column register
+//      blocks) for the rows below with the forward substitution of the RHS
+//      fused in, trailing pivot-column update on the FP64 tensor pipe (DMMA);
+//   3. Schur update U = F22 - L21 L21^T (lower tiles, K = p, DMMA).
 // Backward substitution walks the levels root-first; each instance gathers
 // x_B of its boundary rows (already final), applies L21^T and the transposed
 // triangle, and writes x both to the permuted work vector and (un-permuted)
@@ -665,8 +668,8 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
   static const bool phase_prof = getenv("STFEM_PHASE_PROF") != nullptr;
   static unsigned long long* d_prof = nullptr;
   if (phase_prof) {
-    if (!d_prof) STFEM_CUDA_TRY(cudaMalloc(&d_prof, 8 * sizeof(unsigned long long)));
-    STFEM_CUDA_TRY(cudaMemsetAsync(d_prof, 0, 8 * sizeof(unsigned long long), stream));
+    if (!d_prof) STFEM_CUDA_TRY(cudaMalloc(&d_prof, 16 * sizeof(unsigned long long)));
+    STFEM_CUDA_TRY(cudaMemsetAsync(d_prof, 0, 16 * sizeof(unsigned long long), stream));
   }
   a.prof = phase_prof ? d_prof : nullptr;
   // STFEM_LEVEL_TIMING=1: per-launch CUDA-event times to stderr (diagnostics only)
@@ -743,14 +746,18 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
     for (auto e : evs) cudaEventDestroy(e);
   }
   if (phase_prof) {
-    unsigned long long h[8];
+    unsigned long long h[16];
     cudaMemcpyAsync(h, d_prof, sizeof(h), cudaMemcpyDeviceToHost, stream);
     cudaStreamSynchronize(stream);
-    const char* names[6] = {"assembly", "diag", "writeback+fwd", "trsm", "panel_gemm", "syrk"};
-    double tot = 0;
-    for (int i = 0; i < 6; ++i) tot += (double)h[i];
-    for (int i = 0; i < 6; ++i)
-      fprintf(stderr, "[stfem phase] %-14s %5.1f%%  (%.3e cycles)\n", names[i], 100.0 * h[i] / tot, (double)h[i]);
+    const char* names[12] = {"assembly", "diag", "writeback+fwd", "trsm", "panel_gemm", "syrk", "", "",
+                             "small:gather", "small:diag+trsm", "small:trailing", "small:writeout"};
+    for (int grp = 0; grp < 2; ++grp) {
+      double tot = 0;
+      for (int i = 8 * grp; i < 8 * grp + 6; ++i) tot += (double)h[i];
+      for (int i = 8 * grp; i < 8 * grp + 6; ++i)
+        if (names[i][0])
+          fprintf(stderr, "[stfem phase] %-16s %5.1f%%  (%.3e cycles)\n", names[i], 100.0 * h[i] / tot, (double)h[i]);
+    }
   }
   int h_err = 0;
   STFEM_CUDA_TRY(cudaMemcpyAsync(&h_err, P.d_err, sizeof(int), cudaMemcpyDeviceToHost, stream));

@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
   const int n = Fr.n, p = Fr.p, b = n - p;
   const cplx lam = a.lam[k];
   const int64_t shift = a.shift0 + k;
+  long long t_prev = clock64();
 
   // ---- gather ----
   const int tri = (n * (n + 1)) / 2;
@@ -161,6 +162,7 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
     }
     __syncthreads();
   }
+  STFEM_PROF_MARK(8);
   cplx rv[NR];
 #pragma unroll
   for (int r = 0; r < NR; ++r) rv[r] = i < n ? Rsm[i * NR + r] : zero;
@@ -260,8 +262,10 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
       }
     }
     __syncthreads();
+    STFEM_PROF_MARK(9);
     if (i >= kb + w && i < n) trailing_row(F, PB, av, i, kb + w, n, w);
     __syncthreads();
+    STFEM_PROF_MARK(10);
   }
 
   // ---- write out: L/D (n x p), U (b x b), z = D^{-1} y, forward RHS update ----
@@ -293,6 +297,7 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
     }
   }
   __syncthreads();   // shared memory is reused by the next instance
+  STFEM_PROF_MARK(11);
   }
 }
 

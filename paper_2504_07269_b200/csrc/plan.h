@@ -14,8 +14,10 @@ namespace stfem {
 
 // One front (supernode) of the multifrontal elimination tree.  Front order
 // n = p (pivots, contiguous in the new numbering from pbeg) + b (boundary rows,
-// all belonging to ancestors).  Factor block: n x p column-major (ld n) holding
-// D on the diagonal and unit-lower L below it.  Update block: b x b column-major.
+// all belonging to ancestors).  Factor block: n x p column-major (ld n): for
+// small fronts (shared-memory kernel) D on the diagonal and unit-lower L below;
+// for large fronts the complex-symmetric Cholesky factor C (K = C C^T).
+// Update block: b x b column-major (lower triangle used).
 struct FrontDev {
   int32_t pbeg, p, n, nchild;
   int32_t child_beg;   // into child_ids

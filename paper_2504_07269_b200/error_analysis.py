@@ -55,6 +55,33 @@ def exact_solution(name: str):
     raise KeyError(name)
 
 
+def spacetime_errors_device(ops, mesh_t: TemporalMesh, coeffs, exact_name: str, psi0_nodal=None):
+    """K8 on the GPU (§8(f) rank 1): same quadrature as `spacetime_errors`,
+    for coefficients resident in HBM ((n_t, n_x) complex128 CUDA tensor)
+    against one of the built-in manufactured solutions ('sinpit', 'texp',
+    'paper').  psi0_nodal: (nv,) complex nodal values or None."""
+    import ctypes as C
+
+    import torch
+
+    from . import _native as N
+    from .fem_assembly import SOURCE_KINDS
+    N.require_cuda(coeffs)
+    if coeffs.dtype != torch.complex128 or coeffs.dim() != 2 or coeffs.stride(1) != 1:
+        raise TypeError("coeffs must be a (n_t, n_x) complex128 tensor with unit column stride")
+    bp = np.ascontiguousarray(mesh_t.breakpoints, dtype=np.float64)
+    if coeffs.shape != (len(bp) - 1, ops.n):
+        raise N.DimensionMismatch(N.ERR_DIM, f"coeffs {tuple(coeffs.shape)} vs ({len(bp) - 1}, {ops.n})")
+    p0 = None
+    if psi0_nodal is not None:
+        p0 = torch.as_tensor(np.ascontiguousarray(psi0_nodal, dtype=np.complex128), device=coeffs.device)
+    out = np.zeros(2)
+    N.check(N.lib().stfem_spacetime_errors(ops.handle, SOURCE_KINDS[exact_name], bp.ctypes.data, len(bp) - 1,
+                                           N.ptr(coeffs), coeffs.stride(0), N.ptr(p0), out.ctypes.data,
+                                           N.stream_ptr()))
+    return float(out[0]), float(out[1])
+
+
 def spacetime_errors(coeffs: np.ndarray, exact, mesh_x: SpatialMesh, mesh_t: TemporalMesh,
                      psi0_nodal: np.ndarray | None = None):
     """(||psi - psi_h||_{L2(Q)}, |psi - psi_h|_{H1(Q)}) for P1 x P1 coefficients

@@ -26,7 +26,10 @@ def test_manufactured_errors_full_size(cfg):
     psi = fdm.solve(prob.F)
     res = ks.relative_residual(prob.ops, prob.M_t, prob.B_t, psi, prob.F)
     assert res < 1e-8, res
-    l2, h1 = ea.spacetime_errors(psi[0].cpu().numpy(), ea.exact_solution(prob.cfg.source), prob.mesh, prob.tmesh)
+    l2, h1 = ea.spacetime_errors_device(prob.ops, prob.tmesh, psi[0], prob.cfg.source)
+    if cfg != "C3":   # the host quadrature agrees with the GPU one (C3 would take minutes on the host)
+        l2h, h1h = ea.spacetime_errors(psi[0].cpu().numpy(), ea.exact_solution(prob.cfg.source), prob.mesh, prob.tmesh)
+        assert abs(l2 - l2h) <= 1e-10 * l2h and abs(h1 - h1h) <= 1e-10 * h1h
     want = SURVEY_ERRORS[cfg]
     assert f"{l2:.3g}" == f"{want[0]:.3g}" and f"{h1:.3g}" == f"{want[1]:.3g}", (l2, h1)
 
@@ -64,3 +67,14 @@ def test_sampled_shifts_vs_superlu(cfg):
         ref = O._solve_shift(Mx, Ax, lam[l], G[0, l])
         err = np.linalg.norm(W[0, l] - ref) / np.linalg.norm(ref)
         assert err < 1e-10, (l, err)
+
+
+def test_paper_table2_row1_on_gpu():
+    """PAPER.md:214 through the GPU path: n = 61504, L2 3.2e-03, H1 2.4e-01, kappa 2.3e+02."""
+    prob = Problem("paper0")
+    fdm = ks.FDMSolver(prob.ops, prob.M_t, prob.B_t)
+    assert prob.nx * prob.nt == 61504
+    psi = fdm.solve(prob.F[0])
+    l2, h1 = ea.spacetime_errors_device(prob.ops, prob.tmesh, psi, "paper")
+    assert f"{l2:.1e}" == "3.2e-03" and f"{h1:.1e}" == "2.4e-01" and f"{fdm.kappa2:.1e}" == "2.3e+02"
+    assert abs(l2 - 3.1900e-03) < 5e-8 and abs(h1 - 2.3969e-01) < 5e-6
