@@ -41,6 +41,7 @@ constexpr int LDD = NB + 1;       // diagonal block column stride
 constexpr int MAXR = 16;          // max RHS per call (bv chunks of 16 in the host loop)
 
 constexpr int GEMM_SMEM = (2 * 2 * TK * LDS + 2 * TK) * 16;
+constexpr int SYRK_SMEM = (3 * 2 * TK * LDS) * 16;   // 3-stage pipeline of the standalone Schur kernel
 constexpr int DIAG_SMEM = (NB * LDD + 2 * NB + NB * MAXR) * 16;
 constexpr int FACTOR_SMEM = GEMM_SMEM + DIAG_SMEM;
 
@@ -69,6 +70,8 @@ struct LevelArgs {
   int32_t shift0;
   int* err;
   unsigned long long* prof;   // optional per-phase cycle counters (STFEM_PHASE_PROF)
+  int split_syrk;             // Schur update of large fronts in syrk_level_kernel
+  int unit_diag;              // backward: 1 = unit-L LDL^T fronts, 0 = C C^T fronts
 };
 
 __device__ __forceinline__ int64_t bv_off(const stfem_bv_layout& L, int r, int64_t shift, int64_t j) {
@@ -79,18 +82,22 @@ __device__ __forceinline__ int64_t bv_off(const stfem_bv_layout& L, int r, int64
 // C[i + c*ldC] -= sum_k A[i + k*lda] * B[c + k*ldb],  i < M, c < N.
 // sym: only i >= c is written and only tiles ti >= tj are computed.
 // 8 warps = 2 (M) x 4 (N); warp tile 32 x 16 complex; mma.m16n8k4.f64.
+// STAGES-deep cp.async pipeline (2 inside the factor kernel, 3 in the SYRK kernel).
+template <int STAGES>
 __device__ void gemm_update(cplx* __restrict__ C, int ldC, int M, int N, const cplx* __restrict__ A,
-                            int lda, const cplx* __restrict__ B, int ldb, int K, bool sym, cplx* smem) {
+                            int lda, const cplx* __restrict__ B, int ldb, int K, bool sym, cplx* smem,
+                            int only_ti = -1, int only_tj = -1) {
   if (M <= 0 || N <= 0 || K <= 0) return;
   cplx* As = smem;
-  cplx* Bs = smem + 2 * TK * LDS;
+  cplx* Bs = smem + STAGES * TK * LDS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3, wm = warp & 1, wn = warp >> 1;
   const int tiles_m = (M + TM - 1) / TM, tiles_n = (N + TM - 1) / TM;
   const int nk = (K + TK - 1) / TK;
-  // lower trapezoid (sym) or full rectangle of 64x64 tiles, one CTA walks them all
-  for (int tj = 0; tj < tiles_n; ++tj)
-  for (int ti = sym ? tj : 0; ti < tiles_m; ++ti) {
+  // lower trapezoid (sym) or full rectangle of 64x64 tiles, one CTA walks them
+  // all (or only tile (only_ti, only_tj) when the caller distributes tiles)
+  for (int tj = (only_tj >= 0 ? only_tj : 0); tj < (only_tj >= 0 ? only_tj + 1 : tiles_n); ++tj)
+  for (int ti = (only_ti >= 0 ? only_ti : (sym ? tj : 0)); ti < (only_ti >= 0 ? only_ti + 1 : tiles_m); ++ti) {
     const int i0 = ti * TM, c0 = tj * TM;
 
     auto load = [&](int stage, int kc) {
@@ -112,8 +119,11 @@ __device__ void gemm_update(cplx* __restrict__ C, int ldC, int M, int N, const c
     // accumulators start as C (loads issued together with the first cp.async
     // stage so their latency overlaps); the MMAs subtract A D B^T in place
     double cre[2][2][4], cim[2][2][4];
-    load(0, 0);
-    cp_async_commit();
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (s < nk) load(s, s);
+      cp_async_commit();
+    }
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
@@ -130,16 +140,15 @@ __device__ void gemm_update(cplx* __restrict__ C, int ldC, int M, int N, const c
             cim[mi][ni][2 * h + v] = o.im;
           }
     for (int kc = 0; kc < nk; ++kc) {
-      if (kc + 1 < nk) {
-        load((kc + 1) & 1, kc + 1);
+      cp_async_wait<STAGES - 2>();
+      __syncthreads();   // stage kc landed for everyone; stage (kc-1) % STAGES is free
+      {
+        const int nxt = kc + STAGES - 1;
+        if (nxt < nk) load(nxt % STAGES, nxt);
         cp_async_commit();
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
       }
-      __syncthreads();
-      const cplx* as = As + (kc & 1) * TK * LDS + t * LDS + wm * 32 + g;
-      const cplx* bs = Bs + (kc & 1) * TK * LDS + t * LDS + wn * 16 + g;
+      const cplx* as = As + (kc % STAGES) * TK * LDS + t * LDS + wm * 32 + g;
+      const cplx* bs = Bs + (kc % STAGES) * TK * LDS + t * LDS + wn * 16 + g;
 #pragma unroll
       for (int kk = 0; kk < TK; kk += 4) {
         cplx a[2][2], b[2];
@@ -161,8 +170,9 @@ __device__ void gemm_update(cplx* __restrict__ C, int ldC, int M, int N, const c
             dmma_16x8x4(cim[mi][ni], -a[mi][0].im, -a[mi][1].im, b[ni].re);
           }
       }
-      __syncthreads();
     }
+    cp_async_wait<0>();
+    __syncthreads();   // all warps done with the stages before the next tile refills them
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
@@ -405,13 +415,31 @@ __global__ void __launch_bounds__(NT, 2) factor_level_kernel(LevelArgs a) {
     // trailing pivot-column update (lower part), K = w
     const int base = kb + w;
     if (base < p)
-      gemm_update(P + base + (int64_t)base * n, n, n - base, p - base, P + base + (int64_t)kb * n, n,
+      gemm_update<2>(P + base + (int64_t)base * n, n, n - base, p - base, P + base + (int64_t)kb * n, n,
                   P + base + (int64_t)kb * n, n, w, true, gsm);
     STFEM_PROF_MARK(4);
   }
   // ---- 3. Schur update of the boundary block ----
-  if (b > 0) gemm_update(U, b, b, b, P + p, n, P + p, n, p, true, gsm);
+  // (done by syrk_level_kernel over (instance, tile) work items unless inline)
+  if (!a.split_syrk && b > 0) gemm_update<2>(U, b, b, b, P + p, n, P + p, n, p, true, gsm);
   STFEM_PROF_MARK(5);
+}
+
+// Schur update U = F22 - L21 L21^T of the large fronts of one level, one CTA
+// per (lower 64x64 tile, shift): a plain batched DMMA GEMM with K = p, so the
+// dominant flops of the top levels run fully parallel (no per-instance
+// serialisation, no wave quantisation on a handful of huge fronts).
+// tiles[t] = (front, ti, tj, 0) for the level's fronts.
+__global__ void __launch_bounds__(NT, 2) syrk_level_kernel(LevelArgs a, const int4* __restrict__ tiles) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* gsm = reinterpret_cast<cplx*>(smem_raw);
+  const int k = blockIdx.x % a.nbatch;
+  const int4 tl = tiles[blockIdx.x / a.nbatch];
+  const FrontDev F = a.fronts[tl.x];
+  const int n = F.n, p = F.p, b = n - p;
+  cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
+  cplx* U = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
+  gemm_update<3>(U, b, b, b, P + p, n, P + p, n, p, true, gsm, tl.y, tl.z);
 }
 
 __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int unit) {
@@ -485,6 +513,15 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int uni
 
 #include "multifrontal_small.cuh"
 
+// does depth d run on the shared-memory small-front kernels (unit-L LDL^T)?
+// (measured on C4: fronts of order ~110 factor faster on the large-front kernel,
+// while their backward pass stays on the shared-memory kernel)
+constexpr int SMALL_FACTOR_N = 100;
+bool level_is_small(const Plan& P, int d) {
+  const int lim = P.small_n_cap > 0 ? std::min(P.small_n_cap, SMALL_N) : SMALL_FACTOR_N;
+  return P.level_nmax[d] <= lim && !P.force_big;
+}
+
 // M_x / A_x values of every front entry, in entry order (shift-independent;
 // one coalesced stream per front instead of an indirect gather)
 __global__ void gather_entries_kernel(const int32_t* __restrict__ src, const double* __restrict__ Mv,
@@ -541,6 +578,28 @@ int upload(Plan& P) {
       P.level_nmax[d] = std::max(P.level_nmax[d], P.fronts[f].n);
       P.level_pmax[d] = std::max(P.level_pmax[d], P.fronts[f].p);
     }
+  // Schur-update tiles of the large-front levels (lower 64x64 tiles of each b x b block)
+  {
+    std::vector<int4> tl;
+    P.syrk_off.assign(P.levels.size() + 1, 0);
+    for (size_t d = 0; d < P.levels.size(); ++d) {
+      P.syrk_off[d] = (int64_t)tl.size();
+      const bool small = level_is_small(P, (int)d);
+      if (small) continue;
+      for (int32_t f : P.levels[d]) {
+        const int b = P.fronts[f].n - P.fronts[f].p;
+        const int nt = (b + TM - 1) / TM;
+        for (int tj = 0; tj < nt; ++tj)
+          for (int ti = tj; ti < nt; ++ti) tl.push_back(make_int4(f, ti, tj, 0));
+      }
+    }
+    P.syrk_off[P.levels.size()] = (int64_t)tl.size();
+    STFEM_CUDA_TRY(cudaMalloc(&P.d_syrk_tiles, std::max<size_t>(1, tl.size()) * sizeof(int4)));
+    if (!tl.empty())
+      STFEM_CUDA_TRY(cudaMemcpy(P.d_syrk_tiles, tl.data(), tl.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SYRK_SMEM));
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_level_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  }
   return STFEM_OK;
 }
 
@@ -598,6 +657,8 @@ void Plan::free_device() {
   cudaFree(d_bidx);
   cudaFree(d_relpos);
   cudaFree(d_inv);
+  cudaFree(d_syrk_tiles);
+  d_syrk_tiles = nullptr;
   cudaFree(d_ent_src);
   cudaFree(d_ent_mv);
   cudaFree(d_ent_av);
@@ -665,6 +726,8 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
   a.W = W;
   a.lay = lay;
   a.err = P.d_err;
+  a.split_syrk = getenv("STFEM_INLINE_SYRK") ? 0 : 1;
+  int64_t nlaunch = P.ent_src.empty() ? 0 : 1;   // gather_entries_kernel
   static const bool phase_prof = getenv("STFEM_PHASE_PROF") != nullptr;
   static unsigned long long* d_prof = nullptr;
   if (phase_prof) {
@@ -702,11 +765,19 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
       a.rchild = P.d_rpool[q ^ 1];
       a.rchild_stride = P.rpool_stride[q ^ 1];
       const int nmax = P.level_nmax[d];
-      if (nmax <= SMALL_N && !P.force_big) {
+      if (level_is_small(P, d)) {
         if ((rc = launch_small_factor_any(a, a.nlist * nb, nmax, stream))) return rc;
+        ++nlaunch;
       } else {
         factor_level_kernel<<<a.nlist * nb, NT, FACTOR_SMEM, stream>>>(a);
         STFEM_LAUNCH_CHECK("factor_level_kernel");
+        ++nlaunch;
+        const int64_t ntl = P.syrk_off[d + 1] - P.syrk_off[d];
+        if (a.split_syrk && ntl > 0) {
+          syrk_level_kernel<<<(unsigned)(ntl * nb), NT, SYRK_SMEM, stream>>>(a, P.d_syrk_tiles + P.syrk_off[d]);
+          STFEM_LAUNCH_CHECK("syrk_level_kernel");
+          ++nlaunch;
+        }
       }
       mark();
     }
@@ -716,18 +787,21 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
       const int nmax = P.level_nmax[d], pmax = P.level_pmax[d];
       const int bsm = small_bwd_smem_bytes(nmax, pmax, small_nr(nrhs));
       // factor format of this level: small-front kernel = unit-L LDL^T, large = C C^T
-      const bool ldlt = nmax <= SMALL_N && !P.force_big;
-      if (ldlt && bsm <= 200 * 1024) {
+      const bool ldlt = level_is_small(P, d);
+      a.unit_diag = ldlt ? 1 : 0;
+      if (nmax <= SMALL_N && bsm <= 200 * 1024 && !P.force_big) {
         if ((rc = launch_small_backward_any(a, a.nlist * nb, nmax, pmax, stream))) return rc;
       } else {
         backward_level_kernel<<<a.nlist * nb, NT, 0, stream>>>(a, ldlt ? 1 : 0);
         STFEM_LAUNCH_CHECK("backward_level_kernel");
       }
+      ++nlaunch;
       mark();
     }
   }
   P.last_batch = batch;
-  P.last_launches = (int64_t)((nshift + batch - 1) / batch) * 2 * (P.depth + 1) + (P.ent_src.empty() ? 0 : 1);
+  P.last_launches = nlaunch;
+  P.last_nbatches = (nshift + batch - 1) / batch;
   if (level_timing) {
     cudaStreamSynchronize(stream);
     int L = P.depth + 1;
@@ -869,7 +943,13 @@ extern "C" int stfem_plan_level_report(const stfem_plan* plan, double* ms, doubl
   }
   if (small)
     for (int d = 0; d < L; ++d)
-      small[d] = (d < (int)P.level_nmax.size() && P.level_nmax[d] <= stfem::SMALL_N && !P.force_big) ? 1 : 0;
+      small[d] = (d < (int)P.level_nmax.size() && stfem::level_is_small(P, d)) ? 1 : 0;
+  return STFEM_OK;
+}
+
+extern "C" int stfem_plan_last_batches(const stfem_plan* plan, int32_t* batches) {
+  if (!plan || !batches) return stfem::fail(STFEM_ERR_ARG, "plan_last_batches: null pointer");
+  *batches = reinterpret_cast<const Plan*>(plan)->last_nbatches;
   return STFEM_OK;
 }
 

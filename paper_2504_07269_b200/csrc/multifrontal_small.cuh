@@ -105,16 +105,36 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
   long long t_prev = clock64();
 
   // ---- gather ----
+  // the global loads (original entries, pivot rows of the RHS via perm) are
+  // issued first so their latency overlaps the zero fill of F
+  constexpr int EP = 4;
+  int edst[EP];
+  cplx eval[EP];
+#pragma unroll
+  for (int u = 0; u < EP; ++u) {
+    const int e = i + u * nt;
+    edst[u] = -1;
+    eval[u] = zero;
+    if (e < Fr.ent_cnt) {
+      edst[u] = a.ent_dst[Fr.ent_beg + e];
+      const double mv = a.Mv[Fr.ent_beg + e], av = a.Av[Fr.ent_beg + e];   // entry-ordered values
+      eval[u] = cmk(fma(lam.re, av, mv), lam.im * av);
+    }
+  }
+  const int64_t jrow = (i < p) ? a.perm[Fr.pbeg + i] : 0;
   const int tri = (n * (n + 1)) / 2;
   for (int q = i; q < tri; q += nt) F[q] = zero;
   for (int row = i; row < n; row += nt) {
-    int64_t j = row < p ? a.perm[Fr.pbeg + row] : 0;
+    int64_t j = row < p ? (row == i ? jrow : a.perm[Fr.pbeg + row]) : 0;
 #pragma unroll
     for (int r = 0; r < NR; ++r)
       Rsm[row * NR + r] = (row < p && r < nrhs) ? a.G[bv_off(a.lay, r, shift, j)] : zero;
   }
   __syncthreads();
-  for (int e = i; e < Fr.ent_cnt; e += nt) {
+#pragma unroll
+  for (int u = 0; u < EP; ++u)
+    if (edst[u] >= 0) F[pk(edst[u] % n, edst[u] / n, n)] = eval[u];
+  for (int e = i + EP * nt; e < Fr.ent_cnt; e += nt) {
     const int dst = a.ent_dst[Fr.ent_beg + e];
     const double mv = a.Mv[Fr.ent_beg + e], av = a.Av[Fr.ent_beg + e];   // entry-ordered values
     F[pk(dst % n, dst / n, n)] = cmk(fma(lam.re, av, mv), lam.im * av);
@@ -376,6 +396,7 @@ __global__ void __launch_bounds__(SMALL_N) backward_small_kernel(LevelArgs a, in
       for (int jj = w - 1; jj >= 0; --jj) {
         cplx x = Tsm[jj * NR + lane];
         for (int cc = jj + 1; cc < w; ++cc) x = cfms(x, Ls[(kb + jj) * ldl + kb + cc], Tsm[cc * NR + lane]);
+        if (!a.unit_diag) x = cmul(x, crecip_fast(Ls[(kb + jj) * ldl + kb + jj]));   // C C^T fronts
         Tsm[jj * NR + lane] = x;
         const int col = Fr.pbeg + kb + jj;
         stc(Zk + col + (int64_t)lane * nx, x);

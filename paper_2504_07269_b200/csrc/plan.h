@@ -54,9 +54,12 @@ struct Plan {
   std::vector<int64_t> level_off;          // offsets into d_levels
   std::vector<int32_t> level_nmax, level_pmax;  // per depth: max front order / pivots
   bool force_big = getenv("STFEM_FORCE_BIG") != nullptr;  // diagnostics: disable the small-front path
+  int small_n_cap = getenv("STFEM_SMALL_N") ? atoi(getenv("STFEM_SMALL_N")) : 0;  // tuning: lower the threshold
   int32_t *d_child_ids = nullptr, *d_bidx = nullptr, *d_relpos = nullptr, *d_inv = nullptr;
   int32_t *d_ent_src = nullptr, *d_ent_dst = nullptr, *d_perm = nullptr;
   double *d_ent_mv = nullptr, *d_ent_av = nullptr;   // M_x / A_x values gathered into entry order
+  std::vector<int64_t> syrk_off;           // per depth: offsets into d_syrk_tiles
+  int4* d_syrk_tiles = nullptr;            // (front, ti, tj, 0) Schur-update tiles of the large fronts
   int* d_err = nullptr;
 
   // ---- numeric workspace (per batch of shifts) ----
@@ -65,6 +68,7 @@ struct Plan {
   int32_t ws_nrhs = 0;
   int32_t last_batch = 0;  // batch size used by the last factor_solve
   int64_t last_launches = 0;  // kernel launches issued by the last factor_solve
+  int32_t last_nbatches = 0;  // shift batches of the last factor_solve
   bool record_levels = false;   // record per-level CUDA-event times into level_ms
   std::vector<double> level_ms;
   cplx* d_factor = nullptr;

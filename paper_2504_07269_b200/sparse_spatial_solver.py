@@ -75,7 +75,9 @@ class SpatialPlan:
 
     def last_num_batches(self) -> int:
         """Shift batches used by the last factor_solve call."""
-        return max(1, self.last_launches() // (2 * (self.stats["depth"] + 1)))
+        v = C.c_int32()
+        N.check(N.lib().stfem_plan_last_batches(self._h, C.byref(v)))
+        return max(1, v.value)
 
     def last_launches(self) -> int:
         v = C.c_int64()
