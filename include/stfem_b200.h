@@ -126,6 +126,8 @@ int stfem_plan_set_batch(stfem_plan* plan, int32_t batch, int64_t* bytes_per_shi
  * on the shared-memory small-front kernels (small[depth+1]) */
 int stfem_plan_record_levels(stfem_plan* plan, int32_t on);
 int stfem_plan_level_report(const stfem_plan* plan, double* ms, double* flops, int32_t* small);
+/* largest nrhs one stfem_factor_solve call accepts for this plan (<= 16) */
+int stfem_plan_max_rhs(const stfem_plan* plan, int32_t* max_rhs);
 /* shift batches used by the last stfem_factor_solve call */
 int stfem_plan_last_batches(const stfem_plan* plan, int32_t* batches);
 /* kernel launches of the last stfem_factor_solve call (for launch accounting) */

@@ -68,6 +68,7 @@ def _declare(lib):
         "stfem_plan_set_batch": (C.c_int, [P, I32, C.POINTER(I64)]),
         "stfem_plan_last_launches": (C.c_int, [P, C.POINTER(I64)]),
         "stfem_plan_last_batches": (C.c_int, [P, C.POINTER(I32)]),
+        "stfem_plan_max_rhs": (C.c_int, [P, C.POINTER(I32)]),
         "stfem_plan_record_levels": (C.c_int, [P, I32]),
         "stfem_plan_level_report": (C.c_int, [P, P, P, P]),
         "stfem_factor_solve": (C.c_int, [P, P, P, P, I32, I32, P, P, bv_layout, P]),

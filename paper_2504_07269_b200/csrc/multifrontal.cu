@@ -44,6 +44,7 @@ constexpr int GEMM_SMEM = (2 * 2 * TK * LDS + 2 * TK) * 16;
 constexpr int SYRK_SMEM = (3 * 2 * TK * LDS) * 16;   // 3-stage pipeline of the standalone Schur kernel
 constexpr int DIAG_SMEM = (NB * LDD + 2 * NB + NB * MAXR) * 16;
 constexpr int FACTOR_SMEM = GEMM_SMEM + DIAG_SMEM;
+constexpr int BWD_XS_MAX = 192 * 1024;   // backward_level_kernel: staged x (n x nrhs) per front
 
 struct LevelArgs {
   const FrontDev* fronts;
@@ -455,6 +456,15 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int uni
   cplx* Zk = a.Z + (int64_t)k * nx * nrhs;
   const int32_t* bidx = a.bidx + F.bidx_beg;
   const int64_t shift = a.shift0 + k;
+  // x of the whole front staged in shared memory (n x nrhs): boundary rows
+  // gathered once here, pivot rows filled in as they are solved
+  extern __shared__ __align__(16) unsigned char bwd_smem[];
+  cplx* xs = reinterpret_cast<cplx*>(bwd_smem);
+  for (int q = tid; q < (n - p) * nrhs; q += NT) {
+    const int i = p + q % (n - p), r = q / (n - p);
+    xs[i * nrhs + r] = ldc(Zk + bidx[i - p] + (int64_t)r * nx);
+  }
+  __syncthreads();
 
   for (int kb = ((p - 1) / NB) * NB; kb >= 0; kb -= NB) {
     const int w = min(NB, p - kb);
@@ -465,11 +475,10 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int uni
       for (int r = 0; r < MAXR; ++r) acc[r] = cmk(0.0, 0.0);
       const cplx* col = P + (int64_t)(kb + j) * n;
       for (int i = kb + w + lane; i < n; i += 32) {
-        cplx l = ldc(col + i);
-        int64_t gi = (i < p) ? (int64_t)F.pbeg + i : (int64_t)bidx[i - p];
+        const cplx l = ldc(col + i);
 #pragma unroll
         for (int r = 0; r < MAXR; ++r)
-          if (r < nrhs) acc[r] = cfma(l, ldc(Zk + gi + (int64_t)r * nx), acc[r]);
+          if (r < nrhs) acc[r] = cfma(l, xs[i * nrhs + r], acc[r]);
       }
 #pragma unroll
       for (int r = 0; r < MAXR; ++r) {
@@ -496,15 +505,25 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int uni
       else if (i == c) l11[c * LDD + c] = unit ? cmk(1.0, 0.0) : crecip(ldc(P + (kb + c) + (int64_t)(kb + c) * n));
     }
     __syncthreads();
-    if (tid < nrhs) {
-      const int r = tid;
-      for (int j = w - 1; j >= 0; --j) {
-        cplx x = ts[j * MAXR + r];
-        for (int c = j + 1; c < w; ++c) x = cfms(x, l11[j * LDD + c], ts[c * MAXR + r]);
-        x = cmul(x, l11[j * LDD + j]);
-        ts[j * MAXR + r] = x;
-        stc(Zk + F.pbeg + kb + j + (int64_t)r * nx, x);
-        a.W[bv_off(a.lay, r, shift, a.perm[F.pbeg + kb + j])] = x;
+    if (warp == 0) {
+      // x_j = (t_j - sum_{c>j} L[c][j] x_c) * dinv_j, lane c holds x_c; one warp
+      // reduction per step instead of a single-thread dependent chain
+      for (int r = 0; r < nrhs; ++r) {
+        cplx xl = lane < w ? ts[lane * MAXR + r] : cmk(0.0, 0.0);
+        for (int j = w - 1; j >= 0; --j) {
+          cplx s = (lane > j && lane < w) ? cmul(l11[j * LDD + lane], xl) : cmk(0.0, 0.0);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            s.re += __shfl_xor_sync(0xffffffffu, s.re, o);
+            s.im += __shfl_xor_sync(0xffffffffu, s.im, o);
+          }
+          if (lane == j) xl = cmul(csub(xl, s), l11[j * LDD + j]);
+        }
+        if (lane < w) {
+          stc(Zk + F.pbeg + kb + lane + (int64_t)r * nx, xl);
+          a.W[bv_off(a.lay, r, shift, a.perm[F.pbeg + kb + lane])] = xl;
+          xs[(kb + lane) * nrhs + r] = xl;
+        }
       }
     }
     __syncthreads();
@@ -571,6 +590,9 @@ int upload(Plan& P) {
   STFEM_CUDA_TRY(cudaFuncSetAttribute(factor_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       FACTOR_SMEM));
   STFEM_CUDA_TRY(cudaFuncSetAttribute(factor_level_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      BWD_XS_MAX));
+  STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_level_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   P.level_nmax.assign(P.levels.size(), 0);
   P.level_pmax.assign(P.levels.size(), 0);
   for (size_t d = 0; d < P.levels.size(); ++d)
@@ -689,6 +711,9 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
                  const cplx* G, cplx* W, stfem_bv_layout lay, cudaStream_t stream) {
   if (nshift < 0 || nrhs < 1) return fail(STFEM_ERR_DIM, "factor_solve: nshift >= 0 and nrhs >= 1 required");
   if (nrhs > MAXR) return fail(STFEM_ERR_DIM, "factor_solve: at most 16 right-hand sides per call");
+  if ((int64_t)P.max_front * nrhs * 16 > BWD_XS_MAX)
+    return fail(STFEM_ERR_DIM, "factor_solve: too many right-hand sides per call for this front size "
+                               "(use stfem_plan_max_rhs)");
   if (!Mv || !Av || !lam || !G || !W) return fail(STFEM_ERR_ARG, "factor_solve: null pointer");
   if (lay.chunk_cols <= 0) return fail(STFEM_ERR_ARG, "factor_solve: chunk_cols must be positive");
   if (nshift == 0) return STFEM_OK;
@@ -792,7 +817,7 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
       if (nmax <= SMALL_N && bsm <= 200 * 1024 && !P.force_big) {
         if ((rc = launch_small_backward_any(a, a.nlist * nb, nmax, pmax, stream))) return rc;
       } else {
-        backward_level_kernel<<<a.nlist * nb, NT, 0, stream>>>(a, ldlt ? 1 : 0);
+        backward_level_kernel<<<a.nlist * nb, NT, (size_t)nmax * nrhs * 16, stream>>>(a, ldlt ? 1 : 0);
         STFEM_LAUNCH_CHECK("backward_level_kernel");
       }
       ++nlaunch;
@@ -944,6 +969,13 @@ extern "C" int stfem_plan_level_report(const stfem_plan* plan, double* ms, doubl
   if (small)
     for (int d = 0; d < L; ++d)
       small[d] = (d < (int)P.level_nmax.size() && stfem::level_is_small(P, d)) ? 1 : 0;
+  return STFEM_OK;
+}
+
+extern "C" int stfem_plan_max_rhs(const stfem_plan* plan, int32_t* max_rhs) {
+  if (!plan || !max_rhs) return stfem::fail(STFEM_ERR_ARG, "plan_max_rhs: null pointer");
+  const Plan& P = *reinterpret_cast<const Plan*>(plan);
+  *max_rhs = (int32_t)std::min<int64_t>(stfem::MAXR, stfem::BWD_XS_MAX / (16 * std::max(1, P.max_front)));
   return STFEM_OK;
 }
 

@@ -97,8 +97,11 @@ class SpatialPlan:
         if ops.Mvals is None:
             raise RuntimeError("spatial operators are not assembled")
         lam = lam.to(device=G.device, dtype=torch.complex128).contiguous()
-        for r0 in range(0, nrhs, 16):
-            nr = min(16, nrhs - r0)
+        mr = C.c_int32()
+        N.check(N.lib().stfem_plan_max_rhs(self._h, C.byref(mr)))
+        step = max(1, mr.value)
+        for r0 in range(0, nrhs, step):
+            nr = min(step, nrhs - r0)
             off = r0 * layout.rhs_stride
             N.check(N.lib().stfem_factor_solve(
                 self._h, N.ptr(ops.Mvals), N.ptr(ops.Avals), N.ptr(lam), lam.numel(), nr,
