@@ -134,6 +134,29 @@ int stfem_plan_last_batches(const stfem_plan* plan, int32_t* batches);
 int stfem_plan_last_launches(const stfem_plan* plan, int64_t* launches);
 
 /* ---------------------------------------------------------------------------
+ * K6  spectral subtree elimination (optional; replaces the bottom of the
+ * elimination tree for every shift at once, csrc/spectral.cuh).  Call once
+ * after assembly with host data computed from M_x / A_x (paper_2504_07269_b200
+ * /spectral.py): for subtree t rooted at front root_front[t] with interior
+ * pivots [first[t], first[t] + m_t) and boundary size g_t = the root's
+ * boundary rows, offsets[4t..4t+3] give the double offsets of
+ *   V (m x m, column-major; V^T A_II V = I, V^T M_II V = diag(theta)),
+ *   theta (m), R then Q (g x m each, column-major), C0 then C1 (g x g each).
+ * Fronts inside the subtrees leave the multifrontal levels; the roots' update
+ * blocks, forward RHS and backward solves run as DMMA GEMMs over shifts.
+ * nroots = 0 restores the plain multifrontal plan.  The data must come from
+ * the same operators later passed to stfem_factor_solve.
+ * ------------------------------------------------------------------------- */
+int stfem_plan_set_spectral(stfem_plan* plan, int32_t nroots, const int32_t* root_front,
+                            const int32_t* first, const int64_t* offsets, const double* V,
+                            int64_t nV, const double* theta, int64_t ntheta, const double* RQ,
+                            int64_t nRQ, const double* C01, int64_t nC01);
+/* subtree count, DMMA flops per shift of the update blocks (4 E m summed),
+ * flops per shift per RHS of the RHS GEMMs, and device bytes of the data */
+int stfem_plan_spectral_stats(const stfem_plan* plan, int32_t* nroots, double* flops_u,
+                              double* flops_rhs, int64_t* bytes);
+
+/* ---------------------------------------------------------------------------
  * K1/K2/K7  assembly and the matrix-free residual
  * (apply_global) on the GPU.
  * degree 1: elems ne x 3 (P1 triangles); degree 2: ne x 6 (v0 v1 v2 m01 m12 m20).

@@ -531,6 +531,7 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int uni
 }
 
 #include "multifrontal_small.cuh"
+#include "spectral.cuh"
 
 // does depth d run on the shared-memory small-front kernels (unit-L LDL^T)?
 // (measured on C4: fronts of order ~110 factor faster on the large-front kernel,
@@ -622,6 +623,45 @@ int upload(Plan& P) {
     STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SYRK_SMEM));
     STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_level_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   }
+  // spectral subtrees: data + per-depth work items (fwd1 = U and F1, fwd2 = F2, bwd1 = B1, bwd2 = B2)
+  {
+    const int L = (int)P.levels.size();
+    P.spec_off.assign(4 * L + 1, 0);
+    std::vector<int4> items;
+    for (int d = 0; d < L; ++d) {
+      const std::vector<int32_t> none;
+      const auto& roots = d < (int)P.sub_levels.size() ? P.sub_levels[d] : none;
+      for (int j = 0; j < 4; ++j) {
+        P.spec_off[4 * d + j] = (int64_t)items.size();
+        for (int32_t t : roots) {
+          const SubDev& S = P.subs[t];
+          if (j == 0) {
+            const int nbk = (S.g + 7) / 8;
+            for (int bj = 0; bj < nbk; ++bj)
+              for (int bi = bj; bi < nbk; ++bi) items.push_back(make_int4(OP_U, t, bi, bj));
+            for (int q = 0; q < (S.m + SP_BM - 1) / SP_BM; ++q) items.push_back(make_int4(OP_F1, t, q, 0));
+          } else if (j == 1) {
+            for (int q = 0; q < (S.g + SP_BM - 1) / SP_BM; ++q) items.push_back(make_int4(OP_F2, t, q, 0));
+          } else if (j == 2) {
+            for (int q = 0; q < (S.m + 31) / 32; ++q) items.push_back(make_int4(OP_B1, t, q, 0));
+          } else {
+            for (int q = 0; q < (S.m + SP_BM - 1) / SP_BM; ++q) items.push_back(make_int4(OP_B2, t, q, 0));
+          }
+        }
+      }
+    }
+    P.spec_off[4 * L] = (int64_t)items.size();
+    if (!P.subs.empty()) {
+      if ((rc = up(&P.d_subs, P.subs))) return rc;
+      if ((rc = up(&P.d_V, P.h_V))) return rc;
+      if ((rc = up(&P.d_th, P.h_th))) return rc;
+      if ((rc = up(&P.d_RQ, P.h_RQ))) return rc;
+      if ((rc = up(&P.d_C01, P.h_C01))) return rc;
+      if ((rc = up(&P.d_spec_items, items))) return rc;
+      STFEM_CUDA_TRY(cudaFuncSetAttribute(spectral_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SP_SMEM));
+      STFEM_CUDA_TRY(cudaFuncSetAttribute(spectral_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    }
+  }
   return STFEM_OK;
 }
 
@@ -688,6 +728,15 @@ void Plan::free_device() {
   cudaFree(d_ent_dst);
   cudaFree(d_perm);
   cudaFree(d_err);
+  cudaFree(d_subs);
+  cudaFree(d_V);
+  cudaFree(d_th);
+  cudaFree(d_RQ);
+  cudaFree(d_C01);
+  cudaFree(d_spec_items);
+  d_subs = nullptr;
+  d_V = d_th = d_RQ = d_C01 = nullptr;
+  d_spec_items = nullptr;
   d_fronts = nullptr;
   d_levels = nullptr;
   d_child_ids = d_bidx = d_relpos = d_inv = d_ent_src = d_ent_dst = d_perm = nullptr;
@@ -777,6 +826,24 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
     a.nbatch = nb;
     a.lam = lam + s0;
     a.shift0 = s0;
+    SpecArgs sa{};
+    sa.subs = P.d_subs;
+    sa.V = P.d_V;
+    sa.th = P.d_th;
+    sa.RQ = P.d_RQ;
+    sa.C01 = P.d_C01;
+    sa.fronts = P.d_fronts;
+    sa.bidx = P.d_bidx;
+    sa.perm = P.d_perm;
+    sa.lam = lam + s0;
+    sa.nb = nb;
+    sa.nrhs = nrhs;
+    sa.nx = P.n;
+    sa.shift0 = s0;
+    sa.Z = P.d_Z;
+    sa.G = G;
+    sa.W = W;
+    sa.lay = lay;
     for (int d = P.depth; d >= 0; --d) {
       const int q = d & 1;
       a.list = P.d_levels + P.level_off[d];
@@ -789,6 +856,26 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
       a.rcur_stride = P.rpool_stride[q];
       a.rchild = P.d_rpool[q ^ 1];
       a.rchild_stride = P.rpool_stride[q ^ 1];
+      if (P.spec_off[4 * d + 2] > P.spec_off[4 * d]) {
+        // spectral subtree roots of this depth: update blocks + forward RHS (no factor storage)
+        for (int j = 0; j < 2; ++j) {
+          const int64_t n_it = P.spec_off[4 * d + j + 1] - P.spec_off[4 * d + j];
+          if (n_it == 0) continue;
+          sa.items = P.d_spec_items + P.spec_off[4 * d + j];
+          sa.ucur = a.ucur;
+          sa.ucur_stride = a.ucur_stride;
+          sa.rcur = a.rcur;
+          sa.rcur_stride = a.rcur_stride;
+          spectral_kernel<<<dim3((unsigned)n_it, (unsigned)((nb * nrhs + SP_BN - 1) / SP_BN)), 256, SP_SMEM,
+                            stream>>>(sa);
+          STFEM_LAUNCH_CHECK("spectral_kernel");
+          ++nlaunch;
+        }
+      }
+      if (a.nlist == 0) {
+        mark();
+        continue;
+      }
       const int nmax = P.level_nmax[d];
       if (level_is_small(P, d)) {
         if ((rc = launch_small_factor_any(a, a.nlist * nb, nmax, stream))) return rc;
@@ -809,6 +896,19 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
     for (int d = 0; d <= P.depth; ++d) {
       a.list = P.d_levels + P.level_off[d];
       a.nlist = (int32_t)P.levels[d].size();
+      for (int j = 2; j < 4; ++j) {
+        const int64_t n_it = P.spec_off[4 * d + j + 1] - P.spec_off[4 * d + j];
+        if (n_it == 0) continue;
+        sa.items = P.d_spec_items + P.spec_off[4 * d + j];
+        spectral_kernel<<<dim3((unsigned)n_it, (unsigned)((nb * nrhs + SP_BN - 1) / SP_BN)), 256, SP_SMEM,
+                          stream>>>(sa);
+        STFEM_LAUNCH_CHECK("spectral_kernel");
+        ++nlaunch;
+      }
+      if (a.nlist == 0) {
+        mark();
+        continue;
+      }
       const int nmax = P.level_nmax[d], pmax = P.level_pmax[d];
       const int bsm = small_bwd_smem_bytes(nmax, pmax, small_nr(nrhs));
       // factor format of this level: small-front kernel = unit-L LDL^T, large = C C^T
@@ -848,8 +948,8 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
     unsigned long long h[16];
     cudaMemcpyAsync(h, d_prof, sizeof(h), cudaMemcpyDeviceToHost, stream);
     cudaStreamSynchronize(stream);
-    const char* names[12] = {"assembly", "diag", "writeback+fwd", "trsm", "panel_gemm", "syrk", "", "",
-                             "small:gather", "small:diag+trsm", "small:trailing", "small:writeout"};
+    const char* names[16] = {"assembly", "diag", "writeback+fwd", "trsm", "panel_gemm", "syrk", "", "",
+                             "small:gather", "small:diag+trsm", "small:trailing", "small:writeout", "", "", "", ""};
     for (int grp = 0; grp < 2; ++grp) {
       double tot = 0;
       for (int i = 8 * grp; i < 8 * grp + 6; ++i) tot += (double)h[i];
@@ -884,6 +984,85 @@ extern "C" int stfem_plan_create(int32_t n, const int64_t* rowptr, const int32_t
     return rc;
   }
   *out = reinterpret_cast<stfem_plan*>(P);
+  return STFEM_OK;
+}
+
+extern "C" int stfem_plan_set_spectral(stfem_plan* plan, int32_t nroots, const int32_t* root_front,
+                                       const int32_t* first, const int64_t* offsets, const double* V,
+                                       int64_t nV, const double* theta, int64_t ntheta, const double* RQ,
+                                       int64_t nRQ, const double* C01, int64_t nC01) {
+  if (!plan) return stfem::fail(STFEM_ERR_ARG, "plan_set_spectral: null plan");
+  Plan& P = *reinterpret_cast<Plan*>(plan);
+  const int32_t nf = (int32_t)P.fronts.size();
+  if (nroots < 0 || (nroots > 0 && (!root_front || !first || !offsets || !V || !theta)))
+    return stfem::fail(STFEM_ERR_ARG, "plan_set_spectral: null pointer");
+  // subtree pivot ranges: first pivot of every front's subtree (postorder: children first)
+  std::vector<int32_t> sub_first(nf);
+  for (int32_t f = 0; f < nf; ++f) sub_first[f] = P.fronts[f].pbeg;
+  for (int32_t f = 0; f < nf; ++f)
+    if (P.fronts[f].parent >= 0)
+      sub_first[P.fronts[f].parent] = std::min(sub_first[P.fronts[f].parent], sub_first[f]);
+  std::vector<char> is_root(nf, 0), skip(nf, 0);
+  std::vector<stfem::SubDev> subs(nroots);
+  for (int32_t t = 0; t < nroots; ++t) {
+    const int32_t f = root_front[t];
+    if (f < 0 || f >= nf || is_root[f]) return stfem::fail(STFEM_ERR_ARG, "plan_set_spectral: bad root front");
+    const stfem::FrontDev& F = P.fronts[f];
+    stfem::SubDev& S = subs[t];
+    S.front = f;
+    S.first = first[t];
+    S.m = F.pbeg + F.p - first[t];
+    S.g = F.n - F.p;
+    S.vofs = offsets[4 * t];
+    S.tofs = offsets[4 * t + 1];
+    S.rqofs = offsets[4 * t + 2];
+    S.cofs = offsets[4 * t + 3];
+    if (first[t] != sub_first[f] || S.m < 1)
+      return stfem::fail(STFEM_ERR_DIM, "plan_set_spectral: subtree interior range does not match the plan");
+    if (S.vofs < 0 || S.vofs + (int64_t)S.m * S.m > nV || S.tofs < 0 || S.tofs + S.m > ntheta || S.rqofs < 0 ||
+        S.rqofs + 2LL * S.g * S.m > nRQ || S.cofs < 0 || S.cofs + 2LL * S.g * S.g > nC01)
+      return stfem::fail(STFEM_ERR_DIM, "plan_set_spectral: offsets outside the data arrays");
+    is_root[f] = 1;
+  }
+  for (int32_t f = 0; f < nf; ++f) {
+    for (int32_t a = f; a >= 0; a = P.fronts[a].parent)
+      if (is_root[a]) {
+        skip[f] = 1;
+        break;
+      }
+  }
+  P.free_workspace();
+  P.free_device();
+  P.subs = subs;
+  P.sub_levels.assign(P.depth + 1, {});
+  P.levels.assign(P.depth + 1, {});
+  for (int32_t d = 0; d <= P.depth; ++d)
+    for (int32_t f : P.levels_all[d])
+      if (!skip[f]) P.levels[d].push_back(f);
+  for (int32_t t = 0; t < nroots; ++t) P.sub_levels[P.fronts[root_front[t]].depth].push_back(t);
+  stfem::assign_factor_offsets(P, skip);
+  P.h_V.assign(V, V + (nroots ? nV : 0));
+  P.h_th.assign(theta, theta + (nroots ? ntheta : 0));
+  P.h_RQ.assign(RQ, RQ + (nroots ? nRQ : 0));
+  P.h_C01.assign(C01, C01 + (nroots ? nC01 : 0));
+  P.spectral_flops_u = 0;
+  P.spectral_flops_rhs = 0;
+  for (const auto& S : subs) {
+    const int64_t E = (int64_t)S.g * (S.g + 1) / 2;
+    P.spectral_flops_u += 4 * E * S.m;
+    P.spectral_flops_rhs += 4LL * S.m * S.m * 2 + 4LL * S.g * 2 * S.m * 2;
+  }
+  return STFEM_OK;
+}
+
+extern "C" int stfem_plan_spectral_stats(const stfem_plan* plan, int32_t* nroots, double* flops_u,
+                                         double* flops_rhs, int64_t* bytes) {
+  if (!plan) return stfem::fail(STFEM_ERR_ARG, "plan_spectral_stats: null plan");
+  const Plan& P = *reinterpret_cast<const Plan*>(plan);
+  if (nroots) *nroots = (int32_t)P.subs.size();
+  if (flops_u) *flops_u = (double)P.spectral_flops_u;
+  if (flops_rhs) *flops_rhs = (double)P.spectral_flops_rhs;
+  if (bytes) *bytes = 8 * (int64_t)(P.h_V.size() + P.h_th.size() + P.h_RQ.size() + P.h_C01.size());
   return STFEM_OK;
 }
 

@@ -32,6 +32,15 @@ struct FrontDev {
   int64_t rofs;        // forward-RHS update offset (units of b, times nrhs) within its pool
 };
 
+// One spectrally eliminated subtree (csrc/spectral.cuh): root front, interior
+// size m (pivots [first, first + m) of the plan numbering), boundary size g
+// (= the root's boundary rows), offsets (in doubles) of V (m x m), theta (m),
+// R then Q (g x m each, column-major), C0 then C1 (g x g each).
+struct SubDev {
+  int32_t front, m, g, first;
+  int64_t vofs, tofs, rqofs, cofs;
+};
+
 struct Plan {
   // ---- symbolic (host) ----
   int32_t n = 0;
@@ -47,6 +56,14 @@ struct Plan {
   int64_t nnz_factor = 0;
   double flops = 0;
 
+  // ---- spectral subtrees (optional, stfem_plan_set_spectral) ----
+  std::vector<std::vector<int32_t>> levels_all;   // every front per depth (levels = multifrontal ones)
+  std::vector<SubDev> subs;
+  std::vector<std::vector<int32_t>> sub_levels;   // per depth: indices into subs
+  std::vector<double> h_V, h_th, h_RQ, h_C01;
+  int64_t spectral_flops_u = 0;                   // DMMA flops per shift of OP_U (4 E m)
+  int64_t spectral_flops_rhs = 0;                 // per shift per rhs of F1+F2+B1+B2
+
   // ---- device tables (uploaded lazily) ----
   int device = -1;
   FrontDev* d_fronts = nullptr;
@@ -61,6 +78,10 @@ struct Plan {
   std::vector<int64_t> syrk_off;           // per depth: offsets into d_syrk_tiles
   int4* d_syrk_tiles = nullptr;            // (front, ti, tj, 0) Schur-update tiles of the large fronts
   int* d_err = nullptr;
+  SubDev* d_subs = nullptr;
+  double *d_V = nullptr, *d_th = nullptr, *d_RQ = nullptr, *d_C01 = nullptr;
+  int4* d_spec_items = nullptr;
+  std::vector<int64_t> spec_off;           // (depth+1)*4 + 1: fwd1, fwd2, bwd1, bwd2 item ranges per depth
 
   // ---- numeric workspace (per batch of shifts) ----
   int32_t batch = 0;       // requested (0 = auto)
@@ -80,6 +101,9 @@ struct Plan {
   void free_device();
   void free_workspace();
 };
+
+// factor-block offsets (fofs) and factor_stride over the multifrontal fronts only
+void assign_factor_offsets(Plan& P, const std::vector<char>& skip);
 
 int build_symbolic(Plan& P, int32_t n, const int64_t* rowptr, const int32_t* colind,
                    const double* coords, int32_t dim, int32_t leaf_size);

@@ -1,0 +1,251 @@
+// Spectral subtree elimination (included by multifrontal.cu inside its
+// anonymous namespace; uses FrontDev/SubDev/bv_off/cplx helpers).
+//
+// The bottom of the elimination tree is where the multifrontal method is
+// latency bound: millions of tiny (front, shift) instances per batch.  But
+// every shifted system has the form K(lam) = M + lam A with M, A real SPD,
+// so a whole subtree can be eliminated in closed form.  For a subtree with
+// interior DoFs I (all pivots of the subtree, contiguous in the plan's
+// numbering) and boundary rows Gam (the subtree root's boundary rows):
+//   A_II V = M_II V diag(theta)^{-1}...   precisely  V^T A_II V = I,
+//   V^T M_II V = diag(theta)             (host setup, once per mesh)
+//   K_II(lam)^{-1} = V diag(w) V^T,      w_k = 1 / (theta_k + lam)
+//   K_GI(lam) V = P + lam Q = R + (theta + lam) Q,  P = M_GI V, Q = A_GI V,
+//   R = P - Q diag(theta)
+// so the root's update block (the Schur complement the parent assembles) is
+//   U(lam) = -K_GI K_II^{-1} K_IG = -( R diag(w) R^T + C0 + lam C1 ),
+//   C1 = Q Q^T,  C0 = R Q^T + Q R^T + Q diag(theta) Q^T,
+// the forward RHS contribution to the boundary rows is
+//   c = V^T g_I (kept in Z),   r_Gam = -( R (w o c) + Q c ),
+// and the backward solve of the interior is
+//   y = w o (c - R^T x_Gam) - Q^T x_Gam,   x_I = V y.
+// Every per-shift operation is a real x complex GEMM with the shifts (x RHS)
+// as the N dimension: all of it runs on the FP64 tensor pipe (DMMA) with no
+// per-shift factor storage and no per-front latency chains.
+//
+// One kernel, five operand generators (ops), one 64 x 64(complex) CTA tile:
+//   OP_U  : U(lam)   rows = (i, j) pairs of an 8x8 block, K = m, B = w(k, shift)
+//   OP_F1 : c = V^T g_I           rows = k_out, K = m, B = G gathered through perm
+//   OP_F2 : r_Gam                 rows = i,     K = 2m, B = [w o c ; c]
+//   OP_B1 : y                     rows = 8 R^T rows + 8 Q^T rows per 16, K = gam, B = x_Gam
+//   OP_B2 : x_I = V y             rows = i,     K = m, B = y
+// Register-prefetched double-buffered staging (operands are generated, not
+// copied), 8 warps as 2 (M) x 4 (N), warp tile 32 x 16 complex,
+// mma.sync.m16n8k4.f64: two DMMAs (re, im) per real A fragment.
+#pragma once
+
+constexpr int SP_BM = 64, SP_BN = 64, SP_BK = 16;
+constexpr int SP_LDA = SP_BM + 4;   // As[k][row] doubles: (t*68 + g) mod 16 hits each bank pair twice
+constexpr int SP_LDB = SP_BN + 2;   // Bs[k][col] complex: (t*66 + g) mod 8 hits each 16-B bank group 4x
+constexpr int SP_A_STAGE = SP_BK * SP_LDA;   // doubles
+constexpr int SP_B_STAGE = SP_BK * SP_LDB;   // complex
+constexpr int SP_SMEM = 2 * (SP_A_STAGE * 8 + SP_B_STAGE * 16);
+enum { OP_U = 0, OP_F1 = 1, OP_F2 = 2, OP_B1 = 3, OP_B2 = 4 };
+
+struct SpecArgs {
+  const SubDev* subs;
+  const int4* items;          // (op, subtree, tile_a, tile_b)
+  const double *V, *th, *RQ, *C01;
+  const FrontDev* fronts;
+  const int32_t *bidx, *perm;
+  const cplx* lam;            // this batch's shifts
+  int32_t nb, nrhs, nx, shift0;
+  cplx* ucur;
+  int64_t ucur_stride;
+  cplx* rcur;
+  int64_t rcur_stride;
+  cplx* Z;
+  const cplx* G;
+  cplx* W;
+  stfem_bv_layout lay;
+};
+
+__device__ __forceinline__ cplx spec_w(double th, cplx l) { return crecip_fast(cmk(th + l.re, l.im)); }
+
+template <int OP>
+__device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, double* As, cplx* Bs) {
+  const SubDev S = a.subs[it.y];
+  const FrontDev F = a.fronts[S.front];
+  const int m = S.m, g = S.g, nrhs = a.nrhs, nx = a.nx;
+  const int ncols = OP == OP_U ? a.nb : a.nb * nrhs;
+  const int n0 = blockIdx.y * SP_BN;
+  if (n0 >= ncols) return;
+  const int K = OP == OP_F2 ? 2 * m : OP == OP_B1 ? g : m;
+  const double* __restrict__ V = a.V + S.vofs;
+  const double* __restrict__ th = a.th + S.tofs;
+  const double* __restrict__ Rm = a.RQ + S.rqofs;
+  const double* __restrict__ Qm = Rm + (int64_t)g * m;
+  const int32_t* __restrict__ bidx = a.bidx + F.bidx_beg;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3, wm = warp & 1, wn = warp >> 1;
+  const cplx zero = cmk(0.0, 0.0);
+
+  // ---- operand generators ----
+  auto a_val = [&](int r, int k) -> double {
+    if (k >= K) return 0.0;
+    if (OP == OP_U) {
+      const int i = it.z * 8 + (r >> 3), j = it.w * 8 + (r & 7);
+      if (i >= g || j >= g) return 0.0;
+      return Rm[i + (int64_t)k * g] * Rm[j + (int64_t)k * g];
+    } else if (OP == OP_F1) {
+      const int ko = it.z * SP_BM + r;
+      return ko < m ? V[k + (int64_t)ko * m] : 0.0;
+    } else if (OP == OP_F2) {
+      const int i = it.z * SP_BM + r;
+      if (i >= g) return 0.0;
+      return k < m ? Rm[i + (int64_t)k * g] : Qm[i + (int64_t)(k - m) * g];
+    } else if (OP == OP_B1) {
+      const int kk = it.z * 32 + (r >> 4) * 8 + (r & 7);
+      if (kk >= m) return 0.0;
+      return ((r >> 3) & 1 ? Qm : Rm)[k + (int64_t)kk * g];
+    } else {
+      const int i = it.z * SP_BM + r;
+      return i < m ? V[i + (int64_t)k * m] : 0.0;
+    }
+  };
+  auto b_val = [&](int k, int c) -> cplx {
+    const int cg = n0 + c;
+    if (k >= K || cg >= ncols) return zero;
+    if (OP == OP_U) return spec_w(th[k], a.lam[cg]);
+    const int s = cg / nrhs, r = cg - s * nrhs;
+    const cplx* Zs = a.Z + (int64_t)s * nx * nrhs + (int64_t)r * nx;
+    if (OP == OP_F1) return ldc(a.G + bv_off(a.lay, r, a.shift0 + s, a.perm[S.first + k]));
+    if (OP == OP_F2)
+      return k < m ? cmul(spec_w(th[k], a.lam[s]), ldc(Zs + S.first + k)) : ldc(Zs + S.first + k - m);
+    if (OP == OP_B1) return ldc(Zs + bidx[k]);
+    return ldc(Zs + S.first + k);
+  };
+
+  double ra[4];
+  cplx rb[4];
+  auto fetch = [&](int kc) {
+    const int k0 = kc * SP_BK;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = tid + 256 * u;
+      ra[u] = a_val(idx & 63, k0 + (idx >> 6));
+      rb[u] = b_val(k0 + (idx >> 6), idx & 63);
+    }
+  };
+  auto store = [&](int st) {
+    double* as = As + st * SP_A_STAGE;
+    cplx* bs = Bs + st * SP_B_STAGE;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = tid + 256 * u;
+      as[(idx >> 6) * SP_LDA + (idx & 63)] = ra[u];
+      stc(bs + (idx >> 6) * SP_LDB + (idx & 63), rb[u]);
+    }
+  };
+
+  double acc[2][2][2][4];
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[mi][ni][0][v] = acc[mi][ni][1][v] = 0.0;
+
+  const int nk = (K + SP_BK - 1) / SP_BK;
+  if (nk > 0) {
+    fetch(0);
+    store(0);
+  }
+  __syncthreads();
+  for (int kc = 0; kc < nk; ++kc) {
+    if (kc + 1 < nk) fetch(kc + 1);
+    const double* as = As + (kc & 1) * SP_A_STAGE + tq * SP_LDA + wm * 32 + gq;
+    const cplx* bs = Bs + (kc & 1) * SP_B_STAGE + tq * SP_LDB + wn * 16 + gq;
+#pragma unroll
+    for (int kk = 0; kk < SP_BK; kk += 4) {
+      double af[2][2];
+      cplx bf[2];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        af[mi][0] = as[kk * SP_LDA + mi * 16];
+        af[mi][1] = as[kk * SP_LDA + mi * 16 + 8];
+      }
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) bf[ni] = ldc(bs + kk * SP_LDB + ni * 8);
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) {
+          dmma_16x8x4(acc[mi][ni][0], af[mi][0], af[mi][1], bf[ni].re);
+          dmma_16x8x4(acc[mi][ni][1], af[mi][0], af[mi][1], bf[ni].im);
+        }
+    }
+    if (kc + 1 < nk) store((kc + 1) & 1);
+    __syncthreads();
+  }
+
+  // ---- epilogues ----
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) {
+      const int rbase = wm * 32 + mi * 16 + gq;
+#pragma unroll
+      for (int cv = 0; cv < 2; ++cv) {
+        const int cg = n0 + wn * 16 + ni * 8 + 2 * tq + cv;
+        if (cg >= ncols) continue;
+        if constexpr (OP == OP_B1) {
+          // rows rbase (R^T x) and rbase + 8 (Q^T x) belong to the same interior index
+          const int kk = it.z * 32 + (rbase >> 4) * 8 + (rbase & 7);
+          if (kk >= m) continue;
+          const int s = cg / nrhs, r = cg - s * nrhs;
+          cplx* zp = a.Z + (int64_t)s * nx * nrhs + (int64_t)r * nx + S.first + kk;
+          const cplx t1 = cmk(acc[mi][ni][0][cv], acc[mi][ni][1][cv]);
+          const cplx t2 = cmk(acc[mi][ni][0][2 + cv], acc[mi][ni][1][2 + cv]);
+          const cplx w = spec_w(th[kk], a.lam[s]);
+          stc(zp, csub(cmul(w, csub(ldc(zp), t1)), t2));
+        } else {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int row = rbase + 8 * h;
+          const cplx v = cmk(acc[mi][ni][0][2 * h + cv], acc[mi][ni][1][2 * h + cv]);
+          if (OP == OP_U) {
+            const int i = it.z * 8 + (row >> 3), j = it.w * 8 + (row & 7);
+            if (i >= g || j > i) continue;
+            const double* C0 = a.C01 + S.cofs;
+            const double* C1 = C0 + (int64_t)g * g;
+            const int64_t e = i + (int64_t)j * g;
+            const cplx l = a.lam[cg];
+            cplx* U = a.ucur + (int64_t)cg * a.ucur_stride + F.uofs;
+            stc(U + e, cmk(-(v.re + C0[e] + l.re * C1[e]), -(v.im + l.im * C1[e])));
+          } else if (OP == OP_F1) {
+            const int ko = it.z * SP_BM + row;
+            if (ko >= m) continue;
+            const int s = cg / nrhs, r = cg - s * nrhs;
+            stc(a.Z + (int64_t)s * nx * nrhs + (int64_t)r * nx + S.first + ko, v);
+          } else if (OP == OP_F2) {
+            const int i = it.z * SP_BM + row;
+            if (i >= g) continue;
+            const int s = cg / nrhs, r = cg - s * nrhs;
+            cplx* Rp = a.rcur + ((int64_t)s * a.rcur_stride + F.rofs) * nrhs;
+            stc(Rp + i + (int64_t)r * g, cmk(-v.re, -v.im));
+          } else {
+            const int i = it.z * SP_BM + row;
+            if (i >= m) continue;
+            const int s = cg / nrhs, r = cg - s * nrhs;
+            stc(a.W + bv_off(a.lay, r, a.shift0 + s, a.perm[S.first + i]), v);
+          }
+        }
+        }
+      }
+    }
+}
+
+__global__ void __launch_bounds__(256, 2) spectral_kernel(SpecArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* As = reinterpret_cast<double*>(smem_raw);
+  cplx* Bs = reinterpret_cast<cplx*>(As + 2 * SP_A_STAGE);
+  const int4 it = a.items[blockIdx.x];
+  switch (it.x) {
+    case OP_U: spectral_tile<OP_U>(a, it, As, Bs); break;
+    case OP_F1: spectral_tile<OP_F1>(a, it, As, Bs); break;
+    case OP_F2: spectral_tile<OP_F2>(a, it, As, Bs); break;
+    case OP_B1: spectral_tile<OP_B1>(a, it, As, Bs); break;
+    default: spectral_tile<OP_B2>(a, it, As, Bs); break;
+  }
+}

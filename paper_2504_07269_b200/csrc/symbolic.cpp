@@ -317,8 +317,6 @@ int build_symbolic(Plan& P, int32_t n, const int64_t* rowptr, const int32_t* col
   P.flops = 0;
   P.max_front = P.max_pivots = 0;
   for (auto& F : P.fronts) {
-    F.fofs = P.factor_stride;
-    P.factor_stride += (int64_t)F.n * F.p;
     int64_t b = F.n - F.p;
     P.nnz_factor += (int64_t)F.p * (F.p + 1) / 2 + b * F.p;
     for (int32_t j = 0; j < F.p; ++j) {
@@ -328,6 +326,10 @@ int build_symbolic(Plan& P, int32_t n, const int64_t* rowptr, const int32_t* col
     P.max_front = std::max(P.max_front, F.n);
     P.max_pivots = std::max(P.max_pivots, F.p);
   }
+  P.levels_all = P.levels;
+  P.subs.clear();
+  P.sub_levels.assign(P.depth + 1, {});
+  assign_factor_offsets(P, std::vector<char>(nf, 0));
   P.upool_stride[0] = P.upool_stride[1] = 0;
   P.rpool_stride[0] = P.rpool_stride[1] = 0;
   for (int32_t d = 0; d <= P.depth; ++d) {
@@ -344,6 +346,15 @@ int build_symbolic(Plan& P, int32_t n, const int64_t* rowptr, const int32_t* col
     P.rpool_stride[d & 1] = std::max(P.rpool_stride[d & 1], r);
   }
   return STFEM_OK;
+}
+
+void assign_factor_offsets(Plan& P, const std::vector<char>& skip) {
+  P.factor_stride = 0;
+  for (size_t f = 0; f < P.fronts.size(); ++f) {
+    FrontDev& F = P.fronts[f];
+    F.fofs = P.factor_stride;
+    if (!skip[f]) P.factor_stride += (int64_t)F.n * F.p;
+  }
 }
 
 }  // namespace stfem

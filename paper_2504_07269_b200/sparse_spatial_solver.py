@@ -23,11 +23,20 @@ import numpy as np
 import torch
 
 from . import _native as N
+from . import spectral as SP
 from .fem_assembly import SpatialOperators
 
 
 class SpatialPlan:
-    def __init__(self, ops: SpatialOperators, leaf_size: int = 16):
+    """Symbolic analysis + device tables for one spatial pattern.
+
+    spectral: max interior DoFs of the subtrees eliminated in closed form
+    (K6, spectral.py); 0 = plain multifrontal; None = the default
+    (STFEM_SPECTRAL_M, 256).  The spectral data depends on the operator
+    values, so it is built from `ops` when they are assembled (here, or on the
+    first factor_solve)."""
+
+    def __init__(self, ops: SpatialOperators, leaf_size: int = 16, spectral: int | None = None):
         self.ops = ops
         self.n = ops.n
         h = C.c_void_p()
@@ -37,6 +46,27 @@ class SpatialPlan:
         st = N.plan_stats()
         N.check(N.lib().stfem_plan_stats_get(h, C.byref(st)))
         self.stats = {f: getattr(st, f) for f, _ in N.plan_stats._fields_}
+        self.spectral_m = SP.DEFAULT_MAX_INTERIOR if spectral is None else int(spectral)
+        self.spectral = None          # SpectralData once attached
+        self.t_spectral = 0.0         # host setup seconds
+        if self.spectral_m > 0 and ops.Mvals is not None:
+            self._attach_spectral()
+
+    def _attach_spectral(self):
+        import time
+        t0 = time.perf_counter()
+        fr = self.fronts()
+        data = SP.build(fr, self.front_rows(), self.perm(), self.ops.M_x.to_scipy(), self.ops.A_x.to_scipy(),
+                        self.spectral_m)
+        SP.attach(self._h, data)
+        self.spectral = data
+        self.t_spectral = time.perf_counter() - t0
+        st = N.plan_stats()
+        N.check(N.lib().stfem_plan_stats_get(self._h, C.byref(st)))
+        self.stats = {f: getattr(st, f) for f, _ in N.plan_stats._fields_}
+
+    def spectral_stats(self) -> dict:
+        return SP.stats(self._h)
 
     @property
     def handle(self):
@@ -96,6 +126,8 @@ class SpatialPlan:
         ops = self.ops
         if ops.Mvals is None:
             raise RuntimeError("spatial operators are not assembled")
+        if self.spectral_m > 0 and self.spectral is None:
+            self._attach_spectral()
         lam = lam.to(device=G.device, dtype=torch.complex128).contiguous()
         mr = C.c_int32()
         N.check(N.lib().stfem_plan_max_rhs(self._h, C.byref(mr)))

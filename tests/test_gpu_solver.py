@@ -68,12 +68,16 @@ def test_lifting_matches_oracle():
     assert rel(L, Lo) < 1e-13
 
 
-@pytest.mark.parametrize("force_big", [False, True])
+@pytest.mark.parametrize("mode", ["small", "big", "spec24", "spec"])
 @pytest.mark.parametrize("kind,leaf", [("square9", 4), ("square16", 32), ("p2square6", 8),
-                                        ("lshape5", 16), ("square40", 32)])
-def test_factor_solve_matches_splu(kind, leaf, force_big, monkeypatch):
-    if force_big:  # exercise the global-memory (large-front) kernels on small meshes too
+                                        ("lshape5", 16), ("square40", 32), ("lshape12", 16)])
+def test_factor_solve_matches_splu(kind, leaf, mode, monkeypatch):
+    """mode: small/big = plain multifrontal (shared-memory small-front kernels on,
+    or every front on the global-memory kernels); spec24 / spec = spectral
+    subtrees of <= 24 / <= 256 interior DoFs (K6) under a multifrontal top."""
+    if mode == "big":  # exercise the global-memory (large-front) kernels on small meshes too
         monkeypatch.setenv("STFEM_FORCE_BIG", "1")
+    spectral = {"small": 0, "big": 0, "spec24": 24, "spec": 256}[mode]
     if kind.startswith("p2"):
         mesh, deg = sm.refine_uniform(sm.build_structured_square(int(kind[8:]))), 2
         Mo, Ao = O.assemble_spatial(omesh(mesh), 2, mesh.p2_elements)
@@ -84,7 +88,9 @@ def test_factor_solve_matches_splu(kind, leaf, force_big, monkeypatch):
         mesh, deg = sm.build_structured_square(int(kind[6:])), 1
         Mo, Ao = O.assemble_spatial(omesh(mesh))
     ops = fa.assemble_spatial(mesh, deg)
-    plan = sss.SpatialPlan(ops, leaf_size=leaf)
+    plan = sss.SpatialPlan(ops, leaf_size=leaf, spectral=spectral)
+    if spectral:
+        assert plan.spectral_stats()["nroots"] >= 1
     rng = np.random.default_rng(1)
     nt, nr = 7, 3
     lam = np.array([0.3 - 0.1j, -0.02 - 1e-4j, 1 + 1j, 1e-3 - 2e-3j, -0.5 - 0.01j, 2.0 + 0j, -1e-2 - 5e-1j])
@@ -95,11 +101,12 @@ def test_factor_solve_matches_splu(kind, leaf, force_big, monkeypatch):
         assert rel(W[:, l, :], ref) < 1e-11, (l, rel(W[:, l, :], ref))
 
 
-def test_batching_invariance():
+@pytest.mark.parametrize("spectral", [0, 64])
+def test_batching_invariance(spectral):
     """Results identical whatever the shift batch size."""
     mesh = sm.build_structured_square(20)
     ops = fa.assemble_spatial(mesh)
-    plan = sss.SpatialPlan(ops)
+    plan = sss.SpatialPlan(ops, spectral=spectral)
     rng = np.random.default_rng(5)
     nt = 9
     lam = rng.standard_normal(nt) - 1j * rng.random(nt)
