@@ -72,6 +72,7 @@ struct LevelArgs {
   int* err;
   unsigned long long* prof;   // optional per-phase cycle counters (STFEM_PHASE_PROF)
   int split_syrk;             // Schur update of large fronts in syrk_level_kernel
+  const int32_t* ent_colptr;  // per front (p + 1): first sorted original entry of each pivot column
   int unit_diag;              // backward: 1 = unit-L LDL^T fronts, 0 = C C^T fronts
 };
 
@@ -84,10 +85,21 @@ __device__ __forceinline__ int64_t bv_off(const stfem_bv_layout& L, int r, int64
 // sym: only i >= c is written and only tiles ti >= tj are computed.
 // 8 warps = 2 (M) x 4 (N); warp tile 32 x 16 complex; mma.m16n8k4.f64.
 // STAGES-deep cp.async pipeline (2 inside the factor kernel, 3 in the SYRK kernel).
-template <int STAGES>
+// The accumulator tile starts from cinit(row, col) (default: C itself), so a
+// caller can assemble C on the fly (syrk_level_kernel gathers the children's
+// update blocks instead of reading a pre-assembled U).
+struct CLoad {
+  const cplx* C;
+  int ldC;
+  __device__ __forceinline__ cplx operator()(int row, int col) const {
+    return ldc(C + (int64_t)row + (int64_t)col * ldC);
+  }
+};
+
+template <int STAGES, class CInit>
 __device__ void gemm_update(cplx* __restrict__ C, int ldC, int M, int N, const cplx* __restrict__ A,
                             int lda, const cplx* __restrict__ B, int ldb, int K, bool sym, cplx* smem,
-                            int only_ti = -1, int only_tj = -1) {
+                            int only_ti, int only_tj, const CInit& cinit) {
   if (M <= 0 || N <= 0 || K <= 0) return;
   cplx* As = smem;
   cplx* Bs = smem + STAGES * TK * LDS;
@@ -136,7 +148,7 @@ __device__ void gemm_update(cplx* __restrict__ C, int ldC, int M, int N, const c
             const int row = i0 + wm * 32 + mi * 16 + g + 8 * h;
             const int col = c0 + wn * 16 + ni * 8 + 2 * t + v;
             cplx o = cmk(0.0, 0.0);
-            if (row < M && col < N && (!sym || row >= col)) o = ldc(C + (int64_t)row + (int64_t)col * ldC);
+            if (row < M && col < N && (!sym || row >= col)) o = cinit(row, col);
             cre[mi][ni][2 * h + v] = o.re;
             cim[mi][ni][2 * h + v] = o.im;
           }
@@ -200,231 +212,7 @@ __device__ void gemm_update(cplx* __restrict__ C, int ldC, int M, int N, const c
     }                                                                                    \
   } while (0)
 
-__global__ void __launch_bounds__(NT, 2) factor_level_kernel(LevelArgs a) {
-  long long t_prev = clock64();
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  cplx* gsm = reinterpret_cast<cplx*>(smem_raw);
-  cplx* Ld = gsm + GEMM_SMEM / 16;          // NB x LDD, column-major
-  cplx* dinv_s = Ld + NB * LDD;             // NB
-  cplx* ysm = dinv_s + NB;                  // NB x MAXR
-  cplx* cdg = ysm + NB * MAXR;              // NB: diagonal c_jj of the panel
-
-  const int tid = threadIdx.x;
-  const int inst = blockIdx.x;
-  const int k = inst % a.nbatch;
-  const FrontDev F = a.fronts[a.list[inst / a.nbatch]];
-  const int n = F.n, p = F.p, b = n - p;
-  const int nrhs = a.nrhs, nx = a.nx;
-  const cplx lam = a.lam[k];
-  cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
-  cplx* U = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
-  cplx* R = a.rcur + ((int64_t)k * a.rcur_stride + F.rofs) * nrhs;
-  cplx* Zk = a.Z + (int64_t)k * nx * nrhs;
-  const int64_t shift = a.shift0 + k;
-
-  // ---- 1. assembly: gather once (each front entry written exactly once) ----
-  // parent entry (r1, c2) = sum over children s of U_s[inv_s[r1], inv_s[c2]]
-  // (inverse relpos maps staged in shared memory), then the original entries
-  // M + lam A are added at their unique positions.  No zero fill, no RMW.
-  const cplx zero = cmk(0.0, 0.0);
-  {
-    constexpr int CU = 4, NW = NT / 32;
-    const int lane = tid & 31, warp = tid >> 5;
-    const int nc = min(F.nchild, 2);
-    int* inv_s = reinterpret_cast<int*>(gsm);   // nc x n (aliases the GEMM staging buffers)
-    for (int q = tid; q < nc * n; q += NT) inv_s[q] = a.inv[F.inv_beg + q];
-    const cplx* Ucs[2] = {nullptr, nullptr};
-    const cplx* Rcs[2] = {nullptr, nullptr};
-    int bcs[2] = {0, 0};
-    for (int s = 0; s < nc; ++s) {
-      const FrontDev Cf = a.fronts[a.child_ids[F.child_beg + s]];
-      bcs[s] = Cf.n - Cf.p;
-      Ucs[s] = a.uchild + (int64_t)k * a.uchild_stride + Cf.uofs;
-      Rcs[s] = a.rchild + ((int64_t)k * a.rchild_stride + Cf.rofs) * nrhs;
-    }
-    __syncthreads();
-    for (int c2b = warp; c2b < n; c2b += CU * NW) {
-      int k2[2][CU];
-      cplx* dst[CU];
-#pragma unroll
-      for (int u = 0; u < CU; ++u) {
-        const int c2 = min(c2b + u * NW, n - 1);
-#pragma unroll
-        for (int s = 0; s < 2; ++s) k2[s][u] = s < nc ? inv_s[s * n + c2] : -1;
-        dst[u] = (c2 < p) ? P + (int64_t)c2 * n : U + (int64_t)(c2 - p) * b - p;
-      }
-      for (int r1 = c2b + lane; r1 < n; r1 += 32) {
-        int k1[2];
-#pragma unroll
-        for (int s = 0; s < 2; ++s) k1[s] = s < nc ? inv_s[s * n + r1] : -1;
-        cplx v[CU];
-#pragma unroll
-        for (int u = 0; u < CU; ++u) {
-          v[u] = zero;
-#pragma unroll
-          for (int s = 0; s < 2; ++s)
-            if (k1[s] >= 0 && k2[s][u] >= 0)
-              v[u] = cadd(v[u], ldc(Ucs[s] + (int64_t)k2[s][u] * bcs[s] + k1[s]));
-        }
-#pragma unroll
-        for (int u = 0; u < CU; ++u) {
-          const int c2 = c2b + u * NW;
-          if (c2 < n && r1 >= c2) stc(dst[u] + r1, v[u]);
-        }
-      }
-    }
-    // forward RHS: pivot rows get G (gathered through perm) + children, boundary rows children only
-    for (int q = tid; q < n * nrhs; q += NT) {
-      const int r1 = q % n, r = q / n;
-      cplx v = zero;
-      if (r1 < p) v = a.G[bv_off(a.lay, r, shift, a.perm[F.pbeg + r1])];
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const int kk = s < nc ? inv_s[s * n + r1] : -1;
-        if (kk >= 0) v = cadd(v, ldc(Rcs[s] + kk + (int64_t)r * bcs[s]));
-      }
-      if (r1 < p) stc(Zk + F.pbeg + r1 + (int64_t)r * nx, v);
-      else stc(R + (r1 - p) + (int64_t)r * b, v);
-    }
-  }
-  __syncthreads();
-  for (int e = tid; e < F.ent_cnt; e += NT) {
-    const double mv = a.Mv[F.ent_beg + e], av = a.Av[F.ent_beg + e];   // entry-ordered values
-    cplx* dst = P + a.ent_dst[F.ent_beg + e];
-    const cplx o = ldc(dst);
-    stc(dst, cmk(o.re + fma(lam.re, av, mv), o.im + lam.im * av));
-  }
-  __syncthreads();
-
-  STFEM_PROF_MARK(0);
-  // ---- 2. pivot columns, panels of NB: complex-symmetric Cholesky K = C C^T ----
-  // c_jj = sqrt(d_j) (principal branch), so no diagonal scaling ever enters the
-  // DMMA updates (the D-scaled operand used to compete with DMMA for the FP64 pipe)
-  for (int kb = 0; kb < p; kb += NB) {
-    const int w = min(NB, p - kb);
-    for (int idx = tid; idx < w * w; idx += NT) {
-      int i = idx % w, c = idx / w;
-      if (i >= c) Ld[c * LDD + i] = ldc(P + (kb + i) + (int64_t)(kb + c) * n);
-    }
-    __syncthreads();
-    // diagonal block by warp 0 alone (lane = row, warp-synchronous): step j
-    // applies column j's rank-1 update with unscaled values,
-    // a_ic -= (a_ij / d_j) a_cj, then all columns are scaled by 1/c_j = d_j^{-1/2}.
-    if ((tid >> 5) == 0) {
-      const int lane = tid & 31;
-      for (int j = 0; j < w; ++j) {
-        const cplx d = Ld[j * LDD + j];
-        if (lane > j && lane < w) {
-          // row `lane`, columns c in (j, lane]: 4 independent RMWs in flight
-          const cplx f = cmul(Ld[j * LDD + lane], crecip_fast(d));
-          cplx* __restrict__ rowp = Ld + lane;             // (lane, c) at rowp[c * LDD]
-          const cplx* __restrict__ colj = Ld + j * LDD;    // (c, j)    at colj[c]
-          int c = j + 1;
-          for (; c + 3 <= lane; c += 4) {
-            const cplx x0 = rowp[c * LDD], x1 = rowp[(c + 1) * LDD], x2 = rowp[(c + 2) * LDD],
-                       x3 = rowp[(c + 3) * LDD];
-            const cplx y0 = colj[c], y1 = colj[c + 1], y2 = colj[c + 2], y3 = colj[c + 3];
-            rowp[c * LDD] = cfms(x0, f, y0);
-            rowp[(c + 1) * LDD] = cfms(x1, f, y1);
-            rowp[(c + 2) * LDD] = cfms(x2, f, y2);
-            rowp[(c + 3) * LDD] = cfms(x3, f, y3);
-          }
-          for (; c <= lane; ++c) rowp[c * LDD] = cfms(rowp[c * LDD], f, colj[c]);
-        }
-        __syncwarp();
-      }
-      // off the critical path: pivots d_j -> c_j = sqrt(d_j), 1/c_j (lane j), checks
-      if (lane < w) {
-        const cplx d = Ld[lane * LDD + lane];
-        const double m2 = cabs2(d);
-        if (!(m2 > 1e-300) || !isfinite(m2)) atomicCAS(a.err, 0, (int)shift + 1);
-        const cplx c = csqrt_(d);
-        cdg[lane] = c;
-        dinv_s[lane] = crecip(c);
-      }
-      __syncwarp();
-      for (int j = 0; j < w; ++j) {
-        if (lane == j) Ld[j * LDD + j] = cdg[j];
-        else if (lane > j && lane < w) Ld[j * LDD + lane] = cmul(Ld[j * LDD + lane], dinv_s[j]);
-      }
-    }
-    __syncthreads();
-    STFEM_PROF_MARK(1);
-    // write back C11; forward-solve the panel RHS: y = C11^{-1} r
-    for (int idx = tid; idx < w * w; idx += NT) {
-      int i = idx % w, c = idx / w;
-      if (i >= c) stc(P + (kb + i) + (int64_t)(kb + c) * n, Ld[c * LDD + i]);
-    }
-    if ((tid >> 5) == 0) {
-      // warp 0: y = C11^{-1} r with lane c holding y_c; each step is a warp reduction
-      const int lane = tid & 31;
-      for (int r = 0; r < nrhs; ++r) {
-        cplx* z = Zk + F.pbeg + kb + (int64_t)r * nx;
-        cplx yl = lane < w ? ldc(z + lane) : zero;
-        for (int j = 0; j < w; ++j) {
-          cplx s = lane < j ? cmul(Ld[lane * LDD + j], yl) : zero;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            s.re += __shfl_xor_sync(0xffffffffu, s.re, o);
-            s.im += __shfl_xor_sync(0xffffffffu, s.im, o);
-          }
-          if (lane == j) yl = cmul(csub(yl, s), dinv_s[j]);
-        }
-        if (lane < w) {
-          ysm[lane * MAXR + r] = yl;
-          stc(z + lane, yl);
-        }
-      }
-    }
-    __syncthreads();
-    STFEM_PROF_MARK(2);
-    // TRSM rows below the diagonal block + fused RHS update (thread per row),
-    // 8 columns at a time in registers; earlier columns of the row are re-read (L1)
-    for (int i = kb + w + tid; i < n; i += NT) {
-      cplx* prow = P + i + (int64_t)kb * n;
-      for (int jb = 0; jb < w; jb += 8) {
-        cplx y[8];
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) y[jj] = (jb + jj < w) ? ldc(prow + (int64_t)(jb + jj) * n) : zero;
-        for (int c = 0; c < jb; ++c) {
-          const cplx lc = ldc(prow + (int64_t)c * n);
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj)
-            if (jb + jj < w) y[jj] = cfms(y[jj], lc, Ld[c * LDD + jb + jj]);
-        }
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-          if (jb + jj < w) {
-#pragma unroll
-            for (int cc = 0; cc < jj; ++cc) y[jj] = cfms(y[jj], y[cc], Ld[(jb + cc) * LDD + jb + jj]);
-            y[jj] = cmul(y[jj], dinv_s[jb + jj]);
-            stc(prow + (int64_t)(jb + jj) * n, y[jj]);
-          }
-        }
-        for (int r = 0; r < nrhs; ++r) {
-          cplx* dst = (i < p) ? Zk + F.pbeg + i + (int64_t)r * nx : R + (i - p) + (int64_t)r * b;
-          cplx acc = ldc(dst);
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj)
-            if (jb + jj < w) acc = cfms(acc, y[jj], ysm[(jb + jj) * MAXR + r]);
-          stc(dst, acc);
-        }
-      }
-    }
-    __syncthreads();
-    STFEM_PROF_MARK(3);
-    // trailing pivot-column update (lower part), K = w
-    const int base = kb + w;
-    if (base < p)
-      gemm_update<2>(P + base + (int64_t)base * n, n, n - base, p - base, P + base + (int64_t)kb * n, n,
-                  P + base + (int64_t)kb * n, n, w, true, gsm);
-    STFEM_PROF_MARK(4);
-  }
-  // ---- 3. Schur update of the boundary block ----
-  // (done by syrk_level_kernel over (instance, tile) work items unless inline)
-  if (!a.split_syrk && b > 0) gemm_update<2>(U, b, b, b, P + p, n, P + p, n, p, true, gsm);
-  STFEM_PROF_MARK(5);
-}
+#include "multifrontal_large.cuh"
 
 // Schur update U = F22 - L21 L21^T of the large fronts of one level, one CTA
 // per (lower 64x64 tile, shift): a plain batched DMMA GEMM with K = p, so the
@@ -440,7 +228,7 @@ __global__ void __launch_bounds__(NT, 2) syrk_level_kernel(LevelArgs a, const in
   const int n = F.n, p = F.p, b = n - p;
   cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
   cplx* U = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
-  gemm_update<3>(U, b, b, b, P + p, n, P + p, n, p, true, gsm, tl.y, tl.z);
+  gemm_update<3>(U, b, b, b, P + p, n, P + p, n, p, true, gsm, tl.y, tl.z, CLoad{U, b});
 }
 
 __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int unit) {
@@ -585,12 +373,12 @@ int upload(Plan& P) {
   STFEM_CUDA_TRY(cudaMalloc(&P.d_ent_mv, std::max<size_t>(1, P.ent_src.size()) * sizeof(double)));
   STFEM_CUDA_TRY(cudaMalloc(&P.d_ent_av, std::max<size_t>(1, P.ent_src.size()) * sizeof(double)));
   if ((rc = up(&P.d_ent_dst, P.ent_dst))) return rc;
+  if ((rc = up(&P.d_ent_colptr, P.ent_colptr))) return rc;
   if ((rc = up(&P.d_perm, P.perm))) return rc;
   STFEM_CUDA_TRY(cudaMalloc(&P.d_err, sizeof(int)));
   STFEM_CUDA_TRY(cudaMemset(P.d_err, 0, sizeof(int)));
-  STFEM_CUDA_TRY(cudaFuncSetAttribute(factor_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      FACTOR_SMEM));
-  STFEM_CUDA_TRY(cudaFuncSetAttribute(factor_level_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  STFEM_CUDA_TRY(cudaFuncSetAttribute(panel_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM));
+  STFEM_CUDA_TRY(cudaFuncSetAttribute(panel_update_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       BWD_XS_MAX));
   STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_level_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -658,7 +446,12 @@ int upload(Plan& P) {
       if ((rc = up(&P.d_RQ, P.h_RQ))) return rc;
       if ((rc = up(&P.d_C01, P.h_C01))) return rc;
       if ((rc = up(&P.d_spec_items, items))) return rc;
-      STFEM_CUDA_TRY(cudaFuncSetAttribute(spectral_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SP_SMEM));
+      int mmax = 0;
+      for (const auto& S : P.subs) mmax = std::max(mmax, S.m);
+      P.spec_smem = spectral_smem_bytes(mmax);
+      if (P.spec_smem > 227 * 1024)
+        return fail(STFEM_ERR_DIM, "spectral subtrees: interior too large for the shared-memory staging");
+      STFEM_CUDA_TRY(cudaFuncSetAttribute(spectral_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, P.spec_smem));
       STFEM_CUDA_TRY(cudaFuncSetAttribute(spectral_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     }
   }
@@ -726,6 +519,8 @@ void Plan::free_device() {
   cudaFree(d_ent_av);
   d_ent_mv = d_ent_av = nullptr;
   cudaFree(d_ent_dst);
+  cudaFree(d_ent_colptr);
+  d_ent_colptr = nullptr;
   cudaFree(d_perm);
   cudaFree(d_err);
   cudaFree(d_subs);
@@ -780,6 +575,7 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
   a.bidx = P.d_bidx;
   a.ent_src = P.d_ent_src;
   a.ent_dst = P.d_ent_dst;
+  a.ent_colptr = P.d_ent_colptr;
   a.perm = P.d_perm;
   {
     const int64_t ne = (int64_t)P.ent_src.size();
@@ -800,7 +596,7 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
   a.W = W;
   a.lay = lay;
   a.err = P.d_err;
-  a.split_syrk = getenv("STFEM_INLINE_SYRK") ? 0 : 1;
+  a.split_syrk = 1;
   int64_t nlaunch = P.ent_src.empty() ? 0 : 1;   // gather_entries_kernel
   static const bool phase_prof = getenv("STFEM_PHASE_PROF") != nullptr;
   static unsigned long long* d_prof = nullptr;
@@ -866,7 +662,7 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
           sa.ucur_stride = a.ucur_stride;
           sa.rcur = a.rcur;
           sa.rcur_stride = a.rcur_stride;
-          spectral_kernel<<<dim3((unsigned)n_it, (unsigned)((nb * nrhs + SP_BN - 1) / SP_BN)), 256, SP_SMEM,
+          spectral_kernel<<<dim3((unsigned)n_it, (unsigned)((nb * nrhs + SP_BN - 1) / SP_BN)), 256, P.spec_smem,
                             stream>>>(sa);
           STFEM_LAUNCH_CHECK("spectral_kernel");
           ++nlaunch;
@@ -881,9 +677,29 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
         if ((rc = launch_small_factor_any(a, a.nlist * nb, nmax, stream))) return rc;
         ++nlaunch;
       } else {
-        factor_level_kernel<<<a.nlist * nb, NT, FACTOR_SMEM, stream>>>(a);
-        STFEM_LAUNCH_CHECK("factor_level_kernel");
+        // large fronts: tile-parallel pipeline over all (front, shift) instances of the level
+        const int ninst = a.nlist * nb, pmax = P.level_pmax[d];
+        asm_front_kernel<<<dim3(ninst, (nmax + ASM_COLS - 1) / ASM_COLS), NT, (size_t)2 * nmax * sizeof(int),
+                           stream>>>(a);
+        STFEM_LAUNCH_CHECK("asm_front_kernel");
         ++nlaunch;
+        for (int kb = 0; kb < pmax; kb += NB) {
+          diag_kernel<<<ninst, 32, 0, stream>>>(a, kb);
+          STFEM_LAUNCH_CHECK("diag_kernel");
+          const dim3 tg(ninst, (unsigned)std::max(1, (nmax - kb + TR_ROWS - 1) / TR_ROWS));
+          if (std::min(NB, pmax - kb) <= 16) trsm_kernel<16><<<tg, TR_ROWS, 0, stream>>>(a, kb);
+          else trsm_kernel<32><<<tg, TR_ROWS, 0, stream>>>(a, kb);
+          STFEM_LAUNCH_CHECK("trsm_kernel");
+          nlaunch += 2;
+          int tiles = 0;
+          for (int32_t f : P.levels[d])
+            tiles = std::max(tiles, panel_update_tiles(P.fronts[f].n, P.fronts[f].p, kb));
+          if (tiles > 0) {
+            panel_update_kernel<<<dim3(ninst, tiles), NT, GEMM_SMEM, stream>>>(a, kb);
+            STFEM_LAUNCH_CHECK("panel_update_kernel");
+            ++nlaunch;
+          }
+        }
         const int64_t ntl = P.syrk_off[d + 1] - P.syrk_off[d];
         if (a.split_syrk && ntl > 0) {
           syrk_level_kernel<<<(unsigned)(ntl * nb), NT, SYRK_SMEM, stream>>>(a, P.d_syrk_tiles + P.syrk_off[d]);
@@ -900,7 +716,7 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
         const int64_t n_it = P.spec_off[4 * d + j + 1] - P.spec_off[4 * d + j];
         if (n_it == 0) continue;
         sa.items = P.d_spec_items + P.spec_off[4 * d + j];
-        spectral_kernel<<<dim3((unsigned)n_it, (unsigned)((nb * nrhs + SP_BN - 1) / SP_BN)), 256, SP_SMEM,
+        spectral_kernel<<<dim3((unsigned)n_it, (unsigned)((nb * nrhs + SP_BN - 1) / SP_BN)), 256, P.spec_smem,
                           stream>>>(sa);
         STFEM_LAUNCH_CHECK("spectral_kernel");
         ++nlaunch;

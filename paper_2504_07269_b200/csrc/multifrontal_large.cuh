@@ -1,0 +1,286 @@
+// Large-front path of the multifrontal factorization (included by
+// multifrontal.cu inside its anonymous namespace; uses LevelArgs, gemm_update,
+// NB/NT/LDD/MAXR).
+//
+// A level of large fronts times a batch of shifts is factored by a pipeline of
+// tile-parallel kernels, each launched over every (front, shift) instance of
+// the level, so no kernel serialises a whole front on one CTA:
+//   asm_front_kernel     (instance, 32-column block): gather-once assembly of
+//                        the front (pivot block into the factor storage,
+//                        boundary block into U) from the children's update
+//                        blocks (inverse relpos maps), + M + lam A original
+//                        entries (sorted column-major with per-column
+//                        pointers), + the forward RHS (G through perm +
+//                        children's RHS)
+//   per 32-wide pivot panel kb:
+//     diag_kernel        (instance): one warp factors the w x w diagonal block
+//                        (complex-symmetric Cholesky, c_jj = sqrt(d_j)) and
+//                        forward-solves the panel RHS y = C11^{-1} r
+//     trsm_kernel<W>     (instance, 128-row tile): every row below the block
+//                        solves x C11^T = b in registers (right-looking, W
+//                        independent chains) and updates its RHS r -= x y
+//     panel_update_kernel (instance, 64x64 tile): trailing pivot columns
+//                        F[base:, base:p] -= X X^T on the FP64 tensor pipe
+//   syrk_level_kernel    (instance, 64x64 tile): U = F22 - L21 L21^T, K = p.
+// Factor format: K = C C^T (transpose, not conjugate transpose).
+#pragma once
+
+constexpr int ASM_COLS = 32;
+constexpr int TR_ROWS = 128;
+
+__global__ void __launch_bounds__(NT) asm_front_kernel(LevelArgs a) {
+  extern __shared__ int inv_s[];   // nc x n inverse relpos maps
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int inst = blockIdx.x;
+  const int k = inst % a.nbatch;
+  const FrontDev F = a.fronts[a.list[inst / a.nbatch]];
+  const int n = F.n, p = F.p, b = n - p;
+  const int c0 = blockIdx.y * ASM_COLS;
+  if (c0 >= n) return;
+  const int cend = min(n, c0 + ASM_COLS);
+  cplx* U = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
+  const int nrhs = a.nrhs, nx = a.nx;
+  const cplx lam = a.lam[k];
+  cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
+  const int64_t shift = a.shift0 + k;
+  const int nc = min(F.nchild, 2);
+  for (int q = tid; q < nc * n; q += NT) inv_s[q] = a.inv[F.inv_beg + q];
+  const cplx* Ucs[2] = {nullptr, nullptr};
+  const cplx* Rcs[2] = {nullptr, nullptr};
+  int bcs[2] = {0, 0};
+  for (int s = 0; s < nc; ++s) {
+    const FrontDev Cf = a.fronts[a.child_ids[F.child_beg + s]];
+    bcs[s] = Cf.n - Cf.p;
+    Ucs[s] = a.uchild + (int64_t)k * a.uchild_stride + Cf.uofs;
+    Rcs[s] = a.rchild + ((int64_t)k * a.rchild_stride + Cf.rofs) * nrhs;
+  }
+  // original entries of pivot columns [c0, min(cend, p)): one contiguous range of the sorted list
+  const int* cp = a.ent_colptr + F.colptr_beg;
+  const int ent_lo = c0 < p ? cp[c0] : 0, ent_hi = c0 < p ? cp[min(cend, p)] : 0;
+  __syncthreads();
+  // gather: warp w owns columns c0 + w + 8u (u < 4), lanes run down the rows
+  constexpr int CU = 4, NW = NT / 32;
+  const cplx zero = cmk(0.0, 0.0);
+  {
+    int k2[2][CU];
+    cplx* dst[CU];
+#pragma unroll
+    for (int u = 0; u < CU; ++u) {
+      const int c2 = min(c0 + warp + u * NW, cend - 1);
+#pragma unroll
+      for (int s = 0; s < 2; ++s) k2[s][u] = s < nc ? inv_s[s * n + c2] : -1;
+      dst[u] = (c2 < p) ? P + (int64_t)c2 * n : U + (int64_t)(c2 - p) * b - p;
+    }
+    for (int r1 = c0 + warp + lane; r1 < n; r1 += 32) {
+      int k1[2];
+#pragma unroll
+      for (int s = 0; s < 2; ++s) k1[s] = s < nc ? inv_s[s * n + r1] : -1;
+      cplx v[CU];
+#pragma unroll
+      for (int u = 0; u < CU; ++u) {
+        v[u] = zero;
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+          if (k1[s] >= 0 && k2[s][u] >= 0) v[u] = cadd(v[u], ldc(Ucs[s] + (int64_t)k2[s][u] * bcs[s] + k1[s]));
+      }
+#pragma unroll
+      for (int u = 0; u < CU; ++u) {
+        const int c2 = c0 + warp + u * NW;
+        if (c2 < cend && r1 >= c2) stc(dst[u] + r1, v[u]);
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = ent_lo + tid; e < ent_hi; e += NT) {
+    const double mv = a.Mv[F.ent_beg + e], av = a.Av[F.ent_beg + e];   // entry-ordered values
+    cplx* d = P + a.ent_dst[F.ent_beg + e];
+    const cplx o = ldc(d);
+    stc(d, cmk(o.re + fma(lam.re, av, mv), o.im + lam.im * av));
+  }
+  if (blockIdx.y == 0) {
+    // forward RHS: pivot rows get G (through perm) + children, boundary rows children only
+    cplx* R = a.rcur + ((int64_t)k * a.rcur_stride + F.rofs) * nrhs;
+    cplx* Zk = a.Z + (int64_t)k * nx * nrhs;
+    for (int q = tid; q < n * nrhs; q += NT) {
+      const int r1 = q % n, r = q / n;
+      cplx v = zero;
+      if (r1 < p) v = ldc(a.G + bv_off(a.lay, r, shift, a.perm[F.pbeg + r1]));
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int kk = s < nc ? inv_s[s * n + r1] : -1;
+        if (kk >= 0) v = cadd(v, ldc(Rcs[s] + kk + (int64_t)r * bcs[s]));
+      }
+      if (r1 < p) stc(Zk + F.pbeg + r1 + (int64_t)r * nx, v);
+      else stc(R + (r1 - p) + (int64_t)r * b, v);
+    }
+  }
+}
+
+// one warp per instance: w x w diagonal block of panel kb (lane = row)
+__global__ void __launch_bounds__(32) diag_kernel(LevelArgs a, int kb) {
+  __shared__ cplx Ld[NB * LDD];
+  __shared__ cplx dinv_s[NB], cdg[NB];
+  const int lane = threadIdx.x;
+  const int inst = blockIdx.x;
+  const int k = inst % a.nbatch;
+  const FrontDev F = a.fronts[a.list[inst / a.nbatch]];
+  const int n = F.n, p = F.p;
+  if (kb >= p) return;
+  const int w = min(NB, p - kb);
+  const int nrhs = a.nrhs, nx = a.nx;
+  cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
+  cplx* Zk = a.Z + (int64_t)k * nx * nrhs;
+  const int64_t shift = a.shift0 + k;
+  const cplx zero = cmk(0.0, 0.0);
+  for (int c = 0; c < w; ++c)
+    if (lane >= c && lane < w) Ld[c * LDD + lane] = ldc(P + (kb + lane) + (int64_t)(kb + c) * n);
+  __syncwarp();
+  // step j: a_ic -= (a_ij / d_j) a_cj on unscaled values; then columns scale by 1/c_j = d_j^{-1/2}
+  for (int j = 0; j < w; ++j) {
+    const cplx d = Ld[j * LDD + j];
+    if (lane > j && lane < w) {
+      const cplx f = cmul(Ld[j * LDD + lane], crecip_fast(d));
+      cplx* __restrict__ rowp = Ld + lane;
+      const cplx* __restrict__ colj = Ld + j * LDD;
+      int c = j + 1;
+      for (; c + 3 <= lane; c += 4) {
+        const cplx x0 = rowp[c * LDD], x1 = rowp[(c + 1) * LDD], x2 = rowp[(c + 2) * LDD],
+                   x3 = rowp[(c + 3) * LDD];
+        const cplx y0 = colj[c], y1 = colj[c + 1], y2 = colj[c + 2], y3 = colj[c + 3];
+        rowp[c * LDD] = cfms(x0, f, y0);
+        rowp[(c + 1) * LDD] = cfms(x1, f, y1);
+        rowp[(c + 2) * LDD] = cfms(x2, f, y2);
+        rowp[(c + 3) * LDD] = cfms(x3, f, y3);
+      }
+      for (; c <= lane; ++c) rowp[c * LDD] = cfms(rowp[c * LDD], f, colj[c]);
+    }
+    __syncwarp();
+  }
+  if (lane < w) {
+    const cplx d = Ld[lane * LDD + lane];
+    const double m2 = cabs2(d);
+    if (!(m2 > 1e-300) || !isfinite(m2)) atomicCAS(a.err, 0, (int)shift + 1);
+    const cplx c = csqrt_(d);
+    cdg[lane] = c;
+    dinv_s[lane] = crecip(c);
+  }
+  __syncwarp();
+  for (int j = 0; j < w; ++j) {
+    if (lane == j) Ld[j * LDD + j] = cdg[j];
+    else if (lane > j && lane < w) Ld[j * LDD + lane] = cmul(Ld[j * LDD + lane], dinv_s[j]);
+  }
+  __syncwarp();
+  for (int c = 0; c < w; ++c)
+    if (lane >= c && lane < w) stc(P + (kb + lane) + (int64_t)(kb + c) * n, Ld[c * LDD + lane]);
+  // y = C11^{-1} r, lane c holds y_c; one warp reduction per step
+  for (int r = 0; r < nrhs; ++r) {
+    cplx* z = Zk + F.pbeg + kb + (int64_t)r * nx;
+    cplx yl = lane < w ? ldc(z + lane) : zero;
+    for (int j = 0; j < w; ++j) {
+      cplx s = lane < j ? cmul(Ld[lane * LDD + j], yl) : zero;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        s.re += __shfl_xor_sync(0xffffffffu, s.re, o);
+        s.im += __shfl_xor_sync(0xffffffffu, s.im, o);
+      }
+      if (lane == j) yl = cmul(csub(yl, s), dinv_s[j]);
+    }
+    if (lane < w) stc(z + lane, yl);
+  }
+}
+
+// rows below panel kb: x C11^T = b per row (thread per row, W-wide register
+// block, right-looking so the W updates of a step are independent), then the
+// row's forward RHS r -= x y.  W = panel width rounded up (16 or 32).
+template <int W>
+__global__ void __launch_bounds__(TR_ROWS) trsm_kernel(LevelArgs a, int kb) {
+  __shared__ cplx Ls[W * W];          // Ls[c * W + c'] = C[kb+c][kb+c'] (c' < c); Ls[c*W+c] = 1 / c_cc
+  __shared__ cplx ys[W * MAXR];
+  const int tid = threadIdx.x;
+  const int inst = blockIdx.x;
+  const int k = inst % a.nbatch;
+  const FrontDev F = a.fronts[a.list[inst / a.nbatch]];
+  const int n = F.n, p = F.p, b = n - p;
+  if (kb >= p) return;
+  const int w = min(NB, p - kb);
+  const int r0 = kb + w + blockIdx.y * TR_ROWS;
+  if (r0 >= n) return;
+  const int nrhs = a.nrhs, nx = a.nx;
+  cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
+  cplx* Zk = a.Z + (int64_t)k * nx * nrhs;
+  const cplx zero = cmk(0.0, 0.0);
+  for (int idx = tid; idx < W * W; idx += TR_ROWS) {
+    const int c = idx / W, c2 = idx % W;
+    cplx v = zero;
+    if (c < w && c2 <= c) {
+      v = ldc(P + (kb + c) + (int64_t)(kb + c2) * n);
+      if (c2 == c) v = crecip(v);
+    } else if (c2 == c) {
+      v = cmk(1.0, 0.0);
+    }
+    Ls[idx] = v;
+  }
+  for (int idx = tid; idx < W * nrhs; idx += TR_ROWS) {
+    const int c = idx % W, r = idx / W;
+    ys[c * MAXR + r] = c < w ? ldc(Zk + F.pbeg + kb + c + (int64_t)r * nx) : zero;
+  }
+  __syncthreads();
+  const int i = r0 + tid;
+  if (i >= n) return;
+  cplx* prow = P + i + (int64_t)kb * n;
+  cplx x[W];
+#pragma unroll
+  for (int c = 0; c < W; ++c) x[c] = c < w ? ldc(prow + (int64_t)c * n) : zero;
+#pragma unroll
+  for (int c = 0; c < W; ++c) {
+    x[c] = cmul(x[c], Ls[c * W + c]);
+#pragma unroll
+    for (int c2 = c + 1; c2 < W; ++c2) x[c2] = cfms(x[c2], x[c], Ls[c2 * W + c]);
+  }
+#pragma unroll
+  for (int c = 0; c < W; ++c)
+    if (c < w) stc(prow + (int64_t)c * n, x[c]);
+  for (int r = 0; r < nrhs; ++r) {
+    cplx* dst = (i < p) ? Zk + F.pbeg + i + (int64_t)r * nx : a.rcur + ((int64_t)k * a.rcur_stride + F.rofs) * nrhs +
+                                                                  (i - p) + (int64_t)r * b;
+    cplx acc = ldc(dst);
+#pragma unroll
+    for (int c = 0; c < W; ++c) acc = cfms(acc, x[c], ys[c * MAXR + r]);
+    stc(dst, acc);
+  }
+}
+
+// number of 64x64 tiles of the trailing pivot-column update after panel kb
+__host__ __device__ inline int panel_update_tiles(int n, int p, int kb) {
+  const int base = kb + NB;
+  if (base >= p) return 0;
+  const int tm = (n - base + TM - 1) / TM, tn = (p - base + TM - 1) / TM;
+  return tn * tm - tn * (tn - 1) / 2;
+}
+
+// trailing pivot-column update after a full panel: F[base:n, base:p] -= X X^T
+// (X = the panel's TRSM'd rows), lower trapezoid, one 64x64 tile per CTA, DMMA
+__global__ void __launch_bounds__(NT, 2) panel_update_kernel(LevelArgs a, int kb) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* gsm = reinterpret_cast<cplx*>(smem_raw);
+  const int inst = blockIdx.x;
+  const int k = inst % a.nbatch;
+  const FrontDev F = a.fronts[a.list[inst / a.nbatch]];
+  const int n = F.n, p = F.p;
+  const int base = kb + NB;
+  if (base >= p) return;
+  const int tm = (n - base + TM - 1) / TM, tn = (p - base + TM - 1) / TM;
+  int t = blockIdx.y, ti = -1, tj = 0;
+  for (; tj < tn; ++tj) {
+    if (t < tm - tj) {
+      ti = tj + t;
+      break;
+    }
+    t -= tm - tj;
+  }
+  if (ti < 0) return;
+  cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
+  cplx* C = P + base + (int64_t)base * n;
+  gemm_update<2>(C, n, n - base, p - base, P + base + (int64_t)kb * n, n, P + base + (int64_t)kb * n, n, NB,
+                 true, gsm, ti, tj, CLoad{C, n});
+}

@@ -26,7 +26,7 @@ struct FrontDev {
   int32_t relpos_beg;  // into relpos: position of each boundary row in the parent front
   int32_t parent, depth;
   int32_t inv_beg;     // into inv: nchild x n map parent row -> child boundary row (-1 if none)
-  int32_t pad_;
+  int32_t colptr_beg;  // into ent_colptr: p + 1 offsets (relative to ent_beg) of each pivot column's entries
   int64_t fofs;        // factor block offset (complex elements) within one shift
   int64_t uofs;        // update block offset within the pool of parity depth%2 (one shift)
   int64_t rofs;        // forward-RHS update offset (units of b, times nrhs) within its pool
@@ -47,7 +47,7 @@ struct Plan {
   int64_t nnz_pattern = 0;
   std::vector<int32_t> perm, iperm;       // perm[new] = old
   std::vector<FrontDev> fronts;           // postorder
-  std::vector<int32_t> child_ids, bidx, relpos, ent_src, ent_dst, inv;
+  std::vector<int32_t> child_ids, bidx, relpos, ent_src, ent_dst, inv, ent_colptr;
   std::vector<std::vector<int32_t>> levels;  // fronts per depth
   int32_t depth = 0, max_front = 0, max_pivots = 0;
   int64_t factor_stride = 0;               // complex per shift
@@ -73,7 +73,7 @@ struct Plan {
   bool force_big = getenv("STFEM_FORCE_BIG") != nullptr;  // diagnostics: disable the small-front path
   int small_n_cap = getenv("STFEM_SMALL_N") ? atoi(getenv("STFEM_SMALL_N")) : 0;  // tuning: lower the threshold
   int32_t *d_child_ids = nullptr, *d_bidx = nullptr, *d_relpos = nullptr, *d_inv = nullptr;
-  int32_t *d_ent_src = nullptr, *d_ent_dst = nullptr, *d_perm = nullptr;
+  int32_t *d_ent_src = nullptr, *d_ent_dst = nullptr, *d_perm = nullptr, *d_ent_colptr = nullptr;
   double *d_ent_mv = nullptr, *d_ent_av = nullptr;   // M_x / A_x values gathered into entry order
   std::vector<int64_t> syrk_off;           // per depth: offsets into d_syrk_tiles
   int4* d_syrk_tiles = nullptr;            // (front, ti, tj, 0) Schur-update tiles of the large fronts
@@ -81,7 +81,8 @@ struct Plan {
   SubDev* d_subs = nullptr;
   double *d_V = nullptr, *d_th = nullptr, *d_RQ = nullptr, *d_C01 = nullptr;
   int4* d_spec_items = nullptr;
-  std::vector<int64_t> spec_off;           // (depth+1)*4 + 1: fwd1, fwd2, bwd1, bwd2 item ranges per depth
+  std::vector<int64_t> spec_off;
+  int spec_smem = 0;                       // dynamic shared memory of spectral_kernel           // (depth+1)*4 + 1: fwd1, fwd2, bwd1, bwd2 item ranges per depth
 
   // ---- numeric workspace (per batch of shifts) ----
   int32_t batch = 0;       // requested (0 = auto)

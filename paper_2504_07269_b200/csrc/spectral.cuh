@@ -40,6 +40,8 @@ constexpr int SP_LDB = SP_BN + 2;   // Bs[k][col] complex: (t*66 + g) mod 8 hits
 constexpr int SP_A_STAGE = SP_BK * SP_LDA;   // doubles
 constexpr int SP_B_STAGE = SP_BK * SP_LDB;   // complex
 constexpr int SP_SMEM = 2 * (SP_A_STAGE * 8 + SP_B_STAGE * 16);
+// + OP_U staging: 16 R rows and theta over the subtree's m, 64 shifts
+__host__ __device__ constexpr int spectral_smem_bytes(int mmax) { return SP_SMEM + (17 * mmax + 1) * 8 + SP_BN * 16; }
 enum { OP_U = 0, OP_F1 = 1, OP_F2 = 2, OP_B1 = 3, OP_B2 = 4 };
 
 struct SpecArgs {
@@ -80,13 +82,27 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
   const int gq = lane >> 2, tq = lane & 3, wm = warp & 1, wn = warp >> 1;
   const cplx zero = cmk(0.0, 0.0);
 
+  // OP_U operands are generated from shared memory: the 16 R rows of the
+  // tile's (i, j) block over all k, theta, and the tile's 64 shifts
+  double* Rs = reinterpret_cast<double*>(Bs + 2 * SP_B_STAGE);   // [16][m]
+  double* ths = Rs + 16 * m;
+  cplx* lams = reinterpret_cast<cplx*>(ths + ((17 * m + 1) & ~1) - 16 * m);   // 16-byte aligned
+  if constexpr (OP == OP_U) {
+    for (int q = tid; q < 16 * m; q += 256) {
+      const int rr = q / m, k = q - rr * m;
+      const int row = rr < 8 ? it.z * 8 + rr : it.w * 8 + rr - 8;
+      Rs[q] = row < g ? Rm[row + (int64_t)k * g] : 0.0;
+    }
+    for (int q = tid; q < m; q += 256) ths[q] = th[q];
+    if (tid < SP_BN) lams[tid] = n0 + tid < ncols ? a.lam[n0 + tid] : cmk(1.0, 0.0);
+    __syncthreads();
+  }
+
   // ---- operand generators ----
   auto a_val = [&](int r, int k) -> double {
     if (k >= K) return 0.0;
     if (OP == OP_U) {
-      const int i = it.z * 8 + (r >> 3), j = it.w * 8 + (r & 7);
-      if (i >= g || j >= g) return 0.0;
-      return Rm[i + (int64_t)k * g] * Rm[j + (int64_t)k * g];
+      return Rs[(r >> 3) * m + k] * Rs[(8 + (r & 7)) * m + k];
     } else if (OP == OP_F1) {
       const int ko = it.z * SP_BM + r;
       return ko < m ? V[k + (int64_t)ko * m] : 0.0;
@@ -106,7 +122,7 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
   auto b_val = [&](int k, int c) -> cplx {
     const int cg = n0 + c;
     if (k >= K || cg >= ncols) return zero;
-    if (OP == OP_U) return spec_w(th[k], a.lam[cg]);
+    if (OP == OP_U) return spec_w(ths[k], lams[c]);
     const int s = cg / nrhs, r = cg - s * nrhs;
     const cplx* Zs = a.Z + (int64_t)s * nx * nrhs + (int64_t)r * nx;
     if (OP == OP_F1) return ldc(a.G + bv_off(a.lay, r, a.shift0 + s, a.perm[S.first + k]));

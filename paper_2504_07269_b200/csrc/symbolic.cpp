@@ -292,6 +292,7 @@ int build_symbolic(Plan& P, int32_t n, const int64_t* rowptr, const int32_t* col
     }
   }
   for (int32_t f = 0; f < nf; ++f) cnt[f + 1] += cnt[f];
+  P.ent_colptr.clear();
   P.ent_src.assign(e_src.size(), 0);
   P.ent_dst.assign(e_src.size(), 0);
   {
@@ -305,6 +306,24 @@ int build_symbolic(Plan& P, int32_t n, const int64_t* rowptr, const int32_t* col
   for (int32_t f = 0; f < nf; ++f) {
     P.fronts[f].ent_beg = cnt[f];
     P.fronts[f].ent_cnt = cnt[f + 1] - cnt[f];
+    // column-major order within the front: a column block's entries are one
+    // contiguous range (the large-front assembly binary-searches it)
+    std::vector<std::pair<int32_t, int32_t>> ed(P.fronts[f].ent_cnt);
+    for (int32_t q = 0; q < P.fronts[f].ent_cnt; ++q)
+      ed[q] = {P.ent_dst[cnt[f] + q], P.ent_src[cnt[f] + q]};
+    std::sort(ed.begin(), ed.end());
+    for (int32_t q = 0; q < P.fronts[f].ent_cnt; ++q) {
+      P.ent_dst[cnt[f] + q] = ed[q].first;
+      P.ent_src[cnt[f] + q] = ed[q].second;
+    }
+    // column pointers: entries of pivot column c are [colptr[c], colptr[c+1])
+    FrontDev& F = P.fronts[f];
+    F.colptr_beg = (int32_t)P.ent_colptr.size();
+    int32_t q = 0;
+    for (int32_t c = 0; c <= F.p; ++c) {
+      while (q < F.ent_cnt && ed[q].first < c * F.n) ++q;
+      P.ent_colptr.push_back(q);
+    }
   }
 
   // ---- levels, offsets, statistics ----
