@@ -42,8 +42,6 @@ constexpr int MAXR = 16;          // max RHS per call (bv chunks of 16 in the ho
 
 constexpr int GEMM_SMEM = (2 * 2 * TK * LDS + 2 * TK) * 16;
 constexpr int SYRK_SMEM = (3 * 2 * TK * LDS) * 16;   // 3-stage pipeline of the standalone Schur kernel
-constexpr int DIAG_SMEM = (NB * LDD + 2 * NB + NB * MAXR) * 16;
-constexpr int FACTOR_SMEM = GEMM_SMEM + DIAG_SMEM;
 constexpr int BWD_XS_MAX = 192 * 1024;   // backward_level_kernel: staged x (n x nrhs) per front
 
 struct LevelArgs {
@@ -129,8 +127,8 @@ __device__ void gemm_update(cplx* __restrict__ C, int ldC, int M, int N, const c
       }
     };
 
-    // accumulators start as C (loads issued together with the first cp.async
-    // stage so their latency overlaps); the MMAs subtract A D B^T in place
+    // accumulators start as cinit(row, col) (loads issued together with the
+    // first cp.async stages so their latency overlaps); the MMAs subtract A B^T
     double cre[2][2][4], cim[2][2][4];
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
@@ -231,8 +229,17 @@ __global__ void __launch_bounds__(NT, 2) syrk_level_kernel(LevelArgs a, const in
   gemm_update<3>(U, b, b, b, P + p, n, P + p, n, p, true, gsm, tl.y, tl.z, CLoad{U, b});
 }
 
+// Backward substitution of one level, one CTA per (front, shift) instance:
+//   1. x of the boundary rows (final: they belong to ancestors) is staged in
+//      shared memory together with z of the pivot rows;
+//   2. the boundary part of every pivot column, t_j = z_j - L[p:n, j]^T x_B,
+//      runs for all p columns at once (warp per column, coalesced columns);
+//   3. the pivot triangle is swept in panels of NB from the last one: the
+//      panel's columns subtract the already-solved pivot rows below it, then
+//      one warp solves the transposed w x w triangle.
+// unit = 1: unit-L LDL^T fronts (z already D^{-1}-scaled); 0: C C^T fronts.
+template <int NR>
 __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int unit) {
-  __shared__ cplx ts[NB * MAXR];
   __shared__ cplx l11[NB * LDD];   // l11[c * LDD + i] = L[kb+i][kb+c], i > c; diagonal: 1/L[c][c] (or 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int inst = blockIdx.x;
@@ -244,33 +251,59 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int uni
   cplx* Zk = a.Z + (int64_t)k * nx * nrhs;
   const int32_t* bidx = a.bidx + F.bidx_beg;
   const int64_t shift = a.shift0 + k;
-  // x of the whole front staged in shared memory (n x nrhs): boundary rows
-  // gathered once here, pivot rows filled in as they are solved
+  const cplx zero = cmk(0.0, 0.0);
   extern __shared__ __align__(16) unsigned char bwd_smem[];
-  cplx* xs = reinterpret_cast<cplx*>(bwd_smem);
-  for (int q = tid; q < (n - p) * nrhs; q += NT) {
-    const int i = p + q % (n - p), r = q / (n - p);
-    xs[i * nrhs + r] = ldc(Zk + bidx[i - p] + (int64_t)r * nx);
+  cplx* xs = reinterpret_cast<cplx*>(bwd_smem);   // n x nrhs: x (boundary rows), t then x (pivot rows)
+  for (int q = tid; q < n * nrhs; q += NT) {
+    const int i = q / nrhs, r = q - i * nrhs;
+    xs[q] = ldc(Zk + (i < p ? F.pbeg + i : bidx[i - p]) + (int64_t)r * nx);
   }
   __syncthreads();
-
-  for (int kb = ((p - 1) / NB) * NB; kb >= 0; kb -= NB) {
-    const int w = min(NB, p - kb);
-    // t_j = z_j - sum_{i >= kb+w} L[i][kb+j] x_i   (warp per column)
-    for (int j = warp; j < w; j += NT / 32) {
-      cplx acc[MAXR];
+  // 2. boundary contributions of all pivot columns (parallel over columns)
+  if (n > p) {
+    for (int j = warp; j < p; j += NT / 32) {
+      cplx acc[NR];
 #pragma unroll
-      for (int r = 0; r < MAXR; ++r) acc[r] = cmk(0.0, 0.0);
-      const cplx* col = P + (int64_t)(kb + j) * n;
-      for (int i = kb + w + lane; i < n; i += 32) {
+      for (int r = 0; r < NR; ++r) acc[r] = zero;
+      const cplx* col = P + (int64_t)j * n;
+      for (int i = p + lane; i < n; i += 32) {
         const cplx l = ldc(col + i);
 #pragma unroll
-        for (int r = 0; r < MAXR; ++r)
+        for (int r = 0; r < NR; ++r)
           if (r < nrhs) acc[r] = cfma(l, xs[i * nrhs + r], acc[r]);
       }
 #pragma unroll
-      for (int r = 0; r < MAXR; ++r) {
-        if (r < nrhs) {
+      for (int r = 0; r < NR; ++r) {
+        if (r >= nrhs) break;
+        double re = acc[r].re, im = acc[r].im;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          re += __shfl_xor_sync(0xffffffffu, re, o);
+          im += __shfl_xor_sync(0xffffffffu, im, o);
+        }
+        if (lane == 0) xs[j * nrhs + r] = cmk(xs[j * nrhs + r].re - re, xs[j * nrhs + r].im - im);
+      }
+    }
+    __syncthreads();
+  }
+  // 3. pivot triangle, panels from the last
+  for (int kb = ((p - 1) / NB) * NB; kb >= 0; kb -= NB) {
+    const int w = min(NB, p - kb);
+    if (kb + w < p) {
+      for (int j = warp; j < w; j += NT / 32) {
+        cplx acc[NR];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) acc[r] = zero;
+        const cplx* col = P + (int64_t)(kb + j) * n;
+        for (int i = kb + w + lane; i < p; i += 32) {
+          const cplx l = ldc(col + i);
+#pragma unroll
+          for (int r = 0; r < NR; ++r)
+            if (r < nrhs) acc[r] = cfma(l, xs[i * nrhs + r], acc[r]);
+        }
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          if (r >= nrhs) break;
           double re = acc[r].re, im = acc[r].im;
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) {
@@ -278,15 +311,12 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int uni
             im += __shfl_xor_sync(0xffffffffu, im, o);
           }
           if (lane == 0) {
-            cplx z = ldc(Zk + F.pbeg + kb + j + (int64_t)r * nx);
-            ts[j * MAXR + r] = cmk(z.re - re, z.im - im);
+            cplx* t = xs + (kb + j) * nrhs + r;
+            *t = cmk(t->re - re, t->im - im);
           }
         }
       }
     }
-    __syncthreads();
-    // stage the diagonal block, then the transposed triangle (thread per rhs);
-    // unit = LDL^T fronts (unit L, z already D^{-1}-scaled), else C C^T fronts
     for (int idx = tid; idx < w * w; idx += NT) {
       const int i = idx % w, c = idx / w;
       if (i > c) l11[c * LDD + i] = ldc(P + (kb + i) + (int64_t)(kb + c) * n);
@@ -294,28 +324,42 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int uni
     }
     __syncthreads();
     if (warp == 0) {
-      // x_j = (t_j - sum_{c>j} L[c][j] x_c) * dinv_j, lane c holds x_c; one warp
-      // reduction per step instead of a single-thread dependent chain
+      // x_j = (t_j - sum_{c>j} L[c][j] x_c) * dinv_j, lane c holds x_c; one warp reduction per step
       for (int r = 0; r < nrhs; ++r) {
-        cplx xl = lane < w ? ts[lane * MAXR + r] : cmk(0.0, 0.0);
+        cplx xl = lane < w ? xs[(kb + lane) * nrhs + r] : zero;
         for (int j = w - 1; j >= 0; --j) {
-          cplx s = (lane > j && lane < w) ? cmul(l11[j * LDD + lane], xl) : cmk(0.0, 0.0);
+          cplx sacc = (lane > j && lane < w) ? cmul(l11[j * LDD + lane], xl) : zero;
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) {
-            s.re += __shfl_xor_sync(0xffffffffu, s.re, o);
-            s.im += __shfl_xor_sync(0xffffffffu, s.im, o);
+            sacc.re += __shfl_xor_sync(0xffffffffu, sacc.re, o);
+            sacc.im += __shfl_xor_sync(0xffffffffu, sacc.im, o);
           }
-          if (lane == j) xl = cmul(csub(xl, s), l11[j * LDD + j]);
+          if (lane == j) xl = cmul(csub(xl, sacc), l11[j * LDD + j]);
         }
         if (lane < w) {
           stc(Zk + F.pbeg + kb + lane + (int64_t)r * nx, xl);
-          a.W[bv_off(a.lay, r, shift, a.perm[F.pbeg + kb + lane])] = xl;
+          stc(a.W + bv_off(a.lay, r, shift, a.perm[F.pbeg + kb + lane]), xl);
           xs[(kb + lane) * nrhs + r] = xl;
         }
       }
     }
     __syncthreads();
   }
+}
+
+template <int NR>
+int launch_backward_level(const LevelArgs& a, int grid, int nmax, int unit, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_level_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        BWD_XS_MAX));
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_level_kernel<NR>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        100));
+    attr = true;
+  }
+  backward_level_kernel<NR><<<grid, NT, (size_t)nmax * a.nrhs * 16, s>>>(a, unit);
+  STFEM_LAUNCH_CHECK("backward_level_kernel");
+  return STFEM_OK;
 }
 
 #include "multifrontal_small.cuh"
@@ -379,9 +423,6 @@ int upload(Plan& P) {
   STFEM_CUDA_TRY(cudaMemset(P.d_err, 0, sizeof(int)));
   STFEM_CUDA_TRY(cudaFuncSetAttribute(panel_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM));
   STFEM_CUDA_TRY(cudaFuncSetAttribute(panel_update_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      BWD_XS_MAX));
-  STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_level_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   P.level_nmax.assign(P.levels.size(), 0);
   P.level_pmax.assign(P.levels.size(), 0);
   for (size_t d = 0; d < P.levels.size(); ++d)
@@ -733,8 +774,15 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
       if (nmax <= SMALL_N && bsm <= 200 * 1024 && !P.force_big) {
         if ((rc = launch_small_backward_any(a, a.nlist * nb, nmax, pmax, stream))) return rc;
       } else {
-        backward_level_kernel<<<a.nlist * nb, NT, (size_t)nmax * nrhs * 16, stream>>>(a, ldlt ? 1 : 0);
-        STFEM_LAUNCH_CHECK("backward_level_kernel");
+        const int u = ldlt ? 1 : 0, gsz = a.nlist * nb;
+        switch (small_nr(nrhs)) {
+          case 1: rc = launch_backward_level<1>(a, gsz, nmax, u, stream); break;
+          case 2: rc = launch_backward_level<2>(a, gsz, nmax, u, stream); break;
+          case 4: rc = launch_backward_level<4>(a, gsz, nmax, u, stream); break;
+          case 8: rc = launch_backward_level<8>(a, gsz, nmax, u, stream); break;
+          default: rc = launch_backward_level<16>(a, gsz, nmax, u, stream); break;
+        }
+        if (rc) return rc;
       }
       ++nlaunch;
       mark();
