@@ -248,7 +248,6 @@ def run_ours(args):
     fdm.plan.record_levels(True)
     step(timings=st)
     fdm.plan.record_levels(False)
-    f_ms, b_ms, lvl_flops, lvl_small = fdm.plan.level_report()
     dofs = prob.nx * prob.nt * prob.n_rhs
     value = dofs / t_step
 
@@ -282,30 +281,57 @@ def run_ours(args):
                "ms_per_step": te * 1e3}
         del Ph
 
-    # roofline of the dominant kernel (by time in the recorded step), FP64 tensor/DFMA pipe
+    # roofline of the dominant kernel family (by CUDA-event time in the recorded step)
     flops_factor = fdm.plan.stats["flops_factor"] * prob.nt
     flops_tr = 2 * 8.0 * prob.nt * prob.nt * prob.nx * prob.n_rhs
     peak = dmma_peak_live()
     t_fs = st["factor_solve_s"]
     t_tr = st["forward_transform_s"] + st["back_transform_s"]
-    big_ms, small_ms = float(f_ms[~lvl_small].sum()), float(f_ms[lvl_small].sum())
-    kernels = {"factor_level_kernel": (big_ms, float(lvl_flops[~lvl_small].sum()) * prob.nt,
-                                       int((~lvl_small).sum())),
-               "factor_small_kernel": (small_ms, float(lvl_flops[lvl_small].sum()) * prob.nt,
-                                       int(lvl_small.sum()))}
-    top = max(kernels, key=lambda k: kernels[k][0])
-    ms_top, fl_top, nlev_top = kernels[top]
-    launches_top = nlev_top * fdm.plan.last_num_batches()
-    ach = fl_top / (ms_top / 1e3) / 1e12 if ms_top > 0 else 0.0
-    roof = {"bound": "tensor", "kernel": f"{top} (multifrontal K4, {launches_top} launches/step)",
-            "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "traffic": None,
-            "avg_launch_ms": ms_top / max(1, launches_top),
-            "peak_source": "FP64 DMMA peak measured live by a register-only DMMA probe (not in MEASURED_PEAKS.json)",
-            "algorithmic": "sum over the kernel's fronts of sum_j 4 c_j^2 real flops per shift x n_t shifts"}
-    roof_phase = {"kernel": "whole multifrontal phase (K4+K5)", "achieved": flops_factor / t_fs / 1e12,
-                  "frac": flops_factor / t_fs / 1e12 / peak,
-                  "share_ms": {"factor_level_kernel": big_ms, "factor_small_kernel": small_ms,
-                               "backward_kernels": float(b_ms.sum())}}
+    rep = fdm.plan.kernel_report()
+    if fdm.plan.spectral is not None:
+        ss = fdm.plan.spectral_stats()
+        rep["spectral"] = (rep["spectral"][0], ss["flops_u"] + prob.n_rhs * ss["flops_rhs"], rep["spectral"][2])
+    names = {"spectral": "spectral_kernel (K6 spectral subtrees, DMMA)",
+             "assembly": "asm_front_kernel (front assembly, HBM)",
+             "diag": "diag_kernel (diagonal blocks, FP64)",
+             "trsm": "trsm_kernel (panel TRSM, FP64)",
+             "panel_update": "panel_update_kernel (trailing pivot columns, DMMA)",
+             "syrk": "syrk_level_kernel (Schur update U = F22 - L21 L21^T, DMMA)",
+             "backward": "backward kernels (HBM)",
+             "small_factor": "factor_small_kernel (shared-memory fronts)"}
+    fam = {}
+    for k, (ms, fl, nl) in rep.items():
+        if nl == 0:
+            continue
+        tf = fl * prob.nt / (ms / 1e3) / 1e12 if ms > 0 else 0.0
+        fam[k] = {"ms": ms, "launches": nl, "tflops": tf, "frac_dmma": tf / peak}
+    fam["transform"] = {"ms": t_tr * 1e3, "launches": 2, "tflops": flops_tr / t_tr / 1e12,
+                        "frac_dmma": flops_tr / t_tr / 1e12 / peak}
+    top = max(fam, key=lambda k: fam[k]["ms"])
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tr_all = json.load(f)
+        ent = tr_all.get(f"{args.workload}:{top}")
+        if ent:
+            traffic = ent["dram_bytes_per_launch"]
+    if top == "transform":
+        roof = {"bound": "tensor", "kernel": "time_transform_kernel (K3, DMMA)", "achieved": fam[top]["tflops"],
+                "peak": peak, "unit": "TFLOP/s", "frac": fam[top]["tflops"] / peak, "traffic": traffic,
+                "avg_launch_ms": t_tr * 1e3 / 2}
+    else:
+        f = fam[top]
+        roof = {"bound": "tensor", "kernel": f"{names[top]}; {f['launches']} launches/step",
+                "achieved": f["tflops"], "peak": peak, "unit": "TFLOP/s", "frac": f["tflops"] / peak,
+                "traffic": traffic, "avg_launch_ms": f["ms"] / max(1, f["launches"])}
+    roof.update({"peak_source": "FP64 DMMA peak measured live by a register-only DMMA probe (MEASURED_PEAKS.json "
+                                "has no FP64 entry)",
+                 "algorithmic": "flops per launch = the family's algorithmic real flops (complex MAC = 8) per shift "
+                                "x shifts, e.g. SYRK sum over fronts of 4 b^2 p; traffic = ncu dram bytes per launch "
+                                "(profiles/ncu_traffic.json)"})
+    roof_phase = {"kernel": "whole multifrontal phase (K4+K5+K6), algorithmic LDL^T flops",
+                  "achieved": flops_factor / t_fs / 1e12, "frac": flops_factor / t_fs / 1e12 / peak}
     roof_tr = {"bound": "tensor", "kernel": "time_transform_kernel (K3)", "achieved": flops_tr / t_tr / 1e12,
                "peak": peak, "unit": "TFLOP/s", "frac": flops_tr / t_tr / 1e12 / peak}
     launches = 2 + fdm.plan.last_launches()   # two K3 transforms + the multifrontal level launches
@@ -334,8 +360,10 @@ def run_ours(args):
                    "dofs_per_rhs": prob.nx * prob.nt, "parallelism": f"replicas{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (F, G, Psi each > 126 MB); no flush"},
         "stages_s": st, "setup_s": t_setup, "asm_s": t_asm, "eig_s": fdm.t_eig, "symbolic_s": fdm.t_symbolic,
+        "spectral_setup_s": fdm.plan.t_spectral,
         "paper_time_s": t_setup + t_step, "relative_residual": res, "kappa2": fdm.kappa2,
         "roofline": roof, "roofline_multifrontal": roof_phase, "roofline_transform": roof_tr,
+        "kernel_families": fam,
         "gpu_launches": launches * args.steps,
         "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
     }

@@ -126,6 +126,12 @@ int stfem_plan_set_batch(stfem_plan* plan, int32_t batch, int64_t* bytes_per_shi
  * on the shared-memory small-front kernels (small[depth+1]) */
 int stfem_plan_record_levels(stfem_plan* plan, int32_t on);
 int stfem_plan_level_report(const stfem_plan* plan, double* ms, double* flops, int32_t* small);
+/* per-kernel-family accounting of the last recorded call: ms[f] (CUDA-event
+ * time), launches[f], and algorithmic real flops per shift flops[f] for the families
+ * 0 spectral (K6), 1 front assembly, 2 diagonal blocks, 3 TRSM, 4 trailing
+ * pivot-column update, 5 SYRK (Schur update), 6 backward, 7 small-front factor */
+int stfem_plan_kernel_report(const stfem_plan* plan, int32_t nfam, double* ms, double* flops,
+                             int64_t* launches);
 /* largest nrhs one stfem_factor_solve call accepts for this plan (<= 16) */
 int stfem_plan_max_rhs(const stfem_plan* plan, int32_t* max_rhs);
 /* shift batches used by the last stfem_factor_solve call */

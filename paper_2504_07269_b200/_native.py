@@ -71,6 +71,7 @@ def _declare(lib):
         "stfem_plan_max_rhs": (C.c_int, [P, C.POINTER(I32)]),
         "stfem_plan_record_levels": (C.c_int, [P, I32]),
         "stfem_plan_level_report": (C.c_int, [P, P, P, P]),
+        "stfem_plan_kernel_report": (C.c_int, [P, I32, P, P, P]),
         "stfem_plan_set_spectral": (C.c_int, [P, I32, P, P, P, P, I64, P, I64, P, I64, P, I64]),
         "stfem_plan_spectral_stats": (C.c_int, [P, C.POINTER(I32), C.POINTER(D), C.POINTER(D),
                                                 C.POINTER(I64)]),

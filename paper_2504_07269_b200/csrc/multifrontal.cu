@@ -44,6 +44,9 @@ constexpr int GEMM_SMEM = (2 * 2 * TK * LDS + 2 * TK) * 16;
 constexpr int SYRK_SMEM = (3 * 2 * TK * LDS) * 16;   // 3-stage pipeline of the standalone Schur kernel
 constexpr int BWD_XS_MAX = 192 * 1024;   // backward_level_kernel: staged x (n x nrhs) per front
 
+// kernel families of the per-family accounting (stfem_plan_kernel_report)
+enum { FAM_SPECTRAL = 0, FAM_ASM, FAM_DIAG, FAM_TRSM, FAM_PANEL, FAM_SYRK, FAM_BACKWARD, FAM_SMALL, NFAM };
+
 struct LevelArgs {
   const FrontDev* fronts;
   const int32_t* list;
@@ -544,6 +547,9 @@ int auto_batch(Plan& P, int nshift, int nrhs) {
 Plan::~Plan() {
   free_workspace();
   free_device();
+  for (auto st : lane_streams) cudaStreamDestroy(st);
+  for (auto ev : lane_events) cudaEventDestroy(ev);
+  if (start_event) cudaEventDestroy(start_event);
 }
 
 void Plan::free_device() {
@@ -650,6 +656,17 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
   static const bool level_print = getenv("STFEM_LEVEL_TIMING") != nullptr;
   const bool level_timing = level_print || P.record_levels;
   std::vector<cudaEvent_t> evs;
+  // per-kernel-family accounting (record mode): event after every launch,
+  // the gap to the previous event is charged to the launch's family
+  cudaEvent_t fev_start = nullptr;
+  std::vector<std::pair<cudaEvent_t, int>> fevs;
+  auto fam = [&](int f, cudaStream_t st) {
+    if (!level_timing) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    fevs.push_back({e, f});
+  };
   auto mark = [&]() {
     if (!level_timing) return;
     cudaEvent_t e;
@@ -657,12 +674,37 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
     cudaEventRecord(e, stream);
     evs.push_back(e);
   };
-  mark();
-  for (int s0 = 0; s0 < nshift; s0 += batch) {
-    const int nb = std::min(batch, nshift - s0);
+  // shift lanes (STFEM_STREAMS, default 1: measured no gain on C4 since every
+  // level launch already fills the GPU): the batch workspace is split into `lanes` slices, each run on
+  // its own stream so the latency-bound kernels of one lane overlap the
+  // tensor-core kernels of another (per-level timing runs single-lane)
+  static const int lanes_env = getenv("STFEM_STREAMS") ? std::max(1, atoi(getenv("STFEM_STREAMS"))) : 1;
+  const int lanes = level_timing ? 1 : std::min(lanes_env, batch);
+  if ((int)P.lane_streams.size() < lanes) {
+    for (int j = (int)P.lane_streams.size(); j < lanes; ++j) {
+      cudaStream_t st;
+      cudaEvent_t ev;
+      STFEM_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+      STFEM_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      P.lane_streams.push_back(st);
+      P.lane_events.push_back(ev);
+    }
+    STFEM_CUDA_TRY(cudaEventCreateWithFlags(&P.start_event, cudaEventDisableTiming));
+  }
+  const int sub = (batch + lanes - 1) / lanes;
+  if ((rc = ensure_workspace(P, lanes * sub, nrhs))) return rc;   // lane slices are sub shifts each
+  const LevelArgs a0 = a;
+  auto run_batch = [&](int s0, int nb, int koff, cudaStream_t st) -> int {
+    LevelArgs a = a0;
     a.nbatch = nb;
     a.lam = lam + s0;
     a.shift0 = s0;
+    // this lane's slice of the batch workspace: local shifts [koff, koff + nb)
+    a.factor = P.d_factor + (int64_t)koff * P.factor_stride;
+    a.Z = P.d_Z + (int64_t)koff * P.n * nrhs;
+    cplx* up[2] = {P.d_upool[0] + (int64_t)koff * P.upool_stride[0], P.d_upool[1] + (int64_t)koff * P.upool_stride[1]};
+    cplx* rp[2] = {P.d_rpool[0] + (int64_t)koff * P.rpool_stride[0] * nrhs,
+                   P.d_rpool[1] + (int64_t)koff * P.rpool_stride[1] * nrhs};
     SpecArgs sa{};
     sa.subs = P.d_subs;
     sa.V = P.d_V;
@@ -677,7 +719,7 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
     sa.nrhs = nrhs;
     sa.nx = P.n;
     sa.shift0 = s0;
-    sa.Z = P.d_Z;
+    sa.Z = a.Z;
     sa.G = G;
     sa.W = W;
     sa.lay = lay;
@@ -685,13 +727,13 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
       const int q = d & 1;
       a.list = P.d_levels + P.level_off[d];
       a.nlist = (int32_t)P.levels[d].size();
-      a.ucur = P.d_upool[q];
+      a.ucur = up[q];
       a.ucur_stride = P.upool_stride[q];
-      a.uchild = P.d_upool[q ^ 1];
+      a.uchild = up[q ^ 1];
       a.uchild_stride = P.upool_stride[q ^ 1];
-      a.rcur = P.d_rpool[q];
+      a.rcur = rp[q];
       a.rcur_stride = P.rpool_stride[q];
-      a.rchild = P.d_rpool[q ^ 1];
+      a.rchild = rp[q ^ 1];
       a.rchild_stride = P.rpool_stride[q ^ 1];
       if (P.spec_off[4 * d + 2] > P.spec_off[4 * d]) {
         // spectral subtree roots of this depth: update blocks + forward RHS (no factor storage)
@@ -704,9 +746,10 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
           sa.rcur = a.rcur;
           sa.rcur_stride = a.rcur_stride;
           spectral_kernel<<<dim3((unsigned)n_it, (unsigned)((nb * nrhs + SP_BN - 1) / SP_BN)), 256, P.spec_smem,
-                            stream>>>(sa);
+                            st>>>(sa);
           STFEM_LAUNCH_CHECK("spectral_kernel");
           ++nlaunch;
+          fam(FAM_SPECTRAL, st);
         }
       }
       if (a.nlist == 0) {
@@ -715,37 +758,43 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
       }
       const int nmax = P.level_nmax[d];
       if (level_is_small(P, d)) {
-        if ((rc = launch_small_factor_any(a, a.nlist * nb, nmax, stream))) return rc;
+        if ((rc = launch_small_factor_any(a, a.nlist * nb, nmax, st))) return rc;
         ++nlaunch;
+        fam(FAM_SMALL, st);
       } else {
         // large fronts: tile-parallel pipeline over all (front, shift) instances of the level
         const int ninst = a.nlist * nb, pmax = P.level_pmax[d];
         asm_front_kernel<<<dim3(ninst, (nmax + ASM_COLS - 1) / ASM_COLS), NT, (size_t)2 * nmax * sizeof(int),
-                           stream>>>(a);
+                           st>>>(a);
         STFEM_LAUNCH_CHECK("asm_front_kernel");
         ++nlaunch;
+        fam(FAM_ASM, st);
         for (int kb = 0; kb < pmax; kb += NB) {
-          diag_kernel<<<ninst, 32, 0, stream>>>(a, kb);
+          diag_kernel<<<ninst, 32, 0, st>>>(a, kb);
           STFEM_LAUNCH_CHECK("diag_kernel");
+          fam(FAM_DIAG, st);
           const dim3 tg(ninst, (unsigned)std::max(1, (nmax - kb + TR_ROWS - 1) / TR_ROWS));
-          if (std::min(NB, pmax - kb) <= 16) trsm_kernel<16><<<tg, TR_ROWS, 0, stream>>>(a, kb);
-          else trsm_kernel<32><<<tg, TR_ROWS, 0, stream>>>(a, kb);
+          if (std::min(NB, pmax - kb) <= 16) trsm_kernel<16><<<tg, TR_ROWS, 0, st>>>(a, kb);
+          else trsm_kernel<32><<<tg, TR_ROWS, 0, st>>>(a, kb);
           STFEM_LAUNCH_CHECK("trsm_kernel");
+          fam(FAM_TRSM, st);
           nlaunch += 2;
           int tiles = 0;
           for (int32_t f : P.levels[d])
             tiles = std::max(tiles, panel_update_tiles(P.fronts[f].n, P.fronts[f].p, kb));
           if (tiles > 0) {
-            panel_update_kernel<<<dim3(ninst, tiles), NT, GEMM_SMEM, stream>>>(a, kb);
+            panel_update_kernel<<<dim3(ninst, tiles), NT, GEMM_SMEM, st>>>(a, kb);
             STFEM_LAUNCH_CHECK("panel_update_kernel");
             ++nlaunch;
+            fam(FAM_PANEL, st);
           }
         }
         const int64_t ntl = P.syrk_off[d + 1] - P.syrk_off[d];
         if (a.split_syrk && ntl > 0) {
-          syrk_level_kernel<<<(unsigned)(ntl * nb), NT, SYRK_SMEM, stream>>>(a, P.d_syrk_tiles + P.syrk_off[d]);
+          syrk_level_kernel<<<(unsigned)(ntl * nb), NT, SYRK_SMEM, st>>>(a, P.d_syrk_tiles + P.syrk_off[d]);
           STFEM_LAUNCH_CHECK("syrk_level_kernel");
           ++nlaunch;
+          fam(FAM_SYRK, st);
         }
       }
       mark();
@@ -758,9 +807,10 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
         if (n_it == 0) continue;
         sa.items = P.d_spec_items + P.spec_off[4 * d + j];
         spectral_kernel<<<dim3((unsigned)n_it, (unsigned)((nb * nrhs + SP_BN - 1) / SP_BN)), 256, P.spec_smem,
-                          stream>>>(sa);
+                          st>>>(sa);
         STFEM_LAUNCH_CHECK("spectral_kernel");
         ++nlaunch;
+        fam(FAM_SPECTRAL, st);
       }
       if (a.nlist == 0) {
         mark();
@@ -772,20 +822,42 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
       const bool ldlt = level_is_small(P, d);
       a.unit_diag = ldlt ? 1 : 0;
       if (nmax <= SMALL_N && bsm <= 200 * 1024 && !P.force_big) {
-        if ((rc = launch_small_backward_any(a, a.nlist * nb, nmax, pmax, stream))) return rc;
+        if ((rc = launch_small_backward_any(a, a.nlist * nb, nmax, pmax, st))) return rc;
       } else {
         const int u = ldlt ? 1 : 0, gsz = a.nlist * nb;
         switch (small_nr(nrhs)) {
-          case 1: rc = launch_backward_level<1>(a, gsz, nmax, u, stream); break;
-          case 2: rc = launch_backward_level<2>(a, gsz, nmax, u, stream); break;
-          case 4: rc = launch_backward_level<4>(a, gsz, nmax, u, stream); break;
-          case 8: rc = launch_backward_level<8>(a, gsz, nmax, u, stream); break;
-          default: rc = launch_backward_level<16>(a, gsz, nmax, u, stream); break;
+          case 1: rc = launch_backward_level<1>(a, gsz, nmax, u, st); break;
+          case 2: rc = launch_backward_level<2>(a, gsz, nmax, u, st); break;
+          case 4: rc = launch_backward_level<4>(a, gsz, nmax, u, st); break;
+          case 8: rc = launch_backward_level<8>(a, gsz, nmax, u, st); break;
+          default: rc = launch_backward_level<16>(a, gsz, nmax, u, st); break;
         }
         if (rc) return rc;
       }
       ++nlaunch;
+      fam(FAM_BACKWARD, st);
       mark();
+    }
+    return STFEM_OK;
+  };
+  fev_start = nullptr;
+  if (level_timing) {
+    cudaEventCreate(&fev_start);
+    cudaEventRecord(fev_start, stream);
+  }
+  mark();
+  if (lanes == 1) {
+    for (int s0 = 0; s0 < nshift; s0 += batch)
+      if ((rc = run_batch(s0, std::min(batch, nshift - s0), 0, stream))) return rc;
+  } else {
+    STFEM_CUDA_TRY(cudaEventRecord(P.start_event, stream));
+    for (int j = 0; j < lanes; ++j) STFEM_CUDA_TRY(cudaStreamWaitEvent(P.lane_streams[j], P.start_event, 0));
+    int j = 0;
+    for (int s0 = 0; s0 < nshift; s0 += sub, j = (j + 1) % lanes)
+      if ((rc = run_batch(s0, std::min(sub, nshift - s0), j * sub, P.lane_streams[j]))) return rc;
+    for (int jj = 0; jj < lanes; ++jj) {
+      STFEM_CUDA_TRY(cudaEventRecord(P.lane_events[jj], P.lane_streams[jj]));
+      STFEM_CUDA_TRY(cudaStreamWaitEvent(stream, P.lane_events[jj], 0));
     }
   }
   P.last_batch = batch;
@@ -807,6 +879,18 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
                 j < L ? "factor" : "backward", d, ms);
     }
     for (auto e : evs) cudaEventDestroy(e);
+    P.family_ms.assign(NFAM, 0.0);
+    P.family_launches.assign(NFAM, 0);
+    cudaEvent_t prev = fev_start;
+    for (auto& fe : fevs) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, prev, fe.first);
+      P.family_ms[fe.second] += ms;
+      P.family_launches[fe.second] += 1;
+      prev = fe.first;
+    }
+    for (auto& fe : fevs) cudaEventDestroy(fe.first);
+    cudaEventDestroy(fev_start);
   }
   if (phase_prof) {
     unsigned long long h[16];
@@ -1012,6 +1096,45 @@ extern "C" int stfem_plan_level_report(const stfem_plan* plan, double* ms, doubl
   if (small)
     for (int d = 0; d < L; ++d)
       small[d] = (d < (int)P.level_nmax.size() && stfem::level_is_small(P, d)) ? 1 : 0;
+  return STFEM_OK;
+}
+
+extern "C" int stfem_plan_kernel_report(const stfem_plan* plan, int32_t nfam, double* ms, double* flops,
+                                        int64_t* launches) {
+  if (!plan) return stfem::fail(STFEM_ERR_ARG, "plan_kernel_report: null pointer");
+  const Plan& P = *reinterpret_cast<const Plan*>(plan);
+  const int nf = std::min<int>(nfam, stfem::NFAM);
+  for (int i = 0; i < nf; ++i) {
+    if (ms) ms[i] = i < (int)P.family_ms.size() ? P.family_ms[i] : 0.0;
+    if (launches) launches[i] = i < (int)P.family_launches.size() ? P.family_launches[i] : 0;
+    if (flops) flops[i] = 0.0;
+  }
+  if (flops) {
+    // algorithmic real flops per shift of each family (1 RHS for the spectral RHS GEMMs)
+    auto add = [&](int f, double v) {
+      if (f < nf) flops[f] += v;
+    };
+    add(stfem::FAM_SPECTRAL, (double)P.spectral_flops_u + (double)P.spectral_flops_rhs);
+    for (size_t d = 0; d < P.levels.size(); ++d) {
+      const bool small = !P.level_nmax.empty() && stfem::level_is_small(P, (int)d);
+      for (int32_t f : P.levels[d]) {
+        const auto& F = P.fronts[f];
+        const double n = F.n, p = F.p, b = F.n - F.p;
+        if (small) {
+          for (int j = 0; j < F.p; ++j) add(stfem::FAM_SMALL, 4.0 * (n - 1 - j) * (n - 1 - j));
+          continue;
+        }
+        add(stfem::FAM_SYRK, 4.0 * b * b * p);
+        for (int kb = 0; kb < F.p; kb += stfem::NB) {
+          const double w = std::min(stfem::NB, F.p - kb), rows = n - kb - w;
+          add(stfem::FAM_DIAG, 4.0 * w * w * w / 3.0);
+          add(stfem::FAM_TRSM, 4.0 * rows * w * w);
+          const double base = kb + w;
+          if (base < p) add(stfem::FAM_PANEL, 8.0 * w * ((p - base) * (n - base) - (p - base) * (p - base - 1) / 2));
+        }
+      }
+    }
+  }
   return STFEM_OK;
 }
 

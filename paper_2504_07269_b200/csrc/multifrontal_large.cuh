@@ -189,11 +189,14 @@ __global__ void __launch_bounds__(32) diag_kernel(LevelArgs a, int kb) {
   }
 }
 
-// rows below panel kb: x C11^T = b per row (thread per row, W-wide register
-// block, right-looking so the W updates of a step are independent), then the
-// row's forward RHS r -= x y.  W = panel width rounded up (16 or 32).
+// rows below panel kb: x C11^T = b per row (thread per row), then the row's
+// forward RHS r -= x y.  The W-wide panel is solved in register blocks of 16
+// columns (right-looking inside a block, independent update chains); a later
+// block first subtracts the finished blocks, re-read from global (L1-hot).
+// Register blocks of 16 keep the kernel near 100 registers (4+ CTAs per SM).
 template <int W>
-__global__ void __launch_bounds__(TR_ROWS) trsm_kernel(LevelArgs a, int kb) {
+__global__ void __launch_bounds__(TR_ROWS, 4) trsm_kernel(LevelArgs a, int kb) {
+  constexpr int WB = 16;
   __shared__ cplx Ls[W * W];          // Ls[c * W + c'] = C[kb+c][kb+c'] (c' < c); Ls[c*W+c] = 1 / c_cc
   __shared__ cplx ys[W * MAXR];
   const int tid = threadIdx.x;
@@ -228,25 +231,35 @@ __global__ void __launch_bounds__(TR_ROWS) trsm_kernel(LevelArgs a, int kb) {
   const int i = r0 + tid;
   if (i >= n) return;
   cplx* prow = P + i + (int64_t)kb * n;
-  cplx x[W];
 #pragma unroll
-  for (int c = 0; c < W; ++c) x[c] = c < w ? ldc(prow + (int64_t)c * n) : zero;
+  for (int jb = 0; jb < W; jb += WB) {
+    if (jb >= w) break;
+    cplx x[WB];
 #pragma unroll
-  for (int c = 0; c < W; ++c) {
-    x[c] = cmul(x[c], Ls[c * W + c]);
+    for (int c = 0; c < WB; ++c) x[c] = jb + c < w ? ldc(prow + (int64_t)(jb + c) * n) : zero;
+    // subtract the finished blocks (their x are final in global memory)
+    for (int c2 = 0; c2 < jb; ++c2) {
+      const cplx xc = ldc(prow + (int64_t)c2 * n);
 #pragma unroll
-    for (int c2 = c + 1; c2 < W; ++c2) x[c2] = cfms(x[c2], x[c], Ls[c2 * W + c]);
-  }
+      for (int c = 0; c < WB; ++c) x[c] = cfms(x[c], xc, Ls[(jb + c) * W + c2]);
+    }
 #pragma unroll
-  for (int c = 0; c < W; ++c)
-    if (c < w) stc(prow + (int64_t)c * n, x[c]);
-  for (int r = 0; r < nrhs; ++r) {
-    cplx* dst = (i < p) ? Zk + F.pbeg + i + (int64_t)r * nx : a.rcur + ((int64_t)k * a.rcur_stride + F.rofs) * nrhs +
-                                                                  (i - p) + (int64_t)r * b;
-    cplx acc = ldc(dst);
+    for (int c = 0; c < WB; ++c) {
+      x[c] = cmul(x[c], Ls[(jb + c) * W + jb + c]);
 #pragma unroll
-    for (int c = 0; c < W; ++c) acc = cfms(acc, x[c], ys[c * MAXR + r]);
-    stc(dst, acc);
+      for (int c2 = c + 1; c2 < WB; ++c2) x[c2] = cfms(x[c2], x[c], Ls[(jb + c2) * W + jb + c]);
+    }
+#pragma unroll
+    for (int c = 0; c < WB; ++c)
+      if (jb + c < w) stc(prow + (int64_t)(jb + c) * n, x[c]);
+    for (int r = 0; r < nrhs; ++r) {
+      cplx* dst = (i < p) ? Zk + F.pbeg + i + (int64_t)r * nx
+                          : a.rcur + ((int64_t)k * a.rcur_stride + F.rofs) * nrhs + (i - p) + (int64_t)r * b;
+      cplx acc = ldc(dst);
+#pragma unroll
+      for (int c = 0; c < WB; ++c) acc = cfms(acc, x[c], ys[(jb + c) * MAXR + r]);
+      stc(dst, acc);
+    }
   }
 }
 

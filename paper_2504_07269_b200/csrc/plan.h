@@ -93,10 +93,15 @@ struct Plan {
   int32_t last_nbatches = 0;  // shift batches of the last factor_solve
   bool record_levels = false;   // record per-level CUDA-event times into level_ms
   std::vector<double> level_ms;
+  std::vector<double> family_ms;   // per kernel family (record mode), summed over batches
+  std::vector<int64_t> family_launches;
   cplx* d_factor = nullptr;
   cplx* d_upool[2] = {nullptr, nullptr};
   cplx* d_rpool[2] = {nullptr, nullptr};
   cplx* d_Z = nullptr;
+  std::vector<cudaStream_t> lane_streams;   // shift lanes of factor_solve (STFEM_STREAMS, default 2)
+  std::vector<cudaEvent_t> lane_events;
+  cudaEvent_t start_event = nullptr;
 
   ~Plan();
   void free_device();

@@ -103,6 +103,17 @@ class SpatialPlan:
         N.check(N.lib().stfem_plan_level_report(self._h, ms.ctypes.data, fl.ctypes.data, sm.ctypes.data))
         return ms[:L], ms[L:], fl, sm.astype(bool)
 
+    FAMILIES = ("spectral", "assembly", "diag", "trsm", "panel_update", "syrk", "backward", "small_factor")
+
+    def kernel_report(self) -> dict:
+        """{family: (ms of the last recorded call, algorithmic flops per shift, launches)}."""
+        nf = len(self.FAMILIES)
+        ms = np.zeros(nf)
+        fl = np.zeros(nf)
+        nl = np.zeros(nf, dtype=np.int64)
+        N.check(N.lib().stfem_plan_kernel_report(self._h, nf, ms.ctypes.data, fl.ctypes.data, nl.ctypes.data))
+        return {k: (float(ms[i]), float(fl[i]), int(nl[i])) for i, k in enumerate(self.FAMILIES)}
+
     def last_num_batches(self) -> int:
         """Shift batches used by the last factor_solve call."""
         v = C.c_int32()
