@@ -504,7 +504,8 @@ int upload(Plan& P) {
 
 int64_t bytes_per_shift(const Plan& P, int nrhs) {
   return 16 * (P.factor_stride + P.upool_stride[0] + P.upool_stride[1] +
-               (int64_t)nrhs * (P.rpool_stride[0] + P.rpool_stride[1]) + (int64_t)P.n * nrhs);
+               (int64_t)nrhs * (P.rpool_stride[0] + P.rpool_stride[1]) + (int64_t)P.n * nrhs +
+               (int64_t)P.h_th.size());
 }
 
 int ensure_workspace(Plan& P, int batch, int nrhs) {
@@ -521,6 +522,7 @@ int ensure_workspace(Plan& P, int batch, int nrhs) {
     if ((rc = al(&P.d_rpool[q], P.rpool_stride[q] * batch * nrhs))) return rc;
   }
   if ((rc = al(&P.d_Z, (int64_t)P.n * nrhs * batch))) return rc;
+  if (!P.h_th.empty() && (rc = al(&P.d_wbuf, (int64_t)P.h_th.size() * batch))) return rc;
   P.ws_batch = batch;
   P.ws_nrhs = nrhs;
   return STFEM_OK;
@@ -594,7 +596,8 @@ void Plan::free_workspace() {
     d_upool[q] = d_rpool[q] = nullptr;
   }
   cudaFree(d_Z);
-  d_factor = d_Z = nullptr;
+  cudaFree(d_wbuf);
+  d_factor = d_Z = d_wbuf = nullptr;
   ws_batch = ws_nrhs = 0;
 }
 
@@ -723,6 +726,17 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
     sa.G = G;
     sa.W = W;
     sa.lay = lay;
+    sa.wbuf = P.d_wbuf + koff;
+    sa.wstride = P.ws_batch;
+    if (!P.subs.empty()) {
+      const int64_t nth = (int64_t)P.h_th.size();
+      const int64_t tot = nth * nb;
+      spectral_w_kernel<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 16), 256, 0, st>>>(
+          P.d_th, nth, lam + s0, nb, P.d_wbuf + koff, P.ws_batch);
+      STFEM_LAUNCH_CHECK("spectral_w_kernel");
+      ++nlaunch;
+      fam(FAM_SPECTRAL, st);
+    }
     for (int d = P.depth; d >= 0; --d) {
       const int q = d & 1;
       a.list = P.d_levels + P.level_off[d];

@@ -99,6 +99,7 @@ struct Plan {
   cplx* d_upool[2] = {nullptr, nullptr};
   cplx* d_rpool[2] = {nullptr, nullptr};
   cplx* d_Z = nullptr;
+  cplx* d_wbuf = nullptr;                   // spectral w = 1 / (theta + lam), sum(m) x batch
   std::vector<cudaStream_t> lane_streams;   // shift lanes of factor_solve (STFEM_STREAMS, default 2)
   std::vector<cudaEvent_t> lane_events;
   cudaEvent_t start_event = nullptr;

@@ -40,9 +40,11 @@ constexpr int SP_LDB = SP_BN + 2;   // Bs[k][col] complex: (t*66 + g) mod 8 hits
 constexpr int SP_A_STAGE = SP_BK * SP_LDA;   // doubles
 constexpr int SP_B_STAGE = SP_BK * SP_LDB;   // complex
 constexpr int SP_SMEM = 2 * (SP_A_STAGE * 8 + SP_B_STAGE * 16);
-// + OP_U staging: 16 R rows and theta over the subtree's m, 64 shifts
-__host__ __device__ constexpr int spectral_smem_bytes(int mmax) { return SP_SMEM + (17 * mmax + 1) * 8 + SP_BN * 16; }
+// + OP_U staging: the tile's 16 R rows over the subtree's m
+__host__ __device__ constexpr int spectral_smem_bytes(int mmax) { return SP_SMEM + 16 * (mmax | 1) * 8; }
 enum { OP_U = 0, OP_F1 = 1, OP_F2 = 2, OP_B1 = 3, OP_B2 = 4 };
+
+__device__ __forceinline__ cplx spec_w(double th, cplx l) { return crecip_fast(cmk(th + l.re, l.im)); }
 
 struct SpecArgs {
   const SubDev* subs;
@@ -60,9 +62,22 @@ struct SpecArgs {
   const cplx* G;
   cplx* W;
   stfem_bv_layout lay;
+  const cplx* wbuf;           // w[(tofs + k) * wstride + s] = 1 / (theta_k + lam_s), this lane's shifts
+  int64_t wstride;
 };
 
-__device__ __forceinline__ cplx spec_w(double th, cplx l) { return crecip_fast(cmk(th + l.re, l.im)); }
+// w_k(s) = 1 / (theta_k + lam_s) for every subtree interior index k and shift s
+// of the batch (shared by all row tiles of a subtree instead of recomputed)
+__global__ void spectral_w_kernel(const double* __restrict__ th, int64_t nth, const cplx* __restrict__ lam,
+                                  int nb, cplx* __restrict__ w, int64_t wstride) {
+  const int64_t tot = nth * nb;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < tot;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = idx / nb;
+    const int s = (int)(idx - k * nb);
+    stc(w + k * wstride + s, spec_w(th[k], lam[s]));
+  }
+}
 
 template <int OP>
 __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, double* As, cplx* Bs) {
@@ -84,17 +99,16 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
 
   // OP_U operands are generated from shared memory: the 16 R rows of the
   // tile's (i, j) block over all k, theta, and the tile's 64 shifts
-  double* Rs = reinterpret_cast<double*>(Bs + 2 * SP_B_STAGE);   // [16][m]
-  double* ths = Rs + 16 * m;
-  cplx* lams = reinterpret_cast<cplx*>(ths + ((17 * m + 1) & ~1) - 16 * m);   // 16-byte aligned
+  double* Rs = reinterpret_cast<double*>(Bs + 2 * SP_B_STAGE);   // [16][ms], ms = m | 1 (odd: no bank conflicts)
+  const int ms = m | 1;
+  const cplx* __restrict__ wsub = a.wbuf + (int64_t)S.tofs * a.wstride;   // w[k * wstride + s]
   if constexpr (OP == OP_U) {
+    // rows fastest: each k reads two runs of 8 consecutive doubles of column-major R
     for (int q = tid; q < 16 * m; q += 256) {
-      const int rr = q / m, k = q - rr * m;
+      const int k = q >> 4, rr = q & 15;
       const int row = rr < 8 ? it.z * 8 + rr : it.w * 8 + rr - 8;
-      Rs[q] = row < g ? Rm[row + (int64_t)k * g] : 0.0;
+      Rs[rr * ms + k] = row < g ? Rm[row + (int64_t)k * g] : 0.0;
     }
-    for (int q = tid; q < m; q += 256) ths[q] = th[q];
-    if (tid < SP_BN) lams[tid] = n0 + tid < ncols ? a.lam[n0 + tid] : cmk(1.0, 0.0);
     __syncthreads();
   }
 
@@ -102,7 +116,7 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
   auto a_val = [&](int r, int k) -> double {
     if (k >= K) return 0.0;
     if (OP == OP_U) {
-      return Rs[(r >> 3) * m + k] * Rs[(8 + (r & 7)) * m + k];
+      return Rs[(r >> 3) * ms + k] * Rs[(8 + (r & 7)) * ms + k];
     } else if (OP == OP_F1) {
       const int ko = it.z * SP_BM + r;
       return ko < m ? V[k + (int64_t)ko * m] : 0.0;
@@ -122,12 +136,12 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
   auto b_val = [&](int k, int c) -> cplx {
     const int cg = n0 + c;
     if (k >= K || cg >= ncols) return zero;
-    if (OP == OP_U) return spec_w(ths[k], lams[c]);
+    if (OP == OP_U) return ldc(wsub + (int64_t)k * a.wstride + cg);
     const int s = cg / nrhs, r = cg - s * nrhs;
     const cplx* Zs = a.Z + (int64_t)s * nx * nrhs + (int64_t)r * nx;
     if (OP == OP_F1) return ldc(a.G + bv_off(a.lay, r, a.shift0 + s, a.perm[S.first + k]));
     if (OP == OP_F2)
-      return k < m ? cmul(spec_w(th[k], a.lam[s]), ldc(Zs + S.first + k)) : ldc(Zs + S.first + k - m);
+      return k < m ? cmul(ldc(wsub + (int64_t)k * a.wstride + s), ldc(Zs + S.first + k)) : ldc(Zs + S.first + k - m);
     if (OP == OP_B1) return ldc(Zs + bidx[k]);
     return ldc(Zs + S.first + k);
   };
@@ -139,9 +153,21 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int idx = tid + 256 * u;
-      ra[u] = a_val(idx & 63, k0 + (idx >> 6));
-      rb[u] = b_val(k0 + (idx >> 6), idx & 63);
+      // OP_F1 reads rows of V^T (= columns of V, contiguous in k): k fastest
+      if constexpr (OP == OP_F1) ra[u] = a_val(idx >> 4, k0 + (idx & 15));
+      else ra[u] = a_val(idx & 63, k0 + (idx >> 6));
+      if constexpr (OP == OP_U) {
+        // w streamed straight into its shared-memory stage (16-byte cp.async, zero-filled
+        // outside); the stage was last read before the previous iteration's barrier
+        const int k = k0 + (idx >> 6), cg = n0 + (idx & 63);
+        const bool ok = k < K && cg < ncols;
+        cp_async16(Bs + (kc & 1) * SP_B_STAGE + (idx >> 6) * SP_LDB + (idx & 63),
+                   ok ? wsub + (int64_t)k * a.wstride + cg : wsub, ok);
+      } else {
+        rb[u] = b_val(k0 + (idx >> 6), idx & 63);
+      }
     }
+    if constexpr (OP == OP_U) cp_async_commit();
   };
   auto store = [&](int st) {
     double* as = As + st * SP_A_STAGE;
@@ -149,8 +175,9 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int idx = tid + 256 * u;
-      as[(idx >> 6) * SP_LDA + (idx & 63)] = ra[u];
-      stc(bs + (idx >> 6) * SP_LDB + (idx & 63), rb[u]);
+      if constexpr (OP == OP_F1) as[(idx & 15) * SP_LDA + (idx >> 4)] = ra[u];
+      else as[(idx >> 6) * SP_LDA + (idx & 63)] = ra[u];
+      if constexpr (OP != OP_U) stc(bs + (idx >> 6) * SP_LDB + (idx & 63), rb[u]);
     }
   };
 
@@ -167,6 +194,7 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
     fetch(0);
     store(0);
   }
+  if constexpr (OP == OP_U) cp_async_wait<0>();
   __syncthreads();
   for (int kc = 0; kc < nk; ++kc) {
     if (kc + 1 < nk) fetch(kc + 1);
@@ -192,6 +220,7 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
         }
     }
     if (kc + 1 < nk) store((kc + 1) & 1);
+    if constexpr (OP == OP_U) cp_async_wait<0>();
     __syncthreads();
   }
 
@@ -213,7 +242,7 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
           cplx* zp = a.Z + (int64_t)s * nx * nrhs + (int64_t)r * nx + S.first + kk;
           const cplx t1 = cmk(acc[mi][ni][0][cv], acc[mi][ni][1][cv]);
           const cplx t2 = cmk(acc[mi][ni][0][2 + cv], acc[mi][ni][1][2 + cv]);
-          const cplx w = spec_w(th[kk], a.lam[s]);
+          const cplx w = ldc(wsub + (int64_t)kk * a.wstride + s);
           stc(zp, csub(cmul(w, csub(ldc(zp), t1)), t2));
         } else {
 #pragma unroll
