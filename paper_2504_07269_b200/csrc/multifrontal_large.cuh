@@ -28,7 +28,7 @@
 constexpr int ASM_COLS = 32;
 constexpr int TR_ROWS = 128;
 
-__global__ void __launch_bounds__(NT) asm_front_kernel(LevelArgs a) {
+__global__ void __launch_bounds__(NT, 4) asm_front_kernel(LevelArgs a) {
   extern __shared__ int inv_s[];   // nc x n inverse relpos maps
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int inst = blockIdx.x;
@@ -71,22 +71,32 @@ __global__ void __launch_bounds__(NT) asm_front_kernel(LevelArgs a) {
       for (int s = 0; s < 2; ++s) k2[s][u] = s < nc ? inv_s[s * n + c2] : -1;
       dst[u] = (c2 < p) ? P + (int64_t)c2 * n : U + (int64_t)(c2 - p) * b - p;
     }
-    for (int r1 = c0 + warp + lane; r1 < n; r1 += 32) {
-      int k1[2];
+    // two row blocks per iteration: 16 independent child loads in flight per thread
+    for (int rb = c0 + warp + lane; rb < n; rb += 64) {
+      cplx v[2][CU];
 #pragma unroll
-      for (int s = 0; s < 2; ++s) k1[s] = s < nc ? inv_s[s * n + r1] : -1;
-      cplx v[CU];
+      for (int h = 0; h < 2; ++h) {
+        const int r1 = rb + 32 * h;
+        int k1[2];
 #pragma unroll
-      for (int u = 0; u < CU; ++u) {
-        v[u] = zero;
+        for (int s = 0; s < 2; ++s) k1[s] = (s < nc && r1 < n) ? inv_s[s * n + r1] : -1;
 #pragma unroll
-        for (int s = 0; s < 2; ++s)
-          if (k1[s] >= 0 && k2[s][u] >= 0) v[u] = cadd(v[u], ldc(Ucs[s] + (int64_t)k2[s][u] * bcs[s] + k1[s]));
+        for (int u = 0; u < CU; ++u) {
+          v[h][u] = zero;
+#pragma unroll
+          for (int s = 0; s < 2; ++s)
+            if (k1[s] >= 0 && k2[s][u] >= 0)
+              v[h][u] = cadd(v[h][u], ldc(Ucs[s] + (int64_t)k2[s][u] * bcs[s] + k1[s]));
+        }
       }
 #pragma unroll
-      for (int u = 0; u < CU; ++u) {
-        const int c2 = c0 + warp + u * NW;
-        if (c2 < cend && r1 >= c2) stc(dst[u] + r1, v[u]);
+      for (int h = 0; h < 2; ++h) {
+        const int r1 = rb + 32 * h;
+#pragma unroll
+        for (int u = 0; u < CU; ++u) {
+          const int c2 = c0 + warp + u * NW;
+          if (c2 < cend && r1 < n && r1 >= c2) stc(dst[u] + r1, v[h][u]);
+        }
       }
     }
   }
