@@ -99,7 +99,8 @@ class DistributedFDM:
         if self.P == 1:
             out.copy_(inp)
         else:
-            dist.all_to_all_single(out, inp, group=self.group)
+            # complex128 exchanged as its float64 view (NCCL has no complex type)
+            dist.all_to_all_single(torch.view_as_real(out), torch.view_as_real(inp), group=self.group)
 
     def solve(self, F_p: torch.Tensor, out: torch.Tensor | None = None, timings: dict | None = None):
         """F_p: (n_t, n_rhs, c) shard.  Returns Psi_p in the same layout."""
