@@ -166,18 +166,54 @@ def bench_main(args):
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
+    clk = None
+    if rank == 0:
+        import sys
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        from bench import ClockSampler
+        clk = ClockSampler(local)
+        clk.start()
+        time.sleep(0.3)
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
     for _ in range(args.steps):
         solver.solve(Fp, out)
     e.record()
     torch.cuda.synchronize()
+    clocks = clk.stop() if clk is not None else None
     t_local = s.elapsed_time(e) / 1e3 / args.steps
     tt = torch.tensor([t_local], dtype=torch.float64, device=dev)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     dist.barrier()
     t_step = float(tt.item())
     dofs = prob.nx * nt * prob.n_rhs
+    launches = 2 + plan.last_launches()
+    # e2e: each rank's shard from pinned host memory, the solve, the shard back to the host
+    e2e = None
+    if not args.no_e2e:
+        Fh = Fp.cpu().pin_memory()
+        Ph = torch.empty_like(Fh).pin_memory()
+
+        def e2e_step():
+            Fp.copy_(Fh, non_blocking=True)
+            solver.solve(Fp, out)
+            Ph.copy_(out, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_e2e = max(1, min(args.steps, 3))
+        s2.record()
+        for _ in range(n_e2e):
+            e2e_step()
+        e2.record()
+        torch.cuda.synchronize()
+        te = torch.tensor([s2.elapsed_time(e2) / 1e3 / n_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        nbytes = Fh.numel() * 16 * world
+        e2e = {"value": dofs / float(te.item()), "unit": "DoF/s", "h2d_bytes_per_step": nbytes,
+               "d2h_bytes_per_step": nbytes, "ms_per_step": float(te.item()) * 1e3}
     if rank == 0:
         line = {"metric": "space-time DoF/s (complex fp64) of the FDM direct solve", "value": dofs / t_step,
                 "unit": "DoF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -185,7 +221,9 @@ def bench_main(args):
                 "dtype": "c128", "data": "synthetic (seeded Gaussian RHS; BASELINE.json configs)",
                 "config": {"workload": args.workload, "n_x": prob.nx, "n_t": nt, "n_rhs": prob.n_rhs,
                            "parallelism": f"space-sharded transforms + time-sharded shifts, a2a x2 over {world} GPUs"},
-                "setup_s": t_setup, "asm_s": t_asm, "gpu_launches": None}
+                "setup_s": t_setup, "asm_s": t_asm, "gpu_launches": launches * args.steps,
+                "clocks": clocks, "e2e": e2e, "cpu_baseline": None,
+                "roofline": None}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
 
