@@ -69,6 +69,13 @@ int stfem_time_transform(const void* T, int nt, const void* in, int64_t ld_in,
                          void* out, int64_t ld_out, int64_t ncols, int batch,
                          int64_t bstride_in, int64_t bstride_out, void* stream);
 
+/* Column block [0, ncols) of `rows` rows between host and device
+ * (cudaMemcpy2DAsync; leading dimensions in complex128 elements; kind 0 =
+ * host->device, 1 = device->host).  The pipelined host-buffer solve overlaps
+ * these copies with the time transforms of neighbouring column blocks. */
+int stfem_copy_cols(void* dst, int64_t ld_dst, const void* src, int64_t ld_src, int64_t ncols,
+                    int64_t rows, int32_t kind, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Symbolic analysis (host, once per spatial sparsity pattern; SPEC.md:326,
  * :343 "fill-reducing ordering computed once per sparsity pattern and reused

@@ -16,6 +16,7 @@ CUDA-event times on the launching stream.
 
 from __future__ import annotations
 
+import ctypes as C
 import enum
 import time
 from dataclasses import dataclass, field
@@ -151,6 +152,58 @@ class FDMSolver:
         if out is not None:
             return out
         return G[0] if single else G
+
+
+    def solve_host(self, F_host: torch.Tensor, out_host: torch.Tensor, chunks: int = 8, stream=None,
+                   dev_buffers: tuple | None = None) -> torch.Tensor:
+        """Psi for a PINNED host F (n_rhs, n_t, n_x) into pinned host `out_host`.
+
+        The host->device copy of spatial column block c+1 overlaps the forward
+        transform of block c (each output column needs only its own input
+        column), and the device->host copy of block c overlaps the back
+        transform of block c+1; the spatial solves need every column and run
+        in between.  `dev_buffers` = (F_d, G, W) reuses device storage."""
+        N.require_cuda()
+        Fh = F_host.unsqueeze(0) if F_host.dim() == 2 else F_host
+        Ph = out_host.unsqueeze(0) if out_host.dim() == 2 else out_host
+        if Fh.shape[-2:] != (self.nt, self.ops.n) or Ph.shape != Fh.shape:
+            raise N.DimensionMismatch(N.ERR_DIM, f"solve_host: f {tuple(F_host.shape)} vs ({self.nt}, {self.ops.n})")
+        if not (Fh.is_pinned() and Ph.is_pinned() and Fh.is_contiguous() and Ph.is_contiguous()):
+            raise ValueError("solve_host: host buffers must be contiguous pinned memory")
+        nr, nt, nx = Fh.shape
+        dev = self.X.device
+        if dev_buffers is None:
+            dev_buffers = tuple(torch.empty(Fh.shape, dtype=C128, device=dev) for _ in range(3))
+        Fd, G, W = dev_buffers
+        s = stream if stream is not None else torch.cuda.current_stream()
+        if getattr(self, "_copy_stream", None) is None:
+            self._copy_stream = torch.cuda.Stream(device=dev)
+        cs = self._copy_stream
+        lib = N.lib()
+        cw = -(-nx // max(1, chunks))
+        blocks = [(c0, min(nx, c0 + cw)) for c0 in range(0, nx, cw)]
+        start = torch.cuda.Event()
+        start.record(s)
+        cs.wait_event(start)
+        for c0, c1 in blocks:                                             # (2) pipelined with H2D
+            N.check(lib.stfem_copy_cols(N.ptr(Fd[..., c0:]), nx, C.c_void_p(Fh.data_ptr() + 16 * c0), nx,
+                                        c1 - c0, nr * nt, 0, N.stream_ptr(cs)))
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            s.wait_event(ev)
+            K.time_transform(self.Y, Fd[..., c0:c1], out=G[..., c0:c1], stream=s)
+        self.plan.factor_solve(self.lam, G, W, blockvector_layout(nt, nx), nr, stream=s)   # (3)
+        for c0, c1 in blocks:                                             # (4) pipelined with D2H
+            K.time_transform(self.X, W[..., c0:c1], out=G[..., c0:c1], stream=s)
+            ev = torch.cuda.Event()
+            ev.record(s)
+            cs.wait_event(ev)
+            N.check(lib.stfem_copy_cols(C.c_void_p(Ph.data_ptr() + 16 * c0), nx, N.ptr(G[..., c0:]), nx,
+                                        c1 - c0, nr * nt, 1, N.stream_ptr(cs)))
+        done = torch.cuda.Event()
+        done.record(cs)
+        s.wait_event(done)
+        return out_host
 
 
 def solve(ops: SpatialOperators, M_t: np.ndarray, B_t: np.ndarray, f: torch.Tensor,
