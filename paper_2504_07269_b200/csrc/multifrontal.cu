@@ -326,9 +326,10 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int uni
       else if (i == c) l11[c * LDD + c] = unit ? cmk(1.0, 0.0) : crecip(ldc(P + (kb + c) + (int64_t)(kb + c) * n));
     }
     __syncthreads();
-    if (warp == 0) {
-      // x_j = (t_j - sum_{c>j} L[c][j] x_c) * dinv_j, lane c holds x_c; one warp reduction per step
-      for (int r = 0; r < nrhs; ++r) {
+    {
+      // x_j = (t_j - sum_{c>j} L[c][j] x_c) * dinv_j, lane c holds x_c; one warp
+      // reduction per step; the right-hand sides are spread over the warps
+      for (int r = warp; r < nrhs; r += NT / 32) {
         cplx xl = lane < w ? xs[(kb + lane) * nrhs + r] : zero;
         for (int j = w - 1; j >= 0; --j) {
           cplx sacc = (lane > j && lane < w) ? cmul(l11[j * LDD + lane], xl) : zero;
@@ -784,7 +785,7 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
         ++nlaunch;
         fam(FAM_ASM, st);
         for (int kb = 0; kb < pmax; kb += NB) {
-          diag_kernel<<<ninst, 32, 0, st>>>(a, kb);
+          diag_kernel<<<ninst, 32 * std::min(8, nrhs), 0, st>>>(a, kb);
           STFEM_LAUNCH_CHECK("diag_kernel");
           fam(FAM_DIAG, st);
           const dim3 tg(ninst, (unsigned)std::max(1, (nmax - kb + TR_ROWS - 1) / TR_ROWS));

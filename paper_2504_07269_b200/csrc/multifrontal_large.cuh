@@ -126,11 +126,13 @@ __global__ void __launch_bounds__(NT, 4) asm_front_kernel(LevelArgs a) {
   }
 }
 
-// one warp per instance: w x w diagonal block of panel kb (lane = row)
-__global__ void __launch_bounds__(32) diag_kernel(LevelArgs a, int kb) {
+// w x w diagonal block of panel kb, one CTA per instance: warp 0 factors it
+// (lane = row), then every warp forward-solves its share of the RHS
+// (blockDim = 32 * min(8, nrhs))
+__global__ void __launch_bounds__(256) diag_kernel(LevelArgs a, int kb) {
   __shared__ cplx Ld[NB * LDD];
   __shared__ cplx dinv_s[NB], cdg[NB];
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int inst = blockIdx.x;
   const int k = inst % a.nbatch;
   const FrontDev F = a.fronts[a.list[inst / a.nbatch]];
@@ -142,48 +144,51 @@ __global__ void __launch_bounds__(32) diag_kernel(LevelArgs a, int kb) {
   cplx* Zk = a.Z + (int64_t)k * nx * nrhs;
   const int64_t shift = a.shift0 + k;
   const cplx zero = cmk(0.0, 0.0);
-  for (int c = 0; c < w; ++c)
-    if (lane >= c && lane < w) Ld[c * LDD + lane] = ldc(P + (kb + lane) + (int64_t)(kb + c) * n);
-  __syncwarp();
-  // step j: a_ic -= (a_ij / d_j) a_cj on unscaled values; then columns scale by 1/c_j = d_j^{-1/2}
-  for (int j = 0; j < w; ++j) {
-    const cplx d = Ld[j * LDD + j];
-    if (lane > j && lane < w) {
-      const cplx f = cmul(Ld[j * LDD + lane], crecip_fast(d));
-      cplx* __restrict__ rowp = Ld + lane;
-      const cplx* __restrict__ colj = Ld + j * LDD;
-      int c = j + 1;
-      for (; c + 3 <= lane; c += 4) {
-        const cplx x0 = rowp[c * LDD], x1 = rowp[(c + 1) * LDD], x2 = rowp[(c + 2) * LDD],
-                   x3 = rowp[(c + 3) * LDD];
-        const cplx y0 = colj[c], y1 = colj[c + 1], y2 = colj[c + 2], y3 = colj[c + 3];
-        rowp[c * LDD] = cfms(x0, f, y0);
-        rowp[(c + 1) * LDD] = cfms(x1, f, y1);
-        rowp[(c + 2) * LDD] = cfms(x2, f, y2);
-        rowp[(c + 3) * LDD] = cfms(x3, f, y3);
+  if (warp == 0) {
+    for (int c = 0; c < w; ++c)
+      if (lane >= c && lane < w) Ld[c * LDD + lane] = ldc(P + (kb + lane) + (int64_t)(kb + c) * n);
+    __syncwarp();
+    // step j: a_ic -= (a_ij / d_j) a_cj on unscaled values; then columns scale by 1/c_j = d_j^{-1/2}
+    for (int j = 0; j < w; ++j) {
+      const cplx d = Ld[j * LDD + j];
+      if (lane > j && lane < w) {
+        const cplx f = cmul(Ld[j * LDD + lane], crecip_fast(d));
+        cplx* __restrict__ rowp = Ld + lane;
+        const cplx* __restrict__ colj = Ld + j * LDD;
+        int c = j + 1;
+        for (; c + 3 <= lane; c += 4) {
+          const cplx x0 = rowp[c * LDD], x1 = rowp[(c + 1) * LDD], x2 = rowp[(c + 2) * LDD],
+                     x3 = rowp[(c + 3) * LDD];
+          const cplx y0 = colj[c], y1 = colj[c + 1], y2 = colj[c + 2], y3 = colj[c + 3];
+          rowp[c * LDD] = cfms(x0, f, y0);
+          rowp[(c + 1) * LDD] = cfms(x1, f, y1);
+          rowp[(c + 2) * LDD] = cfms(x2, f, y2);
+          rowp[(c + 3) * LDD] = cfms(x3, f, y3);
+        }
+        for (; c <= lane; ++c) rowp[c * LDD] = cfms(rowp[c * LDD], f, colj[c]);
       }
-      for (; c <= lane; ++c) rowp[c * LDD] = cfms(rowp[c * LDD], f, colj[c]);
+      __syncwarp();
+    }
+    if (lane < w) {
+      const cplx d = Ld[lane * LDD + lane];
+      const double m2 = cabs2(d);
+      if (!(m2 > 1e-300) || !isfinite(m2)) atomicCAS(a.err, 0, (int)shift + 1);
+      const cplx c = csqrt_(d);
+      cdg[lane] = c;
+      dinv_s[lane] = crecip(c);
     }
     __syncwarp();
+    for (int j = 0; j < w; ++j) {
+      if (lane == j) Ld[j * LDD + j] = cdg[j];
+      else if (lane > j && lane < w) Ld[j * LDD + lane] = cmul(Ld[j * LDD + lane], dinv_s[j]);
+    }
+    __syncwarp();
+    for (int c = 0; c < w; ++c)
+      if (lane >= c && lane < w) stc(P + (kb + lane) + (int64_t)(kb + c) * n, Ld[c * LDD + lane]);
   }
-  if (lane < w) {
-    const cplx d = Ld[lane * LDD + lane];
-    const double m2 = cabs2(d);
-    if (!(m2 > 1e-300) || !isfinite(m2)) atomicCAS(a.err, 0, (int)shift + 1);
-    const cplx c = csqrt_(d);
-    cdg[lane] = c;
-    dinv_s[lane] = crecip(c);
-  }
-  __syncwarp();
-  for (int j = 0; j < w; ++j) {
-    if (lane == j) Ld[j * LDD + j] = cdg[j];
-    else if (lane > j && lane < w) Ld[j * LDD + lane] = cmul(Ld[j * LDD + lane], dinv_s[j]);
-  }
-  __syncwarp();
-  for (int c = 0; c < w; ++c)
-    if (lane >= c && lane < w) stc(P + (kb + lane) + (int64_t)(kb + c) * n, Ld[c * LDD + lane]);
-  // y = C11^{-1} r, lane c holds y_c; one warp reduction per step
-  for (int r = 0; r < nrhs; ++r) {
+  __syncthreads();
+  // y = C11^{-1} r, lane c holds y_c; one warp reduction per step, RHS over warps
+  for (int r = warp; r < nrhs; r += nwarp) {
     cplx* z = Zk + F.pbeg + kb + (int64_t)r * nx;
     cplx yl = lane < w ? ldc(z + lane) : zero;
     for (int j = 0; j < w; ++j) {

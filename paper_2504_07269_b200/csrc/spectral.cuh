@@ -89,7 +89,6 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
   if (n0 >= ncols) return;
   const int K = OP == OP_F2 ? 2 * m : OP == OP_B1 ? g : m;
   const double* __restrict__ V = a.V + S.vofs;
-  const double* __restrict__ th = a.th + S.tofs;
   const double* __restrict__ Rm = a.RQ + S.rqofs;
   const double* __restrict__ Qm = Rm + (int64_t)g * m;
   const int32_t* __restrict__ bidx = a.bidx + F.bidx_beg;
