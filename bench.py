@@ -203,6 +203,17 @@ def dmma_peak_live():
     return best
 
 
+def hbm_peak():
+    """(GB/s, source): MEASURED_PEAKS.json's copy bandwidth, else the profiling recipe's fallback."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            v = float(json.load(f)["hbm_gbs"])
+        return v, "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback: 6.65 TB/s from B200_PROFILING.md (MEASURED_PEAKS.json absent)"
+
+
 def run_ours(args):
     import torch
     rank, world, local = dist_env()
@@ -333,6 +344,18 @@ def run_ours(args):
                   "achieved": flops_factor / t_fs / 1e12, "frac": flops_factor / t_fs / 1e12 / peak}
     roof_tr = {"bound": "tensor", "kernel": "time_transform_kernel (K3)", "achieved": flops_tr / t_tr / 1e12,
                "peak": peak, "unit": "TFLOP/s", "frac": flops_tr / t_tr / 1e12 / peak}
+    # batched triangular solves (backward family) against the HBM roofline: the backward sweep
+    # reads every stored factor entry once per shift and reads + writes the solution vectors
+    hbm = hbm_peak()
+    roof_solve = None
+    if "backward" in fam and fam["backward"]["ms"] > 0:
+        sb = 16.0 * fdm.plan.stats["factor_elems"] * prob.nt + 32.0 * prob.nx * prob.nt * prob.n_rhs
+        gbs = sb / (fam["backward"]["ms"] / 1e3) / 1e9
+        roof_solve = {"bound": "hbm", "kernel": "backward kernels (K5 batched triangular solves)",
+                      "achieved": gbs, "peak": hbm[0], "unit": "GB/s", "frac": gbs / hbm[0],
+                      "bytes_per_step": sb, "peak_source": hbm[1],
+                      "algorithmic": "16 B x stored factor entries (multifrontal fronts) x n_t + 32 B x n_x x n_t "
+                                     "x n_rhs (solution read + write)"}
     launches = 2 + fdm.plan.last_launches()   # two K3 transforms + the multifrontal level launches
 
     cpu = None
@@ -362,6 +385,7 @@ def run_ours(args):
         "spectral_setup_s": fdm.plan.t_spectral,
         "paper_time_s": t_setup + t_step, "relative_residual": res, "kappa2": fdm.kappa2,
         "roofline": roof, "roofline_multifrontal": roof_phase, "roofline_transform": roof_tr,
+        "roofline_solve": roof_solve,
         "kernel_families": fam,
         "gpu_launches": launches * args.steps,
         "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,

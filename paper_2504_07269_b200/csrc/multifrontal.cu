@@ -664,12 +664,15 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
   // the gap to the previous event is charged to the launch's family
   cudaEvent_t fev_start = nullptr;
   std::vector<std::pair<cudaEvent_t, int>> fevs;
+  std::vector<int> fev_depth;   // depth of each family event (STFEM_LEVEL_TIMING breakdown)
+  int cur_depth = -1;
   auto fam = [&](int f, cudaStream_t st) {
     if (!level_timing) return;
     cudaEvent_t e;
     cudaEventCreate(&e);
     cudaEventRecord(e, st);
     fevs.push_back({e, f});
+    fev_depth.push_back(cur_depth);
   };
   auto mark = [&]() {
     if (!level_timing) return;
@@ -739,6 +742,7 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
       fam(FAM_SPECTRAL, st);
     }
     for (int d = P.depth; d >= 0; --d) {
+      cur_depth = d;
       const int q = d & 1;
       a.list = P.d_levels + P.level_off[d];
       a.nlist = (int32_t)P.levels[d].size();
@@ -815,6 +819,7 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
       mark();
     }
     for (int d = 0; d <= P.depth; ++d) {
+      cur_depth = d;
       a.list = P.d_levels + P.level_off[d];
       a.nlist = (int32_t)P.levels[d].size();
       for (int j = 2; j < 4; ++j) {
@@ -897,12 +902,26 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
     P.family_ms.assign(NFAM, 0.0);
     P.family_launches.assign(NFAM, 0);
     cudaEvent_t prev = fev_start;
-    for (auto& fe : fevs) {
+    std::vector<double> dfm((size_t)(P.depth + 2) * NFAM, 0.0);
+    for (size_t i = 0; i < fevs.size(); ++i) {
+      const auto& fe = fevs[i];
       float ms = 0;
       cudaEventElapsedTime(&ms, prev, fe.first);
       P.family_ms[fe.second] += ms;
       P.family_launches[fe.second] += 1;
+      dfm[(size_t)(fev_depth[i] + 1) * NFAM + fe.second] += ms;
       prev = fe.first;
+    }
+    if (level_print) {
+      static const char* fn[NFAM] = {"spectral", "asm", "diag", "trsm", "panel", "syrk", "backward", "small"};
+      fprintf(stderr, "[stfem depth x family ms]  depth");
+      for (int f = 0; f < NFAM; ++f) fprintf(stderr, " %9s", fn[f]);
+      fprintf(stderr, "\n");
+      for (int d = -1; d <= P.depth; ++d) {
+        fprintf(stderr, "[stfem depth x family ms]  %5d", d);
+        for (int f = 0; f < NFAM; ++f) fprintf(stderr, " %9.2f", dfm[(size_t)(d + 1) * NFAM + f]);
+        fprintf(stderr, "\n");
+      }
     }
     for (auto& fe : fevs) cudaEventDestroy(fe.first);
     cudaEventDestroy(fev_start);
