@@ -75,6 +75,7 @@ struct LevelArgs {
   int split_syrk;             // Schur update of large fronts in syrk_level_kernel
   const int32_t* ent_colptr;  // per front (p + 1): first sorted original entry of each pivot column
   int unit_diag;              // backward: 1 = unit-L LDL^T fronts, 0 = C C^T fronts
+  int asm_pivots_only;        // asm_front_kernel: pivot columns only (U assembled by syrk_gather_kernel)
 };
 
 __device__ __forceinline__ int64_t bv_off(const stfem_bv_layout& L, int r, int64_t shift, int64_t j) {
@@ -230,6 +231,68 @@ __global__ void __launch_bounds__(NT, 2) syrk_level_kernel(LevelArgs a, const in
   cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
   cplx* U = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
   gemm_update<3>(U, b, b, b, P + p, n, P + p, n, p, true, gsm, tl.y, tl.z, CLoad{U, b});
+}
+
+// Tile initialiser of the fused Schur update: the extend-add of the (at most
+// two) children's update blocks, gathered straight into the accumulators
+// through the inverse relpos maps of the tile's 64 rows and 64 columns
+// (staged in shared memory).  Same sum order as asm_front_kernel (0 + c0 + c1).
+struct GatherInit {
+  const int* inv_r;   // [2][64] child boundary row of tile row r (-1: none)
+  const int* inv_c;   // [2][64] same for tile columns
+  const cplx* Uc[2];
+  int bc[2], nc, i0, c0;
+  __device__ __forceinline__ cplx operator()(int row, int col) const {
+    cplx v = cmk(0.0, 0.0);
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (s >= nc) break;
+      const int kr = inv_r[s * 64 + row - i0], kc = inv_c[s * 64 + col - c0];
+      if (kr >= 0 && kc >= 0) v = cadd(v, ldc(Uc[s] + (int64_t)kc * bc[s] + kr));
+    }
+    return v;
+  }
+};
+
+// Fused assembly + Schur update of the boundary block: U = sum_children
+// extend-add - L21 L21^T in one pass (asm_front_kernel then assembles only the
+// pivot columns).  Saves writing the assembled U and reading it back, i.e. two
+// of the four HBM passes over every update block.
+__global__ void __launch_bounds__(NT, 2) syrk_gather_kernel(LevelArgs a, const int4* __restrict__ tiles) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* gsm = reinterpret_cast<cplx*>(smem_raw);
+  int* inv_s = reinterpret_cast<int*>(smem_raw + SYRK_SMEM);   // [2][64] rows, [2][64] cols
+  const int k = blockIdx.x % a.nbatch;
+  const int4 tl = tiles[blockIdx.x / a.nbatch];
+  const FrontDev F = a.fronts[tl.x];
+  const int n = F.n, p = F.p, b = n - p;
+  const int i0 = tl.y * TM, c0 = tl.z * TM;
+  const int nc = min(F.nchild, 2);
+  GatherInit gi;
+  gi.inv_r = inv_s;
+  gi.inv_c = inv_s + 128;
+  gi.nc = nc;
+  gi.i0 = i0;
+  gi.c0 = c0;
+  for (int q = threadIdx.x; q < 256; q += NT) {
+    const int s = (q >> 6) & 1, r = q & 63, isc = q >> 7;
+    const int fr = (isc ? c0 : i0) + r;
+    inv_s[q] = (s < nc && fr < b) ? a.inv[F.inv_beg + s * n + p + fr] : -1;
+  }
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    gi.Uc[s] = nullptr;
+    gi.bc[s] = 0;
+    if (s < nc) {
+      const FrontDev Cf = a.fronts[a.child_ids[F.child_beg + s]];
+      gi.bc[s] = Cf.n - Cf.p;
+      gi.Uc[s] = a.uchild + (int64_t)k * a.uchild_stride + Cf.uofs;
+    }
+  }
+  __syncthreads();
+  cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
+  cplx* U = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
+  gemm_update<3>(U, b, b, b, P + p, n, P + p, n, p, true, gsm, tl.y, tl.z, gi);
 }
 
 // Backward substitution of one level, one CTA per (front, shift) instance:
@@ -454,6 +517,8 @@ int upload(Plan& P) {
     if (!tl.empty())
       STFEM_CUDA_TRY(cudaMemcpy(P.d_syrk_tiles, tl.data(), tl.size() * sizeof(int4), cudaMemcpyHostToDevice));
     STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SYRK_SMEM));
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        SYRK_SMEM + 1024));
     STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_level_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   }
   // spectral subtrees: data + per-depth work items (fwd1 = U and F1, fwd2 = F2, bwd1 = B1, bwd2 = B2)
@@ -783,7 +848,11 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
       } else {
         // large fronts: tile-parallel pipeline over all (front, shift) instances of the level
         const int ninst = a.nlist * nb, pmax = P.level_pmax[d];
-        asm_front_kernel<<<dim3(ninst, (nmax + ASM_COLS - 1) / ASM_COLS), NT, (size_t)2 * nmax * sizeof(int),
+        const int64_t ntl = P.syrk_off[d + 1] - P.syrk_off[d];
+        // fused levels: the boundary block U is gathered by syrk_gather_kernel, not assembled here
+        a.asm_pivots_only = (ntl > 0 && pmax >= P.fused_min_p) ? 1 : 0;
+        const int asm_cols = a.asm_pivots_only ? pmax : nmax;
+        asm_front_kernel<<<dim3(ninst, (asm_cols + ASM_COLS - 1) / ASM_COLS), NT, (size_t)2 * nmax * sizeof(int),
                            st>>>(a);
         STFEM_LAUNCH_CHECK("asm_front_kernel");
         ++nlaunch;
@@ -808,8 +877,12 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
             fam(FAM_PANEL, st);
           }
         }
-        const int64_t ntl = P.syrk_off[d + 1] - P.syrk_off[d];
-        if (a.split_syrk && ntl > 0) {
+        if (ntl > 0 && a.asm_pivots_only) {
+          syrk_gather_kernel<<<(unsigned)(ntl * nb), NT, SYRK_SMEM + 1024, st>>>(a, P.d_syrk_tiles + P.syrk_off[d]);
+          STFEM_LAUNCH_CHECK("syrk_gather_kernel");
+          ++nlaunch;
+          fam(FAM_SYRK, st);
+        } else if (a.split_syrk && ntl > 0) {
           syrk_level_kernel<<<(unsigned)(ntl * nb), NT, SYRK_SMEM, st>>>(a, P.d_syrk_tiles + P.syrk_off[d]);
           STFEM_LAUNCH_CHECK("syrk_level_kernel");
           ++nlaunch;

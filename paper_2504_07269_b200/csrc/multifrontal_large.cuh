@@ -36,8 +36,9 @@ __global__ void __launch_bounds__(NT, 4) asm_front_kernel(LevelArgs a) {
   const FrontDev F = a.fronts[a.list[inst / a.nbatch]];
   const int n = F.n, p = F.p, b = n - p;
   const int c0 = blockIdx.y * ASM_COLS;
-  if (c0 >= n) return;
-  const int cend = min(n, c0 + ASM_COLS);
+  const int ncol = a.asm_pivots_only ? p : n;   // fused levels: U is gathered by syrk_gather_kernel
+  if (c0 >= ncol) return;
+  const int cend = min(ncol, c0 + ASM_COLS);
   cplx* U = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
   const int nrhs = a.nrhs, nx = a.nx;
   const cplx lam = a.lam[k];
@@ -312,3 +313,4 @@ __global__ void __launch_bounds__(NT, 2) panel_update_kernel(LevelArgs a, int kb
   gemm_update<2>(C, n, n - base, p - base, P + base + (int64_t)kb * n, n, P + base + (int64_t)kb * n, n, NB,
                  true, gsm, ti, tj, CLoad{C, n});
 }
+

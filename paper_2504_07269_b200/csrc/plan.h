@@ -71,6 +71,12 @@ struct Plan {
   std::vector<int64_t> level_off;          // offsets into d_levels
   std::vector<int32_t> level_nmax, level_pmax;  // per depth: max front order / pivots
   bool force_big = getenv("STFEM_FORCE_BIG") != nullptr;  // diagnostics: disable the small-front path
+  // levels whose fronts have >= this many pivots fuse the extend-add of U into the Schur update
+  // (syrk_gather_kernel).  Measured on C4 (per batch of 342 shifts): a net gain for K = p >= 127
+  // (depths 1-4), break-even at p = 63, a loss at p <= 31 where the register-resident gather of a
+  // short-K tile is latency bound.  STFEM_FUSED_MIN_P tunes it at plan creation (0: every level,
+  // a huge value: none).
+  int fused_min_p = getenv("STFEM_FUSED_MIN_P") ? atoi(getenv("STFEM_FUSED_MIN_P")) : 64;
   int small_n_cap = getenv("STFEM_SMALL_N") ? atoi(getenv("STFEM_SMALL_N")) : 0;  // tuning: lower the threshold
   int32_t *d_child_ids = nullptr, *d_bidx = nullptr, *d_relpos = nullptr, *d_inv = nullptr;
   int32_t *d_ent_src = nullptr, *d_ent_dst = nullptr, *d_perm = nullptr, *d_ent_colptr = nullptr;

@@ -68,16 +68,22 @@ def test_lifting_matches_oracle():
     assert rel(L, Lo) < 1e-13
 
 
-@pytest.mark.parametrize("mode", ["small", "big", "spec24", "spec"])
+@pytest.mark.parametrize("mode", ["small", "big", "big_unfused", "spec24", "spec"])
 @pytest.mark.parametrize("kind,leaf", [("square9", 4), ("square16", 32), ("p2square6", 8),
                                         ("lshape5", 16), ("square40", 32), ("lshape12", 16)])
 def test_factor_solve_matches_splu(kind, leaf, mode, monkeypatch):
     """mode: small/big = plain multifrontal (shared-memory small-front kernels on,
-    or every front on the global-memory kernels); spec24 / spec = spectral
-    subtrees of <= 24 / <= 256 interior DoFs (K6) under a multifrontal top."""
-    if mode == "big":  # exercise the global-memory (large-front) kernels on small meshes too
+    or every front on the global-memory kernels, with the extend-add of the
+    update blocks fused into the Schur update or, big_unfused, assembled by
+    asm_front_kernel); spec24 / spec = spectral subtrees of <= 24 / <= 256
+    interior DoFs (K6) under a multifrontal top."""
+    if mode.startswith("big"):  # exercise the global-memory (large-front) kernels on small meshes too
         monkeypatch.setenv("STFEM_FORCE_BIG", "1")
-    spectral = {"small": 0, "big": 0, "spec24": 24, "spec": 256}[mode]
+    if mode == "big":  # every level fused (the default fuses levels with >= 64 pivots only)
+        monkeypatch.setenv("STFEM_FUSED_MIN_P", "0")
+    if mode == "big_unfused":
+        monkeypatch.setenv("STFEM_FUSED_MIN_P", "1000000")
+    spectral = {"small": 0, "big": 0, "big_unfused": 0, "spec24": 24, "spec": 256}[mode]
     if kind.startswith("p2"):
         mesh, deg = sm.refine_uniform(sm.build_structured_square(int(kind[8:]))), 2
         Mo, Ao = O.assemble_spatial(omesh(mesh), 2, mesh.p2_elements)
