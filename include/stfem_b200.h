@@ -208,6 +208,16 @@ int stfem_csr_spmv_c(const stfem_asm* a, const double* vals, const void* v,
  * prism, deterministic reduction. */
 int stfem_spacetime_errors(const stfem_asm* a, int32_t kind, const double* breakpoints, int32_t N,
                            const void* coeffs, int64_t ld, const void* psi0, double* out2, void* stream);
+/* Bartels-Stewart sweep update (Eq. 7, incremental form :418;
+ * replaces the per-step "g_l - sum_{k>l} S[l,k] A_x w_k" of
+ * kronecker_solver.solve(variant=BartelsStewart)):
+ *   G[r][l'][j] -= scol[l'] * (A_x w_r)[j]   for l' < l, j < n_x, r < nrhs.
+ * w: nrhs vectors of n_x c128 (stride ldw); scol: device S[0:l, l] (c128);
+ * G: device c128 with strides g_rhs_stride (between RHS) and g_shift_stride
+ * (between temporal rows). */
+int stfem_bs_update(const stfem_asm* a, const double* Avals, const void* w, int64_t ldw, int32_t nrhs,
+                    const void* scol, int32_t l, void* G, int64_t g_rhs_stride, int64_t g_shift_stride,
+                    void* stream);
 int stfem_apply_global(const stfem_asm* a, const double* Mvals, const double* Avals,
                        const double* Mt_band, const double* Bt_band, int32_t bw, int32_t nt,
                        const void* v, void* out, void* work, void* stream);

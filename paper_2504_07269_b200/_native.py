@@ -84,6 +84,7 @@ def _declare(lib):
         "stfem_asm_rhs": (C.c_int, [P, I32, P, I32, P, I64, P]),
         "stfem_csr_spmv_c": (C.c_int, [P, P, P, I64, P, I64, I32, D, D, D, P]),
         "stfem_apply_global": (C.c_int, [P, P, P, P, P, I32, P, P, P, P]),
+        "stfem_bs_update": (C.c_int, [P, P, P, I64, I32, P, I32, P, I64, I64, P]),
         "stfem_spacetime_errors": (C.c_int, [P, I32, P, I32, P, I64, P, P, P]),
     }
     for name, (res, args) in sig.items():

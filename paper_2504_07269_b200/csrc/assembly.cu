@@ -268,6 +268,44 @@ __global__ void spmv_c_kernel(int n, const int64_t* __restrict__ rp, const int32
   stc(yp, s);
 }
 
+// Bartels-Stewart sweep update: after w_l is solved,
+//   G[r][l'][j] -= S[l', l] * (A_x w_l^{(r)})[j]   for every pending row l' < l.
+// One thread per (spatial row j, RHS r): the CSR row product is formed once
+// and scattered down the l' rows with coalesced (along j) read-modify-writes.
+// The S column is staged in shared memory in chunks of 1024.
+__global__ void bs_update_kernel(int n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                 const double* __restrict__ val, const cplx* __restrict__ w, int64_t ldw,
+                                 int nrhs, const cplx* __restrict__ scol, int l, cplx* G, int64_t g_rhs,
+                                 int64_t g_shift) {
+  __shared__ cplx ss[1024];
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = gid < (int64_t)n * nrhs;
+  const int j = live ? (int)(gid % n) : 0, r = live ? (int)(gid / n) : 0;
+  double sr = 0, si = 0;
+  if (live) {
+    const cplx* wr = w + (int64_t)r * ldw;
+    for (int64_t k = rp[j]; k < rp[j + 1]; ++k) {
+      const cplx x = ldc(wr + ci[k]);
+      sr = fma(val[k], x.re, sr);
+      si = fma(val[k], x.im, si);
+    }
+  }
+  cplx* gp = G + (int64_t)r * g_rhs + j;
+  for (int c0 = 0; c0 < l; c0 += 1024) {
+    const int cn = min(1024, l - c0);
+    __syncthreads();
+    for (int q = threadIdx.x; q < cn; q += blockDim.x) ss[q] = ldc(scol + c0 + q);
+    __syncthreads();
+    if (!live) continue;
+    for (int q = 0; q < cn; ++q) {
+      const cplx s = ss[q];
+      cplx* g = gp + (int64_t)(c0 + q) * g_shift;
+      const cplx o = ldc(g);
+      stc(g, cmk(o.re - (s.re * sr - s.im * si), o.im - (s.re * si + s.im * sr)));
+    }
+  }
+}
+
 __global__ void combine_kernel(int nt, int nx, int bw, const double* __restrict__ Mb,
                                const double* __restrict__ Bb, const cplx* __restrict__ MV,
                                const cplx* __restrict__ AV, cplx* out) {
@@ -625,6 +663,23 @@ extern "C" int stfem_csr_spmv_c(const stfem_asm* a, const double* vals, const vo
       A.n, A.d_rowptr, A.d_colind, vals, (const stfem::cplx*)v, ldv, (stfem::cplx*)y, ldy, nvec,
       stfem::cmk(are, aim), beta);
   STFEM_LAUNCH_CHECK("spmv_c_kernel");
+  return STFEM_OK;
+}
+
+extern "C" int stfem_bs_update(const stfem_asm* a, const double* Avals, const void* w, int64_t ldw,
+                               int32_t nrhs, const void* scol, int32_t l, void* G, int64_t g_rhs_stride,
+                               int64_t g_shift_stride, void* stream) {
+  if (!a || !Avals || !w || !G || (l > 0 && !scol)) return stfem::fail(STFEM_ERR_ARG, "bs_update: null");
+  if (nrhs < 1 || l < 0 || ldw < 0) return stfem::fail(STFEM_ERR_DIM, "bs_update: bad nrhs / l / ldw");
+  const Asm& A = *reinterpret_cast<const Asm*>(a);
+  int rc;
+  if ((rc = stfem::upload(const_cast<Asm&>(A)))) return rc;
+  if (l == 0) return STFEM_OK;
+  const int64_t tot = (int64_t)A.n * nrhs;
+  stfem::bs_update_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      A.n, A.d_rowptr, A.d_colind, Avals, (const stfem::cplx*)w, ldw, nrhs, (const stfem::cplx*)scol, l,
+      (stfem::cplx*)G, g_rhs_stride, g_shift_stride);
+  STFEM_LAUNCH_CHECK("bs_update_kernel");
   return STFEM_OK;
 }
 

@@ -99,6 +99,33 @@ def eigen_decompose(A: np.ndarray, B_t: np.ndarray | None = None) -> TemporalFac
     return TemporalFactors(X=X, S=np.diag(w), Y=Y, kappa2=float(s[0] / s[-1]))
 
 
+def schur_decompose(A: np.ndarray, B_t: np.ndarray | None = None) -> TemporalFactors:
+    """Complex Schur form of the temporal core A = X S X^H:
+    X unitary, S upper triangular with the eigenvalues on its diagonal,
+    Y = X^H (iB_t)^{-1} (unitarity makes the inverse the conjugate transpose),
+    kappa2 = 1.  The Bartels-Stewart variant's decomposition."""
+    A = np.asarray(A, dtype=complex)
+    if not np.isfinite(A).all():
+        raise DecompositionFailure("schur_decompose: non-finite entries")
+    try:
+        S, X = sla.schur(A, output="complex")
+    except sla.LinAlgError as exc:  # pragma: no cover
+        raise DecompositionFailure(f"Schur iteration did not converge: {exc}") from exc
+    n = A.shape[0]
+    eps_dec = 1e-10 * n
+    na = max(np.linalg.norm(A), 1e-300)
+    if np.linalg.norm(A - X @ S @ X.conj().T) > eps_dec * na:
+        raise DecompositionFailure("schur_decompose: residual above 1e-10 n_t ||A||")   # SPEC.md:241
+    XH = X.conj().T
+    Y = XH if B_t is None else XH @ np.linalg.inv(1j * np.asarray(B_t, float))
+    return TemporalFactors(X=X, S=np.triu(S), Y=Y, kappa2=1.0, variant="schur")
+
+
+def schur_factors(M_t: np.ndarray, B_t: np.ndarray) -> TemporalFactors:
+    """Step 1 of the Bartels-Stewart solve: core and its complex Schur form."""
+    return schur_decompose(form_temporal_core(M_t, B_t), B_t)
+
+
 def temporal_factors(M_t: np.ndarray, B_t: np.ndarray) -> TemporalFactors:
     """Step 1 of the FD solve: core, eigendecomposition, Y, kappa_2."""
     return eigen_decompose(form_temporal_core(M_t, B_t), B_t)

@@ -8,9 +8,10 @@
   transform_blocks(T, v)  (SPEC.md:392-400)   -> K3
   apply_global(...)   -> K7 (residual certificate, :405)
 
-Kronecker factors are never materialised.  There is no silent
-Bartels-Stewart fallback: a defective core raises
-`NotDiagonalizable`.  All device work is stream-ordered; stage times are
+Kronecker factors are never materialised.  The Bartels-Stewart
+variant (`BSSolver`) runs the same kernels with a
+strictly sequential sweep; there is no silent fallback between the variants
+(SPEC.md:412): a defective core raises `NotDiagonalizable` under FD.  All device work is stream-ordered; stage times are
 CUDA-event times on the launching stream.
 """
 
@@ -206,15 +207,99 @@ class FDMSolver:
         return out_host
 
 
+class BSSolver:
+    """Bartels-Stewart variant: the fallback
+    for a temporal core that is not diagonalizable.
+
+    setup: complex Schur form C = X S X^H on the host (fp64, kappa2 = 1) +
+    the same symbolic analysis as FD.  solve(F):
+      (2) G = (Y (x) I) F                                   K3
+      (3) for l = n_t-1 .. 0 (strictly sequential, SPEC.md Concurrency Model):
+            (M_x + S[l,l] A_x) w_l = g_l                    K4/K5/K6, one shift
+            g_l' -= S[l',l] A_x w_l  for every l' < l       bs_update_kernel
+          (the incremental form of SPEC.md:418: A_x w_l formed once per l)
+      (4) Psi = (X (x) I) W                                 K3
+    All steps are stream-ordered GPU work; there is no CPU fallback."""
+
+    def __init__(self, ops: SpatialOperators, M_t: np.ndarray, B_t: np.ndarray,
+                 plan: SpatialPlan | None = None, leaf_size: int = 16):
+        from .dense_complex_linalg import schur_factors
+        t0 = time.perf_counter()
+        self.ops = ops
+        self.M_t = np.asarray(M_t, float)
+        self.B_t = np.asarray(B_t, float)
+        self.nt = self.M_t.shape[0]
+        self.tf = schur_factors(self.M_t, self.B_t)
+        t1 = time.perf_counter()
+        self.plan = plan if plan is not None else SpatialPlan(ops, leaf_size)
+        t2 = time.perf_counter()
+        dev = ops.device
+        self.X = torch.as_tensor(self.tf.X, dtype=C128, device=dev)
+        self.Y = torch.as_tensor(self.tf.Y, dtype=C128, device=dev)
+        self.diag = torch.as_tensor(np.diag(self.tf.S).copy(), dtype=C128, device=dev)
+        # row l of S^T = column l of S: the coefficients scattered after step l
+        self.St = torch.as_tensor(np.ascontiguousarray(self.tf.S.T), dtype=C128, device=dev)
+        self.t_eig = t1 - t0
+        self.t_symbolic = t2 - t1
+
+    @property
+    def kappa2(self) -> float:
+        return self.tf.kappa2
+
+    def solve(self, F: torch.Tensor, out: torch.Tensor | None = None, work: torch.Tensor | None = None,
+              stream=None, timings: dict | None = None) -> torch.Tensor:
+        N.require_cuda(F)
+        nt, nx = self.nt, self.ops.n
+        if F.shape[-2:] != (nt, nx):
+            raise N.DimensionMismatch(N.ERR_DIM, f"solve: f {tuple(F.shape)} vs ({nt}, {nx})")
+        if self.ops.Avals is None:
+            raise RuntimeError("spatial operators are not assembled")
+        single = F.dim() == 2
+        Fb = (F.unsqueeze(0) if single else F).contiguous()
+        nr = Fb.shape[0]
+        G = out.reshape(Fb.shape) if out is not None else torch.empty_like(Fb)
+        W = work.reshape(Fb.shape) if work is not None else torch.empty_like(Fb)
+        s = stream if stream is not None else torch.cuda.current_stream()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timings is not None else None
+        if ev:
+            ev[0].record(s)
+        K.time_transform(self.Y, Fb, out=G, stream=s)                           # (2)
+        if ev:
+            ev[1].record(s)
+        lay = blockvector_layout(nt, nx)
+        lib = N.lib()
+        for l in range(nt - 1, -1, -1):                                          # (3)
+            self.plan.factor_solve(self.diag[l:l + 1], G[:, l:l + 1], W[:, l:l + 1], lay, nr, stream=s)
+            if l > 0:
+                N.check(lib.stfem_bs_update(self.ops.handle, N.ptr(self.ops.Avals), N.ptr(W[:, l]),
+                                            nt * nx, nr, N.ptr(self.St[l]), l, N.ptr(G), nt * nx, nx,
+                                            N.stream_ptr(s)))
+        if ev:
+            ev[2].record(s)
+        K.time_transform(self.X, W, out=G, stream=s)                            # (4)
+        if ev:
+            ev[3].record(s)
+            ev[3].synchronize()
+            timings["forward_transform_s"] = ev[0].elapsed_time(ev[1]) / 1e3
+            timings["sweep_s"] = ev[1].elapsed_time(ev[2]) / 1e3
+            timings["back_transform_s"] = ev[2].elapsed_time(ev[3]) / 1e3
+        if out is not None:
+            return out
+        return G[0] if single else G
+
+
 def solve(ops: SpatialOperators, M_t: np.ndarray, B_t: np.ndarray, f: torch.Tensor,
           variant: SolverVariant = SolverVariant.FastDiagonalization, check_residual: bool = True,
           plan: SpatialPlan | None = None) -> SolveReport:
-    """SPEC.md:374-382 (FD variant).  Times steps 1-4."""
-    if variant != SolverVariant.FastDiagonalization:
-        raise NotImplementedError("Bartels-Stewart is out of scope for this build (SURVEY.md §2)")
+    """SPEC.md:374-382, both variants.  Times steps 1-4.  No
+    silent fallback: FD on a defective core raises
+    NotDiagonalizable and the caller retries with BartelsStewart."""
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    fdm = FDMSolver(ops, M_t, B_t, plan=plan)
+    if variant == SolverVariant.BartelsStewart:
+        fdm = BSSolver(ops, M_t, B_t, plan=plan)
+    else:
+        fdm = FDMSolver(ops, M_t, B_t, plan=plan)
     timings = {"eig_s": fdm.t_eig, "symbolic_s": fdm.t_symbolic}
     psi = fdm.solve(f, timings=timings)
     torch.cuda.synchronize()

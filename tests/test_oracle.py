@@ -218,3 +218,64 @@ def test_p2_spatial_sanity():
     assert isinstance(M, sp.csr_matrix)
     inner = ~O.finish(2, mesh.vertices, mesh.elements).boundary
     assert np.abs((A @ x2 + 2 * (M @ one))[inner]).max() < 1e-12
+
+
+# ---------------------------------------------------------------------------
+# Bartels-Stewart variant
+# ---------------------------------------------------------------------------
+
+def test_bs_spec_global_1x1():
+    """both variants give psi = 1/(4/3 + i/16) on the 1 x 1 system."""
+    Mx, Ax = O.assemble_spatial(O.square_mesh(2))
+    Mt, Bt = O.assemble_temporal(np.array([0.0, 1.0]))
+    psi = O.bs_solve(Mx, Ax, O.schur_decompose(Mt, Bt), np.array([[1.0 + 0j]]))
+    assert abs(psi[0, 0] - 1 / (4 / 3 + 1j / 16)) < 1e-15
+
+
+@pytest.mark.parametrize("m,N,graded", [(2, 3, False), (3, 5, True), (4, 4, False), (3, 8, True)])
+def test_bs_vs_dense_oracle(m, N, graded):
+    """the BS variant matches the explicit Kronecker system <= 1e-10."""
+    mesh = O.square_mesh(m)
+    bp = O.temporal_graded(1.0, N, 1.5) if graded else O.temporal_uniform(1.0, N)
+    Mx, Ax = O.assemble_spatial(mesh)
+    Mt, Bt = O.assemble_temporal(bp)
+    f = np.random.default_rng(m * N + 1).standard_normal((2, N, Mx.shape[0])) * (1 - 2j)
+    psi = O.bs_solve(Mx, Ax, O.schur_decompose(Mt, Bt), f)
+    D = O.dense_global(Mx, Ax, Mt, Bt)
+    for r in range(2):
+        ref = np.linalg.solve(D, f[r].ravel()).reshape(f[r].shape)
+        assert np.linalg.norm(psi[r] - ref) / np.linalg.norm(ref) < 1e-10
+
+
+def test_bs_fd_variant_agreement():
+    """BS and FD agree within 1e-8 kappa_2(X_t) (C1 sizes, P1 in time)."""
+    mesh = O.square_mesh(16)
+    Mx, Ax = O.assemble_spatial(mesh)
+    Mt, Bt = O.assemble_temporal(O.temporal_uniform(1.0, 16))
+    f = np.random.default_rng(7).standard_normal((16, Mx.shape[0])) + 0.5j
+    tf = O.eigen_decompose(Mt, Bt)
+    a = O.fdm_solve(Mx, Ax, tf, f)
+    b = O.bs_solve(Mx, Ax, O.schur_decompose(Mt, Bt), f)
+    assert np.linalg.norm(a - b) / np.linalg.norm(b) < 1e-8 * tf.kappa2
+
+
+@pytest.mark.parametrize("N,deg", [(16, 1), (64, 1), (32, 2)])
+def test_host_schur_decompose(N, deg):
+    """SPEC.md:241, :257: unitarity, residual, triangularity, kappa2 = 1, and the
+    Schur diagonal equals the eigenvalues of the core within 1e-8."""
+    from paper_2504_07269_b200 import dense_complex_linalg as dl
+    from paper_2504_07269_b200 import fem_assembly as fa
+    from paper_2504_07269_b200 import temporal_mesh as tm
+    Mt, Bt = fa.assemble_temporal(tm.uniform(1.0, N), deg)
+    n = Mt.shape[0]
+    C = dl.form_temporal_core(Mt, Bt)
+    sf = dl.schur_factors(Mt, Bt)
+    X, S = sf.X, sf.S
+    assert np.linalg.norm(X.conj().T @ X - np.eye(n)) <= 1e-12 * n
+    assert np.linalg.norm(C - X @ S @ X.conj().T) <= 1e-10 * n * np.linalg.norm(C)
+    assert np.abs(np.tril(S, -1)).max() == 0.0 and sf.kappa2 == 1.0 and sf.variant == "schur"
+    assert np.allclose(sf.Y @ (1j * Bt), X.conj().T, atol=1e-12)
+    ev = np.sort_complex(dl.temporal_factors(Mt, Bt).eigenvalues)
+    assert np.abs(np.sort_complex(np.diag(S)) - ev).max() < 1e-8
+    oracle = O.schur_decompose(Mt, Bt)
+    assert np.abs(np.sort_complex(np.diag(oracle.S)) - ev).max() < 1e-8
