@@ -76,6 +76,7 @@ struct LevelArgs {
   const int32_t* ent_colptr;  // per front (p + 1): first sorted original entry of each pivot column
   int unit_diag;              // backward: 1 = unit-L LDL^T fronts, 0 = C C^T fronts
   int asm_pivots_only;        // asm_front_kernel: pivot columns only (U assembled by syrk_gather_kernel)
+  int asm_cpc;                // asm_front_kernel: columns per CTA (a multiple of ASM_COLS)
 };
 
 __device__ __forceinline__ int64_t bv_off(const stfem_bv_layout& L, int r, int64_t shift, int64_t j) {
@@ -390,18 +391,16 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int uni
     }
     __syncthreads();
     {
-      // x_j = (t_j - sum_{c>j} L[c][j] x_c) * dinv_j, lane c holds x_c; one warp
-      // reduction per step; the right-hand sides are spread over the warps
+      // x_j = (t_j - sum_{c>j} L[c][j] x_c) * dinv_j in column (axpy) form: lane j
+      // holds t_j; once x_c is final it is broadcast and every lane j < c subtracts
+      // L[c][j] x_c -- one broadcast per step instead of a 5-level warp reduction.
+      // The right-hand sides are spread over the warps.
       for (int r = warp; r < nrhs; r += NT / 32) {
         cplx xl = lane < w ? xs[(kb + lane) * nrhs + r] : zero;
-        for (int j = w - 1; j >= 0; --j) {
-          cplx sacc = (lane > j && lane < w) ? cmul(l11[j * LDD + lane], xl) : zero;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            sacc.re += __shfl_xor_sync(0xffffffffu, sacc.re, o);
-            sacc.im += __shfl_xor_sync(0xffffffffu, sacc.im, o);
-          }
-          if (lane == j) xl = cmul(csub(xl, sacc), l11[j * LDD + j]);
+        for (int c = w - 1; c >= 0; --c) {
+          if (lane == c) xl = cmul(xl, l11[c * LDD + c]);
+          const cplx xc = cmk(__shfl_sync(0xffffffffu, xl.re, c), __shfl_sync(0xffffffffu, xl.im, c));
+          if (lane < c) xl = cfms(xl, l11[lane * LDD + c], xc);
         }
         if (lane < w) {
           stc(Zk + F.pbeg + kb + lane + (int64_t)r * nx, xl);
@@ -852,7 +851,9 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
         // fused levels: the boundary block U is gathered by syrk_gather_kernel, not assembled here
         a.asm_pivots_only = (ntl > 0 && pmax >= P.fused_min_p) ? 1 : 0;
         const int asm_cols = a.asm_pivots_only ? pmax : nmax;
-        asm_front_kernel<<<dim3(ninst, (asm_cols + ASM_COLS - 1) / ASM_COLS), NT, (size_t)2 * nmax * sizeof(int),
+        // deep levels (fronts of order <= asm_whole_n): one CTA per instance for all columns
+        a.asm_cpc = nmax <= P.asm_whole_n ? ((asm_cols + ASM_COLS - 1) / ASM_COLS) * ASM_COLS : ASM_COLS;
+        asm_front_kernel<<<dim3(ninst, (asm_cols + a.asm_cpc - 1) / a.asm_cpc), NT, (size_t)2 * nmax * sizeof(int),
                            st>>>(a);
         STFEM_LAUNCH_CHECK("asm_front_kernel");
         ++nlaunch;
@@ -867,11 +868,17 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
           STFEM_LAUNCH_CHECK("trsm_kernel");
           fam(FAM_TRSM, st);
           nlaunch += 2;
+          // delayed updates over groups of panel_group panels starting at g0 (see
+          // panel_update_kernel): inside a group only the next panel's columns are updated,
+          // by every panel of the group so far; after its last panel, everything beyond
+          const int GW = NB * P.panel_group, g0 = (kb / GW) * GW;
+          const int narrow = ((kb - g0) / NB < P.panel_group - 1) ? 1 : 0;
+          const int cb = kb + NB, k0 = g0, K = kb + NB - g0;
           int tiles = 0;
           for (int32_t f : P.levels[d])
-            tiles = std::max(tiles, panel_update_tiles(P.fronts[f].n, P.fronts[f].p, kb));
+            tiles = std::max(tiles, panel_update_tiles(P.fronts[f].n, P.fronts[f].p, cb, narrow));
           if (tiles > 0) {
-            panel_update_kernel<<<dim3(ninst, tiles), NT, GEMM_SMEM, st>>>(a, kb);
+            panel_update_kernel<<<dim3(ninst, tiles), NT, GEMM_SMEM, st>>>(a, cb, k0, K, narrow);
             STFEM_LAUNCH_CHECK("panel_update_kernel");
             ++nlaunch;
             fam(FAM_PANEL, st);

@@ -20,7 +20,8 @@
 //                        solves x C11^T = b in registers (right-looking, W
 //                        independent chains) and updates its RHS r -= x y
 //     panel_update_kernel (instance, 64x64 tile): trailing pivot columns
-//                        F[base:, base:p] -= X X^T on the FP64 tensor pipe
+//                        F[base:, base:p] -= X X^T on the FP64 tensor pipe,
+//                        delayed over groups of panels (K up to 128)
 //   syrk_level_kernel    (instance, 64x64 tile): U = F22 - L21 L21^T, K = p.
 // Factor format: K = C C^T (transpose, not conjugate transpose).
 #pragma once
@@ -35,10 +36,13 @@ __global__ void __launch_bounds__(NT, 4) asm_front_kernel(LevelArgs a) {
   const int k = inst % a.nbatch;
   const FrontDev F = a.fronts[a.list[inst / a.nbatch]];
   const int n = F.n, p = F.p, b = n - p;
-  const int c0 = blockIdx.y * ASM_COLS;
+  // this CTA assembles columns [cbeg, cstop) in blocks of ASM_COLS (a.asm_cpc columns per CTA:
+  // one block on the wide top levels, the whole front on deep levels so the per-CTA setup
+  // -- descriptor chain, inverse maps, barriers -- is paid once per instance)
+  const int cbeg = blockIdx.y * a.asm_cpc;
   const int ncol = a.asm_pivots_only ? p : n;   // fused levels: U is gathered by syrk_gather_kernel
-  if (c0 >= ncol) return;
-  const int cend = min(ncol, c0 + ASM_COLS);
+  if (cbeg >= ncol) return;
+  const int cstop = min(ncol, cbeg + a.asm_cpc);
   cplx* U = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
   const int nrhs = a.nrhs, nx = a.nx;
   const cplx lam = a.lam[k];
@@ -55,14 +59,15 @@ __global__ void __launch_bounds__(NT, 4) asm_front_kernel(LevelArgs a) {
     Ucs[s] = a.uchild + (int64_t)k * a.uchild_stride + Cf.uofs;
     Rcs[s] = a.rchild + ((int64_t)k * a.rchild_stride + Cf.rofs) * nrhs;
   }
-  // original entries of pivot columns [c0, min(cend, p)): one contiguous range of the sorted list
+  // original entries of pivot columns [cbeg, min(cstop, p)): one contiguous range of the sorted list
   const int* cp = a.ent_colptr + F.colptr_beg;
-  const int ent_lo = c0 < p ? cp[c0] : 0, ent_hi = c0 < p ? cp[min(cend, p)] : 0;
+  const int ent_lo = cbeg < p ? cp[cbeg] : 0, ent_hi = cbeg < p ? cp[min(cstop, p)] : 0;
   __syncthreads();
   // gather: warp w owns columns c0 + w + 8u (u < 4), lanes run down the rows
   constexpr int CU = 4, NW = NT / 32;
   const cplx zero = cmk(0.0, 0.0);
-  {
+  for (int c0 = cbeg; c0 < cstop; c0 += ASM_COLS) {
+    const int cend = min(cstop, c0 + ASM_COLS);
     int k2[2][CU];
     cplx* dst[CU];
 #pragma unroll
@@ -188,18 +193,15 @@ __global__ void __launch_bounds__(256) diag_kernel(LevelArgs a, int kb) {
       if (lane >= c && lane < w) stc(P + (kb + lane) + (int64_t)(kb + c) * n, Ld[c * LDD + lane]);
   }
   __syncthreads();
-  // y = C11^{-1} r, lane c holds y_c; one warp reduction per step, RHS over warps
+  // y = C11^{-1} r in column (axpy) form: lane i holds r_i; once y_j is final it
+  // is broadcast and every lane i > j subtracts C[i][j] y_j (RHS over warps)
   for (int r = warp; r < nrhs; r += nwarp) {
     cplx* z = Zk + F.pbeg + kb + (int64_t)r * nx;
     cplx yl = lane < w ? ldc(z + lane) : zero;
     for (int j = 0; j < w; ++j) {
-      cplx s = lane < j ? cmul(Ld[lane * LDD + j], yl) : zero;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        s.re += __shfl_xor_sync(0xffffffffu, s.re, o);
-        s.im += __shfl_xor_sync(0xffffffffu, s.im, o);
-      }
-      if (lane == j) yl = cmul(csub(yl, s), dinv_s[j]);
+      if (lane == j) yl = cmul(yl, dinv_s[j]);
+      const cplx yj = cmk(__shfl_sync(0xffffffffu, yl.re, j), __shfl_sync(0xffffffffu, yl.im, j));
+      if (lane > j && lane < w) yl = cfms(yl, Ld[j * LDD + lane], yj);
     }
     if (lane < w) stc(z + lane, yl);
   }
@@ -213,7 +215,8 @@ __global__ void __launch_bounds__(256) diag_kernel(LevelArgs a, int kb) {
 template <int W>
 __global__ void __launch_bounds__(TR_ROWS, 4) trsm_kernel(LevelArgs a, int kb) {
   constexpr int WB = 16;
-  __shared__ cplx Ls[W * W];          // Ls[c * W + c'] = C[kb+c][kb+c'] (c' < c); Ls[c*W+c] = 1 / c_cc
+  constexpr int LW = W + 1;           // padded pitch: the column-wise staging below is conflict-free
+  __shared__ cplx Ls[W * LW];         // Ls[c * LW + c'] = C[kb+c][kb+c'] (c' < c); Ls[c*LW+c] = 1 / c_cc
   __shared__ cplx ys[W * MAXR];
   const int tid = threadIdx.x;
   const int inst = blockIdx.x;
@@ -229,7 +232,7 @@ __global__ void __launch_bounds__(TR_ROWS, 4) trsm_kernel(LevelArgs a, int kb) {
   cplx* Zk = a.Z + (int64_t)k * nx * nrhs;
   const cplx zero = cmk(0.0, 0.0);
   for (int idx = tid; idx < W * W; idx += TR_ROWS) {
-    const int c = idx / W, c2 = idx % W;
+    const int c = idx % W, c2 = idx / W;   // consecutive threads walk down column c2 (coalesced)
     cplx v = zero;
     if (c < w && c2 <= c) {
       v = ldc(P + (kb + c) + (int64_t)(kb + c2) * n);
@@ -237,7 +240,7 @@ __global__ void __launch_bounds__(TR_ROWS, 4) trsm_kernel(LevelArgs a, int kb) {
     } else if (c2 == c) {
       v = cmk(1.0, 0.0);
     }
-    Ls[idx] = v;
+    Ls[c * LW + c2] = v;
   }
   for (int idx = tid; idx < W * nrhs; idx += TR_ROWS) {
     const int c = idx % W, r = idx / W;
@@ -257,13 +260,13 @@ __global__ void __launch_bounds__(TR_ROWS, 4) trsm_kernel(LevelArgs a, int kb) {
     for (int c2 = 0; c2 < jb; ++c2) {
       const cplx xc = ldc(prow + (int64_t)c2 * n);
 #pragma unroll
-      for (int c = 0; c < WB; ++c) x[c] = cfms(x[c], xc, Ls[(jb + c) * W + c2]);
+      for (int c = 0; c < WB; ++c) x[c] = cfms(x[c], xc, Ls[(jb + c) * LW + c2]);
     }
 #pragma unroll
     for (int c = 0; c < WB; ++c) {
-      x[c] = cmul(x[c], Ls[(jb + c) * W + jb + c]);
+      x[c] = cmul(x[c], Ls[(jb + c) * LW + jb + c]);
 #pragma unroll
-      for (int c2 = c + 1; c2 < WB; ++c2) x[c2] = cfms(x[c2], x[c], Ls[(jb + c2) * W + jb + c]);
+      for (int c2 = c + 1; c2 < WB; ++c2) x[c2] = cfms(x[c2], x[c], Ls[(jb + c2) * LW + jb + c]);
     }
 #pragma unroll
     for (int c = 0; c < WB; ++c)
@@ -279,26 +282,38 @@ __global__ void __launch_bounds__(TR_ROWS, 4) trsm_kernel(LevelArgs a, int kb) {
   }
 }
 
-// number of 64x64 tiles of the trailing pivot-column update after panel kb
-__host__ __device__ inline int panel_update_tiles(int n, int p, int kb) {
-  const int base = kb + NB;
-  if (base >= p) return 0;
-  const int tm = (n - base + TM - 1) / TM, tn = (p - base + TM - 1) / TM;
+// Trailing pivot-column updates, delayed over groups of G panels (right-looking
+// across groups, left-looking inside one): inside a group only the next
+// panel's 32 columns are updated, by every panel of the group so far
+// ("narrow"); after the group's last panel the columns beyond it receive all G
+// panels at once ("wide", K = 32 G), so the trailing block is read and written
+// once per 32 G pivots instead of once per 32.
+// Region of one update: rows [cb, n), columns [cb, cb + cols) with
+// cols = narrow ? min(NB, p - cb) : p - cb, updated by the panel columns [k0, k0 + K).
+__host__ __device__ inline int panel_update_cols(int p, int cb, int narrow) {
+  if (cb >= p) return 0;
+  return narrow ? min(NB, p - cb) : p - cb;
+}
+__host__ __device__ inline int panel_update_tiles(int n, int p, int cb, int narrow) {
+  const int cols = panel_update_cols(p, cb, narrow);
+  if (cols <= 0) return 0;
+  const int tm = (n - cb + TM - 1) / TM, tn = (cols + TM - 1) / TM;
   return tn * tm - tn * (tn - 1) / 2;
 }
 
-// trailing pivot-column update after a full panel: F[base:n, base:p] -= X X^T
-// (X = the panel's TRSM'd rows), lower trapezoid, one 64x64 tile per CTA, DMMA
-__global__ void __launch_bounds__(NT, 2) panel_update_kernel(LevelArgs a, int kb) {
+// F[cb:n, cb:cb+cols] -= X X^T, X = F[cb:n, k0:k0+K] (the TRSM'd panel rows),
+// lower trapezoid, one 64x64 tile per CTA, DMMA
+__global__ void __launch_bounds__(NT, 2) panel_update_kernel(LevelArgs a, int cb, int k0, int K, int narrow) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* gsm = reinterpret_cast<cplx*>(smem_raw);
   const int inst = blockIdx.x;
   const int k = inst % a.nbatch;
   const FrontDev F = a.fronts[a.list[inst / a.nbatch]];
   const int n = F.n, p = F.p;
-  const int base = kb + NB;
-  if (base >= p) return;
-  const int tm = (n - base + TM - 1) / TM, tn = (p - base + TM - 1) / TM;
+  const int cols = panel_update_cols(p, cb, narrow);
+  if (cols <= 0) return;
+  const int kk = min(K, p - k0);   // panels beyond this front's p contribute nothing
+  const int tm = (n - cb + TM - 1) / TM, tn = (cols + TM - 1) / TM;
   int t = blockIdx.y, ti = -1, tj = 0;
   for (; tj < tn; ++tj) {
     if (t < tm - tj) {
@@ -309,8 +324,7 @@ __global__ void __launch_bounds__(NT, 2) panel_update_kernel(LevelArgs a, int kb
   }
   if (ti < 0) return;
   cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
-  cplx* C = P + base + (int64_t)base * n;
-  gemm_update<2>(C, n, n - base, p - base, P + base + (int64_t)kb * n, n, P + base + (int64_t)kb * n, n, NB,
+  cplx* C = P + cb + (int64_t)cb * n;
+  gemm_update<2>(C, n, n - cb, cols, P + cb + (int64_t)k0 * n, n, P + cb + (int64_t)k0 * n, n, kk,
                  true, gsm, ti, tj, CLoad{C, n});
 }
-

@@ -6,6 +6,7 @@
 
 #include <stdlib.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "common.cuh"
@@ -77,6 +78,12 @@ struct Plan {
   // short-K tile is latency bound.  STFEM_FUSED_MIN_P tunes it at plan creation (0: every level,
   // a huge value: none).
   int fused_min_p = getenv("STFEM_FUSED_MIN_P") ? atoi(getenv("STFEM_FUSED_MIN_P")) : 64;
+  // trailing pivot-column updates are delayed over groups of this many 32-wide panels
+  // (K = 32 * panel_group for the wide updates; measured on C4: 2 -> 96 ms/step of panel updates,
+  // 1 -> 111, 4 -> 108, 8 -> 121); STFEM_PANEL_GROUP tunes it at plan creation
+  int panel_group = getenv("STFEM_PANEL_GROUP") ? std::max(1, atoi(getenv("STFEM_PANEL_GROUP"))) : 2;
+  // asm_front_kernel assembles a whole front per CTA for levels of order <= this (STFEM_ASM_WHOLE_N)
+  int asm_whole_n = getenv("STFEM_ASM_WHOLE_N") ? atoi(getenv("STFEM_ASM_WHOLE_N")) : 160;
   int small_n_cap = getenv("STFEM_SMALL_N") ? atoi(getenv("STFEM_SMALL_N")) : 0;  // tuning: lower the threshold
   int32_t *d_child_ids = nullptr, *d_bidx = nullptr, *d_relpos = nullptr, *d_inv = nullptr;
   int32_t *d_ent_src = nullptr, *d_ent_dst = nullptr, *d_perm = nullptr, *d_ent_colptr = nullptr;

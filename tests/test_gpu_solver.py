@@ -68,7 +68,7 @@ def test_lifting_matches_oracle():
     assert rel(L, Lo) < 1e-13
 
 
-@pytest.mark.parametrize("mode", ["small", "big", "big_unfused", "spec24", "spec"])
+@pytest.mark.parametrize("mode", ["small", "big", "big_unfused", "big_pg1", "big_pg4", "spec24", "spec"])
 @pytest.mark.parametrize("kind,leaf", [("square9", 4), ("square16", 32), ("p2square6", 8),
                                         ("lshape5", 16), ("square40", 32), ("lshape12", 16)])
 def test_factor_solve_matches_splu(kind, leaf, mode, monkeypatch):
@@ -83,7 +83,9 @@ def test_factor_solve_matches_splu(kind, leaf, mode, monkeypatch):
         monkeypatch.setenv("STFEM_FUSED_MIN_P", "0")
     if mode == "big_unfused":
         monkeypatch.setenv("STFEM_FUSED_MIN_P", "1000000")
-    spectral = {"small": 0, "big": 0, "big_unfused": 0, "spec24": 24, "spec": 256}[mode]
+    if mode in ("big_pg1", "big_pg4"):  # trailing updates delayed over 1 / 4 panels (default 2)
+        monkeypatch.setenv("STFEM_PANEL_GROUP", mode[-1])
+    spectral = {"small": 0, "big": 0, "big_unfused": 0, "big_pg1": 0, "big_pg4": 0, "spec24": 24, "spec": 256}[mode]
     if kind.startswith("p2"):
         mesh, deg = sm.refine_uniform(sm.build_structured_square(int(kind[8:]))), 2
         Mo, Ao = O.assemble_spatial(omesh(mesh), 2, mesh.p2_elements)
