@@ -43,6 +43,7 @@ constexpr int MAXR = 16;          // max RHS per call (bv chunks of 16 in the ho
 constexpr int GEMM_SMEM = (2 * 2 * TK * LDS + 2 * TK) * 16;
 constexpr int SYRK_SMEM = (3 * 2 * TK * LDS) * 16;   // 3-stage pipeline of the standalone Schur kernel
 constexpr int BWD_XS_MAX = 192 * 1024;   // backward_level_kernel: staged x (n x nrhs) per front
+constexpr int BWD_SPLIT_N = 256;         // backward: fronts above this order launch separately
 
 // kernel families of the per-family accounting (stfem_plan_kernel_report)
 enum { FAM_SPECTRAL = 0, FAM_ASM, FAM_DIAG, FAM_TRSM, FAM_PANEL, FAM_SYRK, FAM_BACKWARD, FAM_SMALL, NFAM };
@@ -232,6 +233,106 @@ __global__ void __launch_bounds__(NT, 2) syrk_level_kernel(LevelArgs a, const in
   cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
   cplx* U = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
   gemm_update<3>(U, b, b, b, P + p, n, P + p, n, p, true, gsm, tl.y, tl.z, CLoad{U, b});
+}
+
+// Short-K Schur update (levels with p <= KMAX <= 32 pivots, memory bound; used
+// for p <= 16 by default: C4 depth 9 11.1 -> 10.2 ms per batch, while at p = 31
+// (depths 7-8, 2 CTAs of 85 KB per SM) it lost to gemm_update, 10.7 -> 12.5 ms).  One 32 x 64 half of a 64 x 64 lower tile per CTA of 128
+// threads: the C block (F22), A (its 32 rows of L21) and B (64 rows of L21),
+// all K columns, are requested at once with 16-byte cp.async -- no registers
+// held, ~60-85 KB in flight per CTA, 2-3 CTAs per SM -- then DMMA from shared
+// memory and one store pass.  The register-staged C init of gemm_update caps
+// the in-flight bytes at the register file instead.
+template <int KMAX>
+struct SyrkShort {
+  static constexpr int M = 32, N = 64, LDC = M + 1, LDA = M + 2, LDB = N + 2;
+  static constexpr int SMEM = (N * LDC + KMAX * LDA + KMAX * LDB) * 16;
+};
+
+template <int KMAX>
+__global__ void __launch_bounds__(128) syrk_short_kernel(LevelArgs a, const int4* __restrict__ tiles) {
+  using S = SyrkShort<KMAX>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* Cs = reinterpret_cast<cplx*>(smem_raw);   // Cs[col * LDC + row]
+  cplx* As = Cs + S::N * S::LDC;                   // As[k * LDA + row]
+  cplx* Bs = As + KMAX * S::LDA;                   // Bs[k * LDB + col]
+  const int k = blockIdx.x % a.nbatch;
+  const int half = (blockIdx.x / a.nbatch) & 1;
+  const int4 tl = tiles[blockIdx.x / a.nbatch / 2];
+  const FrontDev F = a.fronts[tl.x];
+  const int n = F.n, p = F.p, b = n - p;
+  const int i0 = tl.y * TM + half * S::M, c0 = tl.z * TM;
+  if (i0 >= b) return;
+  const cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
+  cplx* U = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
+  const int tid = threadIdx.x;
+  // C block: lower entries only (zero-filled elsewhere), rows contiguous per column
+  for (int idx = tid; idx < S::M * S::N; idx += 128) {
+    const int r = idx % S::M, c = idx / S::M;
+    const int row = i0 + r, col = c0 + c;
+    const bool ok = row < b && col < b && row >= col;
+    cp_async16(Cs + c * S::LDC + r, ok ? U + row + (int64_t)col * b : U, ok);
+  }
+  for (int idx = tid; idx < S::M * KMAX; idx += 128) {
+    const int r = idx % S::M, kk = idx / S::M;
+    const bool ok = i0 + r < b && kk < p;
+    cp_async16(As + kk * S::LDA + r, ok ? P + p + i0 + r + (int64_t)kk * n : P, ok);
+  }
+  for (int idx = tid; idx < S::N * KMAX; idx += 128) {
+    const int c = idx % S::N, kk = idx / S::N;
+    const bool ok = c0 + c < b && kk < p;
+    cp_async16(Bs + kk * S::LDB + c, ok ? P + p + c0 + c + (int64_t)kk * n : P, ok);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  const int lane = tid & 31, wn = tid >> 5, g = lane >> 2, t = lane & 3;
+  double cre[2][2][4], cim[2][2][4];
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const cplx o = Cs[(wn * 16 + ni * 8 + 2 * t + v) * S::LDC + mi * 16 + g + 8 * h];
+          cre[mi][ni][2 * h + v] = o.re;
+          cim[mi][ni][2 * h + v] = o.im;
+        }
+  const int kmax = min(p, KMAX);
+  for (int kk = 0; kk < kmax; kk += 4) {
+    cplx av[2][2], bv[2];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+      av[mi][0] = As[(kk + t) * S::LDA + mi * 16 + g];
+      av[mi][1] = As[(kk + t) * S::LDA + mi * 16 + g + 8];
+    }
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) bv[ni] = Bs[(kk + t) * S::LDB + wn * 16 + ni * 8 + g];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) {
+        dmma_16x8x4(cre[mi][ni], -av[mi][0].re, -av[mi][1].re, bv[ni].re);
+        dmma_16x8x4(cre[mi][ni], av[mi][0].im, av[mi][1].im, bv[ni].im);
+        dmma_16x8x4(cim[mi][ni], -av[mi][0].re, -av[mi][1].re, bv[ni].im);
+        dmma_16x8x4(cim[mi][ni], -av[mi][0].im, -av[mi][1].im, bv[ni].re);
+      }
+  }
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int row = i0 + mi * 16 + g + 8 * h;
+          const int col = c0 + wn * 16 + ni * 8 + 2 * t + v;
+          if (row < b && col < b && row >= col)
+            stc(U + row + (int64_t)col * b, cmk(cre[mi][ni][2 * h + v], cim[mi][ni][2 * h + v]));
+        }
 }
 
 // Tile initialiser of the fused Schur update: the extend-add of the (at most
@@ -465,6 +566,23 @@ int upload(Plan& P) {
     if (!vec.empty()) STFEM_CUDA_TRY(cudaMemcpy(*dptr, vec.data(), vec.size() * sizeof(T), cudaMemcpyHostToDevice));
     return STFEM_OK;
   };
+  // fronts of a level in decreasing order: the backward pass launches the few large fronts of an
+  // unbalanced level (C5: n up to ~1000 next to n ~ 100) separately, so the many small ones run
+  // with small shared-memory staging instead of the level maximum
+  P.level_nsplit.assign(P.levels.size(), 0);
+  P.level_tail_nmax.assign(P.levels.size(), 0);
+  P.level_tail_pmax.assign(P.levels.size(), 0);
+  for (size_t d = 0; d < P.levels.size(); ++d) {
+    auto& L = P.levels[d];
+    std::stable_sort(L.begin(), L.end(), [&](int32_t x, int32_t y) { return P.fronts[x].n > P.fronts[y].n; });
+    int ns = 0;
+    while (ns < (int)L.size() && P.fronts[L[ns]].n > BWD_SPLIT_N) ++ns;
+    P.level_nsplit[d] = ns;
+    for (size_t i = ns; i < L.size(); ++i) {
+      P.level_tail_nmax[d] = std::max(P.level_tail_nmax[d], P.fronts[L[i]].n);
+      P.level_tail_pmax[d] = std::max(P.level_tail_pmax[d], P.fronts[L[i]].p);
+    }
+  }
   std::vector<int32_t> lv;
   P.level_off.assign(P.levels.size() + 1, 0);
   for (size_t d = 0; d < P.levels.size(); ++d) {
@@ -518,6 +636,10 @@ int upload(Plan& P) {
     STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SYRK_SMEM));
     STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         SYRK_SMEM + 1024));
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_short_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        SyrkShort<16>::SMEM));
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_short_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        SyrkShort<32>::SMEM));
     STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_level_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   }
   // spectral subtrees: data + per-depth work items (fwd1 = U and F1, fwd2 = F2, bwd1 = B1, bwd2 = B2)
@@ -889,6 +1011,16 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
           STFEM_LAUNCH_CHECK("syrk_gather_kernel");
           ++nlaunch;
           fam(FAM_SYRK, st);
+        } else if (ntl > 0 && pmax <= P.syrk_short_max_p) {
+          if (pmax <= 16)
+            syrk_short_kernel<16><<<(unsigned)(2 * ntl * nb), 128, SyrkShort<16>::SMEM, st>>>(
+                a, P.d_syrk_tiles + P.syrk_off[d]);
+          else
+            syrk_short_kernel<32><<<(unsigned)(2 * ntl * nb), 128, SyrkShort<32>::SMEM, st>>>(
+                a, P.d_syrk_tiles + P.syrk_off[d]);
+          STFEM_LAUNCH_CHECK("syrk_short_kernel");
+          ++nlaunch;
+          fam(FAM_SYRK, st);
         } else if (a.split_syrk && ntl > 0) {
           syrk_level_kernel<<<(unsigned)(ntl * nb), NT, SYRK_SMEM, st>>>(a, P.d_syrk_tiles + P.syrk_off[d]);
           STFEM_LAUNCH_CHECK("syrk_level_kernel");
@@ -916,23 +1048,33 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
         mark();
         continue;
       }
-      const int nmax = P.level_nmax[d], pmax = P.level_pmax[d];
-      const int bsm = small_bwd_smem_bytes(nmax, pmax, small_nr(nrhs));
       // factor format of this level: small-front kernel = unit-L LDL^T, large = C C^T
       const bool ldlt = level_is_small(P, d);
       a.unit_diag = ldlt ? 1 : 0;
-      if (nmax <= SMALL_N && bsm <= 200 * 1024 && !P.force_big) {
-        if ((rc = launch_small_backward_any(a, a.nlist * nb, nmax, pmax, st))) return rc;
-      } else {
-        const int u = ldlt ? 1 : 0, gsz = a.nlist * nb;
+      // one launch per size class: [0, nsplit) fronts of order > BWD_SPLIT_N, then the rest
+      auto bwd = [&](int32_t off, int32_t cnt, int nmax, int pmax) -> int {
+        LevelArgs b = a;
+        b.list = a.list + off;
+        b.nlist = cnt;
+        const int bsm = small_bwd_smem_bytes(nmax, pmax, small_nr(nrhs));
+        if (nmax <= SMALL_N && bsm <= 200 * 1024 && !P.force_big)
+          return launch_small_backward_any(b, cnt * nb, nmax, pmax, st);
+        const int u = ldlt ? 1 : 0, gsz = cnt * nb;
         switch (small_nr(nrhs)) {
-          case 1: rc = launch_backward_level<1>(a, gsz, nmax, u, st); break;
-          case 2: rc = launch_backward_level<2>(a, gsz, nmax, u, st); break;
-          case 4: rc = launch_backward_level<4>(a, gsz, nmax, u, st); break;
-          case 8: rc = launch_backward_level<8>(a, gsz, nmax, u, st); break;
-          default: rc = launch_backward_level<16>(a, gsz, nmax, u, st); break;
+          case 1: return launch_backward_level<1>(b, gsz, nmax, u, st);
+          case 2: return launch_backward_level<2>(b, gsz, nmax, u, st);
+          case 4: return launch_backward_level<4>(b, gsz, nmax, u, st);
+          case 8: return launch_backward_level<8>(b, gsz, nmax, u, st);
+          default: return launch_backward_level<16>(b, gsz, nmax, u, st);
         }
-        if (rc) return rc;
+      };
+      const int ns = P.level_nsplit[d];
+      if (ns > 0 && ns < a.nlist) {
+        if ((rc = bwd(0, ns, P.level_nmax[d], P.level_pmax[d]))) return rc;
+        if ((rc = bwd(ns, a.nlist - ns, P.level_tail_nmax[d], P.level_tail_pmax[d]))) return rc;
+        ++nlaunch;
+      } else if ((rc = bwd(0, a.nlist, P.level_nmax[d], P.level_pmax[d]))) {
+        return rc;
       }
       ++nlaunch;
       fam(FAM_BACKWARD, st);

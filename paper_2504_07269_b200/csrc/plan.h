@@ -71,19 +71,25 @@ struct Plan {
   int32_t* d_levels = nullptr;             // concatenated level lists
   std::vector<int64_t> level_off;          // offsets into d_levels
   std::vector<int32_t> level_nmax, level_pmax;  // per depth: max front order / pivots
+  std::vector<int32_t> level_nsplit;       // per depth: fronts of order > BWD_SPLIT_N (a prefix: levels sorted by n)
+  std::vector<int32_t> level_tail_nmax, level_tail_pmax;   // per depth: max order / pivots of the rest
   bool force_big = getenv("STFEM_FORCE_BIG") != nullptr;  // diagnostics: disable the small-front path
   // levels whose fronts have >= this many pivots fuse the extend-add of U into the Schur update
   // (syrk_gather_kernel).  Measured on C4 (per batch of 342 shifts): a net gain for K = p >= 127
   // (depths 1-4), break-even at p = 63, a loss at p <= 31 where the register-resident gather of a
   // short-K tile is latency bound.  STFEM_FUSED_MIN_P tunes it at plan creation (0: every level,
   // a huge value: none).
-  int fused_min_p = getenv("STFEM_FUSED_MIN_P") ? atoi(getenv("STFEM_FUSED_MIN_P")) : 64;
+  int fused_min_p = getenv("STFEM_FUSED_MIN_P") ? atoi(getenv("STFEM_FUSED_MIN_P")) : 100;
   // trailing pivot-column updates are delayed over groups of this many 32-wide panels
   // (K = 32 * panel_group for the wide updates; measured on C4: 2 -> 96 ms/step of panel updates,
   // 1 -> 111, 4 -> 108, 8 -> 121); STFEM_PANEL_GROUP tunes it at plan creation
   int panel_group = getenv("STFEM_PANEL_GROUP") ? std::max(1, atoi(getenv("STFEM_PANEL_GROUP"))) : 2;
   // asm_front_kernel assembles a whole front per CTA for levels of order <= this (STFEM_ASM_WHOLE_N)
-  int asm_whole_n = getenv("STFEM_ASM_WHOLE_N") ? atoi(getenv("STFEM_ASM_WHOLE_N")) : 160;
+  // (measured on C4: 160 -> 120 ms/step of assembly, 240 -> 118, every level -> 114)
+  int asm_whole_n = getenv("STFEM_ASM_WHOLE_N") ? atoi(getenv("STFEM_ASM_WHOLE_N")) : 1 << 30;
+  // Schur updates of levels with <= this many pivots (at most 32) on syrk_short_kernel
+  // (STFEM_SYRK_SHORT_P; 0 disables it)
+  int syrk_short_max_p = std::min(32, getenv("STFEM_SYRK_SHORT_P") ? atoi(getenv("STFEM_SYRK_SHORT_P")) : 16);
   int small_n_cap = getenv("STFEM_SMALL_N") ? atoi(getenv("STFEM_SMALL_N")) : 0;  // tuning: lower the threshold
   int32_t *d_child_ids = nullptr, *d_bidx = nullptr, *d_relpos = nullptr, *d_inv = nullptr;
   int32_t *d_ent_src = nullptr, *d_ent_dst = nullptr, *d_perm = nullptr, *d_ent_colptr = nullptr;

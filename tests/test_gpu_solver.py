@@ -68,24 +68,33 @@ def test_lifting_matches_oracle():
     assert rel(L, Lo) < 1e-13
 
 
-@pytest.mark.parametrize("mode", ["small", "big", "big_unfused", "big_pg1", "big_pg4", "spec24", "spec"])
+@pytest.mark.parametrize("mode", ["small", "big", "big_allfused", "big_legacy", "big_pg4", "spec24", "spec"])
 @pytest.mark.parametrize("kind,leaf", [("square9", 4), ("square16", 32), ("p2square6", 8),
                                         ("lshape5", 16), ("square40", 32), ("lshape12", 16)])
 def test_factor_solve_matches_splu(kind, leaf, mode, monkeypatch):
-    """mode: small/big = plain multifrontal (shared-memory small-front kernels on,
-    or every front on the global-memory kernels, with the extend-add of the
-    update blocks fused into the Schur update or, big_unfused, assembled by
-    asm_front_kernel); spec24 / spec = spectral subtrees of <= 24 / <= 256
-    interior DoFs (K6) under a multifrontal top."""
+    """mode: small = plain multifrontal with the shared-memory small-front kernels;
+    big* = every front on the global-memory (large-front) kernels: big with the
+    default tuning (extend-add fused into the Schur update for levels with >= 100
+    pivots, trailing updates delayed over panel pairs, short-K Schur kernel for
+    <= 16 pivots, whole-front assembly CTAs), big_allfused = fused on every level, big_legacy = none of
+    the three (asm_front_kernel assembles U, per-panel trailing updates,
+    gemm_update Schur kernel, 32-column assembly CTAs), big_pg4 = trailing
+    updates delayed over 4 panels and the short-K kernel up to 32 pivots;
+    spec24 / spec = spectral subtrees of <= 24 / <= 256 interior DoFs (K6)
+    under a multifrontal top."""
     if mode.startswith("big"):  # exercise the global-memory (large-front) kernels on small meshes too
         monkeypatch.setenv("STFEM_FORCE_BIG", "1")
-    if mode == "big":  # every level fused (the default fuses levels with >= 64 pivots only)
+    if mode == "big_allfused":
         monkeypatch.setenv("STFEM_FUSED_MIN_P", "0")
-    if mode == "big_unfused":
+    if mode == "big_legacy":
         monkeypatch.setenv("STFEM_FUSED_MIN_P", "1000000")
-    if mode in ("big_pg1", "big_pg4"):  # trailing updates delayed over 1 / 4 panels (default 2)
-        monkeypatch.setenv("STFEM_PANEL_GROUP", mode[-1])
-    spectral = {"small": 0, "big": 0, "big_unfused": 0, "big_pg1": 0, "big_pg4": 0, "spec24": 24, "spec": 256}[mode]
+        monkeypatch.setenv("STFEM_PANEL_GROUP", "1")
+        monkeypatch.setenv("STFEM_SYRK_SHORT_P", "0")
+        monkeypatch.setenv("STFEM_ASM_WHOLE_N", "0")
+    if mode == "big_pg4":  # + the short-K Schur kernel up to 32 pivots
+        monkeypatch.setenv("STFEM_PANEL_GROUP", "4")
+        monkeypatch.setenv("STFEM_SYRK_SHORT_P", "32")
+    spectral = {"spec24": 24, "spec": 256}.get(mode, 0)
     if kind.startswith("p2"):
         mesh, deg = sm.refine_uniform(sm.build_structured_square(int(kind[8:]))), 2
         Mo, Ao = O.assemble_spatial(omesh(mesh), 2, mesh.p2_elements)
