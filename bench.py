@@ -359,7 +359,8 @@ def run_ours(args):
              "diag": "diag_kernel (diagonal blocks, FP64)",
              "trsm": "trsm_kernel (panel TRSM, FP64)",
              "panel_update": "panel_update_kernel (trailing pivot columns, DMMA)",
-             "syrk": "syrk_level_kernel (Schur update U = F22 - L21 L21^T, DMMA)",
+             "syrk": "Schur-update kernels (syrk_gather_kernel p >= 100 / syrk_level_kernel / syrk_short_kernel "
+                     "p <= 16: U = F22 - L21 L21^T, DMMA)",
              "backward": "backward kernels (HBM)",
              "small_factor": "factor_small_kernel (shared-memory fronts)"}
     fam = {}

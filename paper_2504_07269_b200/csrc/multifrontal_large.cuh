@@ -213,8 +213,8 @@ __global__ void __launch_bounds__(256) diag_kernel(LevelArgs a, int kb) {
 // block first subtracts the finished blocks, re-read from global (L1-hot).
 // Register blocks of 16 keep the kernel near 100 registers (4+ CTAs per SM).
 template <int W>
-__global__ void __launch_bounds__(TR_ROWS, 4) trsm_kernel(LevelArgs a, int kb) {
-  constexpr int WB = 16;
+__global__ void __launch_bounds__(TR_ROWS, 8) trsm_kernel(LevelArgs a, int kb) {
+  constexpr int WB = 8;
   constexpr int LW = W + 1;           // padded pitch: the column-wise staging below is conflict-free
   __shared__ cplx Ls[W * LW];         // Ls[c * LW + c'] = C[kb+c][kb+c'] (c' < c); Ls[c*LW+c] = 1 / c_cc
   __shared__ cplx ys[W * MAXR];
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(TR_ROWS, 4) trsm_kernel(LevelArgs a, int kb) {
   const int i = r0 + tid;
   if (i >= n) return;
   cplx* prow = P + i + (int64_t)kb * n;
-#pragma unroll
+#pragma unroll 1
   for (int jb = 0; jb < W; jb += WB) {
     if (jb >= w) break;
     cplx x[WB];
