@@ -216,6 +216,59 @@ def hbm_peak():
         return 6650.0, "fallback: 6.65 TB/s from B200_PROFILING.md (MEASURED_PEAKS.json absent)"
 
 
+FAMILY_NAMES = {"spectral": "spectral_kernel (K6 spectral subtrees, DMMA)",
+                "assembly": "asm_front_kernel (front assembly, HBM)",
+                "diag": "diag_kernel (diagonal blocks, FP64)",
+                "trsm": "trsm_kernel (panel TRSM, FP64)",
+                "panel_update": "panel_update_kernel (trailing pivot columns, DMMA)",
+                "syrk": "Schur-update kernels (syrk_gather_kernel p >= 100 / syrk_level_kernel / syrk_short_kernel "
+                        "p <= 16: U = F22 - L21 L21^T, DMMA)",
+                "backward": "backward kernels (HBM)",
+                "small_factor": "factor_small_kernel (shared-memory fronts)"}
+
+
+def family_roofline(plan, nshift, nrhs, peak, workload, t_tr=None, flops_tr=None):
+    """(roofline of the dominant kernel family, per-family table) from the plan's last
+    recorded factor_solve (record_levels) over `nshift` shifts; the transforms join the
+    table when their time t_tr (s) and flops are given."""
+    rep = plan.kernel_report()
+    if plan.spectral is not None:
+        ss = plan.spectral_stats()
+        rep["spectral"] = (rep["spectral"][0], ss["flops_u"] + nrhs * ss["flops_rhs"], rep["spectral"][2])
+    fam = {}
+    for k, (ms, fl, nl) in rep.items():
+        if nl == 0:
+            continue
+        tf = fl * nshift / (ms / 1e3) / 1e12 if ms > 0 else 0.0
+        fam[k] = {"ms": ms, "launches": nl, "tflops": tf, "frac_dmma": tf / peak}
+    if t_tr:
+        fam["transform"] = {"ms": t_tr * 1e3, "launches": 2, "tflops": flops_tr / t_tr / 1e12,
+                            "frac_dmma": flops_tr / t_tr / 1e12 / peak}
+    top = max(fam, key=lambda k: fam[k]["ms"])
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            ent = json.load(f).get(f"{workload}:{top}")
+        if ent:
+            traffic = ent["dram_bytes_per_launch"]
+    if top == "transform":
+        roof = {"bound": "tensor", "kernel": "time_transform_kernel (K3, DMMA)", "achieved": fam[top]["tflops"],
+                "peak": peak, "unit": "TFLOP/s", "frac": fam[top]["tflops"] / peak, "traffic": traffic,
+                "avg_launch_ms": t_tr * 1e3 / 2}
+    else:
+        f = fam[top]
+        roof = {"bound": "tensor", "kernel": f"{FAMILY_NAMES[top]}; {f['launches']} launches/step",
+                "achieved": f["tflops"], "peak": peak, "unit": "TFLOP/s", "frac": f["tflops"] / peak,
+                "traffic": traffic, "avg_launch_ms": f["ms"] / max(1, f["launches"])}
+    roof.update({"peak_source": "FP64 DMMA peak measured live by a register-only DMMA probe (MEASURED_PEAKS.json "
+                                "has no FP64 entry)",
+                 "algorithmic": "flops per launch = the family's algorithmic real flops (complex MAC = 8) per shift "
+                                "x shifts, e.g. SYRK sum over fronts of 4 b^2 p; traffic = ncu dram bytes per launch "
+                                "(profiles/ncu_traffic.json)"})
+    return roof, fam
+
+
 def run_ours_bs(args):
     """Bartels-Stewart variant: one step = steps 2-4 of a
     BS solve (K3, the strictly sequential sweep of single-shift factor+solves with
@@ -350,50 +403,7 @@ def run_ours(args):
     peak = dmma_peak_live()
     t_fs = st["factor_solve_s"]
     t_tr = st["forward_transform_s"] + st["back_transform_s"]
-    rep = fdm.plan.kernel_report()
-    if fdm.plan.spectral is not None:
-        ss = fdm.plan.spectral_stats()
-        rep["spectral"] = (rep["spectral"][0], ss["flops_u"] + prob.n_rhs * ss["flops_rhs"], rep["spectral"][2])
-    names = {"spectral": "spectral_kernel (K6 spectral subtrees, DMMA)",
-             "assembly": "asm_front_kernel (front assembly, HBM)",
-             "diag": "diag_kernel (diagonal blocks, FP64)",
-             "trsm": "trsm_kernel (panel TRSM, FP64)",
-             "panel_update": "panel_update_kernel (trailing pivot columns, DMMA)",
-             "syrk": "Schur-update kernels (syrk_gather_kernel p >= 100 / syrk_level_kernel / syrk_short_kernel "
-                     "p <= 16: U = F22 - L21 L21^T, DMMA)",
-             "backward": "backward kernels (HBM)",
-             "small_factor": "factor_small_kernel (shared-memory fronts)"}
-    fam = {}
-    for k, (ms, fl, nl) in rep.items():
-        if nl == 0:
-            continue
-        tf = fl * prob.nt / (ms / 1e3) / 1e12 if ms > 0 else 0.0
-        fam[k] = {"ms": ms, "launches": nl, "tflops": tf, "frac_dmma": tf / peak}
-    fam["transform"] = {"ms": t_tr * 1e3, "launches": 2, "tflops": flops_tr / t_tr / 1e12,
-                        "frac_dmma": flops_tr / t_tr / 1e12 / peak}
-    top = max(fam, key=lambda k: fam[k]["ms"])
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            tr_all = json.load(f)
-        ent = tr_all.get(f"{args.workload}:{top}")
-        if ent:
-            traffic = ent["dram_bytes_per_launch"]
-    if top == "transform":
-        roof = {"bound": "tensor", "kernel": "time_transform_kernel (K3, DMMA)", "achieved": fam[top]["tflops"],
-                "peak": peak, "unit": "TFLOP/s", "frac": fam[top]["tflops"] / peak, "traffic": traffic,
-                "avg_launch_ms": t_tr * 1e3 / 2}
-    else:
-        f = fam[top]
-        roof = {"bound": "tensor", "kernel": f"{names[top]}; {f['launches']} launches/step",
-                "achieved": f["tflops"], "peak": peak, "unit": "TFLOP/s", "frac": f["tflops"] / peak,
-                "traffic": traffic, "avg_launch_ms": f["ms"] / max(1, f["launches"])}
-    roof.update({"peak_source": "FP64 DMMA peak measured live by a register-only DMMA probe (MEASURED_PEAKS.json "
-                                "has no FP64 entry)",
-                 "algorithmic": "flops per launch = the family's algorithmic real flops (complex MAC = 8) per shift "
-                                "x shifts, e.g. SYRK sum over fronts of 4 b^2 p; traffic = ncu dram bytes per launch "
-                                "(profiles/ncu_traffic.json)"})
+    roof, fam = family_roofline(fdm.plan, prob.nt, prob.n_rhs, peak, args.workload, t_tr, flops_tr)
     roof_phase = {"kernel": "whole multifrontal phase (K4+K5+K6), algorithmic LDL^T flops",
                   "achieved": flops_factor / t_fs / 1e12, "frac": flops_factor / t_fs / 1e12 / peak}
     roof_tr = {"bound": "tensor", "kernel": "time_transform_kernel (K3)", "achieved": flops_tr / t_tr / 1e12,

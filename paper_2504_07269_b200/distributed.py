@@ -167,9 +167,9 @@ def bench_main(args):
     dist.barrier()
     torch.cuda.synchronize()
     clk = None
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     if rank == 0:
-        import sys
-        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
         from bench import ClockSampler
         clk = ClockSampler(local)
         clk.start()
@@ -188,6 +188,18 @@ def bench_main(args):
     t_step = float(tt.item())
     dofs = prob.nx * nt * prob.n_rhs
     launches = 2 + plan.last_launches()
+    # roofline of the dominant kernel family: one extra step with per-launch events on every
+    # rank (the all-to-alls keep the ranks in step); rank 0 reports its own shifts
+    roof = None
+    if rank == 0:
+        plan.record_levels(True)
+    solver.solve(Fp, out)
+    torch.cuda.synchronize()
+    if rank == 0:
+        plan.record_levels(False)
+        from bench import dmma_peak_live, family_roofline
+        roof, fam = family_roofline(plan, nt // world, prob.n_rhs, dmma_peak_live(), args.workload)
+        roof["per_rank_families"] = fam
     # e2e: each rank's shard from pinned host memory, the solve, the shard back to the host
     e2e = None
     if not args.no_e2e:
@@ -223,7 +235,7 @@ def bench_main(args):
                            "parallelism": f"space-sharded transforms + time-sharded shifts, a2a x2 over {world} GPUs"},
                 "setup_s": t_setup, "asm_s": t_asm, "gpu_launches": launches * args.steps,
                 "clocks": clocks, "e2e": e2e, "cpu_baseline": None,
-                "roofline": None}
+                "roofline": roof}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
 
