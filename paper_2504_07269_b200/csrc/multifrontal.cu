@@ -300,6 +300,14 @@ __global__ void __launch_bounds__(128) syrk_short_kernel(LevelArgs a, const int4
           cre[mi][ni][2 * h + v] = o.re;
           cim[mi][ni][2 * h + v] = o.im;
         }
+  bool live[2][2];   // fragments outside the block or above the diagonal skip their DMMAs
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) {
+      const int r_lo = i0 + mi * 16, c_lo = c0 + wn * 16 + ni * 8;
+      live[mi][ni] = r_lo < b && c_lo < b && r_lo + 15 >= c_lo;
+    }
   const int kmax = min(p, KMAX);
   for (int kk = 0; kk < kmax; kk += 4) {
     cplx av[2][2], bv[2];
@@ -314,6 +322,7 @@ __global__ void __launch_bounds__(128) syrk_short_kernel(LevelArgs a, const int4
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
       for (int ni = 0; ni < 2; ++ni) {
+        if (!live[mi][ni]) continue;
         dmma_16x8x4(cre[mi][ni], -av[mi][0].re, -av[mi][1].re, bv[ni].re);
         dmma_16x8x4(cre[mi][ni], av[mi][0].im, av[mi][1].im, bv[ni].im);
         dmma_16x8x4(cim[mi][ni], -av[mi][0].re, -av[mi][1].re, bv[ni].im);
@@ -333,6 +342,106 @@ __global__ void __launch_bounds__(128) syrk_short_kernel(LevelArgs a, const int4
           if (row < b && col < b && row >= col)
             stc(U + row + (int64_t)col * b, cmk(cre[mi][ni][2 * h + v], cim[mi][ni][2 * h + v]));
         }
+}
+
+// Short-K Schur update at 16 x 16 granularity (levels with p <= 32 pivots and
+// b <= 208 boundary rows: C4 depths 7-9).  There the 64 x 64 tiles are mostly
+// waste -- b ~ 100 computes 2.4x the lower triangle, and the DMMA pipe is the
+// bottleneck (ncu: 65-72% active) -- so one CTA per (front, shift) instance
+// stages its L21 panel (b x p) in shared memory with cp.async and its 8 warps
+// walk the lower 16 x 16 blocks of U (1.2-1.4x the triangle): per block the
+// F22 entries are loaded into the accumulators (the next block's are
+// prefetched into registers while this one multiplies), K/4 DMMA steps on two
+// 16 x 8 fragments, lower entries stored.
+constexpr int B16_KMAX = 32, B16_BMAX = 208;
+__host__ __device__ inline int b16_ld(int b) { return b + ((10 - b % 8) % 8); }   // = 2 (mod 8)
+__host__ __device__ inline int b16_smem_bytes(int bmax) { return b16_ld(bmax) * B16_KMAX * 16; }
+
+__global__ void __launch_bounds__(NT, 2) syrk_block16_kernel(LevelArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* Ls = reinterpret_cast<cplx*>(smem_raw);   // Ls[k * ld + r] = L21[r][k]
+  const int inst = blockIdx.x;
+  const int k = inst % a.nbatch;
+  const FrontDev F = a.fronts[a.list[inst / a.nbatch]];
+  const int n = F.n, p = F.p, b = n - p;
+  if (b <= 0) return;
+  const int ld = b16_ld(b);
+  const cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
+  cplx* U = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
+  const int tid = threadIdx.x;
+  const int kpad = (p + 3) & ~3;
+  for (int idx = tid; idx < b * kpad; idx += NT) {
+    const int r = idx % b, kk = idx / b;
+    const bool ok = kk < p;
+    cp_async16(Ls + kk * ld + r, ok ? P + p + r + (int64_t)kk * n : P, ok);
+  }
+  cp_async_commit();
+  const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int nbk = (b + 15) >> 4, nblk = nbk * (nbk + 1) / 2;
+  // block q -> (bi, bj), bj <= bi, row-major over the lower triangle
+  auto coords = [](int q, int& bi, int& bj) {
+    bi = (int)((sqrtf(8.0f * q + 1.0f) - 1.0f) * 0.5f);
+    while ((bi + 1) * (bi + 2) / 2 <= q) ++bi;
+    while (bi * (bi + 1) / 2 > q) --bi;
+    bj = q - bi * (bi + 1) / 2;
+  };
+  auto load_c = [&](int bi, int bj, cplx (&c)[2][4]) {
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int row = bi * 16 + g + 8 * h, col = bj * 16 + ni * 8 + 2 * t + v;
+          c[ni][2 * h + v] = (row < b && col < b && row >= col) ? ldc(U + row + (int64_t)col * b) : cmk(0.0, 0.0);
+        }
+  };
+  int q = warp, bi = 0, bj = 0;
+  cplx cn[2][4];
+  if (q < nblk) {
+    coords(q, bi, bj);
+    load_c(bi, bj, cn);
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  for (; q < nblk; q += NT / 32) {
+    double cre[2][4], cim[2][4];
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        cre[ni][e] = cn[ni][e].re;
+        cim[ni][e] = cn[ni][e].im;
+      }
+    const int ci = bi, cj = bj;
+    if (q + NT / 32 < nblk) {   // prefetch the next block's F22 entries
+      coords(q + NT / 32, bi, bj);
+      load_c(bi, bj, cn);
+    }
+    const int ra = min(ci * 16 + g, b - 1), ra8 = min(ci * 16 + g + 8, b - 1);
+    const int rb0 = min(cj * 16 + g, b - 1), rb1 = min(cj * 16 + 8 + g, b - 1);
+    for (int kk = 0; kk < kpad; kk += 4) {
+      const cplx* col = Ls + (kk + t) * ld;
+      const cplx a0 = col[ra], a1 = col[ra8], b0 = col[rb0], b1 = col[rb1];
+      dmma_16x8x4(cre[0], -a0.re, -a1.re, b0.re);
+      dmma_16x8x4(cre[0], a0.im, a1.im, b0.im);
+      dmma_16x8x4(cim[0], -a0.re, -a1.re, b0.im);
+      dmma_16x8x4(cim[0], -a0.im, -a1.im, b0.re);
+      dmma_16x8x4(cre[1], -a0.re, -a1.re, b1.re);
+      dmma_16x8x4(cre[1], a0.im, a1.im, b1.im);
+      dmma_16x8x4(cim[1], -a0.re, -a1.re, b1.im);
+      dmma_16x8x4(cim[1], -a0.im, -a1.im, b1.re);
+    }
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int row = ci * 16 + g + 8 * h, col = cj * 16 + ni * 8 + 2 * t + v;
+          if (row < b && col < b && row >= col) stc(U + row + (int64_t)col * b, cmk(cre[ni][2 * h + v], cim[ni][2 * h + v]));
+        }
+  }
 }
 
 // Tile initialiser of the fused Schur update: the extend-add of the (at most
@@ -541,6 +650,13 @@ bool level_is_small(const Plan& P, int d) {
   return P.level_nmax[d] <= lim && !P.force_big;
 }
 
+// largest boundary block b = n - p among the fronts of depth d
+int level_bmax(const Plan& P, int d) {
+  int bm = 0;
+  for (int32_t f : P.levels[d]) bm = std::max(bm, P.fronts[f].n - P.fronts[f].p);
+  return bm;
+}
+
 // M_x / A_x values of every front entry, in entry order (shift-independent;
 // one coalesced stream per front instead of an indirect gather)
 __global__ void gather_entries_kernel(const int32_t* __restrict__ src, const double* __restrict__ Mv,
@@ -636,6 +752,8 @@ int upload(Plan& P) {
     STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SYRK_SMEM));
     STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         SYRK_SMEM + 1024));
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_block16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        b16_smem_bytes(B16_BMAX)));
     STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_short_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         SyrkShort<16>::SMEM));
     STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_short_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1009,6 +1127,11 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
         if (ntl > 0 && a.asm_pivots_only) {
           syrk_gather_kernel<<<(unsigned)(ntl * nb), NT, SYRK_SMEM + 1024, st>>>(a, P.d_syrk_tiles + P.syrk_off[d]);
           STFEM_LAUNCH_CHECK("syrk_gather_kernel");
+          ++nlaunch;
+          fam(FAM_SYRK, st);
+        } else if (ntl > 0 && pmax <= B16_KMAX && P.syrk_block16 && level_bmax(P, d) <= B16_BMAX) {
+          syrk_block16_kernel<<<ninst, NT, b16_smem_bytes(level_bmax(P, d)), st>>>(a);
+          STFEM_LAUNCH_CHECK("syrk_block16_kernel");
           ++nlaunch;
           fam(FAM_SYRK, st);
         } else if (ntl > 0 && pmax <= P.syrk_short_max_p) {

@@ -87,6 +87,8 @@ struct Plan {
   // asm_front_kernel assembles a whole front per CTA for levels of order <= this (STFEM_ASM_WHOLE_N)
   // (measured on C4: 160 -> 120 ms/step of assembly, 240 -> 118, every level -> 114)
   int asm_whole_n = getenv("STFEM_ASM_WHOLE_N") ? atoi(getenv("STFEM_ASM_WHOLE_N")) : 1 << 30;
+  // Schur updates of short-K levels (p <= 32, b <= 208) on 16 x 16 blocks (STFEM_SYRK_B16=0 disables)
+  bool syrk_block16 = !(getenv("STFEM_SYRK_B16") && atoi(getenv("STFEM_SYRK_B16")) == 0);
   // Schur updates of levels with <= this many pivots (at most 32) on syrk_short_kernel
   // (STFEM_SYRK_SHORT_P; 0 disables it)
   int syrk_short_max_p = std::min(32, getenv("STFEM_SYRK_SHORT_P") ? atoi(getenv("STFEM_SYRK_SHORT_P")) : 16);

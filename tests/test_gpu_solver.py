@@ -75,11 +75,11 @@ def test_factor_solve_matches_splu(kind, leaf, mode, monkeypatch):
     """mode: small = plain multifrontal with the shared-memory small-front kernels;
     big* = every front on the global-memory (large-front) kernels: big with the
     default tuning (extend-add fused into the Schur update for levels with >= 100
-    pivots, trailing updates delayed over panel pairs, short-K Schur kernel for
-    <= 16 pivots, whole-front assembly CTAs), big_allfused = fused on every level, big_legacy = none of
+    pivots, trailing updates delayed over panel pairs, 16 x 16-block Schur
+    kernel for <= 32 pivots, whole-front assembly CTAs), big_allfused = fused on every level, big_legacy = none of
     the three (asm_front_kernel assembles U, per-panel trailing updates,
     gemm_update Schur kernel, 32-column assembly CTAs), big_pg4 = trailing
-    updates delayed over 4 panels and the short-K kernel up to 32 pivots;
+    updates delayed over 4 panels and the 32 x 64 short-K kernel up to 32 pivots;
     spec24 / spec = spectral subtrees of <= 24 / <= 256 interior DoFs (K6)
     under a multifrontal top."""
     if mode.startswith("big"):  # exercise the global-memory (large-front) kernels on small meshes too
@@ -90,10 +90,12 @@ def test_factor_solve_matches_splu(kind, leaf, mode, monkeypatch):
         monkeypatch.setenv("STFEM_FUSED_MIN_P", "1000000")
         monkeypatch.setenv("STFEM_PANEL_GROUP", "1")
         monkeypatch.setenv("STFEM_SYRK_SHORT_P", "0")
+        monkeypatch.setenv("STFEM_SYRK_B16", "0")
         monkeypatch.setenv("STFEM_ASM_WHOLE_N", "0")
-    if mode == "big_pg4":  # + the short-K Schur kernel up to 32 pivots
+    if mode == "big_pg4":  # + the 32 x 64 short-K Schur kernel up to 32 pivots instead of 16 x 16 blocks
         monkeypatch.setenv("STFEM_PANEL_GROUP", "4")
         monkeypatch.setenv("STFEM_SYRK_SHORT_P", "32")
+        monkeypatch.setenv("STFEM_SYRK_B16", "0")
     spectral = {"spec24": 24, "spec": 256}.get(mode, 0)
     if kind.startswith("p2"):
         mesh, deg = sm.refine_uniform(sm.build_structured_square(int(kind[8:]))), 2
