@@ -444,6 +444,187 @@ __global__ void __launch_bounds__(NT, 2) syrk_block16_kernel(LevelArgs a) {
   }
 }
 
+// Schur update on 32 x 32 lower tiles (levels below the fused threshold that
+// the 16 x 16 kernel does not take: p > 32 or b > 208; C4 depths 5-6).  The
+// 64 x 64 tiles of gemm_update compute ~2x the lower triangle of b ~ 200-380
+// blocks with the DMMA pipe already the bottleneck; 32 x 32 tiles cut that
+// to ~1.3x.  128 threads = 2 x 2 warps of 16 x 16, 3-stage cp.async K pipeline
+// (52 KB), F22 into the accumulators, 4 CTAs per SM.
+constexpr int S32_LD = 32 + 2, S32_STAGE = 16 * S32_LD;   // [k][m] complex
+constexpr int S32_SMEM = 3 * 2 * S32_STAGE * 16 + 128 * 4;
+
+// GATHER: the tile starts from the children's extend-add (fused levels, U never
+// assembled; the tile's 32 row / 32 column inverse maps staged in shared memory)
+// instead of the assembled F22.
+// One 32 x 32 lower tile of C -= A A^T (C: M x N lower trapezoid, ld ldC; A: M
+// rows x K, ld lda; row c of A pairs with column c of C).  cinit(row, col) gives
+// the tile's starting values.  128 threads = 2 x 2 warps of 16 x 16, 3-stage
+// cp.async K pipeline.
+template <class CInit>
+__device__ __forceinline__ void sym_tile32(cplx* __restrict__ C, int ldC, int M, int N, const cplx* __restrict__ A,
+                                           int lda, int K, int i0, int c0, cplx* As, cplx* Bs, const CInit& cinit) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3, wm = warp & 1, wn = warp >> 1;
+  const int nk = (K + 15) / 16;
+  auto load = [&](int stage, int kc) {
+    cplx* as = As + stage * S32_STAGE;
+    cplx* bs = Bs + stage * S32_STAGE;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = tid + 128 * u, m = idx & 31, kk = kc * 16 + (idx >> 5);
+      const bool oka = kk < K && i0 + m < M, okb = kk < K && c0 + m < N;
+      cp_async16(as + (idx >> 5) * S32_LD + m, oka ? A + i0 + m + (int64_t)kk * lda : A, oka);
+      cp_async16(bs + (idx >> 5) * S32_LD + m, okb ? A + c0 + m + (int64_t)kk * lda : A, okb);
+    }
+  };
+#pragma unroll
+  for (int st = 0; st < 2; ++st) {
+    if (st < nk) load(st, st);
+    cp_async_commit();
+  }
+  double cre[2][4], cim[2][4];
+#pragma unroll
+  for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int row = i0 + wm * 16 + g + 8 * h, col = c0 + wn * 16 + ni * 8 + 2 * t + v;
+        const cplx o = (row < M && col < N && row >= col) ? cinit(row, col) : cmk(0.0, 0.0);
+        cre[ni][2 * h + v] = o.re;
+        cim[ni][2 * h + v] = o.im;
+      }
+  for (int kc = 0; kc < nk; ++kc) {
+    cp_async_wait<1>();
+    __syncthreads();
+    if (kc + 2 < nk) load((kc + 2) % 3, kc + 2);
+    cp_async_commit();
+    const cplx* as = As + (kc % 3) * S32_STAGE + t * S32_LD + wm * 16 + g;
+    const cplx* bs = Bs + (kc % 3) * S32_STAGE + t * S32_LD + wn * 16 + g;
+#pragma unroll
+    for (int kk = 0; kk < 16; kk += 4) {
+      const cplx a0 = as[kk * S32_LD], a1 = as[kk * S32_LD + 8];
+      const cplx b0 = bs[kk * S32_LD], b1 = bs[kk * S32_LD + 8];
+      dmma_16x8x4(cre[0], -a0.re, -a1.re, b0.re);
+      dmma_16x8x4(cre[0], a0.im, a1.im, b0.im);
+      dmma_16x8x4(cim[0], -a0.re, -a1.re, b0.im);
+      dmma_16x8x4(cim[0], -a0.im, -a1.im, b0.re);
+      dmma_16x8x4(cre[1], -a0.re, -a1.re, b1.re);
+      dmma_16x8x4(cre[1], a0.im, a1.im, b1.im);
+      dmma_16x8x4(cim[1], -a0.re, -a1.re, b1.im);
+      dmma_16x8x4(cim[1], -a0.im, -a1.im, b1.re);
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int row = i0 + wm * 16 + g + 8 * h, col = c0 + wn * 16 + ni * 8 + 2 * t + v;
+        if (row < M && col < N && row >= col)
+          stc(C + row + (int64_t)col * ldC, cmk(cre[ni][2 * h + v], cim[ni][2 * h + v]));
+      }
+}
+
+// extend-add of the (at most two) children's update blocks for one 32 x 32 tile
+struct Gather32 {
+  const int* inv_s;   // [2 children][rows 32 | cols 32]
+  const cplx* Uc[2];
+  int bc[2], nc, i0, c0;
+  __device__ __forceinline__ cplx operator()(int row, int col) const {
+    cplx o = cmk(0.0, 0.0);
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {   // same sum order as asm_front_kernel: 0 + c0 + c1
+      const int kr = s < nc ? inv_s[s * 64 + row - i0] : -1;
+      const int kc = s < nc ? inv_s[s * 64 + 32 + col - c0] : -1;
+      if (kr >= 0 && kc >= 0) o = cadd(o, ldc(Uc[s] + (int64_t)kc * bc[s] + kr));
+    }
+    return o;
+  }
+};
+
+// GATHER: the tile starts from the children's extend-add (fused levels, U never
+// assembled; the tile's 32 row / 32 column inverse maps staged in shared memory)
+// instead of the assembled F22.
+template <bool GATHER>
+__global__ void __launch_bounds__(128, 4) syrk32_kernel(LevelArgs a, const int4* __restrict__ tiles) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* As = reinterpret_cast<cplx*>(smem_raw);
+  cplx* Bs = As + 3 * S32_STAGE;
+  int* inv_s = reinterpret_cast<int*>(Bs + 3 * S32_STAGE);
+  const int k = blockIdx.x % a.nbatch;
+  const int4 tl = tiles[blockIdx.x / a.nbatch];
+  const FrontDev F = a.fronts[tl.x];
+  const int n = F.n, p = F.p, b = n - p;
+  const int i0 = tl.y * 32, c0 = tl.z * 32;
+  const cplx* L = a.factor + (int64_t)k * a.fstride + F.fofs + p;   // L21: row r, column kk at L[r + kk n]
+  cplx* U = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
+  if constexpr (GATHER) {
+    Gather32 gi;
+    gi.inv_s = inv_s;
+    gi.nc = min(F.nchild, 2);
+    gi.i0 = i0;
+    gi.c0 = c0;
+    for (int q = threadIdx.x; q < 128; q += 128) {
+      const int s = q >> 6, r = q & 31, isc = (q >> 5) & 1;
+      const int fr = (isc ? c0 : i0) + r;
+      inv_s[q] = (s < gi.nc && fr < b) ? a.inv[F.inv_beg + s * n + p + fr] : -1;
+    }
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      gi.Uc[s] = nullptr;
+      gi.bc[s] = 0;
+      if (s < gi.nc) {
+        const FrontDev Cf = a.fronts[a.child_ids[F.child_beg + s]];
+        gi.bc[s] = Cf.n - Cf.p;
+        gi.Uc[s] = a.uchild + (int64_t)k * a.uchild_stride + Cf.uofs;
+      }
+    }
+    __syncthreads();
+    sym_tile32(U, b, b, b, L, n, p, i0, c0, As, Bs, gi);
+  } else {
+    sym_tile32(U, b, b, b, L, n, p, i0, c0, As, Bs, CLoad{U, b});
+  }
+}
+
+// 32 x 32-tile trailing pivot-column update (see panel_update_kernel for the
+// delayed-update regions): the narrow (32-column) updates no longer fill half
+// of a 64-wide tile with waste.
+__host__ __device__ inline int panel_update_tiles32(int n, int p, int cb, int narrow) {
+  const int cols = cb >= p ? 0 : (narrow ? min(NB, p - cb) : p - cb);
+  if (cols <= 0) return 0;
+  const int tm = (n - cb + 31) / 32, tn = (cols + 31) / 32;
+  return tn * tm - tn * (tn - 1) / 2;
+}
+
+__global__ void __launch_bounds__(128, 4) panel_update32_kernel(LevelArgs a, int cb, int k0, int K, int narrow) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* As = reinterpret_cast<cplx*>(smem_raw);
+  cplx* Bs = As + 3 * S32_STAGE;
+  const int inst = blockIdx.x;
+  const int k = inst % a.nbatch;
+  const FrontDev F = a.fronts[a.list[inst / a.nbatch]];
+  const int n = F.n, p = F.p;
+  const int cols = cb >= p ? 0 : (narrow ? min(NB, p - cb) : p - cb);
+  if (cols <= 0) return;
+  const int kk = min(K, p - k0);
+  const int tm = (n - cb + 31) / 32, tn = (cols + 31) / 32;
+  int t = blockIdx.y, ti = -1, tj = 0;
+  for (; tj < tn; ++tj) {
+    if (t < tm - tj) {
+      ti = tj + t;
+      break;
+    }
+    t -= tm - tj;
+  }
+  if (ti < 0) return;
+  cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
+  cplx* C = P + cb + (int64_t)cb * n;
+  sym_tile32(C, n, n - cb, cols, P + cb + (int64_t)k0 * n, n, kk, ti * 32, tj * 32, As, Bs, CLoad{C, n});
+}
+
 // Tile initialiser of the fused Schur update: the extend-add of the (at most
 // two) children's update blocks, gathered straight into the accumulators
 // through the inverse relpos maps of the tile's 64 rows and 64 columns
@@ -749,6 +930,26 @@ int upload(Plan& P) {
     STFEM_CUDA_TRY(cudaMalloc(&P.d_syrk_tiles, std::max<size_t>(1, tl.size()) * sizeof(int4)));
     if (!tl.empty())
       STFEM_CUDA_TRY(cudaMemcpy(P.d_syrk_tiles, tl.data(), tl.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    // the same at 32 x 32 granularity (syrk32_kernel)
+    std::vector<int4> t32;
+    P.syrk32_off.assign(P.levels.size() + 1, 0);
+    for (size_t d = 0; d < P.levels.size(); ++d) {
+      P.syrk32_off[d] = (int64_t)t32.size();
+      if (level_is_small(P, (int)d)) continue;
+      for (int32_t f : P.levels[d]) {
+        const int b = P.fronts[f].n - P.fronts[f].p;
+        const int nt = (b + 31) / 32;
+        for (int tj = 0; tj < nt; ++tj)
+          for (int ti = tj; ti < nt; ++ti) t32.push_back(make_int4(f, ti, tj, 0));
+      }
+    }
+    P.syrk32_off[P.levels.size()] = (int64_t)t32.size();
+    STFEM_CUDA_TRY(cudaMalloc(&P.d_syrk32_tiles, std::max<size_t>(1, t32.size()) * sizeof(int4)));
+    if (!t32.empty())
+      STFEM_CUDA_TRY(cudaMemcpy(P.d_syrk32_tiles, t32.data(), t32.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk32_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, S32_SMEM));
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk32_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, S32_SMEM));
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(panel_update32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, S32_SMEM));
     STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SYRK_SMEM));
     STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         SYRK_SMEM + 1024));
@@ -868,6 +1069,8 @@ void Plan::free_device() {
   cudaFree(d_inv);
   cudaFree(d_syrk_tiles);
   d_syrk_tiles = nullptr;
+  cudaFree(d_syrk32_tiles);
+  d_syrk32_tiles = nullptr;
   cudaFree(d_ent_src);
   cudaFree(d_ent_mv);
   cudaFree(d_ent_av);
@@ -1116,15 +1319,27 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
           const int cb = kb + NB, k0 = g0, K = kb + NB - g0;
           int tiles = 0;
           for (int32_t f : P.levels[d])
-            tiles = std::max(tiles, panel_update_tiles(P.fronts[f].n, P.fronts[f].p, cb, narrow));
-          if (tiles > 0) {
+            tiles = std::max(tiles, P.syrk32 ? panel_update_tiles32(P.fronts[f].n, P.fronts[f].p, cb, narrow)
+                                             : panel_update_tiles(P.fronts[f].n, P.fronts[f].p, cb, narrow));
+          if (tiles > 0 && P.syrk32) {
+            panel_update32_kernel<<<dim3(ninst, tiles), 128, S32_SMEM, st>>>(a, cb, k0, K, narrow);
+            STFEM_LAUNCH_CHECK("panel_update32_kernel");
+            ++nlaunch;
+            fam(FAM_PANEL, st);
+          } else if (tiles > 0) {
             panel_update_kernel<<<dim3(ninst, tiles), NT, GEMM_SMEM, st>>>(a, cb, k0, K, narrow);
             STFEM_LAUNCH_CHECK("panel_update_kernel");
             ++nlaunch;
             fam(FAM_PANEL, st);
           }
         }
-        if (ntl > 0 && a.asm_pivots_only) {
+        if (ntl > 0 && a.asm_pivots_only && P.syrk32) {
+          const int64_t n32 = P.syrk32_off[d + 1] - P.syrk32_off[d];
+          syrk32_kernel<true><<<(unsigned)(n32 * nb), 128, S32_SMEM, st>>>(a, P.d_syrk32_tiles + P.syrk32_off[d]);
+          STFEM_LAUNCH_CHECK("syrk32_kernel<gather>");
+          ++nlaunch;
+          fam(FAM_SYRK, st);
+        } else if (ntl > 0 && a.asm_pivots_only) {
           syrk_gather_kernel<<<(unsigned)(ntl * nb), NT, SYRK_SMEM + 1024, st>>>(a, P.d_syrk_tiles + P.syrk_off[d]);
           STFEM_LAUNCH_CHECK("syrk_gather_kernel");
           ++nlaunch;
@@ -1142,6 +1357,12 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
             syrk_short_kernel<32><<<(unsigned)(2 * ntl * nb), 128, SyrkShort<32>::SMEM, st>>>(
                 a, P.d_syrk_tiles + P.syrk_off[d]);
           STFEM_LAUNCH_CHECK("syrk_short_kernel");
+          ++nlaunch;
+          fam(FAM_SYRK, st);
+        } else if (ntl > 0 && P.syrk32) {
+          const int64_t n32 = P.syrk32_off[d + 1] - P.syrk32_off[d];
+          syrk32_kernel<false><<<(unsigned)(n32 * nb), 128, S32_SMEM, st>>>(a, P.d_syrk32_tiles + P.syrk32_off[d]);
+          STFEM_LAUNCH_CHECK("syrk32_kernel");
           ++nlaunch;
           fam(FAM_SYRK, st);
         } else if (a.split_syrk && ntl > 0) {

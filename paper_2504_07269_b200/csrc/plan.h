@@ -75,11 +75,11 @@ struct Plan {
   std::vector<int32_t> level_tail_nmax, level_tail_pmax;   // per depth: max order / pivots of the rest
   bool force_big = getenv("STFEM_FORCE_BIG") != nullptr;  // diagnostics: disable the small-front path
   // levels whose fronts have >= this many pivots fuse the extend-add of U into the Schur update
-  // (syrk_gather_kernel).  Measured on C4 (per batch of 342 shifts): a net gain for K = p >= 127
-  // (depths 1-4), break-even at p = 63, a loss at p <= 31 where the register-resident gather of a
-  // short-K tile is latency bound.  STFEM_FUSED_MIN_P tunes it at plan creation (0: every level,
-  // a huge value: none).
-  int fused_min_p = getenv("STFEM_FUSED_MIN_P") ? atoi(getenv("STFEM_FUSED_MIN_P")) : 100;
+  // (syrk32_kernel<true>, or syrk_gather_kernel with STFEM_SYRK32=0).  Measured with the 32 x 32
+  // tiles (C4, ms/step): threshold 50 -> 899, 100 -> 902, no fusion -> 907; C5 neutral.  With the
+  // 64 x 64 tiles the short-K gather was latency bound (p <= 31 lost up to 14 ms per batch per
+  // level).  STFEM_FUSED_MIN_P tunes it at plan creation (0: every level, a huge value: none).
+  int fused_min_p = getenv("STFEM_FUSED_MIN_P") ? atoi(getenv("STFEM_FUSED_MIN_P")) : 50;
   // trailing pivot-column updates are delayed over groups of this many 32-wide panels
   // (K = 32 * panel_group for the wide updates; measured on C4: 2 -> 96 ms/step of panel updates,
   // 1 -> 111, 4 -> 108, 8 -> 121); STFEM_PANEL_GROUP tunes it at plan creation
@@ -89,6 +89,8 @@ struct Plan {
   int asm_whole_n = getenv("STFEM_ASM_WHOLE_N") ? atoi(getenv("STFEM_ASM_WHOLE_N")) : 1 << 30;
   // Schur updates of short-K levels (p <= 32, b <= 208) on 16 x 16 blocks (STFEM_SYRK_B16=0 disables)
   bool syrk_block16 = !(getenv("STFEM_SYRK_B16") && atoi(getenv("STFEM_SYRK_B16")) == 0);
+  // Schur updates of the remaining unfused levels on 32 x 32 tiles (STFEM_SYRK32=0: 64 x 64 gemm_update)
+  bool syrk32 = !(getenv("STFEM_SYRK32") && atoi(getenv("STFEM_SYRK32")) == 0);
   // Schur updates of levels with <= this many pivots (at most 32) on syrk_short_kernel
   // (STFEM_SYRK_SHORT_P; 0 disables it)
   int syrk_short_max_p = std::min(32, getenv("STFEM_SYRK_SHORT_P") ? atoi(getenv("STFEM_SYRK_SHORT_P")) : 16);
@@ -98,6 +100,8 @@ struct Plan {
   double *d_ent_mv = nullptr, *d_ent_av = nullptr;   // M_x / A_x values gathered into entry order
   std::vector<int64_t> syrk_off;           // per depth: offsets into d_syrk_tiles
   int4* d_syrk_tiles = nullptr;            // (front, ti, tj, 0) Schur-update tiles of the large fronts
+  std::vector<int64_t> syrk32_off;         // per depth: offsets into d_syrk32_tiles
+  int4* d_syrk32_tiles = nullptr;          // the same at 32 x 32 granularity (syrk32_kernel)
   int* d_err = nullptr;
   SubDev* d_subs = nullptr;
   double *d_V = nullptr, *d_th = nullptr, *d_RQ = nullptr, *d_C01 = nullptr;

@@ -68,34 +68,46 @@ def test_lifting_matches_oracle():
     assert rel(L, Lo) < 1e-13
 
 
-@pytest.mark.parametrize("mode", ["small", "big", "big_allfused", "big_legacy", "big_pg4", "spec24", "spec"])
+@pytest.mark.parametrize("mode", ["small", "big", "big_allfused", "big_gather64", "big_legacy", "big_pg4", "big_s32",
+                                  "spec24", "spec"])
 @pytest.mark.parametrize("kind,leaf", [("square9", 4), ("square16", 32), ("p2square6", 8),
                                         ("lshape5", 16), ("square40", 32), ("lshape12", 16)])
 def test_factor_solve_matches_splu(kind, leaf, mode, monkeypatch):
     """mode: small = plain multifrontal with the shared-memory small-front kernels;
-    big* = every front on the global-memory (large-front) kernels: big with the
-    default tuning (extend-add fused into the Schur update for levels with >= 100
-    pivots, trailing updates delayed over panel pairs, 16 x 16-block Schur
-    kernel for <= 32 pivots, whole-front assembly CTAs), big_allfused = fused on every level, big_legacy = none of
-    the three (asm_front_kernel assembles U, per-panel trailing updates,
-    gemm_update Schur kernel, 32-column assembly CTAs), big_pg4 = trailing
-    updates delayed over 4 panels and the 32 x 64 short-K kernel up to 32 pivots;
+    big* = every front on the global-memory (large-front) kernels:
+      big          the default tuning: extend-add fused into the 32 x 32-tile Schur
+                   update for levels with >= 50 pivots, 16 x 16-block Schur kernel
+                   for <= 32 pivots, 32 x 32 tiles elsewhere and for the trailing
+                   updates (delayed over panel pairs), whole-front assembly CTAs;
+      big_allfused fused on every level (32 x 32 tiles);
+      big_gather64 fused on every level on the 64 x 64 gather kernel;
+      big_legacy   none of it: asm_front_kernel assembles U, per-panel 64 x 64
+                   trailing updates, 64 x 64 gemm_update Schur kernel, 32-column
+                   assembly CTAs;
+      big_pg4      trailing updates delayed over 4 panels, 32 x 64 short-K kernel;
+      big_s32      the 32 x 32-tile Schur kernel on every unfused level;
     spec24 / spec = spectral subtrees of <= 24 / <= 256 interior DoFs (K6)
     under a multifrontal top."""
     if mode.startswith("big"):  # exercise the global-memory (large-front) kernels on small meshes too
         monkeypatch.setenv("STFEM_FORCE_BIG", "1")
-    if mode == "big_allfused":
+    if mode in ("big_allfused", "big_gather64"):
         monkeypatch.setenv("STFEM_FUSED_MIN_P", "0")
+    if mode == "big_gather64":  # fused levels on the 64 x 64 gather kernel
+        monkeypatch.setenv("STFEM_SYRK32", "0")
     if mode == "big_legacy":
         monkeypatch.setenv("STFEM_FUSED_MIN_P", "1000000")
         monkeypatch.setenv("STFEM_PANEL_GROUP", "1")
         monkeypatch.setenv("STFEM_SYRK_SHORT_P", "0")
         monkeypatch.setenv("STFEM_SYRK_B16", "0")
+        monkeypatch.setenv("STFEM_SYRK32", "0")
         monkeypatch.setenv("STFEM_ASM_WHOLE_N", "0")
     if mode == "big_pg4":  # + the 32 x 64 short-K Schur kernel up to 32 pivots instead of 16 x 16 blocks
         monkeypatch.setenv("STFEM_PANEL_GROUP", "4")
         monkeypatch.setenv("STFEM_SYRK_SHORT_P", "32")
         monkeypatch.setenv("STFEM_SYRK_B16", "0")
+    if mode == "big_s32":  # every unfused level on the 32 x 32-tile Schur kernel
+        monkeypatch.setenv("STFEM_SYRK_B16", "0")
+        monkeypatch.setenv("STFEM_SYRK_SHORT_P", "0")
     spectral = {"spec24": 24, "spec": 256}.get(mode, 0)
     if kind.startswith("p2"):
         mesh, deg = sm.refine_uniform(sm.build_structured_square(int(kind[8:]))), 2
