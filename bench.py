@@ -220,9 +220,9 @@ FAMILY_NAMES = {"spectral": "spectral_kernel (K6 spectral subtrees, DMMA)",
                 "assembly": "asm_front_kernel (front assembly, HBM)",
                 "diag": "diag_kernel (diagonal blocks, FP64)",
                 "trsm": "trsm_kernel (panel TRSM, FP64)",
-                "panel_update": "panel_update_kernel (trailing pivot columns, DMMA)",
-                "syrk": "Schur-update kernels (syrk_gather_kernel p >= 100 / syrk_level_kernel / syrk_short_kernel "
-                        "p <= 16: U = F22 - L21 L21^T, DMMA)",
+                "panel_update": "panel_update32_kernel (trailing pivot columns, DMMA)",
+                "syrk": "Schur-update kernels (syrk32_kernel<gather> p >= 50 / syrk32_kernel / syrk_block16_kernel "
+                        "p <= 32: U = F22 - L21 L21^T, DMMA)",
                 "backward": "backward kernels (HBM)",
                 "small_factor": "factor_small_kernel (shared-memory fronts)"}
 
