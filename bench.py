@@ -4,7 +4,7 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C4] [--impl ours|reference]
 
 One step = one FD solve of the workload's RHS stack: forward time transform
-(K3, DMMA), n_t batched multifrontal factor+solve (K4/K5), back transform (K3)
+(K3p, DMMA), n_t batched multifrontal factor+solve (K4/K5), back transform (K3p)
 (+ the two all-to-alls when N > 1).  `value` = n_x * n_t * n_rhs / t_step
 (whole job), inputs resident in HBM (each input array is larger than L2, so no
 flush is needed).  `e2e` = the same metric through the public API with the
@@ -253,7 +253,7 @@ def family_roofline(plan, nshift, nrhs, peak, workload, t_tr=None, flops_tr=None
         if ent:
             traffic = ent["dram_bytes_per_launch"]
     if top == "transform":
-        roof = {"bound": "tensor", "kernel": "time_transform_kernel (K3, DMMA)", "achieved": fam[top]["tflops"],
+        roof = {"bound": "tensor", "kernel": "time transforms (K3/K3p, DMMA)", "achieved": fam[top]["tflops"],
                 "peak": peak, "unit": "TFLOP/s", "frac": fam[top]["tflops"] / peak, "traffic": traffic,
                 "avg_launch_ms": t_tr * 1e3 / 2}
     else:
@@ -399,15 +399,23 @@ def run_ours(args):
 
     # roofline of the dominant kernel family (by CUDA-event time in the recorded step)
     flops_factor = fdm.plan.stats["flops_factor"] * prob.nt
-    flops_tr = 2 * 8.0 * prob.nt * prob.nt * prob.nx * prob.n_rhs
+    flops_tr_alg = 2 * 8.0 * prob.nt * prob.nt * prob.nx * prob.n_rhs   # 16 n_t^2 n_x n_rhs
+    # K3p (eigenpair-paired transforms) executes half of them: real x complex products
+    flops_tr = flops_tr_alg / 2 if fdm.pairs is not None else flops_tr_alg
     peak = dmma_peak_live()
     t_fs = st["factor_solve_s"]
     t_tr = st["forward_transform_s"] + st["back_transform_s"]
     roof, fam = family_roofline(fdm.plan, prob.nt, prob.n_rhs, peak, args.workload, t_tr, flops_tr)
     roof_phase = {"kernel": "whole multifrontal phase (K4+K5+K6), algorithmic LDL^T flops",
                   "achieved": flops_factor / t_fs / 1e12, "frac": flops_factor / t_fs / 1e12 / peak}
-    roof_tr = {"bound": "tensor", "kernel": "time_transform_kernel (K3)", "achieved": flops_tr / t_tr / 1e12,
-               "peak": peak, "unit": "TFLOP/s", "frac": flops_tr / t_tr / 1e12 / peak}
+    roof_tr = {"bound": "tensor",
+               "kernel": ("transform_rc_kernel (K3p, eigenpair-paired: real x complex DMMA) + pair_mix_kernel"
+                          if fdm.pairs is not None else "time_transform_kernel (K3)"),
+               "achieved": flops_tr / t_tr / 1e12, "peak": peak, "unit": "TFLOP/s",
+               "frac": flops_tr / t_tr / 1e12 / peak,
+               "algorithmic_tflops": flops_tr_alg / t_tr / 1e12,
+               "flops": "achieved/frac count the executed real flops (K3p: 8 n_t^2 n_x n_rhs); algorithmic_tflops "
+                        "counts SURVEY's 16 n_t^2 n_x n_rhs of the complex transform it replaces"}
     # batched triangular solves (backward family) against the HBM roofline: the backward sweep
     # reads every stored factor entry once per shift and reads + writes the solution vectors
     hbm = hbm_peak()
@@ -420,7 +428,8 @@ def run_ours(args):
                       "bytes_per_step": sb, "peak_source": hbm[1],
                       "algorithmic": "16 B x stored factor entries (multifrontal fronts) x n_t + 32 B x n_x x n_t "
                                      "x n_rhs (solution read + write)"}
-    launches = 2 + fdm.plan.last_launches()   # two K3 transforms + the multifrontal level launches
+    # two transforms (+ the K3p pair pre-pass) + the multifrontal level launches
+    launches = (3 if fdm.pairs is not None else 2) + fdm.plan.last_launches()
 
     cpu = None
     if not args.no_cpu_baseline:

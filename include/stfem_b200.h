@@ -69,6 +69,32 @@ int stfem_time_transform(const void* T, int nt, const void* in, int64_t ld_in,
                          void* out, int64_t ld_out, int64_t ncols, int batch,
                          int64_t bstride_in, int64_t bstride_out, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * K3p  eigenpair-paired transforms (same contract as K3 for FD factors whose
+ * eigenvalues pair as (lam, -conj(lam)) -- always the case for the real
+ * temporal pencil of SPEC.md:181-189; host pairing and derivation in
+ * paper_2504_07269_b200/paired_transform.py).  Half the flops of K3: a real
+ * (M x n_t) x complex (n_t x ncols) product on DMMA.
+ *   fwd:  G = Y F.  A: device float64 (mrows x nt), mrows a multiple of 16,
+ *         rows in blocks of 16 = [Re y_l of 8 sources; Im y_l of the same 8];
+ *         rows: int32 (nsrc, 2) = (l, p or -1); scale: c128 (nsrc,) with
+ *         y_p = scale * conj(y_l).  Writes out rows l and p.
+ *   back: Psi = X W.  A: device float64 (nt x nt), column l = Re x_l, column
+ *         p = Im x_l (self-paired: the real part r of x_l = e^{i phi} r).
+ *         `in` is CLOBBERED: an in-place pre-pass mixes each pair of rows
+ *         [W_l; W_p] <- [[m00, m01], [m10, m11]] [W_l; W_p] (mix_coef c128
+ *         (nmix, 4); p = -1: W_l <- m00 W_l).  in and out must not alias.
+ * Replaces the two transform_blocks calls of solve on the FD path.
+ * ------------------------------------------------------------------------- */
+int stfem_transform_pair_fwd(const double* A, int mrows, int nt, const int32_t* rows,
+                             const void* scale, int nsrc, const void* in, int64_t ld_in, void* out,
+                             int64_t ld_out, int64_t ncols, int batch, int64_t bstride_in,
+                             int64_t bstride_out, void* stream);
+int stfem_transform_pair_back(const double* A, int nt, const int32_t* mix_rows, const void* mix_coef,
+                              int nmix, void* in, int64_t ld_in, void* out, int64_t ld_out,
+                              int64_t ncols, int batch, int64_t bstride_in, int64_t bstride_out,
+                              void* stream);
+
 /* Column block [0, ncols) of `rows` rows between host and device
  * (cudaMemcpy2DAsync; leading dimensions in complex128 elements; kind 0 =
  * host->device, 1 = device->host).  The pipelined host-buffer solve overlaps

@@ -41,3 +41,49 @@ def time_transform(T: torch.Tensor, v: torch.Tensor, out: torch.Tensor | None = 
         N.ptr(T), nt, N.ptr(vb), vb.stride(-2), N.ptr(ob), ob.stride(-2), ncols, B,
         vb.stride(0) if B > 1 else 0, ob.stride(0) if B > 1 else 0, N.stream_ptr(stream)))
     return out
+
+
+def transform_pair_fwd(pairs, v: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """G = Y v through the eigenpair-paired kernel (K3p forward); `pairs` is a
+    paired_transform.DevicePairs.  Same shapes/strides contract as time_transform."""
+    _c128(v, "v")
+    nt = pairs.nt
+    if v.shape[-2] != nt:
+        raise N.DimensionMismatch(N.ERR_DIM, f"transform: n_t {nt} vs v {tuple(v.shape)}")
+    vb = v.unsqueeze(0) if v.dim() == 2 else v
+    if vb.stride(-1) != 1:
+        vb = vb.contiguous()
+    if out is None:
+        out = torch.empty(v.shape, dtype=C128, device=v.device)
+    ob = out.unsqueeze(0) if out.dim() == 2 else out
+    if ob.stride(-1) != 1 or ob.shape != vb.shape:
+        raise N.DimensionMismatch(N.ERR_DIM, "transform: bad output tensor")
+    B, _, ncols = vb.shape
+    N.check(N.lib().stfem_transform_pair_fwd(
+        N.ptr(pairs.A_fwd), pairs.A_fwd.shape[0], nt, N.ptr(pairs.rows_fwd), N.ptr(pairs.scale_fwd),
+        pairs.rows_fwd.shape[0], N.ptr(vb), vb.stride(-2), N.ptr(ob), ob.stride(-2), ncols, B,
+        vb.stride(0) if B > 1 else 0, ob.stride(0) if B > 1 else 0, N.stream_ptr(stream)))
+    return out
+
+
+def transform_pair_back(pairs, w: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Psi = X w through the paired kernel (K3p back).  `w` is CLOBBERED (the
+    in-place pair pre-pass); it must have unit column stride."""
+    _c128(w, "w")
+    nt = pairs.nt
+    if w.shape[-2] != nt:
+        raise N.DimensionMismatch(N.ERR_DIM, f"transform: n_t {nt} vs w {tuple(w.shape)}")
+    wb = w.unsqueeze(0) if w.dim() == 2 else w
+    if wb.stride(-1) != 1:
+        raise N.DimensionMismatch(N.ERR_DIM, "transform_pair_back: w needs unit column stride (updated in place)")
+    if out is None:
+        out = torch.empty(w.shape, dtype=C128, device=w.device)
+    ob = out.unsqueeze(0) if out.dim() == 2 else out
+    if ob.stride(-1) != 1 or ob.shape != wb.shape:
+        raise N.DimensionMismatch(N.ERR_DIM, "transform: bad output tensor")
+    B, _, ncols = wb.shape
+    N.check(N.lib().stfem_transform_pair_back(
+        N.ptr(pairs.A_back), nt, N.ptr(pairs.mix_rows), N.ptr(pairs.mix_coef), pairs.mix_rows.shape[0],
+        N.ptr(wb), wb.stride(-2), N.ptr(ob), ob.stride(-2), ncols, B,
+        wb.stride(0) if B > 1 else 0, ob.stride(0) if B > 1 else 0, N.stream_ptr(stream)))
+    return out

@@ -58,6 +58,10 @@ def _declare(lib):
         "stfem_version": (C.c_int, []),
         "stfem_cuda_device_count": (C.c_int, []),
         "stfem_time_transform": (C.c_int, [P, C.c_int, P, I64, P, I64, I64, C.c_int, I64, I64, P]),
+        "stfem_transform_pair_fwd": (C.c_int, [P, C.c_int, C.c_int, P, P, C.c_int, P, I64, P, I64, I64, C.c_int,
+                                               I64, I64, P]),
+        "stfem_transform_pair_back": (C.c_int, [P, C.c_int, P, P, C.c_int, P, I64, P, I64, I64, C.c_int, I64, I64,
+                                                P]),
         "stfem_copy_cols": (C.c_int, [P, I64, P, I64, I64, I64, I32, P]),
         "stfem_plan_create": (C.c_int, [I32, P, P, P, I32, I32, C.POINTER(P)]),
         "stfem_plan_destroy": (C.c_int, [P]),

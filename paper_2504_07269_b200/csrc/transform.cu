@@ -14,6 +14,8 @@
 // once; T (<= 16 MB) stays L2-resident).
 #include "common.cuh"
 
+#include <algorithm>
+
 namespace stfem {
 namespace {
 
@@ -128,6 +130,179 @@ time_transform_kernel(const cplx* __restrict__ T, int nt, const cplx* __restrict
       }
 }
 
+// ---------------------------------------------------------------------------
+// K3p — eigenpair-paired transforms (host side and derivation:
+// paper_2504_07269_b200/paired_transform.py).  Both FD transforms become a
+// REAL (M x K) x COMPLEX (K x N) product on DMMA: 2 real DMMAs (re, im) per
+// real A fragment, half the work of the 4-product complex GEMM above.
+//   EPI_PAIR  (forward G = Y F): A rows in blocks of 16 = [Re y of 8 sources;
+//             Im y of the same 8], so one accumulator fragment holds u = c F
+//             (row g) and v = d F (row g + 8) of source s; the epilogue writes
+//             G_l = u + i v and G_p = s_p (u - i v).
+//   EPI_PLAIN (back Psi = A W' after pair_mix_kernel): plain store.
+// CTA tile 64 rows x 64 complex columns, k-tile 16, 3-stage cp.async, 8 warps
+// as 2 x 4, warp tile 32 rows x 16 complex (2 x 2 fragments x re/im).
+constexpr int RC_LDA = BK + 4;   // As[m][k] doubles: (g*20 + t) mod 16 -> 2 wavefronts per LDS.64
+constexpr int RC_A_STAGE = BM * RC_LDA;
+constexpr int RC_SMEM = STAGES * (RC_A_STAGE * 8 + B_STAGE * 16);
+enum { EPI_PLAIN = 0, EPI_PAIR = 1 };
+
+template <int EPI>
+__global__ void __launch_bounds__(256, 2)
+transform_rc_kernel(const double* __restrict__ A, int M, int K, const cplx* __restrict__ in, int64_t ld_in,
+                    cplx* __restrict__ out, int64_t ld_out, int64_t ncols, int64_t bs_in, int64_t bs_out,
+                    const int2* __restrict__ rows, const cplx* __restrict__ scale, int nsrc) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* As = reinterpret_cast<double*>(smem_raw);
+  cplx* Bs = reinterpret_cast<cplx*>(As + STAGES * RC_A_STAGE);
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int m0 = blockIdx.x * BM;
+  const int64_t j0 = (int64_t)blockIdx.y * BN;
+  in += (int64_t)blockIdx.z * bs_in;
+  out += (int64_t)blockIdx.z * bs_out;
+  const int nk = (K + BK - 1) / BK;
+
+  auto load_stage = [&](int stage, int kt) {
+    const int k0 = kt * BK;
+    double* as = As + stage * RC_A_STAGE;
+    cplx* bs = Bs + stage * B_STAGE;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {          // 64 x 16 doubles as 512 16-byte pairs (K even)
+      const int idx = tid + 256 * r;
+      const int m = idx >> 3, kq = (idx & 7) * 2;
+      const bool ok = (m0 + m < M) && (k0 + kq < K);
+      cp_async16(as + m * RC_LDA + kq, ok ? A + (int64_t)(m0 + m) * K + (k0 + kq) : A, ok);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int idx = tid + 256 * r;
+      const int k = idx >> 6, n = idx & 63;
+      const bool ok = (k0 + k < K) && (j0 + n < ncols);
+      cp_async16(bs + k * LDB + n, ok ? in + (int64_t)(k0 + k) * ld_in + (j0 + n) : in, ok);
+    }
+  };
+
+  double cre[2][2][4], cim[2][2][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) cre[i][j][v] = cim[i][j][v] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_stage(s, s);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nxt = kt + STAGES - 1;
+      if (nxt < nk) load_stage(nxt % STAGES, nxt);
+      cp_async_commit();
+    }
+    const double* as = As + (kt % STAGES) * RC_A_STAGE + (wm * 32 + g) * RC_LDA + t;
+    const cplx* bs = Bs + (kt % STAGES) * B_STAGE + t * LDB + wn * 16 + g;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double a[2][2];
+      cplx b[2];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        a[mi][0] = as[(mi * 16) * RC_LDA + kk];
+        a[mi][1] = as[(mi * 16 + 8) * RC_LDA + kk];
+      }
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) b[ni] = ldc(bs + kk * LDB + ni * 8);
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) {
+          dmma_16x8x4(cre[mi][ni], a[mi][0], a[mi][1], b[ni].re);
+          dmma_16x8x4(cim[mi][ni], a[mi][0], a[mi][1], b[ni].im);
+        }
+    }
+  }
+  cp_async_wait<0>();
+
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) {
+      const int64_t col = j0 + wn * 16 + ni * 8 + 2 * t;
+      if constexpr (EPI == EPI_PAIR) {
+        const int src = ((m0 + wm * 32 + mi * 16) >> 4) * 8 + g;
+        if (src >= nsrc) continue;
+        const int2 lp = rows[src];
+        const cplx sc = scale[src];
+#pragma unroll
+        for (int cv = 0; cv < 2; ++cv) {
+          if (col + cv >= ncols) continue;
+          const cplx u = cmk(cre[mi][ni][cv], cim[mi][ni][cv]);        // c F
+          const cplx v = cmk(cre[mi][ni][2 + cv], cim[mi][ni][2 + cv]);  // d F
+          stc(out + (int64_t)lp.x * ld_out + col + cv, cmk(u.re - v.im, u.im + v.re));
+          if (lp.y >= 0) stc(out + (int64_t)lp.y * ld_out + col + cv, cmul(sc, cmk(u.re + v.im, u.im - v.re)));
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int row = m0 + wm * 32 + mi * 16 + g + 8 * h;
+          if (row >= M) continue;
+          cplx* dst = out + (int64_t)row * ld_out + col;
+          if (col < ncols) stc(dst, cmk(cre[mi][ni][2 * h], cim[mi][ni][2 * h]));
+          if (col + 1 < ncols) stc(dst + 1, cmk(cre[mi][ni][2 * h + 1], cim[mi][ni][2 * h + 1]));
+        }
+      }
+    }
+}
+
+// In-place pre-pass of the paired back transform: for every pair (l, p)
+// [W_l; W_p] <- [[m00, m01], [m10, m11]] [W_l; W_p]; self-paired (p < 0):
+// W_l <- m00 W_l.  Columns fastest (coalesced), one pair per grid row.
+__global__ void pair_mix_kernel(cplx* __restrict__ W, int64_t ld, int64_t ncols, int64_t bs,
+                                const int2* __restrict__ rows, const cplx* __restrict__ coef) {
+  const int q = blockIdx.y;
+  const int2 lp = rows[q];
+  const cplx m00 = coef[4 * q], m01 = coef[4 * q + 1], m10 = coef[4 * q + 2], m11 = coef[4 * q + 3];
+  cplx* wl = W + (int64_t)blockIdx.z * bs + (int64_t)lp.x * ld;
+  cplx* wp = W + (int64_t)blockIdx.z * bs + (int64_t)lp.y * ld;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < ncols; j += (int64_t)gridDim.x * blockDim.x) {
+    const cplx u = ldc(wl + j);
+    if (lp.y >= 0) {
+      const cplx v = ldc(wp + j);
+      stc(wl + j, cadd(cmul(m00, u), cmul(m01, v)));
+      stc(wp + j, cadd(cmul(m10, u), cmul(m11, v)));
+    } else {
+      stc(wl + j, cmul(m00, u));
+    }
+  }
+}
+
+template <int EPI>
+int launch_rc(const double* A, int M, int K, const cplx* in, int64_t ld_in, cplx* out, int64_t ld_out,
+              int64_t ncols, int batch, int64_t bs_in, int64_t bs_out, const int2* rows, const cplx* scale,
+              int nsrc, cudaStream_t stream) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(transform_rc_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        RC_SMEM));
+    attr_set = true;
+  }
+  for (int64_t c0 = 0; c0 < ncols; c0 += 65535LL * BN) {
+    const int64_t cn = ncols - c0 < 65535LL * BN ? ncols - c0 : 65535LL * BN;
+    dim3 grid((M + BM - 1) / BM, (unsigned)((cn + BN - 1) / BN), batch);
+    transform_rc_kernel<EPI><<<grid, 256, RC_SMEM, stream>>>(A, M, K, in + c0, ld_in, out + c0, ld_out, cn, bs_in,
+                                                             bs_out, rows, scale, nsrc);
+    STFEM_LAUNCH_CHECK("transform_rc_kernel");
+  }
+  return STFEM_OK;
+}
+
 }  // namespace
 
 int time_transform(const void* T, int nt, const void* in, int64_t ld_in, void* out,
@@ -170,4 +345,41 @@ extern "C" int stfem_time_transform(const void* T, int nt, const void* in, int64
                                     int64_t bstride_in, int64_t bstride_out, void* stream) {
   return stfem::time_transform(T, nt, in, ld_in, out, ld_out, ncols, batch, bstride_in,
                                bstride_out, (cudaStream_t)stream);
+}
+
+extern "C" int stfem_transform_pair_fwd(const double* A, int mrows, int nt, const int32_t* rows,
+                                        const void* scale, int nsrc, const void* in, int64_t ld_in, void* out,
+                                        int64_t ld_out, int64_t ncols, int batch, int64_t bstride_in,
+                                        int64_t bstride_out, void* stream) {
+  using namespace stfem;
+  if (nt <= 0 || (nt & 1) || mrows <= 0 || (mrows & 15) || nsrc <= 0 || 2 * nsrc > mrows + 16 || ncols < 0 ||
+      batch < 0 || ld_in < ncols || ld_out < ncols)
+    return fail(STFEM_ERR_DIM, "transform_pair_fwd: bad dimensions");
+  if (!A || !rows || !scale || !in || !out) return fail(STFEM_ERR_ARG, "transform_pair_fwd: null pointer");
+  if (((uintptr_t)A | (uintptr_t)in | (uintptr_t)out) & 15)
+    return fail(STFEM_ERR_ARG, "transform_pair_fwd: buffers must be 16-byte aligned");
+  if (ncols == 0 || batch == 0) return STFEM_OK;
+  return launch_rc<EPI_PAIR>(A, mrows, nt, (const cplx*)in, ld_in, (cplx*)out, ld_out, ncols, batch, bstride_in,
+                             bstride_out, (const int2*)rows, (const cplx*)scale, nsrc, (cudaStream_t)stream);
+}
+
+extern "C" int stfem_transform_pair_back(const double* A, int nt, const int32_t* mix_rows, const void* mix_coef,
+                                         int nmix, void* in, int64_t ld_in, void* out, int64_t ld_out,
+                                         int64_t ncols, int batch, int64_t bstride_in, int64_t bstride_out,
+                                         void* stream) {
+  using namespace stfem;
+  if (nt <= 0 || (nt & 1) || nmix <= 0 || nmix > nt || ncols < 0 || batch < 0 || ld_in < ncols || ld_out < ncols)
+    return fail(STFEM_ERR_DIM, "transform_pair_back: bad dimensions");
+  if (!A || !mix_rows || !mix_coef || !in || !out) return fail(STFEM_ERR_ARG, "transform_pair_back: null pointer");
+  if (((uintptr_t)A | (uintptr_t)in | (uintptr_t)out) & 15)
+    return fail(STFEM_ERR_ARG, "transform_pair_back: buffers must be 16-byte aligned");
+  if (in == out) return fail(STFEM_ERR_ARG, "transform_pair_back: in and out must not alias");
+  if (ncols == 0 || batch == 0) return STFEM_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t gx = std::min<int64_t>((ncols + 255) / 256, 1024);
+  pair_mix_kernel<<<dim3((unsigned)gx, nmix, batch), 256, 0, st>>>((cplx*)in, ld_in, ncols, bstride_in,
+                                                                    (const int2*)mix_rows, (const cplx*)mix_coef);
+  STFEM_LAUNCH_CHECK("pair_mix_kernel");
+  return launch_rc<EPI_PLAIN>(A, nt, nt, (const cplx*)in, ld_in, (cplx*)out, ld_out, ncols, batch, bstride_in,
+                              bstride_out, nullptr, nullptr, 0, st);
 }

@@ -34,12 +34,28 @@ C128 = torch.complex128
 class CudaBackend:
     """K3 transforms + K4/K5 factor/solve through the C-ABI."""
 
-    def __init__(self, plan):
+    def __init__(self, plan, pairs=None):
         self.plan = plan
+        self.pairs = pairs   # paired_transform.DevicePairs: K3p transforms (half the flops of K3)
 
     def transform(self, T, x, out):
         from . import _kernels as K
         K.time_transform(T, x, out=out)
+
+    def transform_fwd(self, Y, x, out):
+        from . import _kernels as K
+        if self.pairs is None:
+            K.time_transform(Y, x, out=out)
+        else:
+            K.transform_pair_fwd(self.pairs, x, out=out)
+
+    def transform_back(self, X, x, out):
+        """x is scratch (K3p mixes its pair rows in place)."""
+        from . import _kernels as K
+        if self.pairs is None:
+            K.time_transform(X, x, out=out)
+        else:
+            K.transform_pair_back(self.pairs, x, out=out)
 
     def factor_solve(self, lam, G, W, layout, nrhs):
         self.plan.factor_solve(lam, G, W, layout, nrhs)
@@ -109,11 +125,13 @@ class DistributedFDM:
             raise N.DimensionMismatch(N.ERR_DIM, f"shard {tuple(F_p.shape)} != {(nt, nr, c)}")
         out = out if out is not None else torch.empty_like(F_p)
         t = [time.perf_counter()]
-        self.backend.transform(self.Y, F_p.view(nt, nr * c), self.G.view(nt, nr * c))      # (2)
+        fwd = getattr(self.backend, "transform_fwd", self.backend.transform)
+        back = getattr(self.backend, "transform_back", self.backend.transform)
+        fwd(self.Y, F_p.view(nt, nr * c), self.G.view(nt, nr * c))                         # (2)
         self._a2a(self.R, self.G)                                                           # a2a #1
         self.backend.factor_solve(self.lam_local, self.R, self.W, self.layout, nr)         # (3)
         self._a2a(self.G, self.W)                                                           # a2a #2
-        self.backend.transform(self.X, self.G.view(nt, nr * c), out.view(nt, nr * c))      # (4)
+        back(self.X, self.G.view(nt, nr * c), out.view(nt, nr * c))                        # (4)
         return out
 
 
@@ -149,15 +167,24 @@ def bench_main(args):
     torch.cuda.synchronize()
     t_asm = time.perf_counter() - t0
     t1 = time.perf_counter()
-    tf = temporal_factors(prob.M_t, prob.B_t) if rank == 0 else None
+    from . import paired_transform as PT
     nt = prob.nt
-    X = tf.X if rank == 0 else np.zeros((nt, nt), complex)
-    Y = tf.Y if rank == 0 else np.zeros((nt, nt), complex)
-    lam = tf.eigenvalues if rank == 0 else np.zeros(nt, complex)
+    X, Y, lam = np.zeros((nt, nt), complex), np.zeros((nt, nt), complex), np.zeros(nt, complex)
+    if rank == 0:
+        tf = temporal_factors(prob.M_t, prob.B_t)
+        X, Y, lam = tf.X, tf.Y, tf.eigenvalues
+        pf0 = PT.build(lam, X, prob.B_t) if PT.enabled() else None
+        if pf0 is not None:
+            X, Y, lam = pf0.X, pf0.Y, pf0.lam       # the paired eigenbasis
     Xt, Yt, lt = broadcast_factors(X, Y, lam, dev)
+    # every rank derives the K3p tables from the broadcast (already paired) factors
+    pf = PT.build(lt.cpu().numpy(), Xt.cpu().numpy(), prob.B_t) if PT.enabled() else None
+    if pf is not None:
+        Yt = torch.as_tensor(pf.Y, dtype=C128, device=dev)
+    pairs = PT.DevicePairs(pf, dev) if pf is not None else None
     plan = SpatialPlan(prob.ops)
     t_setup = time.perf_counter() - t1
-    solver = DistributedFDM(prob.nx, nt, prob.n_rhs, Xt, Yt, lt, CudaBackend(plan))
+    solver = DistributedFDM(prob.nx, nt, prob.n_rhs, Xt, Yt, lt, CudaBackend(plan, pairs))
     # this rank's RHS shard: deterministic part on device + Gaussian columns from the shared streams
     Fp = _local_rhs(prob, rank, world, dev)
     out = torch.empty_like(Fp)
@@ -187,7 +214,7 @@ def bench_main(args):
     dist.barrier()
     t_step = float(tt.item())
     dofs = prob.nx * nt * prob.n_rhs
-    launches = 2 + plan.last_launches()
+    launches = (3 if pairs is not None else 2) + plan.last_launches()
     # roofline of the dominant kernel family: one extra step with per-launch events on every
     # rank (the all-to-alls keep the ranks in step); rank 0 reports its own shifts
     roof = None

@@ -2,9 +2,12 @@
 
   solve(ops, M_t, B_t, f, variant=FastDiagonalization) -> SolveReport
     (1) temporal core + eigendecomposition (host fp64, `t_setup`)
-    (2) G = (Y (x) I) F                     K3 DMMA GEMM
+    (2) G = (Y (x) I) F                     K3p/K3 DMMA GEMM
     (3) (M_x + lam_l A_x) w_l = g_l         K4/K5 multifrontal SPEC.md:377, :415
-    (4) Psi = (X (x) I) W                   K3 DMMA GEMM
+    (4) Psi = (X (x) I) W                   K3p/K3 DMMA GEMM
+  K3p (paired_transform.py) runs both transforms at half the flops of the
+  complex GEMM K3 by pairing the eigenvalues (lam, -conj(lam)) of the real
+  temporal pencil; K3 remains for factors that do not pair (and for BS).
   transform_blocks(T, v)  (SPEC.md:392-400)   -> K3
   apply_global(...)   -> K7 (residual certificate, :405)
 
@@ -27,6 +30,7 @@ import torch
 
 from . import _kernels as K
 from . import _native as N
+from . import paired_transform as PT
 from .dense_complex_linalg import TemporalFactors, temporal_factors
 from .fem_assembly import SpatialOperators, temporal_band
 from .sparse_spatial_solver import SpatialPlan, blockvector_layout
@@ -100,7 +104,7 @@ class FDMSolver:
 
     def __init__(self, ops: SpatialOperators, M_t: np.ndarray, B_t: np.ndarray,
                  plan: SpatialPlan | None = None, factors: TemporalFactors | None = None,
-                 leaf_size: int = 16):
+                 leaf_size: int = 16, paired: bool = True):
         t0 = time.perf_counter()
         self.ops = ops
         self.M_t = np.asarray(M_t, float)
@@ -111,19 +115,40 @@ class FDMSolver:
         self.plan = plan if plan is not None else SpatialPlan(ops, leaf_size)
         t2 = time.perf_counter()
         dev = ops.device
-        self.X = torch.as_tensor(self.tf.X, dtype=C128, device=dev)
-        self.Y = torch.as_tensor(self.tf.Y, dtype=C128, device=dev)
-        self.lam = torch.as_tensor(self.tf.eigenvalues, dtype=C128, device=dev)
-        self.t_eig = t1 - t0
+        lam, X, Y = self.tf.eigenvalues, self.tf.X, self.tf.Y
+        self.pairs = None
+        if paired and PT.enabled():
+            pf = PT.build(lam, X, self.B_t)
+            if pf is not None:
+                # the paired eigenbasis (partners rebuilt from their leads) drives every stage
+                lam, X, Y = pf.lam, pf.X, pf.Y
+                self.pairs = PT.DevicePairs(pf, dev)
+        self.X = torch.as_tensor(X, dtype=C128, device=dev)
+        self.Y = torch.as_tensor(Y, dtype=C128, device=dev)
+        self.lam = torch.as_tensor(lam, dtype=C128, device=dev)
+        self.t_eig = time.perf_counter() - t2 + t1 - t0
         self.t_symbolic = t2 - t1
 
     @property
     def kappa2(self) -> float:
         return self.tf.kappa2
 
+    def forward_transform(self, F: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
+        """G = (Y (x) I) F (step 2): K3p when the eigenvalues pair, else K3."""
+        if self.pairs is not None:
+            return K.transform_pair_fwd(self.pairs, F, out=out, stream=stream)
+        return K.time_transform(self.Y, F, out=out, stream=stream)
+
+    def back_transform(self, W: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
+        """Psi = (X (x) I) W (step 4).  W is scratch: K3p mixes its pair rows in place."""
+        if self.pairs is not None:
+            return K.transform_pair_back(self.pairs, W, out=out, stream=stream)
+        return K.time_transform(self.X, W, out=out, stream=stream)
+
     def solve(self, F: torch.Tensor, out: torch.Tensor | None = None, work: torch.Tensor | None = None,
               stream=None, timings: dict | None = None) -> torch.Tensor:
-        """Psi for F of shape (n_t, n_x) or (n_rhs, n_t, n_x), complex128 on the GPU."""
+        """Psi for F of shape (n_t, n_x) or (n_rhs, n_t, n_x), complex128 on the GPU.
+        `work` (if given) is scratch and is overwritten."""
         N.require_cuda(F)
         if F.shape[-2:] != (self.nt, self.ops.n):
             raise N.DimensionMismatch(N.ERR_DIM, f"solve: f {tuple(F.shape)} vs ({self.nt}, {self.ops.n})")
@@ -137,13 +162,13 @@ class FDMSolver:
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timings is not None else None
         if ev:
             ev[0].record(s)
-        K.time_transform(self.Y, Fb, out=G, stream=s)                 # (2)
+        self.forward_transform(Fb, G, s)                               # (2)
         if ev:
             ev[1].record(s)
         self.plan.factor_solve(self.lam, G, W, blockvector_layout(self.nt, self.ops.n), nr, stream=s)  # (3)
         if ev:
             ev[2].record(s)
-        K.time_transform(self.X, W, out=G, stream=s)                  # (4)
+        self.back_transform(W, G, s)                                   # (4) (W is scratch)
         if ev:
             ev[3].record(s)
             ev[3].synchronize()
@@ -192,10 +217,10 @@ class FDMSolver:
             ev = torch.cuda.Event()
             ev.record(cs)
             s.wait_event(ev)
-            K.time_transform(self.Y, Fd[..., c0:c1], out=G[..., c0:c1], stream=s)
+            self.forward_transform(Fd[..., c0:c1], G[..., c0:c1], s)
         self.plan.factor_solve(self.lam, G, W, blockvector_layout(nt, nx), nr, stream=s)   # (3)
         for c0, c1 in blocks:                                             # (4) pipelined with D2H
-            K.time_transform(self.X, W[..., c0:c1], out=G[..., c0:c1], stream=s)
+            self.back_transform(W[..., c0:c1], G[..., c0:c1], s)
             ev = torch.cuda.Event()
             ev.record(s)
             cs.wait_event(ev)

@@ -51,3 +51,82 @@ def test_transform_identity_and_diag():
     D = np.diag([2.0, 3.0]).astype(complex)
     out = K.time_transform(torch.from_numpy(D).cuda(), torch.from_numpy(v).cuda()).cpu().numpy()
     assert np.allclose(out, np.diag([2.0, 3.0]) @ v, rtol=0, atol=1e-15)
+
+
+# ---- K3p: eigenpair-paired transforms (paired_transform.py) ----
+from paper_2504_07269_b200 import dense_complex_linalg as dcl  # noqa: E402
+from paper_2504_07269_b200 import fem_assembly as fa  # noqa: E402
+from paper_2504_07269_b200 import paired_transform as PT  # noqa: E402
+from paper_2504_07269_b200 import temporal_mesh as tm  # noqa: E402
+
+
+def _pairs(N, deg, T=1.0):
+    Mt, Bt = fa.assemble_temporal(tm.uniform(T, N), deg)
+    tf = dcl.temporal_factors(Mt, Bt)
+    pf = PT.build(tf.eigenvalues, tf.X, Bt)
+    assert pf is not None
+    return pf, PT.DevicePairs(pf, "cuda")
+
+
+@pytest.mark.parametrize("N,deg,ncols", [(16, 1, 450), (64, 1, 7938), (256, 1, 4097), (512, 2, 3000),
+                                         (1024, 1, 700), (40, 2, 65), (8, 1, 1)])
+def test_paired_transforms_match_dense(N, deg, ncols):
+    pf, dp = _pairs(N, deg)
+    nt = pf.X.shape[0]
+    rng = np.random.default_rng(N + ncols)
+    F = crand(rng, nt, ncols)
+    G = K.transform_pair_fwd(dp, torch.from_numpy(F).cuda()).cpu().numpy()
+    ref = pf.Y @ F
+    assert np.linalg.norm(G - ref) / np.linalg.norm(ref) < 1e-14
+    W = torch.from_numpy(F).cuda()
+    P = K.transform_pair_back(dp, W).cpu().numpy()
+    ref = pf.X @ F
+    assert np.linalg.norm(P - ref) / np.linalg.norm(ref) < 1e-14
+
+
+def test_paired_transforms_batched_strided():
+    pf, dp = _pairs(48, 1)
+    nt, n = pf.X.shape[0], 300
+    rng = np.random.default_rng(5)
+    v = crand(rng, 3, nt, n)
+    G = K.transform_pair_fwd(dp, torch.from_numpy(v).cuda()).cpu().numpy()
+    ref = np.einsum("lk,bkj->blj", pf.Y, v)
+    assert np.linalg.norm(G - ref) / np.linalg.norm(ref) < 1e-14
+    wide = crand(rng, 2, nt, 2 * n)
+    full = torch.from_numpy(wide).cuda()
+    sl = full[..., 7:7 + n]
+    out = torch.empty((2, nt, n), dtype=torch.complex128, device="cuda")
+    K.transform_pair_back(dp, sl, out=out)
+    ref = np.einsum("lk,bkj->blj", pf.X, wide[..., 7:7 + n])
+    got = out.cpu().numpy()
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-14
+    # columns outside the slice are untouched by the in-place pre-pass
+    back = full.cpu().numpy()
+    assert np.array_equal(back[..., :7], wide[..., :7]) and np.array_equal(back[..., 7 + n:], wide[..., 7 + n:])
+
+
+def test_paired_transform_self_pairs():
+    """Purely imaginary (self-paired) eigenvalues: x = e^{i phi} r, one output row per source."""
+    rng = np.random.default_rng(11)
+    npair, nself = 13, 6
+    nt = 2 * npair + nself
+    X = np.zeros((nt, nt), complex)
+    lam = np.zeros(nt, complex)
+    for q in range(npair):
+        x = crand(rng, nt)
+        lam[2 * q] = rng.uniform(0.5, 3) - 1j * rng.uniform(0.1, 2)
+        lam[2 * q + 1] = -np.conj(lam[2 * q])
+        X[:, 2 * q], X[:, 2 * q + 1] = x, np.exp(0.3j * q) * np.conj(x)
+    for q in range(nself):
+        lam[2 * npair + q] = -1j * (q + 1)
+        X[:, 2 * npair + q] = np.exp(0.7j * q) * rng.standard_normal(nt)
+    B = rng.standard_normal((nt, nt)) + nt * np.eye(nt)
+    pf = PT.build(lam, X, B)
+    assert pf is not None and pf.nself == nself
+    dp = PT.DevicePairs(pf, "cuda")
+    F = crand(rng, nt, 333)
+    G = K.transform_pair_fwd(dp, torch.from_numpy(F).cuda()).cpu().numpy()
+    Y = np.linalg.solve(X, np.linalg.inv(1j * B))
+    assert np.linalg.norm(G - Y @ F) / np.linalg.norm(Y @ F) < 1e-13
+    P = K.transform_pair_back(dp, torch.from_numpy(F).cuda()).cpu().numpy()
+    assert np.linalg.norm(P - X @ F) / np.linalg.norm(X @ F) < 1e-13
