@@ -232,6 +232,88 @@ class FDMSolver:
         return out_host
 
 
+    def solve_host_stream(self, F_hosts, out_hosts, chunks: int = 8, stream=None,
+                          dev_buffers: tuple | None = None):
+        """Psi_k for a sequence of PINNED host RHS stacks F_hosts[k] into out_hosts[k]
+        (streamed solves, e.g. a serving loop): every step still copies its F in and its
+        Psi out, but step k+1's host->device copy runs on its own copy stream during
+        step k's spatial solves, and step k's device->host copy (column blocks, behind
+        the back transform) during step k+1's forward transform.  Three device buffers
+        rotate: A holds the uploaded F; G and W swap roles every step (G_k = W_{k-1}:
+        the buffer of Psi_{k-1} is only rewritten by factor_solve(k+1) once its copy has
+        drained).  Returns out_hosts."""
+        N.require_cuda()
+        n = len(F_hosts)
+        if n == 0:
+            return out_hosts
+        Fh = [f.unsqueeze(0) if f.dim() == 2 else f for f in F_hosts]
+        Ph = [o.unsqueeze(0) if o.dim() == 2 else o for o in out_hosts]
+        shape = Fh[0].shape
+        for f, o in zip(Fh, Ph):
+            if f.shape != shape or o.shape != shape or f.shape[-2:] != (self.nt, self.ops.n):
+                raise N.DimensionMismatch(N.ERR_DIM, f"solve_host_stream: f {tuple(f.shape)} vs ({self.nt}, {self.ops.n})")
+            if not (f.is_pinned() and o.is_pinned() and f.is_contiguous() and o.is_contiguous()):
+                raise ValueError("solve_host_stream: host buffers must be contiguous pinned memory")
+        nr, nt, nx = shape
+        dev = self.X.device
+        if dev_buffers is None:
+            dev_buffers = tuple(torch.empty(shape, dtype=C128, device=dev) for _ in range(3))
+        A = dev_buffers[0]
+        s = stream if stream is not None else torch.cuda.current_stream()
+        if getattr(self, "_h2d_stream", None) is None:
+            self._h2d_stream = torch.cuda.Stream(device=dev)
+            self._d2h_stream = torch.cuda.Stream(device=dev)
+        hs, ds = self._h2d_stream, self._d2h_stream
+        lib = N.lib()
+        cw = -(-nx // max(1, chunks))
+        blocks = [(c0, min(nx, c0 + cw)) for c0 in range(0, nx, cw)]
+        layout = blockvector_layout(nt, nx)
+
+        def h2d(k, c0, c1):
+            N.check(lib.stfem_copy_cols(N.ptr(A[..., c0:]), nx, C.c_void_p(Fh[k].data_ptr() + 16 * c0), nx,
+                                        c1 - c0, nr * nt, 0, N.stream_ptr(hs)))
+
+        start = torch.cuda.Event()
+        start.record(s)
+        hs.wait_event(start)
+        ds.wait_event(start)
+        d2h_done = None
+        for k in range(n):
+            G, W = (dev_buffers[1], dev_buffers[2]) if k % 2 == 0 else (dev_buffers[2], dev_buffers[1])
+            if k == 0:                                   # prologue: H2D(0) block-pipelined with the transform
+                for c0, c1 in blocks:
+                    h2d(0, c0, c1)
+                    ev = torch.cuda.Event()
+                    ev.record(hs)
+                    s.wait_event(ev)
+                    self.forward_transform(A[..., c0:c1], G[..., c0:c1], s)
+            else:
+                s.wait_event(h2d_done)
+                self.forward_transform(A, G, s)          # G_k = W_{k-1}: dead since back(k-1)
+            if k + 1 < n:                                # H2D(k+1) during factor_solve(k)
+                fwd_done = torch.cuda.Event()
+                fwd_done.record(s)
+                hs.wait_event(fwd_done)
+                for c0, c1 in [(0, nx)]:
+                    h2d(k + 1, c0, c1)
+                h2d_done = torch.cuda.Event()
+                h2d_done.record(hs)
+            if d2h_done is not None:                     # W_k = G_{k-1} holds Psi_{k-1} until drained
+                s.wait_event(d2h_done)
+            self.plan.factor_solve(self.lam, G, W, layout, nr, stream=s)
+            for c0, c1 in blocks:                        # back transform W -> G, D2H block-pipelined
+                self.back_transform(W[..., c0:c1], G[..., c0:c1], s)
+                ev = torch.cuda.Event()
+                ev.record(s)
+                ds.wait_event(ev)
+                N.check(lib.stfem_copy_cols(C.c_void_p(Ph[k].data_ptr() + 16 * c0), nx, N.ptr(G[..., c0:]), nx,
+                                            c1 - c0, nr * nt, 1, N.stream_ptr(ds)))
+            d2h_done = torch.cuda.Event()
+            d2h_done.record(ds)
+        s.wait_event(d2h_done)
+        return out_hosts
+
+
 class BSSolver:
     """Bartels-Stewart variant: the fallback
     for a temporal core that is not diagonalizable.
