@@ -1058,6 +1058,7 @@ Plan::~Plan() {
   for (auto st : lane_streams) cudaStreamDestroy(st);
   for (auto ev : lane_events) cudaEventDestroy(ev);
   if (start_event) cudaEventDestroy(start_event);
+  if (stagger_event) cudaEventDestroy(stagger_event);
 }
 
 void Plan::free_device() {
@@ -1208,6 +1209,12 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
   const int sub = (batch + lanes - 1) / lanes;
   if ((rc = ensure_workspace(P, lanes * sub, nrhs))) return rc;   // lane slices are sub shifts each
   const LevelArgs a0 = a;
+  // staggered lanes (STFEM_STAGGER = d >= 0, with STFEM_STREAMS >= 2): lane 1 starts once lane 0
+  // has factored depth d of its first slice, so one lane's deep, latency-bound levels run beside
+  // the other lane's tensor-core-bound top levels instead of in phase with them
+  static const int stagger_env = getenv("STFEM_STAGGER") ? atoi(getenv("STFEM_STAGGER")) : -1;
+  const int stagger_depth = stagger_env;
+  cudaEvent_t stagger_rec = nullptr;
   auto run_batch = [&](int s0, int nb, int koff, cudaStream_t st) -> int {
     LevelArgs a = a0;
     a.nbatch = nb;
@@ -1373,6 +1380,7 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
         }
       }
       mark();
+      if (stagger_rec && d == stagger_depth) STFEM_CUDA_TRY(cudaEventRecord(stagger_rec, st));
     }
     for (int d = 0; d <= P.depth; ++d) {
       cur_depth = d;
@@ -1439,8 +1447,14 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
     STFEM_CUDA_TRY(cudaEventRecord(P.start_event, stream));
     for (int j = 0; j < lanes; ++j) STFEM_CUDA_TRY(cudaStreamWaitEvent(P.lane_streams[j], P.start_event, 0));
     int j = 0;
-    for (int s0 = 0; s0 < nshift; s0 += sub, j = (j + 1) % lanes)
+    const bool stagger = stagger_depth >= 0 && stagger_depth <= P.depth && nshift > sub;
+    if (stagger && !P.stagger_event) STFEM_CUDA_TRY(cudaEventCreateWithFlags(&P.stagger_event, cudaEventDisableTiming));
+    for (int s0 = 0; s0 < nshift; s0 += sub, j = (j + 1) % lanes) {
+      stagger_rec = (stagger && s0 == 0) ? P.stagger_event : nullptr;
+      if (stagger && j == 1 && s0 == sub) STFEM_CUDA_TRY(cudaStreamWaitEvent(P.lane_streams[1], P.stagger_event, 0));
       if ((rc = run_batch(s0, std::min(sub, nshift - s0), j * sub, P.lane_streams[j]))) return rc;
+    }
+    stagger_rec = nullptr;
     for (int jj = 0; jj < lanes; ++jj) {
       STFEM_CUDA_TRY(cudaEventRecord(P.lane_events[jj], P.lane_streams[jj]));
       STFEM_CUDA_TRY(cudaStreamWaitEvent(stream, P.lane_events[jj], 0));

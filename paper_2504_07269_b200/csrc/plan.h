@@ -125,6 +125,7 @@ struct Plan {
   cplx* d_rpool[2] = {nullptr, nullptr};
   cplx* d_Z = nullptr;
   cplx* d_wbuf = nullptr;                   // spectral w = 1 / (theta + lam), sum(m) x batch
+  cudaEvent_t stagger_event = nullptr;      // STFEM_STAGGER: lane 1 waits for lane 0 mid-slice
   std::vector<cudaStream_t> lane_streams;   // shift lanes of factor_solve (STFEM_STREAMS, default 2)
   std::vector<cudaEvent_t> lane_events;
   cudaEvent_t start_event = nullptr;

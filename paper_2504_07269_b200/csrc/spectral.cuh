@@ -195,12 +195,16 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
   }
   if constexpr (OP == OP_U) cp_async_wait<0>();
   __syncthreads();
+  // the last column tile of a batch is partial (e.g. 342 shifts = 5 x 64 + 22): warps whose
+  // 16 (or upper 8) columns are all past ncols skip their DMMAs (warp-uniform)
+  const bool wact = n0 + wn * 16 < ncols, wact1 = n0 + wn * 16 + 8 < ncols;
   for (int kc = 0; kc < nk; ++kc) {
     if (kc + 1 < nk) fetch(kc + 1);
     const double* as = As + (kc & 1) * SP_A_STAGE + tq * SP_LDA + wm * 32 + gq;
     const cplx* bs = Bs + (kc & 1) * SP_B_STAGE + tq * SP_LDB + wn * 16 + gq;
 #pragma unroll
     for (int kk = 0; kk < SP_BK; kk += 4) {
+      if (!wact) break;
       double af[2][2];
       cplx bf[2];
 #pragma unroll
@@ -214,6 +218,7 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
       for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
         for (int ni = 0; ni < 2; ++ni) {
+          if (ni == 1 && !wact1) continue;
           dmma_16x8x4(acc[mi][ni][0], af[mi][0], af[mi][1], bf[ni].re);
           dmma_16x8x4(acc[mi][ni][1], af[mi][0], af[mi][1], bf[ni].im);
         }
