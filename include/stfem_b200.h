@@ -75,6 +75,8 @@ int stfem_time_transform(const void* T, int nt, const void* in, int64_t ld_in,
  * temporal pencil of SPEC.md:181-189; host pairing and derivation in
  * paper_2504_07269_b200/paired_transform.py).  Half the flops of K3: a real
  * (M x n_t) x complex (n_t x ncols) product on DMMA.
+ * Both A matrices are passed fragment-packed: P[mb][k][g][h] = A[16 mb + g + 8 h][k]
+ * (rows zero-padded to a multiple of 16; paired_transform.pack_fragments).
  *   fwd:  G = Y F.  A: device float64 (mrows x nt), mrows a multiple of 16,
  *         rows in blocks of 16 = [Re y_l of 8 sources; Im y_l of the same 8];
  *         rows: int32 (nsrc, 2) = (l, p or -1); scale: c128 (nsrc,) with

@@ -60,7 +60,7 @@ def transform_pair_fwd(pairs, v: torch.Tensor, out: torch.Tensor | None = None, 
         raise N.DimensionMismatch(N.ERR_DIM, "transform: bad output tensor")
     B, _, ncols = vb.shape
     N.check(N.lib().stfem_transform_pair_fwd(
-        N.ptr(pairs.A_fwd), pairs.A_fwd.shape[0], nt, N.ptr(pairs.rows_fwd), N.ptr(pairs.scale_fwd),
+        N.ptr(pairs.A_fwd), pairs.mrows_fwd, nt, N.ptr(pairs.rows_fwd), N.ptr(pairs.scale_fwd),
         pairs.rows_fwd.shape[0], N.ptr(vb), vb.stride(-2), N.ptr(ob), ob.stride(-2), ncols, B,
         vb.stride(0) if B > 1 else 0, ob.stride(0) if B > 1 else 0, N.stream_ptr(stream)))
     return out

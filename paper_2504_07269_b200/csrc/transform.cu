@@ -142,9 +142,18 @@ time_transform_kernel(const cplx* __restrict__ T, int nt, const cplx* __restrict
 //   EPI_PLAIN (back Psi = A W' after pair_mix_kernel): plain store.
 // CTA tile 64 rows x 64 complex columns, k-tile 16, 3-stage cp.async, 8 warps
 // as 2 x 4, warp tile 32 rows x 16 complex (2 x 2 fragments x re/im).
-constexpr int RC_LDA = BK + 4;   // As[m][k] doubles: (g*20 + t) mod 16 -> 2 wavefronts per LDS.64
-constexpr int RC_A_STAGE = BM * RC_LDA;
-constexpr int RC_SMEM = STAGES * (RC_A_STAGE * 8 + B_STAGE * 16);
+// A arrives PACKED from the host: A[mb][k][g][h] = A_logical[16 mb + g + 8 h][k], i.e. for
+// every 16-row block and k the 8 (row g, row g + 8) pairs of one DMMA A fragment, so a
+// thread fetches both fragment halves with one LDS.128 and the tile is a straight
+// 16-byte cp.async copy.  Shared layout As[mb][k][20 doubles] (16 + 4 pad): the 32
+// lanes' (t * 160 + 16 g) byte offsets cover 8 distinct 16-byte slots of each 128 B.
+constexpr int RC_KS = 20;
+// k-tile 16 in 3 stages (measured: a 32-deep tile in 2 stages, for half the barriers per
+// DMMA, ran 33.7 vs 33.2 ms on C4)
+constexpr int RC_BK = 16, RC_STAGES = 3;
+constexpr int RC_A_STAGE = (BM / 16) * RC_BK * RC_KS;
+constexpr int RC_B_STAGE = RC_BK * LDB;
+constexpr int RC_SMEM = RC_STAGES * (RC_A_STAGE * 8 + RC_B_STAGE * 16);
 enum { EPI_PLAIN = 0, EPI_PAIR = 1 };
 
 template <int EPI>
@@ -152,9 +161,10 @@ __global__ void __launch_bounds__(256, 2)
 transform_rc_kernel(const double* __restrict__ A, int M, int K, const cplx* __restrict__ in, int64_t ld_in,
                     cplx* __restrict__ out, int64_t ld_out, int64_t ncols, int64_t bs_in, int64_t bs_out,
                     const int2* __restrict__ rows, const cplx* __restrict__ scale, int nsrc) {
+  // M: output rows (EPI_PLAIN) / A rows; A holds ceil(M / 16) packed 16-row blocks
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* As = reinterpret_cast<double*>(smem_raw);
-  cplx* Bs = reinterpret_cast<cplx*>(As + STAGES * RC_A_STAGE);
+  cplx* Bs = reinterpret_cast<cplx*>(As + RC_STAGES * RC_A_STAGE);
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -163,21 +173,23 @@ transform_rc_kernel(const double* __restrict__ A, int M, int K, const cplx* __re
   const int64_t j0 = (int64_t)blockIdx.y * BN;
   in += (int64_t)blockIdx.z * bs_in;
   out += (int64_t)blockIdx.z * bs_out;
-  const int nk = (K + BK - 1) / BK;
+  const int nk = (K + RC_BK - 1) / RC_BK;
 
   auto load_stage = [&](int stage, int kt) {
-    const int k0 = kt * BK;
+    const int k0 = kt * RC_BK;
     double* as = As + stage * RC_A_STAGE;
-    cplx* bs = Bs + stage * B_STAGE;
+    cplx* bs = Bs + stage * RC_B_STAGE;
+    const int mblks = (M + 15) >> 4;
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {          // 64 x 16 doubles as 512 16-byte pairs (K even)
+    for (int r = 0; r < RC_BK / 8; ++r) {   // 4 row blocks x RC_BK k x 8 fragment pairs (16-byte chunks)
       const int idx = tid + 256 * r;
-      const int m = idx >> 3, kq = (idx & 7) * 2;
-      const bool ok = (m0 + m < M) && (k0 + kq < K);
-      cp_async16(as + m * RC_LDA + kq, ok ? A + (int64_t)(m0 + m) * K + (k0 + kq) : A, ok);
+      const int mb = idx / (RC_BK * 8), k = (idx >> 3) % RC_BK, gg = idx & 7;
+      const int gmb = (m0 >> 4) + mb;
+      const bool ok = (gmb < mblks) && (k0 + k < K);
+      cp_async16(as + (mb * RC_BK + k) * RC_KS + 2 * gg, ok ? A + ((int64_t)gmb * K + (k0 + k)) * 16 + 2 * gg : A, ok);
     }
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < RC_BK / 4; ++r) {
       const int idx = tid + 256 * r;
       const int k = idx >> 6, n = idx & 63;
       const bool ok = (k0 + k < K) && (j0 + n < ncols);
@@ -194,28 +206,29 @@ transform_rc_kernel(const double* __restrict__ A, int M, int K, const cplx* __re
       for (int v = 0; v < 4; ++v) cre[i][j][v] = cim[i][j][v] = 0.0;
 
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
+  for (int s = 0; s < RC_STAGES - 1; ++s) {
     if (s < nk) load_stage(s, s);
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
-    cp_async_wait<STAGES - 2>();
+    cp_async_wait<RC_STAGES - 2>();
     __syncthreads();
     {
-      const int nxt = kt + STAGES - 1;
-      if (nxt < nk) load_stage(nxt % STAGES, nxt);
+      const int nxt = kt + RC_STAGES - 1;
+      if (nxt < nk) load_stage(nxt % RC_STAGES, nxt);
       cp_async_commit();
     }
-    const double* as = As + (kt % STAGES) * RC_A_STAGE + (wm * 32 + g) * RC_LDA + t;
-    const cplx* bs = Bs + (kt % STAGES) * B_STAGE + t * LDB + wn * 16 + g;
+    const double* as = As + (kt % RC_STAGES) * RC_A_STAGE + ((wm * 2) * RC_BK + t) * RC_KS + 2 * g;
+    const cplx* bs = Bs + (kt % RC_STAGES) * RC_B_STAGE + t * LDB + wn * 16 + g;
 #pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
+    for (int kk = 0; kk < RC_BK; kk += 4) {
       double a[2][2];
       cplx b[2];
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi) {
-        a[mi][0] = as[(mi * 16) * RC_LDA + kk];
-        a[mi][1] = as[(mi * 16 + 8) * RC_LDA + kk];
+        const cplx pr = ldc(reinterpret_cast<const cplx*>(as + (mi * RC_BK + kk) * RC_KS));   // rows g, g + 8
+        a[mi][0] = pr.re;
+        a[mi][1] = pr.im;
       }
 #pragma unroll
       for (int ni = 0; ni < 2; ++ni) b[ni] = ldc(bs + kk * LDB + ni * 8);

@@ -22,6 +22,8 @@ PAIR_TOL relative of LAPACK's); if any check fails the solver keeps the complex 
 (`time_transform`) - a GPU kernel either way, no CPU path.
 
 Host layout handed to the C-ABI (stfem_transform_pair_fwd / _back):
+  * (both A matrices go to the device in the fragment-packed layout of
+    pack_fragments: per 16-row block and k, the (row g, row g + 8) pairs)
   * A_fwd: (16 ceil(nsrc / 8), n_t) float64; block q of 16 rows holds
     Re y of sources 8q..8q+7 in rows 0-7 and Im y in rows 8-15, so one DMMA
     accumulator fragment holds c F and d F of the same source;
@@ -186,6 +188,16 @@ def back_host(pf: PairedFactors, W: np.ndarray) -> np.ndarray:
     return pf.A_back @ W
 
 
+def pack_fragments(A: np.ndarray) -> np.ndarray:
+    """The kernels' A layout: P[mb, k, g, h] = A[16 mb + g + 8 h, k] (rows zero-padded to a
+    multiple of 16), i.e. per 16-row block and k the 8 row pairs of one DMMA A fragment."""
+    M, K = A.shape
+    mb = -(-M // 16)
+    Ap = np.zeros((16 * mb, K))
+    Ap[:M] = A
+    return np.ascontiguousarray(Ap.reshape(mb, 2, 8, K).transpose(0, 3, 2, 1))
+
+
 class DevicePairs:
     """Device copies of a PairedFactors for the K3p kernels."""
 
@@ -193,10 +205,11 @@ class DevicePairs:
         import torch
         self.host = pf
         self.nt = pf.A_back.shape[0]
-        self.A_fwd = torch.as_tensor(np.ascontiguousarray(pf.A_fwd), device=device)
+        self.A_fwd = torch.as_tensor(pack_fragments(pf.A_fwd), device=device)
+        self.mrows_fwd = pf.A_fwd.shape[0]
         self.rows_fwd = torch.as_tensor(np.ascontiguousarray(pf.rows_fwd), device=device)
         self.scale_fwd = torch.as_tensor(np.ascontiguousarray(pf.scale_fwd), device=device)
-        self.A_back = torch.as_tensor(np.ascontiguousarray(pf.A_back), device=device)
+        self.A_back = torch.as_tensor(pack_fragments(pf.A_back), device=device)
         self.mix_rows = torch.as_tensor(np.ascontiguousarray(pf.mix_rows), device=device)
         self.mix_coef = torch.as_tensor(np.ascontiguousarray(pf.mix_coef), device=device)
 
