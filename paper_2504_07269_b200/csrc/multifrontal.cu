@@ -494,11 +494,15 @@ __device__ __forceinline__ void sym_tile32(cplx* __restrict__ C, int ldC, int M,
         cre[ni][2 * h + v] = o.re;
         cim[ni][2 * h + v] = o.im;
       }
+  // warps whose 16 x 16 block lies strictly above the diagonal (diagonal tiles) or below
+  // the last row skip their DMMAs (warp-uniform; their outputs are never stored)
+  const bool wact = (i0 + wm * 16 + 15 >= c0 + wn * 16) && (i0 + wm * 16 < M) && (c0 + wn * 16 < N);
   for (int kc = 0; kc < nk; ++kc) {
     cp_async_wait<1>();
     __syncthreads();
     if (kc + 2 < nk) load((kc + 2) % 3, kc + 2);
     cp_async_commit();
+    if (!wact) continue;
     const cplx* as = As + (kc % 3) * S32_STAGE + t * S32_LD + wm * 16 + g;
     const cplx* bs = Bs + (kc % 3) * S32_STAGE + t * S32_LD + wn * 16 + g;
 #pragma unroll
