@@ -702,6 +702,7 @@ __global__ void __launch_bounds__(NT, 2) syrk_gather_kernel(LevelArgs a, const i
 // unit = 1: unit-L LDL^T fronts (z already D^{-1}-scaled); 0: C C^T fronts.
 template <int NR>
 __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int unit) {
+  constexpr int RB = NR < 4 ? NR : 4;   // right-hand sides per register chunk
   __shared__ cplx l11[NB * LDD];   // l11[c * LDD + i] = L[kb+i][kb+c], i > c; diagonal: 1/L[c][c] (or 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int inst = blockIdx.x;
@@ -721,29 +722,33 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int uni
     xs[q] = ldc(Zk + (i < p ? F.pbeg + i : bidx[i - p]) + (int64_t)r * nx);
   }
   __syncthreads();
-  // 2. boundary contributions of all pivot columns (parallel over columns)
+  // 2. boundary contributions of all pivot columns (parallel over columns); the right-hand
+  // sides in register chunks of RB (the column is re-read from L1 per chunk) so many-RHS
+  // solves keep the register count -- and the occupancy -- of the few-RHS ones
   if (n > p) {
     for (int j = warp; j < p; j += NT / 32) {
-      cplx acc[NR];
-#pragma unroll
-      for (int r = 0; r < NR; ++r) acc[r] = zero;
       const cplx* col = P + (int64_t)j * n;
-      for (int i = p + lane; i < n; i += 32) {
-        const cplx l = ldc(col + i);
+      for (int r0 = 0; r0 < nrhs; r0 += RB) {
+        cplx acc[RB];
 #pragma unroll
-        for (int r = 0; r < NR; ++r)
-          if (r < nrhs) acc[r] = cfma(l, xs[i * nrhs + r], acc[r]);
-      }
+        for (int r = 0; r < RB; ++r) acc[r] = zero;
+        for (int i = p + lane; i < n; i += 32) {
+          const cplx l = ldc(col + i);
 #pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        if (r >= nrhs) break;
-        double re = acc[r].re, im = acc[r].im;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          re += __shfl_xor_sync(0xffffffffu, re, o);
-          im += __shfl_xor_sync(0xffffffffu, im, o);
+          for (int r = 0; r < RB; ++r)
+            if (r0 + r < nrhs) acc[r] = cfma(l, xs[i * nrhs + r0 + r], acc[r]);
         }
-        if (lane == 0) xs[j * nrhs + r] = cmk(xs[j * nrhs + r].re - re, xs[j * nrhs + r].im - im);
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          if (r0 + r >= nrhs) break;
+          double re = acc[r].re, im = acc[r].im;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            re += __shfl_xor_sync(0xffffffffu, re, o);
+            im += __shfl_xor_sync(0xffffffffu, im, o);
+          }
+          if (lane == 0) xs[j * nrhs + r0 + r] = cmk(xs[j * nrhs + r0 + r].re - re, xs[j * nrhs + r0 + r].im - im);
+        }
       }
     }
     __syncthreads();
@@ -753,28 +758,30 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int uni
     const int w = min(NB, p - kb);
     if (kb + w < p) {
       for (int j = warp; j < w; j += NT / 32) {
-        cplx acc[NR];
-#pragma unroll
-        for (int r = 0; r < NR; ++r) acc[r] = zero;
         const cplx* col = P + (int64_t)(kb + j) * n;
-        for (int i = kb + w + lane; i < p; i += 32) {
-          const cplx l = ldc(col + i);
+        for (int r0 = 0; r0 < nrhs; r0 += RB) {
+          cplx acc[RB];
 #pragma unroll
-          for (int r = 0; r < NR; ++r)
-            if (r < nrhs) acc[r] = cfma(l, xs[i * nrhs + r], acc[r]);
-        }
+          for (int r = 0; r < RB; ++r) acc[r] = zero;
+          for (int i = kb + w + lane; i < p; i += 32) {
+            const cplx l = ldc(col + i);
 #pragma unroll
-        for (int r = 0; r < NR; ++r) {
-          if (r >= nrhs) break;
-          double re = acc[r].re, im = acc[r].im;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            re += __shfl_xor_sync(0xffffffffu, re, o);
-            im += __shfl_xor_sync(0xffffffffu, im, o);
+            for (int r = 0; r < RB; ++r)
+              if (r0 + r < nrhs) acc[r] = cfma(l, xs[i * nrhs + r0 + r], acc[r]);
           }
-          if (lane == 0) {
-            cplx* t = xs + (kb + j) * nrhs + r;
-            *t = cmk(t->re - re, t->im - im);
+#pragma unroll
+          for (int r = 0; r < RB; ++r) {
+            if (r0 + r >= nrhs) break;
+            double re = acc[r].re, im = acc[r].im;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              re += __shfl_xor_sync(0xffffffffu, re, o);
+              im += __shfl_xor_sync(0xffffffffu, im, o);
+            }
+            if (lane == 0) {
+              cplx* t = xs + (kb + j) * nrhs + r0 + r;
+              *t = cmk(t->re - re, t->im - im);
+            }
           }
         }
       }
