@@ -151,8 +151,17 @@ __global__ void __launch_bounds__(256) diag_kernel(LevelArgs a, int kb) {
   const int64_t shift = a.shift0 + k;
   const cplx zero = cmk(0.0, 0.0);
   if (warp == 0) {
-    for (int c = 0; c < w; ++c)
-      if (lane >= c && lane < w) Ld[c * LDD + lane] = ldc(P + (kb + lane) + (int64_t)(kb + c) * n);
+    {
+      // all of the lane's (row's) loads in flight at once, then staged: one global latency
+      // per instance instead of one per column
+      cplx v[NB];
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        v[c] = (c < w && lane >= c && lane < w) ? ldc(P + (kb + lane) + (int64_t)(kb + c) * n) : zero;
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        if (c < w && lane >= c && lane < w) Ld[c * LDD + lane] = v[c];
+    }
     __syncwarp();
     // step j: a_ic -= (a_ij / d_j) a_cj on unscaled values; then columns scale by 1/c_j = d_j^{-1/2}
     for (int j = 0; j < w; ++j) {
