@@ -1320,7 +1320,10 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
         ++nlaunch;
         fam(FAM_ASM, st);
         for (int kb = 0; kb < pmax; kb += NB) {
-          diag_kernel<<<ninst, 32 * std::min(8, nrhs), 0, st>>>(a, kb);
+          if (nrhs == 1)
+            diag_kernel<true><<<ninst, 32, 0, st>>>(a, kb);
+          else
+            diag_kernel<false><<<ninst, 32 * std::min(8, nrhs), 0, st>>>(a, kb);
           STFEM_LAUNCH_CHECK("diag_kernel");
           fam(FAM_DIAG, st);
           const dim3 tg(ninst, (unsigned)std::max(1, (nmax - kb + TR_ROWS - 1) / TR_ROWS));

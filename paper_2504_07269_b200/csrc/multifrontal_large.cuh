@@ -135,8 +135,20 @@ __global__ void __launch_bounds__(NT, 4) asm_front_kernel(LevelArgs a) {
 // w x w diagonal block of panel kb, one CTA per instance: warp 0 factors it
 // (lane = row), then every warp forward-solves its share of the RHS
 // (blockDim = 32 * min(8, nrhs))
+// packed lower triangle of the w x w block (column-major): element (row r, column c), r >= c
+__device__ __forceinline__ int lp(int c, int r) { return c * (2 * NB - c + 1) / 2 + r - c; }
+constexpr int LP_SIZE = NB * (NB + 1) / 2;
+
+// PACK (one-warp CTAs, nrhs == 1): packed triangle, 8.4 KB instead of 17 KB of shared memory
+// per instance -- those CTAs are shared-memory limited, so twice as many resident instances
+// per SM.  Multi-RHS CTAs (up to 8 warps) are thread limited; they keep the padded square,
+// whose constant column stride keeps integer work off the serial factorization chain.
+template <bool PACK>
+__device__ __forceinline__ int dix(int c, int r) { return PACK ? lp(c, r) : c * LDD + r; }
+
+template <bool PACK>
 __global__ void __launch_bounds__(256) diag_kernel(LevelArgs a, int kb) {
-  __shared__ cplx Ld[NB * LDD];
+  __shared__ cplx Ld[PACK ? LP_SIZE : NB * LDD];
   __shared__ cplx dinv_s[NB], cdg[NB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int inst = blockIdx.x;
@@ -160,32 +172,37 @@ __global__ void __launch_bounds__(256) diag_kernel(LevelArgs a, int kb) {
         v[c] = (c < w && lane >= c && lane < w) ? ldc(P + (kb + lane) + (int64_t)(kb + c) * n) : zero;
 #pragma unroll
       for (int c = 0; c < NB; ++c)
-        if (c < w && lane >= c && lane < w) Ld[c * LDD + lane] = v[c];
+        if (c < w && lane >= c && lane < w) Ld[dix<PACK>(c, lane)] = v[c];
     }
     __syncwarp();
     // step j: a_ic -= (a_ij / d_j) a_cj on unscaled values; then columns scale by 1/c_j = d_j^{-1/2}
     for (int j = 0; j < w; ++j) {
-      const cplx d = Ld[j * LDD + j];
+      const cplx d = Ld[dix<PACK>(j, j)];
       if (lane > j && lane < w) {
-        const cplx f = cmul(Ld[j * LDD + lane], crecip_fast(d));
-        cplx* __restrict__ rowp = Ld + lane;
-        const cplx* __restrict__ colj = Ld + j * LDD;
+        const cplx f = cmul(Ld[dix<PACK>(j, lane)], crecip_fast(d));
+        const cplx* __restrict__ colj = Ld + dix<PACK>(j, 0);   // colj[c] = (row c, column j), c >= j
         int c = j + 1;
+        int o = dix<PACK>(c, lane);                       // (row lane, column c)
         for (; c + 3 <= lane; c += 4) {
-          const cplx x0 = rowp[c * LDD], x1 = rowp[(c + 1) * LDD], x2 = rowp[(c + 2) * LDD],
-                     x3 = rowp[(c + 3) * LDD];
+          const int o1 = PACK ? o + NB - 1 - c : o + LDD, o2 = PACK ? o1 + NB - 2 - c : o1 + LDD,
+                    o3 = PACK ? o2 + NB - 3 - c : o2 + LDD;
+          const cplx x0 = Ld[o], x1 = Ld[o1], x2 = Ld[o2], x3 = Ld[o3];
           const cplx y0 = colj[c], y1 = colj[c + 1], y2 = colj[c + 2], y3 = colj[c + 3];
-          rowp[c * LDD] = cfms(x0, f, y0);
-          rowp[(c + 1) * LDD] = cfms(x1, f, y1);
-          rowp[(c + 2) * LDD] = cfms(x2, f, y2);
-          rowp[(c + 3) * LDD] = cfms(x3, f, y3);
+          Ld[o] = cfms(x0, f, y0);
+          Ld[o1] = cfms(x1, f, y1);
+          Ld[o2] = cfms(x2, f, y2);
+          Ld[o3] = cfms(x3, f, y3);
+          o = PACK ? o3 + NB - 4 - c : o3 + LDD;
         }
-        for (; c <= lane; ++c) rowp[c * LDD] = cfms(rowp[c * LDD], f, colj[c]);
+        for (; c <= lane; ++c) {
+          Ld[o] = cfms(Ld[o], f, colj[c]);
+          o += PACK ? NB - 1 - c : LDD;
+        }
       }
       __syncwarp();
     }
     if (lane < w) {
-      const cplx d = Ld[lane * LDD + lane];
+      const cplx d = Ld[dix<PACK>(lane, lane)];
       const double m2 = cabs2(d);
       if (!(m2 > 1e-300) || !isfinite(m2)) atomicCAS(a.err, 0, (int)shift + 1);
       const cplx c = csqrt_(d);
@@ -194,12 +211,12 @@ __global__ void __launch_bounds__(256) diag_kernel(LevelArgs a, int kb) {
     }
     __syncwarp();
     for (int j = 0; j < w; ++j) {
-      if (lane == j) Ld[j * LDD + j] = cdg[j];
-      else if (lane > j && lane < w) Ld[j * LDD + lane] = cmul(Ld[j * LDD + lane], dinv_s[j]);
+      if (lane == j) Ld[dix<PACK>(j, j)] = cdg[j];
+      else if (lane > j && lane < w) Ld[dix<PACK>(j, lane)] = cmul(Ld[dix<PACK>(j, lane)], dinv_s[j]);
     }
     __syncwarp();
     for (int c = 0; c < w; ++c)
-      if (lane >= c && lane < w) stc(P + (kb + lane) + (int64_t)(kb + c) * n, Ld[c * LDD + lane]);
+      if (lane >= c && lane < w) stc(P + (kb + lane) + (int64_t)(kb + c) * n, Ld[dix<PACK>(c, lane)]);
   }
   __syncthreads();
   // y = C11^{-1} r in column (axpy) form: lane i holds r_i; once y_j is final it
@@ -210,7 +227,7 @@ __global__ void __launch_bounds__(256) diag_kernel(LevelArgs a, int kb) {
     for (int j = 0; j < w; ++j) {
       if (lane == j) yl = cmul(yl, dinv_s[j]);
       const cplx yj = cmk(__shfl_sync(0xffffffffu, yl.re, j), __shfl_sync(0xffffffffu, yl.im, j));
-      if (lane > j && lane < w) yl = cfms(yl, Ld[j * LDD + lane], yj);
+      if (lane > j && lane < w) yl = cfms(yl, Ld[dix<PACK>(j, lane)], yj);
     }
     if (lane < w) stc(z + lane, yl);
   }
