@@ -297,13 +297,23 @@ __global__ void __launch_bounds__(TR_ROWS, 8) trsm_kernel(LevelArgs a, int kb) {
 #pragma unroll
     for (int c = 0; c < WB; ++c)
       if (jb + c < w) stc(prow + (int64_t)(jb + c) * n, x[c]);
-    for (int r = 0; r < nrhs; ++r) {
-      cplx* dst = (i < p) ? Zk + F.pbeg + i + (int64_t)r * nx
-                          : a.rcur + ((int64_t)k * a.rcur_stride + F.rofs) * nrhs + (i - p) + (int64_t)r * b;
+    if (nrhs == 1) {
+      cplx* dst = (i < p) ? Zk + F.pbeg + i : a.rcur + ((int64_t)k * a.rcur_stride + F.rofs) + (i - p);
       cplx acc = ldc(dst);
 #pragma unroll
-      for (int c = 0; c < WB; ++c) acc = cfms(acc, x[c], ys[(jb + c) * MAXR + r]);
+      for (int c = 0; c < WB; ++c) acc = cfms(acc, x[c], ys[(jb + c) * MAXR]);
       stc(dst, acc);
+    } else {
+      // (measured: one update per RHS after the whole panel, x re-read from L1, is slower)
+      cplx* dst0 = (i < p) ? Zk + F.pbeg + i : a.rcur + ((int64_t)k * a.rcur_stride + F.rofs) * nrhs + (i - p);
+      const int64_t rs = (i < p) ? (int64_t)nx : (int64_t)b;
+#pragma unroll 4
+      for (int r = 0; r < nrhs; ++r) {
+        cplx acc = ldc(dst0 + r * rs);
+#pragma unroll
+        for (int c = 0; c < WB; ++c) acc = cfms(acc, x[c], ys[(jb + c) * MAXR + r]);
+        stc(dst0 + r * rs, acc);
+      }
     }
   }
 }
