@@ -2,16 +2,18 @@
 merged into profiles/ncu_traffic.json under "<workload>:<family>" (read by
 bench.py for roofline.traffic).
 
-    python tools/ncu_traffic.py gpurun_out/syrk_full.ncu-rep C4 syrk
+    python tools/ncu_traffic.py gpurun_out/syrk_full.ncu-rep C4 syrk [kernel-name regex]
 """
 import csv
 import io
 import json
 import os
+import re
 import subprocess
 import sys
 
 rep, workload, family = sys.argv[1:4]
+pat = re.compile(sys.argv[4]) if len(sys.argv) > 4 else None
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, data = rows[0], rows[1], rows[2:]
@@ -25,6 +27,8 @@ def val(r, name):
     return float(v) * scale
 
 
+if pat is not None:
+    data = [r for r in data if pat.search(r[col["Kernel Name"]])]
 tot_b, tot_ms = 0.0, 0.0
 for r in data:
     tot_b += val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum")
