@@ -78,6 +78,13 @@ class ClockSampler:
         for ln in self.proc.stdout:
             self.lines.append(ln.strip())
 
+    def wait_first(self, timeout=10.0):
+        """Block until nvidia-smi has produced its first sample: its NVML start-up stalls the
+        driver for a moment and must not land inside a short timed region (C2 steps are ~1 ms)."""
+        t0 = time.time()
+        while self.proc is not None and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.02)
+
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -288,6 +295,7 @@ def run_ours_bs(args):
     torch.cuda.synchronize()
     clk = ClockSampler(local)
     clk.start()
+    clk.wait_first()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for _ in range(args.steps):
@@ -350,6 +358,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     clk = ClockSampler(local)
     clk.start()
+    clk.wait_first()
     time.sleep(0.3)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()

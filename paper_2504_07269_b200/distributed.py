@@ -191,8 +191,6 @@ def bench_main(args):
     for _ in range(args.warmup):
         solver.solve(Fp, out)
     torch.cuda.synchronize()
-    dist.barrier()
-    torch.cuda.synchronize()
     clk = None
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -200,7 +198,11 @@ def bench_main(args):
         from bench import ClockSampler
         clk = ClockSampler(local)
         clk.start()
+        clk.wait_first()
         time.sleep(0.3)
+    # the barrier after the sampler start-up: no rank's timed region waits on rank 0's sampler
+    dist.barrier()
+    torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
     for _ in range(args.steps):
