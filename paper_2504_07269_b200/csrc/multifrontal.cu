@@ -1056,9 +1056,13 @@ int auto_batch(Plan& P, int nshift, int nrhs) {
   double budget = frac * (double)(fr + owned);
   int64_t per = bytes_per_shift(P, nrhs);
   int64_t bmax = std::min<int64_t>(std::max<int64_t>(1, (int64_t)(budget / (double)per)), 4096);
-  // equal-sized batches: fewer, evenly filled waves at the top levels of the tree
+  // equal-sized batches: fewer, evenly filled waves at the top levels of the tree; rounded up
+  // to a multiple of the spectral kernel's 64-shift column tile when that still fits (e.g. 1024
+  // shifts: 384 + 384 + 256 instead of 3 x 342, whose last spectral column tile is 22/64 full)
   const int64_t nb = (nshift + bmax - 1) / bmax;
-  return (int)((nshift + nb - 1) / nb);
+  const int64_t even = (nshift + nb - 1) / nb;
+  const int64_t r64 = ((even + 63) / 64) * 64;
+  return (int)((r64 <= bmax && (nshift + r64 - 1) / r64 == nb) ? r64 : even);
 }
 
 }  // namespace
