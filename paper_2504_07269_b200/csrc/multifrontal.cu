@@ -786,10 +786,23 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int uni
         }
       }
     }
-    for (int idx = tid; idx < w * w; idx += NT) {
-      const int i = idx % w, c = idx / w;
-      if (i > c) l11[c * LDD + i] = ldc(P + (kb + i) + (int64_t)(kb + c) * n);
-      else if (i == c) l11[c * LDD + c] = unit ? cmk(1.0, 0.0) : crecip(ldc(P + (kb + c) + (int64_t)(kb + c) * n));
+    {
+      // the block's loads issued together (compile-time trip count), then staged
+      constexpr int U = NB * NB / NT;
+      cplx v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int idx = tid + u * NT, i = idx % NB, c = idx / NB;
+        v[u] = (i < w && c < w && i >= c) ? ldc(P + (kb + i) + (int64_t)(kb + c) * n) : zero;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int idx = tid + u * NT, i = idx % NB, c = idx / NB;
+        if (i < w && c < w) {
+          if (i > c) l11[c * LDD + i] = v[u];
+          else if (i == c) l11[c * LDD + c] = unit ? cmk(1.0, 0.0) : crecip(v[u]);
+        }
+      }
     }
     __syncthreads();
     {
