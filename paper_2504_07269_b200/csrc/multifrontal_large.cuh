@@ -62,6 +62,19 @@ __global__ void __launch_bounds__(NT, 4) asm_front_kernel(LevelArgs a) {
   // original entries of pivot columns [cbeg, min(cstop, p)): one contiguous range of the sorted list
   const int* cp = a.ent_colptr + F.colptr_beg;
   const int ent_lo = cbeg < p ? cp[cbeg] : 0, ent_hi = cbeg < p ? cp[min(cstop, p)] : 0;
+  // the first EP original entries of this thread: their (value, destination) loads are issued
+  // now so their latency hides behind the gather below
+  constexpr int EP = 1;
+  double pm[EP], pa[EP];
+  int pd[EP];
+#pragma unroll
+  for (int u = 0; u < EP; ++u) {
+    const int e = ent_lo + tid + u * NT;
+    const bool ok = e < ent_hi;
+    pm[u] = ok ? a.Mv[F.ent_beg + e] : 0.0;
+    pa[u] = ok ? a.Av[F.ent_beg + e] : 0.0;
+    pd[u] = ok ? a.ent_dst[F.ent_beg + e] : -1;
+  }
   __syncthreads();
   // gather: warp w owns columns c0 + w + 8u (u < 4), lanes run down the rows
   constexpr int CU = 4, NW = NT / 32;
@@ -107,7 +120,14 @@ __global__ void __launch_bounds__(NT, 4) asm_front_kernel(LevelArgs a) {
     }
   }
   __syncthreads();
-  for (int e = ent_lo + tid; e < ent_hi; e += NT) {
+#pragma unroll
+  for (int u = 0; u < EP; ++u) {
+    if (pd[u] < 0) continue;
+    cplx* d = P + pd[u];
+    const cplx o = ldc(d);
+    stc(d, cmk(o.re + fma(lam.re, pa[u], pm[u]), o.im + lam.im * pa[u]));
+  }
+  for (int e = ent_lo + tid + EP * NT; e < ent_hi; e += NT) {
     const double mv = a.Mv[F.ent_beg + e], av = a.Av[F.ent_beg + e];   // entry-ordered values
     cplx* d = P + a.ent_dst[F.ent_beg + e];
     const cplx o = ldc(d);
