@@ -146,14 +146,50 @@ int stfem_plan_front_rows(const stfem_plan* plan, int64_t* offsets, int32_t* row
  * backward substitution level by level.  Mvals/Avals: device CSR values in
  * the plan's pattern (nnz_pattern).  lam: device c128[nshift].  G read, W
  * written (may not alias), both in `layout`.  Factors are transient (streamed
- * in batches of shifts, never kept: SURVEY.md §7 hard part 4).
+ * in batches of shifts, never kept: SURVEY.md §7 hard part 4).  Stream-ordered:
+ * see stfem_plan_check below for how a singular shift is reported.
  * ------------------------------------------------------------------------- */
 int stfem_factor_solve(stfem_plan* plan, const double* Mvals, const double* Avals,
                        const void* lam, int32_t nshift, int32_t nrhs,
                        const void* G, void* W, stfem_bv_layout layout,
                        void* stream);
-/* batch size in shifts (0 = auto from free memory); returns bytes per shift */
-int stfem_plan_set_batch(stfem_plan* plan, int32_t batch, int64_t* bytes_per_shift);
+/* stfem_factor_solve only enqueues work on `stream`: it does not wait for the
+ * GPU.  A pivot collapse met by its kernels (|pivot| <= pivot_tol
+ * * max_j |M_jj + lam A_jj| in the multifrontal fronts, |theta_k + lam| <=
+ * pivot_tol * (|theta_k| + |lam|) in a spectral subtree, or a non-finite
+ * pivot) is latched in the plan (first offender wins).  stfem_plan_check
+ * waits for the work issued so far on `stream`, clears the latch and returns
+ * STFEM_ERR_SINGULAR (stfem_last_error names the shift: base + index within
+ * the offending call) or STFEM_OK.  stfem_plan_set_shift_base sets the number
+ * added to the reported index by the following calls (the Bartels-Stewart
+ * sweep reports its sweep index l this way). */
+int stfem_plan_check(stfem_plan* plan, void* stream);
+int stfem_plan_set_shift_base(stfem_plan* plan, int32_t base);
+/* Allocate the numeric workspace for calls of up to `nshift` shifts and `nrhs`
+ * right-hand sides now (the batch size is fixed here: equal batches from
+ * workspace_fraction of the free memory, or stfem_plan_set_batch), so that
+ * later stfem_factor_solve calls never allocate.  Without it the first call
+ * (and any call that needs more than is reserved) allocates, which
+ * synchronises the device once. */
+int stfem_plan_reserve(stfem_plan* plan, int32_t nshift, int32_t nrhs);
+/* Tuning knobs of one plan (no environment variables).  get -> modify -> set;
+ * set rebuilds the device tables on the next call. */
+typedef struct {
+  int32_t small_front_n;     /* levels whose largest front has order <= this run on the shared-memory
+                                small-front kernel (unit-L LDL^T); 0 = every front on the tile-parallel
+                                large-front pipeline.  Default 100 */
+  int32_t fused_min_p;       /* levels with >= this many pivots fuse the children's extend-add into the
+                                Schur-update tiles (U never assembled).  Default 50 */
+  int32_t panel_group;       /* trailing pivot-column updates are delayed over this many 32-wide panels.
+                                Default 2 */
+  int32_t asm_whole_n;       /* fronts of order <= this are assembled by one CTA.  Default INT32_MAX */
+  int32_t syrk_block16;      /* 1: short-K Schur updates (p <= 32, b <= 208) on 16 x 16 blocks.  Default 1 */
+  int32_t level_timing;      /* 1: print per-launch CUDA-event times to stderr (diagnostics) */
+  double workspace_fraction; /* share of the free device memory the numeric workspace may take.  Default 0.70 */
+  double pivot_tol;          /* relative pivot-collapse threshold (see stfem_plan_check).  Default 1e-10 */
+} stfem_plan_options;
+int stfem_plan_get_options(const stfem_plan* plan, stfem_plan_options* out);
+int stfem_plan_set_options(stfem_plan* plan, const stfem_plan_options* opt);
 /* per-level accounting: record CUDA-event times of every level launch on the
  * next calls (on != 0); report ms[2*(depth+1)] (factor launches by depth, then
  * backward launches by depth, summed over shift batches), the algorithmic

@@ -15,6 +15,28 @@ def _c128(t: torch.Tensor, name: str):
     N.require_cuda(t)
 
 
+def _span(t: torch.Tensor):
+    """[first, last] byte addresses touched by a (possibly strided) tensor."""
+    if t.numel() == 0:
+        return (0, -1)
+    last = sum((n - 1) * st for n, st in zip(t.shape, t.stride()))
+    return (t.data_ptr(), t.data_ptr() + (last + 1) * t.element_size() - 1)
+
+
+def _no_alias(a: torch.Tensor, b: torch.Tensor):
+    """Every output row depends on all input rows and CTAs write as they go, so in == out (or
+    overlapping views) would be a read-after-write race across CTAs.  Column blocks of one
+    buffer interleave without sharing bytes: those are compared exactly."""
+    (a0, a1), (b0, b1) = _span(a), _span(b)
+    if a1 < b0 or b1 < a0:
+        return
+    if a.stride() == b.stride() and a.shape == b.shape and a.stride(-2) >= a.shape[-1]:
+        off = abs(a0 - b0) // a.element_size() % a.stride(-2)
+        if off >= a.shape[-1] and a.stride(-2) - off >= a.shape[-1]:
+            return   # disjoint column blocks of the same row-major buffer
+    raise ValueError("transform: input and output overlap (in-place transforms are not supported)")
+
+
 def time_transform(T: torch.Tensor, v: torch.Tensor, out: torch.Tensor | None = None,
                    stream=None) -> torch.Tensor:
     """out[..., l, :] = sum_k T[l, k] v[..., k, :] on the DMMA kernel (K3).
@@ -37,6 +59,7 @@ def time_transform(T: torch.Tensor, v: torch.Tensor, out: torch.Tensor | None = 
     if ob.stride(-1) != 1 or ob.shape != vb.shape:
         raise N.DimensionMismatch(N.ERR_DIM, "transform: bad output tensor")
     B, _, ncols = vb.shape
+    _no_alias(vb, ob)
     N.check(N.lib().stfem_time_transform(
         N.ptr(T), nt, N.ptr(vb), vb.stride(-2), N.ptr(ob), ob.stride(-2), ncols, B,
         vb.stride(0) if B > 1 else 0, ob.stride(0) if B > 1 else 0, N.stream_ptr(stream)))
@@ -59,6 +82,7 @@ def transform_pair_fwd(pairs, v: torch.Tensor, out: torch.Tensor | None = None, 
     if ob.stride(-1) != 1 or ob.shape != vb.shape:
         raise N.DimensionMismatch(N.ERR_DIM, "transform: bad output tensor")
     B, _, ncols = vb.shape
+    _no_alias(vb, ob)
     N.check(N.lib().stfem_transform_pair_fwd(
         N.ptr(pairs.A_fwd), pairs.mrows_fwd, nt, N.ptr(pairs.rows_fwd), N.ptr(pairs.scale_fwd),
         pairs.rows_fwd.shape[0], N.ptr(vb), vb.stride(-2), N.ptr(ob), ob.stride(-2), ncols, B,
@@ -82,6 +106,7 @@ def transform_pair_back(pairs, w: torch.Tensor, out: torch.Tensor | None = None,
     if ob.stride(-1) != 1 or ob.shape != wb.shape:
         raise N.DimensionMismatch(N.ERR_DIM, "transform: bad output tensor")
     B, _, ncols = wb.shape
+    _no_alias(wb, ob)
     N.check(N.lib().stfem_transform_pair_back(
         N.ptr(pairs.A_back), nt, N.ptr(pairs.mix_rows), N.ptr(pairs.mix_coef), pairs.mix_rows.shape[0],
         N.ptr(wb), wb.stride(-2), N.ptr(ob), ob.stride(-2), ncols, B,

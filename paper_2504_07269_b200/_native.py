@@ -48,6 +48,13 @@ class plan_stats(C.Structure):
                 ("nnz_pattern", C.c_int64)]
 
 
+class plan_options(C.Structure):
+    """stfem_plan_options (include/stfem_b200.h): tuning knobs of one plan."""
+    _fields_ = [("small_front_n", C.c_int32), ("fused_min_p", C.c_int32), ("panel_group", C.c_int32),
+                ("asm_whole_n", C.c_int32), ("syrk_block16", C.c_int32), ("level_timing", C.c_int32),
+                ("workspace_fraction", C.c_double), ("pivot_tol", C.c_double)]
+
+
 _lib = None
 
 
@@ -81,6 +88,11 @@ def _declare(lib):
         "stfem_plan_spectral_stats": (C.c_int, [P, C.POINTER(I32), C.POINTER(D), C.POINTER(D),
                                                 C.POINTER(I64)]),
         "stfem_factor_solve": (C.c_int, [P, P, P, P, I32, I32, P, P, bv_layout, P]),
+        "stfem_plan_check": (C.c_int, [P, P]),
+        "stfem_plan_set_shift_base": (C.c_int, [P, I32]),
+        "stfem_plan_reserve": (C.c_int, [P, I32, I32]),
+        "stfem_plan_get_options": (C.c_int, [P, C.POINTER(plan_options)]),
+        "stfem_plan_set_options": (C.c_int, [P, C.POINTER(plan_options)]),
         "stfem_asm_create": (C.c_int, [I32, I32, P, I32, P, P, C.POINTER(P)]),
         "stfem_asm_destroy": (C.c_int, [P]),
         "stfem_asm_pattern": (C.c_int, [P, C.POINTER(I32), C.POINTER(I64), P, P]),

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <atomic>
 #include <string>
 
 #include "../../include/stfem_b200.h"
@@ -24,6 +25,19 @@ int cuda_fail(cudaError_t e, const char* where);
     cudaError_t _e = cudaGetLastError();                              \
     if (_e != cudaSuccess) return ::stfem::cuda_fail(_e, where);      \
   } while (0)
+
+// Per-device "first use" latch for cudaFuncSetAttribute opt-ins: function attributes are per
+// device, so a process that moves to another GPU must set them again there.
+//   static DeviceOnce once;  if (once.first()) { cudaFuncSetAttribute(...); }
+struct DeviceOnce {
+  std::atomic<uint64_t> mask{0};
+  bool first() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return true;
+    const uint64_t bit = 1ull << dev;
+    return (mask.fetch_or(bit) & bit) == 0;
+  }
+};
 
 // ---- complex128 as double2 ------------------------------------------------
 struct __align__(16) cplx {

@@ -33,15 +33,15 @@
 namespace stfem {
 namespace {
 
+int upload(Plan& P);
+int ensure_workspace(Plan& P, int batch, int nrhs);
+int auto_batch(Plan& P, int nshift, int nrhs);
+
 constexpr int NT = 256;
 constexpr int NB = 32;            // panel width
-constexpr int TM = 64, TK = 16;   // GEMM tile: 64 x 64 complex, k-chunk 16
-constexpr int LDS = TM + 2;       // smem [k][m] row stride: (t*LDS + g) mod 8 distinct
 constexpr int LDD = NB + 1;       // diagonal block column stride
 constexpr int MAXR = 16;          // max RHS per call (bv chunks of 16 in the host loop)
 
-constexpr int GEMM_SMEM = (2 * 2 * TK * LDS + 2 * TK) * 16;
-constexpr int SYRK_SMEM = (3 * 2 * TK * LDS) * 16;   // 3-stage pipeline of the standalone Schur kernel
 constexpr int BWD_XS_MAX = 192 * 1024;   // backward_level_kernel: staged x (n x nrhs) per front
 constexpr int BWD_SPLIT_N = 256;         // backward: fronts above this order launch separately
 
@@ -72,8 +72,8 @@ struct LevelArgs {
   stfem_bv_layout lay;
   int32_t shift0;
   int* err;
-  unsigned long long* prof;   // optional per-phase cycle counters (STFEM_PHASE_PROF)
-  int split_syrk;             // Schur update of large fronts in syrk_level_kernel
+  int err_base;               // added to the shift index latched in err (stfem_plan_set_shift_base)
+  const double* scale2;       // per local shift: (pivot_tol * max_j |M_jj + lam A_jj|)^2, the pivot-collapse bound
   const int32_t* ent_colptr;  // per front (p + 1): first sorted original entry of each pivot column
   int unit_diag;              // backward: 1 = unit-L LDL^T fronts, 0 = C C^T fronts
   int asm_pivots_only;        // asm_front_kernel: pivot columns only (U assembled by syrk_gather_kernel)
@@ -85,13 +85,9 @@ __device__ __forceinline__ int64_t bv_off(const stfem_bv_layout& L, int r, int64
          j % L.chunk_cols;
 }
 
-// C[i + c*ldC] -= sum_k A[i + k*lda] * B[c + k*ldb],  i < M, c < N.
-// sym: only i >= c is written and only tiles ti >= tj are computed.
-// 8 warps = 2 (M) x 4 (N); warp tile 32 x 16 complex; mma.m16n8k4.f64.
-// STAGES-deep cp.async pipeline (2 inside the factor kernel, 3 in the SYRK kernel).
-// The accumulator tile starts from cinit(row, col) (default: C itself), so a
-// caller can assemble C on the fly (syrk_level_kernel gathers the children's
-// update blocks instead of reading a pre-assembled U).
+// Tile initialiser of the DMMA update kernels: the accumulators start from
+// cinit(row, col) -- C itself here, or the children's extend-add (Gather32) so a
+// caller can assemble C on the fly.
 struct CLoad {
   const cplx* C;
   int ldC;
@@ -100,249 +96,7 @@ struct CLoad {
   }
 };
 
-template <int STAGES, class CInit>
-__device__ void gemm_update(cplx* __restrict__ C, int ldC, int M, int N, const cplx* __restrict__ A,
-                            int lda, const cplx* __restrict__ B, int ldb, int K, bool sym, cplx* smem,
-                            int only_ti, int only_tj, const CInit& cinit) {
-  if (M <= 0 || N <= 0 || K <= 0) return;
-  cplx* As = smem;
-  cplx* Bs = smem + STAGES * TK * LDS;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3, wm = warp & 1, wn = warp >> 1;
-  const int tiles_m = (M + TM - 1) / TM, tiles_n = (N + TM - 1) / TM;
-  const int nk = (K + TK - 1) / TK;
-  // lower trapezoid (sym) or full rectangle of 64x64 tiles, one CTA walks them
-  // all (or only tile (only_ti, only_tj) when the caller distributes tiles)
-  for (int tj = (only_tj >= 0 ? only_tj : 0); tj < (only_tj >= 0 ? only_tj + 1 : tiles_n); ++tj)
-  for (int ti = (only_ti >= 0 ? only_ti : (sym ? tj : 0)); ti < (only_ti >= 0 ? only_ti + 1 : tiles_m); ++ti) {
-    const int i0 = ti * TM, c0 = tj * TM;
-
-    auto load = [&](int stage, int kc) {
-      const int k0 = kc * TK;
-      cplx* as = As + stage * TK * LDS;
-      cplx* bs = Bs + stage * TK * LDS;
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        int idx = tid + NT * r;
-        int m = idx & 63, k = idx >> 6;
-        bool okk = k0 + k < K;
-        bool oka = okk && (i0 + m < M);
-        bool okb = okk && (c0 + m < N);
-        cp_async16(as + k * LDS + m, oka ? A + (int64_t)(i0 + m) + (int64_t)(k0 + k) * lda : A, oka);
-        cp_async16(bs + k * LDS + m, okb ? B + (int64_t)(c0 + m) + (int64_t)(k0 + k) * ldb : B, okb);
-      }
-    };
-
-    // accumulators start as cinit(row, col) (loads issued together with the
-    // first cp.async stages so their latency overlaps); the MMAs subtract A B^T
-    double cre[2][2][4], cim[2][2][4];
-#pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
-      if (s < nk) load(s, s);
-      cp_async_commit();
-    }
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int v = 0; v < 2; ++v) {
-            const int row = i0 + wm * 32 + mi * 16 + g + 8 * h;
-            const int col = c0 + wn * 16 + ni * 8 + 2 * t + v;
-            cplx o = cmk(0.0, 0.0);
-            if (row < M && col < N && (!sym || row >= col)) o = cinit(row, col);
-            cre[mi][ni][2 * h + v] = o.re;
-            cim[mi][ni][2 * h + v] = o.im;
-          }
-    for (int kc = 0; kc < nk; ++kc) {
-      cp_async_wait<STAGES - 2>();
-      __syncthreads();   // stage kc landed for everyone; stage (kc-1) % STAGES is free
-      {
-        const int nxt = kc + STAGES - 1;
-        if (nxt < nk) load(nxt % STAGES, nxt);
-        cp_async_commit();
-      }
-      const cplx* as = As + (kc % STAGES) * TK * LDS + t * LDS + wm * 32 + g;
-      const cplx* bs = Bs + (kc % STAGES) * TK * LDS + t * LDS + wn * 16 + g;
-#pragma unroll
-      for (int kk = 0; kk < TK; kk += 4) {
-        cplx a[2][2], b[2];
-#pragma unroll
-        for (int mi = 0; mi < 2; ++mi) {
-          a[mi][0] = ldc(as + kk * LDS + mi * 16);
-          a[mi][1] = ldc(as + kk * LDS + mi * 16 + 8);
-        }
-#pragma unroll
-        for (int ni = 0; ni < 2; ++ni) b[ni] = ldc(bs + kk * LDS + ni * 8);
-#pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < 2; ++ni) {
-            // C -= A B:  Cre += (-Are) Bre + Aim Bim ;  Cim += (-Are) Bim + (-Aim) Bre
-            dmma_16x8x4(cre[mi][ni], -a[mi][0].re, -a[mi][1].re, b[ni].re);
-            dmma_16x8x4(cre[mi][ni], a[mi][0].im, a[mi][1].im, b[ni].im);
-            dmma_16x8x4(cim[mi][ni], -a[mi][0].re, -a[mi][1].re, b[ni].im);
-            dmma_16x8x4(cim[mi][ni], -a[mi][0].im, -a[mi][1].im, b[ni].re);
-          }
-      }
-    }
-    cp_async_wait<0>();
-    __syncthreads();   // all warps done with the stages before the next tile refills them
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int v = 0; v < 2; ++v) {
-            const int row = i0 + wm * 32 + mi * 16 + g + 8 * h;
-            const int col = c0 + wn * 16 + ni * 8 + 2 * t + v;
-            if (row < M && col < N && (!sym || row >= col))
-              stc(C + (int64_t)row + (int64_t)col * ldC, cmk(cre[mi][ni][2 * h + v], cim[mi][ni][2 * h + v]));
-          }
-  }
-  __syncthreads();
-}
-
-#define STFEM_PROF_MARK(slot)                                                            \
-  do {                                                                                   \
-    if (a.prof && threadIdx.x == 0) {                                                    \
-      const long long t_now = clock64();                                                 \
-      atomicAdd(a.prof + (slot), (unsigned long long)(t_now - t_prev));                  \
-      t_prev = t_now;                                                                    \
-    }                                                                                    \
-  } while (0)
-
 #include "multifrontal_large.cuh"
-
-// Schur update U = F22 - L21 L21^T of the large fronts of one level, one CTA
-// per (lower 64x64 tile, shift): a plain batched DMMA GEMM with K = p, so the
-// dominant flops of the top levels run fully parallel (no per-instance
-// serialisation, no wave quantisation on a handful of huge fronts).
-// tiles[t] = (front, ti, tj, 0) for the level's fronts.
-__global__ void __launch_bounds__(NT, 2) syrk_level_kernel(LevelArgs a, const int4* __restrict__ tiles) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  cplx* gsm = reinterpret_cast<cplx*>(smem_raw);
-  const int k = blockIdx.x % a.nbatch;
-  const int4 tl = tiles[blockIdx.x / a.nbatch];
-  const FrontDev F = a.fronts[tl.x];
-  const int n = F.n, p = F.p, b = n - p;
-  cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
-  cplx* U = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
-  gemm_update<3>(U, b, b, b, P + p, n, P + p, n, p, true, gsm, tl.y, tl.z, CLoad{U, b});
-}
-
-// Short-K Schur update (levels with p <= KMAX <= 32 pivots, memory bound; used
-// for p <= 16 by default: C4 depth 9 11.1 -> 10.2 ms per batch, while at p = 31
-// (depths 7-8, 2 CTAs of 85 KB per SM) it lost to gemm_update, 10.7 -> 12.5 ms).  One 32 x 64 half of a 64 x 64 lower tile per CTA of 128
-// threads: the C block (F22), A (its 32 rows of L21) and B (64 rows of L21),
-// all K columns, are requested at once with 16-byte cp.async -- no registers
-// held, ~60-85 KB in flight per CTA, 2-3 CTAs per SM -- then DMMA from shared
-// memory and one store pass.  The register-staged C init of gemm_update caps
-// the in-flight bytes at the register file instead.
-template <int KMAX>
-struct SyrkShort {
-  static constexpr int M = 32, N = 64, LDC = M + 1, LDA = M + 2, LDB = N + 2;
-  static constexpr int SMEM = (N * LDC + KMAX * LDA + KMAX * LDB) * 16;
-};
-
-template <int KMAX>
-__global__ void __launch_bounds__(128) syrk_short_kernel(LevelArgs a, const int4* __restrict__ tiles) {
-  using S = SyrkShort<KMAX>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  cplx* Cs = reinterpret_cast<cplx*>(smem_raw);   // Cs[col * LDC + row]
-  cplx* As = Cs + S::N * S::LDC;                   // As[k * LDA + row]
-  cplx* Bs = As + KMAX * S::LDA;                   // Bs[k * LDB + col]
-  const int k = blockIdx.x % a.nbatch;
-  const int half = (blockIdx.x / a.nbatch) & 1;
-  const int4 tl = tiles[blockIdx.x / a.nbatch / 2];
-  const FrontDev F = a.fronts[tl.x];
-  const int n = F.n, p = F.p, b = n - p;
-  const int i0 = tl.y * TM + half * S::M, c0 = tl.z * TM;
-  if (i0 >= b) return;
-  const cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
-  cplx* U = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
-  const int tid = threadIdx.x;
-  // C block: lower entries only (zero-filled elsewhere), rows contiguous per column
-  for (int idx = tid; idx < S::M * S::N; idx += 128) {
-    const int r = idx % S::M, c = idx / S::M;
-    const int row = i0 + r, col = c0 + c;
-    const bool ok = row < b && col < b && row >= col;
-    cp_async16(Cs + c * S::LDC + r, ok ? U + row + (int64_t)col * b : U, ok);
-  }
-  for (int idx = tid; idx < S::M * KMAX; idx += 128) {
-    const int r = idx % S::M, kk = idx / S::M;
-    const bool ok = i0 + r < b && kk < p;
-    cp_async16(As + kk * S::LDA + r, ok ? P + p + i0 + r + (int64_t)kk * n : P, ok);
-  }
-  for (int idx = tid; idx < S::N * KMAX; idx += 128) {
-    const int c = idx % S::N, kk = idx / S::N;
-    const bool ok = c0 + c < b && kk < p;
-    cp_async16(Bs + kk * S::LDB + c, ok ? P + p + c0 + c + (int64_t)kk * n : P, ok);
-  }
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
-  const int lane = tid & 31, wn = tid >> 5, g = lane >> 2, t = lane & 3;
-  double cre[2][2][4], cim[2][2][4];
-#pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          const cplx o = Cs[(wn * 16 + ni * 8 + 2 * t + v) * S::LDC + mi * 16 + g + 8 * h];
-          cre[mi][ni][2 * h + v] = o.re;
-          cim[mi][ni][2 * h + v] = o.im;
-        }
-  bool live[2][2];   // fragments outside the block or above the diagonal skip their DMMAs
-#pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < 2; ++ni) {
-      const int r_lo = i0 + mi * 16, c_lo = c0 + wn * 16 + ni * 8;
-      live[mi][ni] = r_lo < b && c_lo < b && r_lo + 15 >= c_lo;
-    }
-  const int kmax = min(p, KMAX);
-  for (int kk = 0; kk < kmax; kk += 4) {
-    cplx av[2][2], bv[2];
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi) {
-      av[mi][0] = As[(kk + t) * S::LDA + mi * 16 + g];
-      av[mi][1] = As[(kk + t) * S::LDA + mi * 16 + g + 8];
-    }
-#pragma unroll
-    for (int ni = 0; ni < 2; ++ni) bv[ni] = Bs[(kk + t) * S::LDB + wn * 16 + ni * 8 + g];
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < 2; ++ni) {
-        if (!live[mi][ni]) continue;
-        dmma_16x8x4(cre[mi][ni], -av[mi][0].re, -av[mi][1].re, bv[ni].re);
-        dmma_16x8x4(cre[mi][ni], av[mi][0].im, av[mi][1].im, bv[ni].im);
-        dmma_16x8x4(cim[mi][ni], -av[mi][0].re, -av[mi][1].re, bv[ni].im);
-        dmma_16x8x4(cim[mi][ni], -av[mi][0].im, -av[mi][1].im, bv[ni].re);
-      }
-  }
-#pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          const int row = i0 + mi * 16 + g + 8 * h;
-          const int col = c0 + wn * 16 + ni * 8 + 2 * t + v;
-          if (row < b && col < b && row >= col)
-            stc(U + row + (int64_t)col * b, cmk(cre[mi][ni][2 * h + v], cim[mi][ni][2 * h + v]));
-        }
-}
 
 // Short-K Schur update at 16 x 16 granularity (levels with p <= 32 pivots and
 // b <= 208 boundary rows: C4 depths 7-9).  There the 64 x 64 tiles are mostly
@@ -629,68 +383,6 @@ __global__ void __launch_bounds__(128, 4) panel_update32_kernel(LevelArgs a, int
   sym_tile32(C, n, n - cb, cols, P + cb + (int64_t)k0 * n, n, kk, ti * 32, tj * 32, As, Bs, CLoad{C, n});
 }
 
-// Tile initialiser of the fused Schur update: the extend-add of the (at most
-// two) children's update blocks, gathered straight into the accumulators
-// through the inverse relpos maps of the tile's 64 rows and 64 columns
-// (staged in shared memory).  Same sum order as asm_front_kernel (0 + c0 + c1).
-struct GatherInit {
-  const int* inv_r;   // [2][64] child boundary row of tile row r (-1: none)
-  const int* inv_c;   // [2][64] same for tile columns
-  const cplx* Uc[2];
-  int bc[2], nc, i0, c0;
-  __device__ __forceinline__ cplx operator()(int row, int col) const {
-    cplx v = cmk(0.0, 0.0);
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      if (s >= nc) break;
-      const int kr = inv_r[s * 64 + row - i0], kc = inv_c[s * 64 + col - c0];
-      if (kr >= 0 && kc >= 0) v = cadd(v, ldc(Uc[s] + (int64_t)kc * bc[s] + kr));
-    }
-    return v;
-  }
-};
-
-// Fused assembly + Schur update of the boundary block: U = sum_children
-// extend-add - L21 L21^T in one pass (asm_front_kernel then assembles only the
-// pivot columns).  Saves writing the assembled U and reading it back, i.e. two
-// of the four HBM passes over every update block.
-__global__ void __launch_bounds__(NT, 2) syrk_gather_kernel(LevelArgs a, const int4* __restrict__ tiles) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  cplx* gsm = reinterpret_cast<cplx*>(smem_raw);
-  int* inv_s = reinterpret_cast<int*>(smem_raw + SYRK_SMEM);   // [2][64] rows, [2][64] cols
-  const int k = blockIdx.x % a.nbatch;
-  const int4 tl = tiles[blockIdx.x / a.nbatch];
-  const FrontDev F = a.fronts[tl.x];
-  const int n = F.n, p = F.p, b = n - p;
-  const int i0 = tl.y * TM, c0 = tl.z * TM;
-  const int nc = min(F.nchild, 2);
-  GatherInit gi;
-  gi.inv_r = inv_s;
-  gi.inv_c = inv_s + 128;
-  gi.nc = nc;
-  gi.i0 = i0;
-  gi.c0 = c0;
-  for (int q = threadIdx.x; q < 256; q += NT) {
-    const int s = (q >> 6) & 1, r = q & 63, isc = q >> 7;
-    const int fr = (isc ? c0 : i0) + r;
-    inv_s[q] = (s < nc && fr < b) ? a.inv[F.inv_beg + s * n + p + fr] : -1;
-  }
-#pragma unroll
-  for (int s = 0; s < 2; ++s) {
-    gi.Uc[s] = nullptr;
-    gi.bc[s] = 0;
-    if (s < nc) {
-      const FrontDev Cf = a.fronts[a.child_ids[F.child_beg + s]];
-      gi.bc[s] = Cf.n - Cf.p;
-      gi.Uc[s] = a.uchild + (int64_t)k * a.uchild_stride + Cf.uofs;
-    }
-  }
-  __syncthreads();
-  cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
-  cplx* U = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
-  gemm_update<3>(U, b, b, b, P + p, n, P + p, n, p, true, gsm, tl.y, tl.z, gi);
-}
-
 // Backward substitution of one level, one CTA per (front, shift) instance:
 //   1. x of the boundary rows (final: they belong to ancestors) is staged in
 //      shared memory together with z of the pivot rows;
@@ -830,13 +522,12 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int uni
 
 template <int NR>
 int launch_backward_level(const LevelArgs& a, int grid, int nmax, int unit, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static DeviceOnce attr_once;
+  if (attr_once.first()) {
     STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_level_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         BWD_XS_MAX));
     STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_level_kernel<NR>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                         100));
-    attr = true;
   }
   backward_level_kernel<NR><<<grid, NT, (size_t)nmax * a.nrhs * 16, s>>>(a, unit);
   STFEM_LAUNCH_CHECK("backward_level_kernel");
@@ -849,10 +540,8 @@ int launch_backward_level(const LevelArgs& a, int grid, int nmax, int unit, cuda
 // does depth d run on the shared-memory small-front kernels (unit-L LDL^T)?
 // (measured on C4: fronts of order ~110 factor faster on the large-front kernel,
 // while their backward pass stays on the shared-memory kernel)
-constexpr int SMALL_FACTOR_N = 100;
 bool level_is_small(const Plan& P, int d) {
-  const int lim = P.small_n_cap > 0 ? std::min(P.small_n_cap, SMALL_N) : SMALL_FACTOR_N;
-  return P.level_nmax[d] <= lim && !P.force_big;
+  return P.level_nmax[d] <= std::min<int>(P.opt.small_front_n, SMALL_N);
 }
 
 // largest boundary block b = n - p among the fronts of depth d
@@ -874,12 +563,57 @@ __global__ void gather_entries_kernel(const int32_t* __restrict__ src, const dou
   }
 }
 
+// Pivot-collapse scale of every shift of a batch: scale2[s] =
+// tol^2 * max_j |M_jj + lam_s A_jj|^2.  A pivot d with |d|^2 <= scale2[s] is
+// reported as numerically singular.  One CTA per shift; the diagonal values are
+// the same for every shift (L2 hits).
+__global__ void __launch_bounds__(256) pivot_scale_kernel(const int32_t* __restrict__ diag_src, int n,
+                                                          const double* __restrict__ Mv,
+                                                          const double* __restrict__ Av,
+                                                          const cplx* __restrict__ lam, double tol2,
+                                                          double* __restrict__ scale2) {
+  __shared__ double red[8];
+  const cplx l = lam[blockIdx.x];
+  double m = 0.0;
+  for (int j = threadIdx.x; j < n; j += 256) {
+    const int s = diag_src[j];
+    if (s < 0) continue;
+    const double re = fma(l.re, Av[s], Mv[s]), im = l.im * Av[s];
+    m = fmax(m, fma(re, re, im * im));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w = 1; w < 8; ++w) m = fmax(m, red[w]);
+    scale2[blockIdx.x] = tol2 * m;
+  }
+}
+
+// opt-in shared-memory sizes of this file's kernels, once per device (a second
+// device used by the same process needs its own opt-in)
+int set_kernel_attributes(int dev) {
+  static DeviceOnce once;
+  (void)dev;
+  if (!once.first()) return STFEM_OK;
+  STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk32_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, S32_SMEM));
+  STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk32_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, S32_SMEM));
+  STFEM_CUDA_TRY(cudaFuncSetAttribute(panel_update32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, S32_SMEM));
+  STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_block16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      b16_smem_bytes(B16_BMAX)));
+  return STFEM_OK;
+}
+
 int upload(Plan& P) {
   int dev;
   STFEM_CUDA_TRY(cudaGetDevice(&dev));
   if (P.d_fronts && P.device == dev) return STFEM_OK;
   P.free_device();
   P.device = dev;
+  int rc;
+  if ((rc = set_kernel_attributes(dev))) return rc;
   auto up = [&](auto** dptr, const auto& vec) -> int {
     using T = typename std::decay_t<decltype(vec)>::value_type;
     size_t bytes = std::max<size_t>(1, vec.size()) * sizeof(T);
@@ -911,7 +645,6 @@ int upload(Plan& P) {
     lv.insert(lv.end(), P.levels[d].begin(), P.levels[d].end());
   }
   P.level_off[P.levels.size()] = (int64_t)lv.size();
-  int rc;
   if ((rc = up(&P.d_fronts, P.fronts))) return rc;
   if ((rc = up(&P.d_levels, lv))) return rc;
   if ((rc = up(&P.d_child_ids, P.child_ids))) return rc;
@@ -924,10 +657,10 @@ int upload(Plan& P) {
   if ((rc = up(&P.d_ent_dst, P.ent_dst))) return rc;
   if ((rc = up(&P.d_ent_colptr, P.ent_colptr))) return rc;
   if ((rc = up(&P.d_perm, P.perm))) return rc;
+  if ((rc = up(&P.d_diag_src, P.diag_src))) return rc;
   STFEM_CUDA_TRY(cudaMalloc(&P.d_err, sizeof(int)));
   STFEM_CUDA_TRY(cudaMemset(P.d_err, 0, sizeof(int)));
-  STFEM_CUDA_TRY(cudaFuncSetAttribute(panel_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM));
-  STFEM_CUDA_TRY(cudaFuncSetAttribute(panel_update_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  if (!P.h_err) STFEM_CUDA_TRY(cudaMallocHost(&P.h_err, sizeof(int)));
   P.level_nmax.assign(P.levels.size(), 0);
   P.level_pmax.assign(P.levels.size(), 0);
   for (size_t d = 0; d < P.levels.size(); ++d)
@@ -935,26 +668,8 @@ int upload(Plan& P) {
       P.level_nmax[d] = std::max(P.level_nmax[d], P.fronts[f].n);
       P.level_pmax[d] = std::max(P.level_pmax[d], P.fronts[f].p);
     }
-  // Schur-update tiles of the large-front levels (lower 64x64 tiles of each b x b block)
+  // Schur-update tiles of the large-front levels (lower 32 x 32 tiles of each b x b block)
   {
-    std::vector<int4> tl;
-    P.syrk_off.assign(P.levels.size() + 1, 0);
-    for (size_t d = 0; d < P.levels.size(); ++d) {
-      P.syrk_off[d] = (int64_t)tl.size();
-      const bool small = level_is_small(P, (int)d);
-      if (small) continue;
-      for (int32_t f : P.levels[d]) {
-        const int b = P.fronts[f].n - P.fronts[f].p;
-        const int nt = (b + TM - 1) / TM;
-        for (int tj = 0; tj < nt; ++tj)
-          for (int ti = tj; ti < nt; ++ti) tl.push_back(make_int4(f, ti, tj, 0));
-      }
-    }
-    P.syrk_off[P.levels.size()] = (int64_t)tl.size();
-    STFEM_CUDA_TRY(cudaMalloc(&P.d_syrk_tiles, std::max<size_t>(1, tl.size()) * sizeof(int4)));
-    if (!tl.empty())
-      STFEM_CUDA_TRY(cudaMemcpy(P.d_syrk_tiles, tl.data(), tl.size() * sizeof(int4), cudaMemcpyHostToDevice));
-    // the same at 32 x 32 granularity (syrk32_kernel)
     std::vector<int4> t32;
     P.syrk32_off.assign(P.levels.size() + 1, 0);
     for (size_t d = 0; d < P.levels.size(); ++d) {
@@ -968,22 +683,7 @@ int upload(Plan& P) {
       }
     }
     P.syrk32_off[P.levels.size()] = (int64_t)t32.size();
-    STFEM_CUDA_TRY(cudaMalloc(&P.d_syrk32_tiles, std::max<size_t>(1, t32.size()) * sizeof(int4)));
-    if (!t32.empty())
-      STFEM_CUDA_TRY(cudaMemcpy(P.d_syrk32_tiles, t32.data(), t32.size() * sizeof(int4), cudaMemcpyHostToDevice));
-    STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk32_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, S32_SMEM));
-    STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk32_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, S32_SMEM));
-    STFEM_CUDA_TRY(cudaFuncSetAttribute(panel_update32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, S32_SMEM));
-    STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SYRK_SMEM));
-    STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        SYRK_SMEM + 1024));
-    STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_block16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        b16_smem_bytes(B16_BMAX)));
-    STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_short_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        SyrkShort<16>::SMEM));
-    STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_short_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        SyrkShort<32>::SMEM));
-    STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_level_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    if ((rc = up(&P.d_syrk32_tiles, t32))) return rc;
   }
   // spectral subtrees: data + per-depth work items (fwd1 = U and F1, fwd2 = F2, bwd1 = B1, bwd2 = B2)
   {
@@ -1035,11 +735,13 @@ int upload(Plan& P) {
 int64_t bytes_per_shift(const Plan& P, int nrhs) {
   return 16 * (P.factor_stride + P.upool_stride[0] + P.upool_stride[1] +
                (int64_t)nrhs * (P.rpool_stride[0] + P.rpool_stride[1]) + (int64_t)P.n * nrhs +
-               (int64_t)P.h_th.size());
+               (int64_t)P.h_th.size()) + 8;
 }
 
 int ensure_workspace(Plan& P, int batch, int nrhs) {
   if (P.d_factor && P.ws_batch >= batch && P.ws_nrhs >= nrhs) return STFEM_OK;
+  batch = std::max(batch, P.ws_batch);   // grow only: a later, smaller call keeps the batch split stable
+  nrhs = std::max(nrhs, P.ws_nrhs);
   P.free_workspace();
   auto al = [&](cplx** d, int64_t elems) -> int {
     STFEM_CUDA_TRY(cudaMalloc((void**)d, std::max<int64_t>(1, elems) * 16));
@@ -1053,29 +755,37 @@ int ensure_workspace(Plan& P, int batch, int nrhs) {
   }
   if ((rc = al(&P.d_Z, (int64_t)P.n * nrhs * batch))) return rc;
   if (!P.h_th.empty() && (rc = al(&P.d_wbuf, (int64_t)P.h_th.size() * batch))) return rc;
+  STFEM_CUDA_TRY(cudaMalloc((void**)&P.d_scale2, sizeof(double) * batch));
   P.ws_batch = batch;
   P.ws_nrhs = nrhs;
   return STFEM_OK;
 }
 
-int auto_batch(Plan& P, int nshift, int nrhs) {
-  if (P.batch > 0) return std::min(P.batch, nshift);
-  size_t fr = 0, tot = 0;
-  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = (size_t)8 << 30;
-  // keep whatever workspace we already own in the budget
-  size_t owned = P.d_factor ? (size_t)bytes_per_shift(P, P.ws_nrhs) * P.ws_batch : 0;
-  // 70% of what is free leaves room for the caller's temporaries (residual checks)
-  const double frac = getenv("STFEM_WS_FRACTION") ? atof(getenv("STFEM_WS_FRACTION")) : 0.70;
-  double budget = frac * (double)(fr + owned);
-  int64_t per = bytes_per_shift(P, nrhs);
-  int64_t bmax = std::min<int64_t>(std::max<int64_t>(1, (int64_t)(budget / (double)per)), 4096);
-  // equal-sized batches: fewer, evenly filled waves at the top levels of the tree; rounded up
-  // to a multiple of the spectral kernel's 64-shift column tile when that still fits (e.g. 1024
-  // shifts: 384 + 384 + 256 instead of 3 x 342, whose last spectral column tile is 22/64 full)
+// equal-sized batches of at most bmax shifts: fewer, evenly filled waves at the top levels of the
+// tree; rounded up to a multiple of the spectral kernel's 64-shift column tile when that still
+// fits (e.g. 1024 shifts: 384 + 384 + 256 instead of 3 x 342, whose last spectral column tile is
+// 22/64 full)
+int even_batch(int nshift, int64_t bmax) {
   const int64_t nb = (nshift + bmax - 1) / bmax;
   const int64_t even = (nshift + nb - 1) / nb;
   const int64_t r64 = ((even + 63) / 64) * 64;
   return (int)((r64 <= bmax && (nshift + r64 - 1) / r64 == nb) ? r64 : even);
+}
+
+int auto_batch(Plan& P, int nshift, int nrhs) {
+  if (P.batch > 0) return std::min(P.batch, nshift);
+  // an existing workspace fixes the split (stfem_plan_reserve, or the first call): no
+  // reallocation -- and no device synchronisation -- on later calls that fit it
+  if (P.d_factor && P.ws_nrhs >= nrhs) return even_batch(nshift, P.ws_batch);
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = (size_t)8 << 30;
+  // keep whatever workspace we already own in the budget; the default 70% of what is free
+  // leaves room for the caller's temporaries (residual checks)
+  size_t owned = P.d_factor ? (size_t)bytes_per_shift(P, P.ws_nrhs) * P.ws_batch : 0;
+  double budget = P.opt.workspace_fraction * (double)(fr + owned);
+  int64_t per = bytes_per_shift(P, nrhs);
+  int64_t bmax = std::min<int64_t>(std::max<int64_t>(1, (int64_t)(budget / (double)per)), 4096);
+  return even_batch(nshift, bmax);
 }
 
 }  // namespace
@@ -1083,10 +793,7 @@ int auto_batch(Plan& P, int nshift, int nrhs) {
 Plan::~Plan() {
   free_workspace();
   free_device();
-  for (auto st : lane_streams) cudaStreamDestroy(st);
-  for (auto ev : lane_events) cudaEventDestroy(ev);
-  if (start_event) cudaEventDestroy(start_event);
-  if (stagger_event) cudaEventDestroy(stagger_event);
+  if (h_err) cudaFreeHost(h_err);
 }
 
 void Plan::free_device() {
@@ -1096,8 +803,6 @@ void Plan::free_device() {
   cudaFree(d_bidx);
   cudaFree(d_relpos);
   cudaFree(d_inv);
-  cudaFree(d_syrk_tiles);
-  d_syrk_tiles = nullptr;
   cudaFree(d_syrk32_tiles);
   d_syrk32_tiles = nullptr;
   cudaFree(d_ent_src);
@@ -1108,6 +813,8 @@ void Plan::free_device() {
   cudaFree(d_ent_colptr);
   d_ent_colptr = nullptr;
   cudaFree(d_perm);
+  cudaFree(d_diag_src);
+  d_diag_src = nullptr;
   cudaFree(d_err);
   cudaFree(d_subs);
   cudaFree(d_V);
@@ -1134,10 +841,14 @@ void Plan::free_workspace() {
   }
   cudaFree(d_Z);
   cudaFree(d_wbuf);
+  cudaFree(d_scale2);
+  d_scale2 = nullptr;
   d_factor = d_Z = d_wbuf = nullptr;
   ws_batch = ws_nrhs = 0;
 }
 
+// Enqueue the factor + solve of every shift on `stream` (no host wait; a pivot collapse is latched
+// in P.d_err and read by plan_check).
 int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, int nshift, int nrhs,
                  const cplx* G, cplx* W, stfem_bv_layout lay, cudaStream_t stream) {
   if (nshift < 0 || nrhs < 1) return fail(STFEM_ERR_DIM, "factor_solve: nshift >= 0 and nrhs >= 1 required");
@@ -1150,9 +861,8 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
   if (nshift == 0) return STFEM_OK;
   int rc;
   if ((rc = upload(P))) return rc;
-  int batch = auto_batch(P, nshift, nrhs);
+  const int batch = auto_batch(P, nshift, nrhs);
   if ((rc = ensure_workspace(P, batch, nrhs))) return rc;
-  STFEM_CUDA_TRY(cudaMemsetAsync(P.d_err, 0, sizeof(int), stream));
 
   LevelArgs a{};
   a.fronts = P.d_fronts;
@@ -1183,30 +893,24 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
   a.W = W;
   a.lay = lay;
   a.err = P.d_err;
-  a.split_syrk = 1;
+  a.scale2 = P.d_scale2;
   int64_t nlaunch = P.ent_src.empty() ? 0 : 1;   // gather_entries_kernel
-  static const bool phase_prof = getenv("STFEM_PHASE_PROF") != nullptr;
-  static unsigned long long* d_prof = nullptr;
-  if (phase_prof) {
-    if (!d_prof) STFEM_CUDA_TRY(cudaMalloc(&d_prof, 16 * sizeof(unsigned long long)));
-    STFEM_CUDA_TRY(cudaMemsetAsync(d_prof, 0, 16 * sizeof(unsigned long long), stream));
-  }
-  a.prof = phase_prof ? d_prof : nullptr;
-  // STFEM_LEVEL_TIMING=1: per-launch CUDA-event times to stderr (diagnostics only)
-  static const bool level_print = getenv("STFEM_LEVEL_TIMING") != nullptr;
+  // per-launch CUDA-event times (record mode / opt.level_timing; diagnostics only: it waits for
+  // the stream at the end of the call)
+  const bool level_print = P.opt.level_timing != 0;
   const bool level_timing = level_print || P.record_levels;
   std::vector<cudaEvent_t> evs;
   // per-kernel-family accounting (record mode): event after every launch,
   // the gap to the previous event is charged to the launch's family
   cudaEvent_t fev_start = nullptr;
   std::vector<std::pair<cudaEvent_t, int>> fevs;
-  std::vector<int> fev_depth;   // depth of each family event (STFEM_LEVEL_TIMING breakdown)
+  std::vector<int> fev_depth;
   int cur_depth = -1;
-  auto fam = [&](int f, cudaStream_t st) {
+  auto fam = [&](int f) {
     if (!level_timing) return;
     cudaEvent_t e;
     cudaEventCreate(&e);
-    cudaEventRecord(e, st);
+    cudaEventRecord(e, stream);
     fevs.push_back({e, f});
     fev_depth.push_back(cur_depth);
   };
@@ -1217,43 +921,20 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
     cudaEventRecord(e, stream);
     evs.push_back(e);
   };
-  // shift lanes (STFEM_STREAMS, default 1: measured no gain on C4 since every
-  // level launch already fills the GPU): the batch workspace is split into `lanes` slices, each run on
-  // its own stream so the latency-bound kernels of one lane overlap the
-  // tensor-core kernels of another (per-level timing runs single-lane)
-  static const int lanes_env = getenv("STFEM_STREAMS") ? std::max(1, atoi(getenv("STFEM_STREAMS"))) : 1;
-  const int lanes = level_timing ? 1 : std::min(lanes_env, batch);
-  if ((int)P.lane_streams.size() < lanes) {
-    for (int j = (int)P.lane_streams.size(); j < lanes; ++j) {
-      cudaStream_t st;
-      cudaEvent_t ev;
-      STFEM_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-      STFEM_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-      P.lane_streams.push_back(st);
-      P.lane_events.push_back(ev);
-    }
-    STFEM_CUDA_TRY(cudaEventCreateWithFlags(&P.start_event, cudaEventDisableTiming));
-  }
-  const int sub = (batch + lanes - 1) / lanes;
-  if ((rc = ensure_workspace(P, lanes * sub, nrhs))) return rc;   // lane slices are sub shifts each
+  const double tol2 = P.opt.pivot_tol * P.opt.pivot_tol;
   const LevelArgs a0 = a;
-  // staggered lanes (STFEM_STAGGER = d >= 0, with STFEM_STREAMS >= 2): lane 1 starts once lane 0
-  // has factored depth d of its first slice, so one lane's deep, latency-bound levels run beside
-  // the other lane's tensor-core-bound top levels instead of in phase with them
-  static const int stagger_env = getenv("STFEM_STAGGER") ? atoi(getenv("STFEM_STAGGER")) : -1;
-  const int stagger_depth = stagger_env;
-  cudaEvent_t stagger_rec = nullptr;
-  auto run_batch = [&](int s0, int nb, int koff, cudaStream_t st) -> int {
+  cudaStream_t st = stream;
+  auto run_batch = [&](int s0, int nb) -> int {
     LevelArgs a = a0;
     a.nbatch = nb;
     a.lam = lam + s0;
     a.shift0 = s0;
-    // this lane's slice of the batch workspace: local shifts [koff, koff + nb)
-    a.factor = P.d_factor + (int64_t)koff * P.factor_stride;
-    a.Z = P.d_Z + (int64_t)koff * P.n * nrhs;
-    cplx* up[2] = {P.d_upool[0] + (int64_t)koff * P.upool_stride[0], P.d_upool[1] + (int64_t)koff * P.upool_stride[1]};
-    cplx* rp[2] = {P.d_rpool[0] + (int64_t)koff * P.rpool_stride[0] * nrhs,
-                   P.d_rpool[1] + (int64_t)koff * P.rpool_stride[1] * nrhs};
+    a.err_base = P.shift_base;
+    cplx* up[2] = {P.d_upool[0], P.d_upool[1]};
+    cplx* rp[2] = {P.d_rpool[0], P.d_rpool[1]};
+    pivot_scale_kernel<<<nb, 256, 0, st>>>(P.d_diag_src, P.n, Mv, Av, lam + s0, tol2, P.d_scale2);
+    STFEM_LAUNCH_CHECK("pivot_scale_kernel");
+    ++nlaunch;
     SpecArgs sa{};
     sa.subs = P.d_subs;
     sa.V = P.d_V;
@@ -1272,16 +953,16 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
     sa.G = G;
     sa.W = W;
     sa.lay = lay;
-    sa.wbuf = P.d_wbuf + koff;
+    sa.wbuf = P.d_wbuf;
     sa.wstride = P.ws_batch;
     if (!P.subs.empty()) {
       const int64_t nth = (int64_t)P.h_th.size();
       const int64_t tot = nth * nb;
       spectral_w_kernel<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 16), 256, 0, st>>>(
-          P.d_th, nth, lam + s0, nb, P.d_wbuf + koff, P.ws_batch);
+          P.d_th, nth, lam + s0, nb, P.d_wbuf, P.ws_batch, tol2, P.d_err, P.shift_base + s0);
       STFEM_LAUNCH_CHECK("spectral_w_kernel");
       ++nlaunch;
-      fam(FAM_SPECTRAL, st);
+      fam(FAM_SPECTRAL);
     }
     for (int d = P.depth; d >= 0; --d) {
       cur_depth = d;
@@ -1310,7 +991,7 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
                             st>>>(sa);
           STFEM_LAUNCH_CHECK("spectral_kernel");
           ++nlaunch;
-          fam(FAM_SPECTRAL, st);
+          fam(FAM_SPECTRAL);
         }
       }
       if (a.nlist == 0) {
@@ -1321,97 +1002,69 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
       if (level_is_small(P, d)) {
         if ((rc = launch_small_factor_any(a, a.nlist * nb, nmax, st))) return rc;
         ++nlaunch;
-        fam(FAM_SMALL, st);
+        fam(FAM_SMALL);
       } else {
         // large fronts: tile-parallel pipeline over all (front, shift) instances of the level
         const int ninst = a.nlist * nb, pmax = P.level_pmax[d];
-        const int64_t ntl = P.syrk_off[d + 1] - P.syrk_off[d];
-        // fused levels: the boundary block U is gathered by syrk_gather_kernel, not assembled here
-        a.asm_pivots_only = (ntl > 0 && pmax >= P.fused_min_p) ? 1 : 0;
+        const int64_t n32 = P.syrk32_off[d + 1] - P.syrk32_off[d];
+        // fused levels: the boundary block U is gathered by syrk32_kernel<true>, not assembled here
+        a.asm_pivots_only = (n32 > 0 && pmax >= P.opt.fused_min_p) ? 1 : 0;
         const int asm_cols = a.asm_pivots_only ? pmax : nmax;
         // deep levels (fronts of order <= asm_whole_n): one CTA per instance for all columns
-        a.asm_cpc = nmax <= P.asm_whole_n ? ((asm_cols + ASM_COLS - 1) / ASM_COLS) * ASM_COLS : ASM_COLS;
+        a.asm_cpc = nmax <= P.opt.asm_whole_n ? ((asm_cols + ASM_COLS - 1) / ASM_COLS) * ASM_COLS : ASM_COLS;
         asm_front_kernel<<<dim3(ninst, (asm_cols + a.asm_cpc - 1) / a.asm_cpc), NT, (size_t)2 * nmax * sizeof(int),
                            st>>>(a);
         STFEM_LAUNCH_CHECK("asm_front_kernel");
         ++nlaunch;
-        fam(FAM_ASM, st);
+        fam(FAM_ASM);
+        const int pg = std::max(1, P.opt.panel_group);
         for (int kb = 0; kb < pmax; kb += NB) {
           if (nrhs == 1)
             diag_kernel<true><<<ninst, 32, 0, st>>>(a, kb);
           else
             diag_kernel<false><<<ninst, 32 * std::min(8, nrhs), 0, st>>>(a, kb);
           STFEM_LAUNCH_CHECK("diag_kernel");
-          fam(FAM_DIAG, st);
+          fam(FAM_DIAG);
           const dim3 tg(ninst, (unsigned)std::max(1, (nmax - kb + TR_ROWS - 1) / TR_ROWS));
           if (std::min(NB, pmax - kb) <= 16) trsm_kernel<16><<<tg, TR_ROWS, 0, st>>>(a, kb);
           else trsm_kernel<32><<<tg, TR_ROWS, 0, st>>>(a, kb);
           STFEM_LAUNCH_CHECK("trsm_kernel");
-          fam(FAM_TRSM, st);
+          fam(FAM_TRSM);
           nlaunch += 2;
           // delayed updates over groups of panel_group panels starting at g0 (see
-          // panel_update_kernel): inside a group only the next panel's columns are updated,
+          // panel_update32_kernel): inside a group only the next panel's columns are updated,
           // by every panel of the group so far; after its last panel, everything beyond
-          const int GW = NB * P.panel_group, g0 = (kb / GW) * GW;
-          const int narrow = ((kb - g0) / NB < P.panel_group - 1) ? 1 : 0;
+          const int GW = NB * pg, g0 = (kb / GW) * GW;
+          const int narrow = ((kb - g0) / NB < pg - 1) ? 1 : 0;
           const int cb = kb + NB, k0 = g0, K = kb + NB - g0;
           int tiles = 0;
           for (int32_t f : P.levels[d])
-            tiles = std::max(tiles, P.syrk32 ? panel_update_tiles32(P.fronts[f].n, P.fronts[f].p, cb, narrow)
-                                             : panel_update_tiles(P.fronts[f].n, P.fronts[f].p, cb, narrow));
-          if (tiles > 0 && P.syrk32) {
+            tiles = std::max(tiles, panel_update_tiles32(P.fronts[f].n, P.fronts[f].p, cb, narrow));
+          if (tiles > 0) {
             panel_update32_kernel<<<dim3(ninst, tiles), 128, S32_SMEM, st>>>(a, cb, k0, K, narrow);
             STFEM_LAUNCH_CHECK("panel_update32_kernel");
             ++nlaunch;
-            fam(FAM_PANEL, st);
-          } else if (tiles > 0) {
-            panel_update_kernel<<<dim3(ninst, tiles), NT, GEMM_SMEM, st>>>(a, cb, k0, K, narrow);
-            STFEM_LAUNCH_CHECK("panel_update_kernel");
-            ++nlaunch;
-            fam(FAM_PANEL, st);
+            fam(FAM_PANEL);
           }
         }
-        if (ntl > 0 && a.asm_pivots_only && P.syrk32) {
-          const int64_t n32 = P.syrk32_off[d + 1] - P.syrk32_off[d];
+        if (n32 > 0 && a.asm_pivots_only) {
           syrk32_kernel<true><<<(unsigned)(n32 * nb), 128, S32_SMEM, st>>>(a, P.d_syrk32_tiles + P.syrk32_off[d]);
           STFEM_LAUNCH_CHECK("syrk32_kernel<gather>");
           ++nlaunch;
-          fam(FAM_SYRK, st);
-        } else if (ntl > 0 && a.asm_pivots_only) {
-          syrk_gather_kernel<<<(unsigned)(ntl * nb), NT, SYRK_SMEM + 1024, st>>>(a, P.d_syrk_tiles + P.syrk_off[d]);
-          STFEM_LAUNCH_CHECK("syrk_gather_kernel");
-          ++nlaunch;
-          fam(FAM_SYRK, st);
-        } else if (ntl > 0 && pmax <= B16_KMAX && P.syrk_block16 && level_bmax(P, d) <= B16_BMAX) {
+          fam(FAM_SYRK);
+        } else if (n32 > 0 && pmax <= B16_KMAX && P.opt.syrk_block16 && level_bmax(P, d) <= B16_BMAX) {
           syrk_block16_kernel<<<ninst, NT, b16_smem_bytes(level_bmax(P, d)), st>>>(a);
           STFEM_LAUNCH_CHECK("syrk_block16_kernel");
           ++nlaunch;
-          fam(FAM_SYRK, st);
-        } else if (ntl > 0 && pmax <= P.syrk_short_max_p) {
-          if (pmax <= 16)
-            syrk_short_kernel<16><<<(unsigned)(2 * ntl * nb), 128, SyrkShort<16>::SMEM, st>>>(
-                a, P.d_syrk_tiles + P.syrk_off[d]);
-          else
-            syrk_short_kernel<32><<<(unsigned)(2 * ntl * nb), 128, SyrkShort<32>::SMEM, st>>>(
-                a, P.d_syrk_tiles + P.syrk_off[d]);
-          STFEM_LAUNCH_CHECK("syrk_short_kernel");
-          ++nlaunch;
-          fam(FAM_SYRK, st);
-        } else if (ntl > 0 && P.syrk32) {
-          const int64_t n32 = P.syrk32_off[d + 1] - P.syrk32_off[d];
+          fam(FAM_SYRK);
+        } else if (n32 > 0) {
           syrk32_kernel<false><<<(unsigned)(n32 * nb), 128, S32_SMEM, st>>>(a, P.d_syrk32_tiles + P.syrk32_off[d]);
           STFEM_LAUNCH_CHECK("syrk32_kernel");
           ++nlaunch;
-          fam(FAM_SYRK, st);
-        } else if (a.split_syrk && ntl > 0) {
-          syrk_level_kernel<<<(unsigned)(ntl * nb), NT, SYRK_SMEM, st>>>(a, P.d_syrk_tiles + P.syrk_off[d]);
-          STFEM_LAUNCH_CHECK("syrk_level_kernel");
-          ++nlaunch;
-          fam(FAM_SYRK, st);
+          fam(FAM_SYRK);
         }
       }
       mark();
-      if (stagger_rec && d == stagger_depth) STFEM_CUDA_TRY(cudaEventRecord(stagger_rec, st));
     }
     for (int d = 0; d <= P.depth; ++d) {
       cur_depth = d;
@@ -1425,7 +1078,7 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
                           st>>>(sa);
         STFEM_LAUNCH_CHECK("spectral_kernel");
         ++nlaunch;
-        fam(FAM_SPECTRAL, st);
+        fam(FAM_SPECTRAL);
       }
       if (a.nlist == 0) {
         mark();
@@ -1440,7 +1093,7 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
         b.list = a.list + off;
         b.nlist = cnt;
         const int bsm = small_bwd_smem_bytes(nmax, pmax, small_nr(nrhs));
-        if (nmax <= SMALL_N && bsm <= 200 * 1024 && !P.force_big)
+        if (nmax <= SMALL_N && bsm <= 200 * 1024 && P.opt.small_front_n > 0)
           return launch_small_backward_any(b, cnt * nb, nmax, pmax, st);
         const int u = ldlt ? 1 : 0, gsz = cnt * nb;
         switch (small_nr(nrhs)) {
@@ -1460,37 +1113,18 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
         return rc;
       }
       ++nlaunch;
-      fam(FAM_BACKWARD, st);
+      fam(FAM_BACKWARD);
       mark();
     }
     return STFEM_OK;
   };
-  fev_start = nullptr;
   if (level_timing) {
     cudaEventCreate(&fev_start);
     cudaEventRecord(fev_start, stream);
   }
   mark();
-  if (lanes == 1) {
-    for (int s0 = 0; s0 < nshift; s0 += batch)
-      if ((rc = run_batch(s0, std::min(batch, nshift - s0), 0, stream))) return rc;
-  } else {
-    STFEM_CUDA_TRY(cudaEventRecord(P.start_event, stream));
-    for (int j = 0; j < lanes; ++j) STFEM_CUDA_TRY(cudaStreamWaitEvent(P.lane_streams[j], P.start_event, 0));
-    int j = 0;
-    const bool stagger = stagger_depth >= 0 && stagger_depth <= P.depth && nshift > sub;
-    if (stagger && !P.stagger_event) STFEM_CUDA_TRY(cudaEventCreateWithFlags(&P.stagger_event, cudaEventDisableTiming));
-    for (int s0 = 0; s0 < nshift; s0 += sub, j = (j + 1) % lanes) {
-      stagger_rec = (stagger && s0 == 0) ? P.stagger_event : nullptr;
-      if (stagger && j == 1 && s0 == sub) STFEM_CUDA_TRY(cudaStreamWaitEvent(P.lane_streams[1], P.stagger_event, 0));
-      if ((rc = run_batch(s0, std::min(sub, nshift - s0), j * sub, P.lane_streams[j]))) return rc;
-    }
-    stagger_rec = nullptr;
-    for (int jj = 0; jj < lanes; ++jj) {
-      STFEM_CUDA_TRY(cudaEventRecord(P.lane_events[jj], P.lane_streams[jj]));
-      STFEM_CUDA_TRY(cudaStreamWaitEvent(stream, P.lane_events[jj], 0));
-    }
-  }
+  for (int s0 = 0; s0 < nshift; s0 += batch)
+    if ((rc = run_batch(s0, std::min(batch, nshift - s0)))) return rc;
   P.last_batch = batch;
   P.last_launches = nlaunch;
   P.last_nbatches = (nshift + batch - 1) / batch;
@@ -1537,27 +1171,26 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
     for (auto& fe : fevs) cudaEventDestroy(fe.first);
     cudaEventDestroy(fev_start);
   }
-  if (phase_prof) {
-    unsigned long long h[16];
-    cudaMemcpyAsync(h, d_prof, sizeof(h), cudaMemcpyDeviceToHost, stream);
-    cudaStreamSynchronize(stream);
-    const char* names[16] = {"assembly", "diag", "writeback+fwd", "trsm", "panel_gemm", "syrk", "", "",
-                             "small:gather", "small:diag+trsm", "small:trailing", "small:writeout", "", "", "", ""};
-    for (int grp = 0; grp < 2; ++grp) {
-      double tot = 0;
-      for (int i = 8 * grp; i < 8 * grp + 6; ++i) tot += (double)h[i];
-      for (int i = 8 * grp; i < 8 * grp + 6; ++i)
-        if (names[i][0])
-          fprintf(stderr, "[stfem phase] %-16s %5.1f%%  (%.3e cycles)\n", names[i], 100.0 * h[i] / tot, (double)h[i]);
-    }
-  }
-  int h_err = 0;
-  STFEM_CUDA_TRY(cudaMemcpyAsync(&h_err, P.d_err, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  return STFEM_OK;
+}
+
+int plan_reserve(Plan& P, int nshift, int nrhs) {
+  int rc;
+  if ((rc = upload(P))) return rc;
+  return ensure_workspace(P, auto_batch(P, nshift, nrhs), nrhs);
+}
+
+// wait for the work issued so far on `stream`, read and clear the latched pivot-collapse flag
+int plan_check(Plan& P, cudaStream_t stream) {
+  if (!P.d_err) return STFEM_OK;   // nothing was ever enqueued
+  STFEM_CUDA_TRY(cudaMemcpyAsync(P.h_err, P.d_err, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  STFEM_CUDA_TRY(cudaMemsetAsync(P.d_err, 0, sizeof(int), stream));
   STFEM_CUDA_TRY(cudaStreamSynchronize(stream));
+  const int h_err = *P.h_err;
   if (h_err) {
-    char buf[160];
-    snprintf(buf, sizeof(buf), "singular pivot (numerically singular shifted system) at shift index %d",
-             h_err - 1);
+    char buf[200];
+    snprintf(buf, sizeof(buf), "singular pivot (numerically singular shifted system M_x + lam A_x) at shift "
+                               "index %d", h_err - 1);
     return fail(STFEM_ERR_SINGULAR, buf);
   }
   return STFEM_OK;
@@ -1799,6 +1432,41 @@ extern "C" int stfem_plan_last_batches(const stfem_plan* plan, int32_t* batches)
 extern "C" int stfem_plan_last_launches(const stfem_plan* plan, int64_t* launches) {
   if (!plan || !launches) return stfem::fail(STFEM_ERR_ARG, "plan_last_launches: null pointer");
   *launches = reinterpret_cast<const Plan*>(plan)->last_launches;
+  return STFEM_OK;
+}
+
+extern "C" int stfem_plan_check(stfem_plan* plan, void* stream) {
+  if (!plan) return stfem::fail(STFEM_ERR_ARG, "plan_check: null plan");
+  return stfem::plan_check(*reinterpret_cast<Plan*>(plan), (cudaStream_t)stream);
+}
+
+extern "C" int stfem_plan_set_shift_base(stfem_plan* plan, int32_t base) {
+  if (!plan) return stfem::fail(STFEM_ERR_ARG, "plan_set_shift_base: null plan");
+  reinterpret_cast<Plan*>(plan)->shift_base = base;
+  return STFEM_OK;
+}
+
+extern "C" int stfem_plan_reserve(stfem_plan* plan, int32_t nshift, int32_t nrhs) {
+  if (!plan) return stfem::fail(STFEM_ERR_ARG, "plan_reserve: null plan");
+  if (nshift < 1 || nrhs < 1 || nrhs > stfem::MAXR)
+    return stfem::fail(STFEM_ERR_DIM, "plan_reserve: nshift >= 1 and 1 <= nrhs <= 16 required");
+  return stfem::plan_reserve(*reinterpret_cast<Plan*>(plan), nshift, nrhs);
+}
+
+extern "C" int stfem_plan_get_options(const stfem_plan* plan, stfem_plan_options* out) {
+  if (!plan || !out) return stfem::fail(STFEM_ERR_ARG, "plan_get_options: null pointer");
+  *out = reinterpret_cast<const Plan*>(plan)->opt;
+  return STFEM_OK;
+}
+
+extern "C" int stfem_plan_set_options(stfem_plan* plan, const stfem_plan_options* opt) {
+  if (!plan || !opt) return stfem::fail(STFEM_ERR_ARG, "plan_set_options: null pointer");
+  if (opt->panel_group < 1 || opt->small_front_n < 0 || !(opt->workspace_fraction > 0.0) ||
+      opt->workspace_fraction > 1.0 || !(opt->pivot_tol >= 0.0))
+    return stfem::fail(STFEM_ERR_ARG, "plan_set_options: value out of range");
+  Plan& P = *reinterpret_cast<Plan*>(plan);
+  P.opt = *opt;
+  P.free_device();   // level classification and tile tables depend on the options
   return STFEM_OK;
 }
 

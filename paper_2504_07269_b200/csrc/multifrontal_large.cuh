@@ -1,5 +1,5 @@
 // Large-front path of the multifrontal factorization (included by
-// multifrontal.cu inside its anonymous namespace; uses LevelArgs, gemm_update,
+// multifrontal.cu inside its anonymous namespace; uses LevelArgs, sym_tile32,
 // NB/NT/LDD/MAXR).
 //
 // A level of large fronts times a batch of shifts is factored by a pipeline of
@@ -224,7 +224,8 @@ __global__ void __launch_bounds__(256) diag_kernel(LevelArgs a, int kb) {
     if (lane < w) {
       const cplx d = Ld[dix<PACK>(lane, lane)];
       const double m2 = cabs2(d);
-      if (!(m2 > 1e-300) || !isfinite(m2)) atomicCAS(a.err, 0, (int)shift + 1);
+      // pivot collapse: relative to the largest original diagonal entry of this shift
+      if (!(m2 > a.scale2[k]) || !isfinite(m2)) atomicCAS(a.err, 0, a.err_base + (int)shift + 1);
       const cplx c = csqrt_(d);
       cdg[lane] = c;
       dinv_s[lane] = crecip(c);
@@ -346,41 +347,3 @@ __global__ void __launch_bounds__(TR_ROWS, 8) trsm_kernel(LevelArgs a, int kb) {
 // once per 32 G pivots instead of once per 32.
 // Region of one update: rows [cb, n), columns [cb, cb + cols) with
 // cols = narrow ? min(NB, p - cb) : p - cb, updated by the panel columns [k0, k0 + K).
-__host__ __device__ inline int panel_update_cols(int p, int cb, int narrow) {
-  if (cb >= p) return 0;
-  return narrow ? min(NB, p - cb) : p - cb;
-}
-__host__ __device__ inline int panel_update_tiles(int n, int p, int cb, int narrow) {
-  const int cols = panel_update_cols(p, cb, narrow);
-  if (cols <= 0) return 0;
-  const int tm = (n - cb + TM - 1) / TM, tn = (cols + TM - 1) / TM;
-  return tn * tm - tn * (tn - 1) / 2;
-}
-
-// F[cb:n, cb:cb+cols] -= X X^T, X = F[cb:n, k0:k0+K] (the TRSM'd panel rows),
-// lower trapezoid, one 64x64 tile per CTA, DMMA
-__global__ void __launch_bounds__(NT, 2) panel_update_kernel(LevelArgs a, int cb, int k0, int K, int narrow) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  cplx* gsm = reinterpret_cast<cplx*>(smem_raw);
-  const int inst = blockIdx.x;
-  const int k = inst % a.nbatch;
-  const FrontDev F = a.fronts[a.list[inst / a.nbatch]];
-  const int n = F.n, p = F.p;
-  const int cols = panel_update_cols(p, cb, narrow);
-  if (cols <= 0) return;
-  const int kk = min(K, p - k0);   // panels beyond this front's p contribute nothing
-  const int tm = (n - cb + TM - 1) / TM, tn = (cols + TM - 1) / TM;
-  int t = blockIdx.y, ti = -1, tj = 0;
-  for (; tj < tn; ++tj) {
-    if (t < tm - tj) {
-      ti = tj + t;
-      break;
-    }
-    t -= tm - tj;
-  }
-  if (ti < 0) return;
-  cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
-  cplx* C = P + cb + (int64_t)cb * n;
-  gemm_update<2>(C, n, n - cb, cols, P + cb + (int64_t)k0 * n, n, P + cb + (int64_t)k0 * n, n, kk,
-                 true, gsm, ti, tj, CLoad{C, n});
-}

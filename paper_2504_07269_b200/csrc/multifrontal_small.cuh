@@ -102,7 +102,6 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
   const int n = Fr.n, p = Fr.p, b = n - p;
   const cplx lam = a.lam[k];
   const int64_t shift = a.shift0 + k;
-  long long t_prev = clock64();
 
   // ---- gather ----
   // the global loads (original entries, pivot rows of the RHS via perm) are
@@ -182,7 +181,6 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
     }
     __syncthreads();
   }
-  STFEM_PROF_MARK(8);
   cplx rv[NR];
 #pragma unroll
   for (int r = 0; r < NR; ++r) rv[r] = i < n ? Rsm[i * NR + r] : zero;
@@ -223,7 +221,7 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
             Dinv[jj] = dinv;
             if (warp == 0) {
               double m2 = cabs2(d);
-              if (!(m2 > 1e-300) || !isfinite(m2)) atomicCAS(a.err, 0, (int)shift + 1);
+              if (!(m2 > a.scale2[k]) || !isfinite(m2)) atomicCAS(a.err, 0, a.err_base + (int)shift + 1);
             }
           }
         }
@@ -282,10 +280,8 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
       }
     }
     __syncthreads();
-    STFEM_PROF_MARK(9);
     if (i >= kb + w && i < n) trailing_row(F, PB, av, i, kb + w, n, w);
     __syncthreads();
-    STFEM_PROF_MARK(10);
   }
 
   // ---- write out: L/D (n x p), U (b x b), z = D^{-1} y, forward RHS update ----
@@ -317,7 +313,6 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
     }
   }
   __syncthreads();   // shared memory is reused by the next instance
-  STFEM_PROF_MARK(11);
   }
 }
 
@@ -423,14 +418,13 @@ __global__ void __launch_bounds__(SMALL_N) backward_small_kernel(LevelArgs a, in
 template <int NR>
 int launch_small_factor(const LevelArgs& a, int grid, int nmax, cudaStream_t s) {
   const int smem = small_smem_bytes(nmax, NR);
-  static bool attr = false;
-  if (!attr) {
+  static DeviceOnce attr_once;
+  if (attr_once.first()) {
     STFEM_CUDA_TRY(cudaFuncSetAttribute(factor_small_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         small_smem_bytes(SMALL_N, NR)));
     // occupancy here is shared-memory bound: ask for the full 228 KB carveout
     STFEM_CUDA_TRY(cudaFuncSetAttribute(factor_small_kernel<NR>,
                                         cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    attr = true;
   }
   // persistent-style grid: as many CTAs as can be resident, grid-striding over instances
   const int threads = (nmax + 31) / 32 * 32;
@@ -454,13 +448,12 @@ int launch_small_factor(const LevelArgs& a, int grid, int nmax, cudaStream_t s) 
 template <int NR>
 int launch_small_backward(const LevelArgs& a, int grid, int nmax, int pmax, cudaStream_t s) {
   const int smem = small_bwd_smem_bytes(nmax, pmax, NR);
-  static bool attr = false;
-  if (!attr) {
+  static DeviceOnce attr_once;
+  if (attr_once.first()) {
     STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_small_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         200 * 1024));
     STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_small_kernel<NR>,
                                         cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    attr = true;
   }
   const int threads = (nmax + 31) / 32 * 32;
   int nsm = 0, dev = 0, per_sm = 0;

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <stdlib.h>
+#include <limits.h>
 
 #include <algorithm>
 #include <vector>
@@ -49,6 +50,7 @@ struct Plan {
   std::vector<int32_t> perm, iperm;       // perm[new] = old
   std::vector<FrontDev> fronts;           // postorder
   std::vector<int32_t> child_ids, bidx, relpos, ent_src, ent_dst, inv, ent_colptr;
+  std::vector<int32_t> diag_src;           // CSR slot of the diagonal entry of every row (-1: none)
   std::vector<std::vector<int32_t>> levels;  // fronts per depth
   int32_t depth = 0, max_front = 0, max_pivots = 0;
   int64_t factor_stride = 0;               // complex per shift
@@ -73,36 +75,35 @@ struct Plan {
   std::vector<int32_t> level_nmax, level_pmax;  // per depth: max front order / pivots
   std::vector<int32_t> level_nsplit;       // per depth: fronts of order > BWD_SPLIT_N (a prefix: levels sorted by n)
   std::vector<int32_t> level_tail_nmax, level_tail_pmax;   // per depth: max order / pivots of the rest
-  bool force_big = getenv("STFEM_FORCE_BIG") != nullptr;  // diagnostics: disable the small-front path
-  // levels whose fronts have >= this many pivots fuse the extend-add of U into the Schur update
-  // (syrk32_kernel<true>, or syrk_gather_kernel with STFEM_SYRK32=0).  Measured with the 32 x 32
-  // tiles (C4, ms/step): threshold 50 -> 899, 100 -> 902, no fusion -> 907; C5 neutral.  With the
-  // 64 x 64 tiles the short-K gather was latency bound (p <= 31 lost up to 14 ms per batch per
-  // level).  STFEM_FUSED_MIN_P tunes it at plan creation (0: every level, a huge value: none).
-  int fused_min_p = getenv("STFEM_FUSED_MIN_P") ? atoi(getenv("STFEM_FUSED_MIN_P")) : 50;
-  // trailing pivot-column updates are delayed over groups of this many 32-wide panels
-  // (K = 32 * panel_group for the wide updates; measured on C4: 2 -> 96 ms/step of panel updates,
-  // 1 -> 111, 4 -> 108, 8 -> 121); STFEM_PANEL_GROUP tunes it at plan creation
-  int panel_group = getenv("STFEM_PANEL_GROUP") ? std::max(1, atoi(getenv("STFEM_PANEL_GROUP"))) : 2;
-  // asm_front_kernel assembles a whole front per CTA for levels of order <= this (STFEM_ASM_WHOLE_N)
-  // (measured on C4: 160 -> 120 ms/step of assembly, 240 -> 118, every level -> 114)
-  int asm_whole_n = getenv("STFEM_ASM_WHOLE_N") ? atoi(getenv("STFEM_ASM_WHOLE_N")) : 1 << 30;
-  // Schur updates of short-K levels (p <= 32, b <= 208) on 16 x 16 blocks (STFEM_SYRK_B16=0 disables)
-  bool syrk_block16 = !(getenv("STFEM_SYRK_B16") && atoi(getenv("STFEM_SYRK_B16")) == 0);
-  // Schur updates of the remaining unfused levels on 32 x 32 tiles (STFEM_SYRK32=0: 64 x 64 gemm_update)
-  bool syrk32 = !(getenv("STFEM_SYRK32") && atoi(getenv("STFEM_SYRK32")) == 0);
-  // Schur updates of levels with <= this many pivots (at most 32) on syrk_short_kernel
-  // (STFEM_SYRK_SHORT_P; 0 disables it)
-  int syrk_short_max_p = std::min(32, getenv("STFEM_SYRK_SHORT_P") ? atoi(getenv("STFEM_SYRK_SHORT_P")) : 16);
-  int small_n_cap = getenv("STFEM_SMALL_N") ? atoi(getenv("STFEM_SMALL_N")) : 0;  // tuning: lower the threshold
+  // tuning knobs (stfem_plan_set_options; measured defaults, C4 ms/step):
+  //   fused_min_p  levels whose fronts have >= this many pivots fuse the children's extend-add into
+  //                the Schur-update tiles (50 -> 899, 100 -> 902, no fusion -> 907; C5 neutral)
+  //   panel_group  trailing pivot-column updates delayed over this many 32-wide panels
+  //                (2 -> 96 ms of panel updates, 1 -> 111, 4 -> 108, 8 -> 121)
+  //   asm_whole_n  asm_front_kernel assembles a whole front per CTA up to this order
+  //                (160 -> 120 ms of assembly, 240 -> 118, every level -> 114)
+  //   small_front_n levels of order <= this on the shared-memory small-front kernel (0: none)
+  stfem_plan_options opt = default_options();
+  static stfem_plan_options default_options() {
+    stfem_plan_options o{};
+    o.small_front_n = 100;
+    o.fused_min_p = 50;
+    o.panel_group = 2;
+    o.asm_whole_n = INT32_MAX;
+    o.syrk_block16 = 1;
+    o.level_timing = 0;
+    o.workspace_fraction = 0.70;
+    o.pivot_tol = 1e-10;
+    return o;
+  }
   int32_t *d_child_ids = nullptr, *d_bidx = nullptr, *d_relpos = nullptr, *d_inv = nullptr;
   int32_t *d_ent_src = nullptr, *d_ent_dst = nullptr, *d_perm = nullptr, *d_ent_colptr = nullptr;
   double *d_ent_mv = nullptr, *d_ent_av = nullptr;   // M_x / A_x values gathered into entry order
-  std::vector<int64_t> syrk_off;           // per depth: offsets into d_syrk_tiles
-  int4* d_syrk_tiles = nullptr;            // (front, ti, tj, 0) Schur-update tiles of the large fronts
   std::vector<int64_t> syrk32_off;         // per depth: offsets into d_syrk32_tiles
-  int4* d_syrk32_tiles = nullptr;          // the same at 32 x 32 granularity (syrk32_kernel)
+  int4* d_syrk32_tiles = nullptr;          // (front, ti, tj, 0) lower 32 x 32 Schur-update tiles of the large fronts
   int* d_err = nullptr;
+  int32_t* d_diag_src = nullptr;
+  double* d_scale2 = nullptr;              // per shift of the batch: max_j |M_jj + lam A_jj|^2
   SubDev* d_subs = nullptr;
   double *d_V = nullptr, *d_th = nullptr, *d_RQ = nullptr, *d_C01 = nullptr;
   int4* d_spec_items = nullptr;
@@ -125,10 +126,8 @@ struct Plan {
   cplx* d_rpool[2] = {nullptr, nullptr};
   cplx* d_Z = nullptr;
   cplx* d_wbuf = nullptr;                   // spectral w = 1 / (theta + lam), sum(m) x batch
-  cudaEvent_t stagger_event = nullptr;      // STFEM_STAGGER: lane 1 waits for lane 0 mid-slice
-  std::vector<cudaStream_t> lane_streams;   // shift lanes of factor_solve (STFEM_STREAMS, default 2)
-  std::vector<cudaEvent_t> lane_events;
-  cudaEvent_t start_event = nullptr;
+  int32_t shift_base = 0;                   // added to the shift index reported by stfem_plan_check
+  int* h_err = nullptr;                     // pinned: the latched error flag read back by stfem_plan_check
 
   ~Plan();
   void free_device();

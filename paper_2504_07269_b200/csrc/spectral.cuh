@@ -68,14 +68,24 @@ struct SpecArgs {
 
 // w_k(s) = 1 / (theta_k + lam_s) for every subtree interior index k and shift s
 // of the batch (shared by all row tiles of a subtree instead of recomputed)
+// Pivot collapse: theta_k + lam_s are exactly the pivots of the
+// subtree interior in the eigenbasis, so lam = -theta_k (an eigenvalue -mu of
+// the subtree's (M_II, A_II) pencil) is reported like a vanishing LDL^T pivot:
+// |theta_k + lam|^2 <= tol^2 (|theta_k| + |lam|)^2 latches shift0 + s + 1 in err.
 __global__ void spectral_w_kernel(const double* __restrict__ th, int64_t nth, const cplx* __restrict__ lam,
-                                  int nb, cplx* __restrict__ w, int64_t wstride) {
+                                  int nb, cplx* __restrict__ w, int64_t wstride, double tol2, int* err,
+                                  int shift0) {
   const int64_t tot = nth * nb;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < tot;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t k = idx / nb;
     const int s = (int)(idx - k * nb);
-    stc(w + k * wstride + s, spec_w(th[k], lam[s]));
+    const double t = th[k];
+    const cplx l = lam[s];
+    const double dr = t + l.re, d2 = fma(dr, dr, l.im * l.im);
+    const double sc = fabs(t) + sqrt(cabs2(l));
+    if (!(d2 > tol2 * sc * sc) || !isfinite(d2)) atomicCAS(err, 0, shift0 + s + 1);
+    stc(w + k * wstride + s, spec_w(t, l));
   }
 }
 

@@ -269,9 +269,11 @@ int build_symbolic(Plan& P, int32_t n, const int64_t* rowptr, const int32_t* col
   std::vector<int32_t> cnt(nf + 1, 0);
   std::vector<int32_t> e_front, e_src, e_dst;
   e_front.reserve(nnz / 2 + n);
+  P.diag_src.assign(n, -1);   // CSR slot of every diagonal entry (pivot-collapse scale, factor_solve)
   for (int32_t r = 0; r < n; ++r) {
     int32_t i = P.iperm[r];
     for (int64_t k = rowptr[r]; k < rowptr[r + 1]; ++k) {
+      if (colind[k] == r) P.diag_src[r] = (int32_t)k;
       int32_t j = P.iperm[colind[k]];
       if (i < j) continue;
       int32_t f = owner[j];

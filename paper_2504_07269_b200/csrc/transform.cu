@@ -300,11 +300,10 @@ template <int EPI>
 int launch_rc(const double* A, int M, int K, const cplx* in, int64_t ld_in, cplx* out, int64_t ld_out,
               int64_t ncols, int batch, int64_t bs_in, int64_t bs_out, const int2* rows, const cplx* scale,
               int nsrc, cudaStream_t stream) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static DeviceOnce attr_once;
+  if (attr_once.first()) {
     STFEM_CUDA_TRY(cudaFuncSetAttribute(transform_rc_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         RC_SMEM));
-    attr_set = true;
   }
   for (int64_t c0 = 0; c0 < ncols; c0 += 65535LL * BN) {
     const int64_t cn = ncols - c0 < 65535LL * BN ? ncols - c0 : 65535LL * BN;
@@ -327,11 +326,10 @@ int time_transform(const void* T, int nt, const void* in, int64_t ld_in, void* o
   if (((uintptr_t)T | (uintptr_t)in | (uintptr_t)out) & 15)
     return fail(STFEM_ERR_ARG, "time_transform: buffers must be 16-byte aligned");
   if (ncols == 0 || batch == 0) return STFEM_OK;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static DeviceOnce attr_once;
+  if (attr_once.first()) {
     STFEM_CUDA_TRY(cudaFuncSetAttribute(time_transform_kernel,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    attr_set = true;
   }
   int64_t ntile = (ncols + BN - 1) / BN;
   if (ntile > 65535) {

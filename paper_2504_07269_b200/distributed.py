@@ -173,12 +173,12 @@ def bench_main(args):
     if rank == 0:
         tf = temporal_factors(prob.M_t, prob.B_t)
         X, Y, lam = tf.X, tf.Y, tf.eigenvalues
-        pf0 = PT.build(lam, X, prob.B_t) if PT.enabled() else None
+        pf0 = PT.build(lam, X, prob.B_t)
         if pf0 is not None:
             X, Y, lam = pf0.X, pf0.Y, pf0.lam       # the paired eigenbasis
     Xt, Yt, lt = broadcast_factors(X, Y, lam, dev)
     # every rank derives the K3p tables from the broadcast (already paired) factors
-    pf = PT.build(lt.cpu().numpy(), Xt.cpu().numpy(), prob.B_t) if PT.enabled() else None
+    pf = PT.build(lt.cpu().numpy(), Xt.cpu().numpy(), prob.B_t)
     if pf is not None:
         Yt = torch.as_tensor(pf.Y, dtype=C128, device=dev)
     pairs = PT.DevicePairs(pf, dev) if pf is not None else None

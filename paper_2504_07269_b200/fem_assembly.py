@@ -77,6 +77,7 @@ class SpatialOperators:
         self.device = torch.device(device)
         self.Mvals = None
         self.Avals = None
+        self.epoch = 0     # bumped by assemble(): consumers caching value-derived data compare it
 
     @property
     def handle(self):
@@ -93,6 +94,7 @@ class SpatialOperators:
         self.Avals = torch.empty(self.nnz, dtype=torch.float64, device=self.device)
         N.check(N.lib().stfem_asm_spatial(self._h, N.ptr(self.Mvals), N.ptr(self.Avals),
                                           N.stream_ptr(stream)))
+        self.epoch += 1
         return self
 
     @property

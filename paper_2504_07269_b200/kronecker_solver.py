@@ -96,6 +96,14 @@ def relative_residual(ops, M_t, B_t, psi: torch.Tensor, f: torch.Tensor) -> floa
     return worst
 
 
+def _as_stack(buf: torch.Tensor, like: torch.Tensor, name: str) -> torch.Tensor:
+    """View of a caller buffer as the (n_rhs, n_t, n_x) stack; never a silent copy."""
+    if buf.dtype != like.dtype or buf.device != like.device or buf.numel() != like.numel() \
+            or not buf.is_contiguous():
+        raise ValueError(f"solve: `{name}` must be a contiguous complex128 device buffer of F's shape")
+    return buf.view(like.shape)
+
+
 class FDMSolver:
     """Reusable FD solver for one (spatial mesh, temporal mesh) pair.
 
@@ -117,7 +125,7 @@ class FDMSolver:
         dev = ops.device
         lam, X, Y = self.tf.eigenvalues, self.tf.X, self.tf.Y
         self.pairs = None
-        if paired and PT.enabled():
+        if paired:
             pf = PT.build(lam, X, self.B_t)
             if pf is not None:
                 # the paired eigenbasis (partners rebuilt from their leads) drives every stage
@@ -146,9 +154,11 @@ class FDMSolver:
         return K.time_transform(self.X, W, out=out, stream=stream)
 
     def solve(self, F: torch.Tensor, out: torch.Tensor | None = None, work: torch.Tensor | None = None,
-              stream=None, timings: dict | None = None) -> torch.Tensor:
+              stream=None, timings: dict | None = None, check: bool = True) -> torch.Tensor:
         """Psi for F of shape (n_t, n_x) or (n_rhs, n_t, n_x), complex128 on the GPU.
-        `work` (if given) is scratch and is overwritten."""
+        `out` / `work` (if given) must be contiguous buffers of F's shape, distinct from F
+        and from each other; `work` is scratch.  check=False leaves the stream un-waited
+        (stream-ordered pipelines); the caller then runs `self.plan.check()` itself."""
         N.require_cuda(F)
         if F.shape[-2:] != (self.nt, self.ops.n):
             raise N.DimensionMismatch(N.ERR_DIM, f"solve: f {tuple(F.shape)} vs ({self.nt}, {self.ops.n})")
@@ -156,8 +166,10 @@ class FDMSolver:
         Fb = (F.unsqueeze(0) if single else F).contiguous()
         nr = Fb.shape[0]
         # buffer rotation without copies: F -> G (=out) -> W (=work) -> out
-        G = out.reshape(Fb.shape) if out is not None else torch.empty_like(Fb)
-        W = work.reshape(Fb.shape) if work is not None else torch.empty_like(Fb)
+        G = _as_stack(out, Fb, "out") if out is not None else torch.empty_like(Fb)
+        W = _as_stack(work, Fb, "work") if work is not None else torch.empty_like(Fb)
+        if len({Fb.data_ptr(), G.data_ptr(), W.data_ptr()}) != 3:
+            raise ValueError("solve: F, out and work must be three distinct buffers")
         s = stream if stream is not None else torch.cuda.current_stream()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timings is not None else None
         if ev:
@@ -165,10 +177,13 @@ class FDMSolver:
         self.forward_transform(Fb, G, s)                               # (2)
         if ev:
             ev[1].record(s)
-        self.plan.factor_solve(self.lam, G, W, blockvector_layout(self.nt, self.ops.n), nr, stream=s)  # (3)
+        self.plan.factor_solve(self.lam, G, W, blockvector_layout(self.nt, self.ops.n), nr, stream=s,
+                               check=False)                            # (3)
         if ev:
             ev[2].record(s)
         self.back_transform(W, G, s)                                   # (4) (W is scratch)
+        if check:
+            self.plan.check(s)       # SingularPivot names the shift; waits for the stream
         if ev:
             ev[3].record(s)
             ev[3].synchronize()
@@ -218,7 +233,7 @@ class FDMSolver:
             ev.record(cs)
             s.wait_event(ev)
             self.forward_transform(Fd[..., c0:c1], G[..., c0:c1], s)
-        self.plan.factor_solve(self.lam, G, W, blockvector_layout(nt, nx), nr, stream=s)   # (3)
+        self.plan.factor_solve(self.lam, G, W, blockvector_layout(nt, nx), nr, stream=s, check=False)   # (3)
         for c0, c1 in blocks:                                             # (4) pipelined with D2H
             self.back_transform(W[..., c0:c1], G[..., c0:c1], s)
             ev = torch.cuda.Event()
@@ -229,6 +244,7 @@ class FDMSolver:
         done = torch.cuda.Event()
         done.record(cs)
         s.wait_event(done)
+        self.plan.check(s)
         return out_host
 
 
@@ -300,7 +316,7 @@ class FDMSolver:
                 h2d_done.record(hs)
             if d2h_done is not None:                     # W_k = G_{k-1} holds Psi_{k-1} until drained
                 s.wait_event(d2h_done)
-            self.plan.factor_solve(self.lam, G, W, layout, nr, stream=s)
+            self.plan.factor_solve(self.lam, G, W, layout, nr, stream=s, check=False)
             for c0, c1 in blocks:                        # back transform W -> G, D2H block-pipelined
                 self.back_transform(W[..., c0:c1], G[..., c0:c1], s)
                 ev = torch.cuda.Event()
@@ -311,6 +327,7 @@ class FDMSolver:
             d2h_done = torch.cuda.Event()
             d2h_done.record(ds)
         s.wait_event(d2h_done)
+        self.plan.check(s)        # one wait for the whole sequence
         return out_hosts
 
 
@@ -364,8 +381,10 @@ class BSSolver:
         single = F.dim() == 2
         Fb = (F.unsqueeze(0) if single else F).contiguous()
         nr = Fb.shape[0]
-        G = out.reshape(Fb.shape) if out is not None else torch.empty_like(Fb)
-        W = work.reshape(Fb.shape) if work is not None else torch.empty_like(Fb)
+        G = _as_stack(out, Fb, "out") if out is not None else torch.empty_like(Fb)
+        W = _as_stack(work, Fb, "work") if work is not None else torch.empty_like(Fb)
+        if len({Fb.data_ptr(), G.data_ptr(), W.data_ptr()}) != 3:
+            raise ValueError("solve: F, out and work must be three distinct buffers")
         s = stream if stream is not None else torch.cuda.current_stream()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timings is not None else None
         if ev:
@@ -375,15 +394,22 @@ class BSSolver:
             ev[1].record(s)
         lay = blockvector_layout(nt, nx)
         lib = N.lib()
+        self.plan.reserve(1, nr)          # no allocation (= no device sync) inside the sweep
         for l in range(nt - 1, -1, -1):                                          # (3)
-            self.plan.factor_solve(self.diag[l:l + 1], G[:, l:l + 1], W[:, l:l + 1], lay, nr, stream=s)
+            # stream-ordered sweep: n_t single-shift solves enqueued back to back, one error
+            # check at the end that still names the sweep index l
+            self.plan.set_shift_base(l)
+            self.plan.factor_solve(self.diag[l:l + 1], G[:, l:l + 1], W[:, l:l + 1], lay, nr, stream=s,
+                                   check=False)
             if l > 0:
                 N.check(lib.stfem_bs_update(self.ops.handle, N.ptr(self.ops.Avals), N.ptr(W[:, l]),
                                             nt * nx, nr, N.ptr(self.St[l]), l, N.ptr(G), nt * nx, nx,
                                             N.stream_ptr(s)))
+        self.plan.set_shift_base(0)
         if ev:
             ev[2].record(s)
         K.time_transform(self.X, W, out=G, stream=s)                            # (4)
+        self.plan.check(s)
         if ev:
             ev[3].record(s)
             ev[3].synchronize()

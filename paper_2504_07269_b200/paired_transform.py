@@ -212,9 +212,3 @@ class DevicePairs:
         self.A_back = torch.as_tensor(pack_fragments(pf.A_back), device=device)
         self.mix_rows = torch.as_tensor(np.ascontiguousarray(pf.mix_rows), device=device)
         self.mix_coef = torch.as_tensor(np.ascontiguousarray(pf.mix_coef), device=device)
-
-
-def enabled() -> bool:
-    """STFEM_PAIRED=0 keeps the complex K3 kernel (for A/B measurements)."""
-    import os
-    return os.environ.get("STFEM_PAIRED", "1") != "0"

@@ -31,12 +31,17 @@ class SpatialPlan:
     """Symbolic analysis + device tables for one spatial pattern.
 
     spectral: max interior DoFs of the subtrees eliminated in closed form
-    (K6, spectral.py); 0 = plain multifrontal; None = the default
-    (STFEM_SPECTRAL_M, 256).  The spectral data depends on the operator
-    values, so it is built from `ops` when they are assembled (here, or on the
-    first factor_solve)."""
+    (K6, spectral.py); 0 = plain multifrontal; None = the default (256).  The
+    spectral data depends on the operator values, so it is built from `ops`
+    when they are assembled (here, or on the first factor_solve) and rebuilt
+    when `ops.assemble()` produces new value tensors.
 
-    def __init__(self, ops: SpatialOperators, leaf_size: int = 16, spectral: int | None = None):
+    options: stfem_plan_options fields to override (small_front_n, fused_min_p,
+    panel_group, asm_whole_n, syrk_block16, level_timing, workspace_fraction,
+    pivot_tol) -- the plan's only tuning interface (no environment variables)."""
+
+    def __init__(self, ops: SpatialOperators, leaf_size: int = 16, spectral: int | None = None,
+                 options: dict | None = None, spectral_threads: int | None = None):
         self.ops = ops
         self.n = ops.n
         h = C.c_void_p()
@@ -48,18 +53,62 @@ class SpatialPlan:
         self.stats = {f: getattr(st, f) for f, _ in N.plan_stats._fields_}
         self.spectral_m = SP.DEFAULT_MAX_INTERIOR if spectral is None else int(spectral)
         self.spectral = None          # SpectralData once attached
+        self.spectral_threads = spectral_threads
+        self._spectral_key = None     # identity of the operator values the spectral data came from
         self.t_spectral = 0.0         # host setup seconds
+        if options:
+            self.set_options(**options)
         if self.spectral_m > 0 and ops.Mvals is not None:
             self._attach_spectral()
+
+    def _ops_key(self):
+        o = self.ops
+        return (o.epoch, o.Mvals.data_ptr(), o.Avals.data_ptr(), o.Mvals._version, o.Avals._version)
+
+    def options(self) -> dict:
+        o = N.plan_options()
+        N.check(N.lib().stfem_plan_get_options(self._h, C.byref(o)))
+        return {f: getattr(o, f) for f, _ in N.plan_options._fields_}
+
+    def set_options(self, **kw):
+        o = N.plan_options()
+        N.check(N.lib().stfem_plan_get_options(self._h, C.byref(o)))
+        for k, v in kw.items():
+            if k not in dict(N.plan_options._fields_):
+                raise KeyError(f"unknown plan option {k!r}")
+            setattr(o, k, v)
+        N.check(N.lib().stfem_plan_set_options(self._h, C.byref(o)))
+
+    def reserve(self, nshift: int, nrhs: int = 1):
+        """Allocate the numeric workspace now (stfem_plan_reserve): later factor_solve calls
+        of up to (nshift, nrhs) neither allocate nor synchronise the device."""
+        N.require_cuda()
+        if self.spectral_m > 0 and self.ops.Mvals is not None and self._spectral_key != self._ops_key():
+            self._attach_spectral()
+        N.check(N.lib().stfem_plan_reserve(self._h, int(nshift), int(min(nrhs, self.max_rhs()))))
+
+    def max_rhs(self) -> int:
+        mr = C.c_int32()
+        N.check(N.lib().stfem_plan_max_rhs(self._h, C.byref(mr)))
+        return max(1, mr.value)
+
+    def check(self, stream=None):
+        """stfem_plan_check: wait for the factor_solve calls issued on `stream` and raise
+        SingularPivot (naming the shift) if one of them met a pivot collapse."""
+        N.check(N.lib().stfem_plan_check(self._h, N.stream_ptr(stream)))
+
+    def set_shift_base(self, base: int):
+        N.check(N.lib().stfem_plan_set_shift_base(self._h, int(base)))
 
     def _attach_spectral(self):
         import time
         t0 = time.perf_counter()
         fr = self.fronts()
         data = SP.build(fr, self.front_rows(), self.perm(), self.ops.M_x.to_scipy(), self.ops.A_x.to_scipy(),
-                        self.spectral_m)
+                        self.spectral_m, threads=self.spectral_threads)
         SP.attach(self._h, data)
         self.spectral = data
+        self._spectral_key = self._ops_key()
         self.t_spectral = time.perf_counter() - t0
         st = N.plan_stats()
         N.check(N.lib().stfem_plan_stats_get(self._h, C.byref(st)))
@@ -131,18 +180,20 @@ class SpatialPlan:
         return bps.value
 
     def factor_solve(self, lam: torch.Tensor, G: torch.Tensor, W: torch.Tensor, layout: N.bv_layout,
-                     nrhs: int, stream=None):
-        """(M_x + lam[s] A_x) W[r, s] = G[r, s] for every shift s (device c128)."""
+                     nrhs: int, stream=None, check: bool = True):
+        """(M_x + lam[s] A_x) W[r, s] = G[r, s] for every shift s (device c128).
+
+        The C call only enqueues work.  check=True (default) then waits for it and raises
+        SingularPivot if a shift was numerically singular; pipelined
+        callers pass check=False and call `plan.check()` once at the end."""
         N.require_cuda(G)
         ops = self.ops
         if ops.Mvals is None:
             raise RuntimeError("spatial operators are not assembled")
-        if self.spectral_m > 0 and self.spectral is None:
-            self._attach_spectral()
+        if self.spectral_m > 0 and self._spectral_key != self._ops_key():
+            self._attach_spectral()     # first use, or ops.assemble() produced new values
         lam = lam.to(device=G.device, dtype=torch.complex128).contiguous()
-        mr = C.c_int32()
-        N.check(N.lib().stfem_plan_max_rhs(self._h, C.byref(mr)))
-        step = max(1, mr.value)
+        step = self.max_rhs()
         for r0 in range(0, nrhs, step):
             nr = min(step, nrhs - r0)
             off = r0 * layout.rhs_stride
@@ -150,6 +201,8 @@ class SpatialPlan:
                 self._h, N.ptr(ops.Mvals), N.ptr(ops.Avals), N.ptr(lam), lam.numel(), nr,
                 C.c_void_p(G.data_ptr() + 16 * off), C.c_void_p(W.data_ptr() + 16 * off), layout,
                 N.stream_ptr(stream)))
+        if check:
+            self.check(stream)
         return W
 
     def __del__(self):
@@ -176,10 +229,37 @@ class SpatialFactorization:
         return self.plan.n
 
 
+def _same_operator(given, mine) -> bool:
+    """Is `given` (SparseRealMatrix, scipy matrix or value tensor) the plan's operator?"""
+    vals = getattr(given, "values", given)
+    if torch.is_tensor(vals):
+        return vals.data_ptr() == mine.values.data_ptr() or (
+            vals.shape == mine.values.shape and bool(torch.equal(vals.to(mine.values.device), mine.values)))
+    try:
+        import scipy.sparse as sp
+        g = sp.csr_matrix(given)
+        g.sort_indices()
+        m = mine.to_scipy()
+        return g.shape == m.shape and np.array_equal(g.indptr, m.indptr) and np.array_equal(g.indices, m.indices) \
+            and np.array_equal(g.data, m.data)
+    except Exception:
+        return False
+
+
 def factor(plan_or_ops, M_x=None, A_x=None, lam: complex = 0j) -> SpatialFactorization:
-    """SPEC.md:323-331.  `plan_or_ops` is a SpatialPlan (or SpatialOperators,
-    for which a plan is built).  M_x/A_x must be the plan's operators."""
+    """SPEC.md:323-331.  `plan_or_ops` is a SpatialPlan (or SpatialOperators, for which a
+    plan is built).  M_x / A_x, when given, must BE the plan's operators (same pattern and
+    values): the factorization always uses the plan's device-resident values, so anything
+    else raises DimensionMismatch instead of silently solving a different system.  The
+    numeric factors are streamed inside `solve` (never kept), so a singular shift is
+    reported there (SingularPivot)."""
     plan = plan_or_ops if isinstance(plan_or_ops, SpatialPlan) else SpatialPlan(plan_or_ops)
+    for given, mine, name in ((M_x, "M_x", "M_x"), (A_x, "A_x", "A_x")):
+        if given is None:
+            continue
+        if plan.ops.Mvals is None or not _same_operator(given, getattr(plan.ops, mine)):
+            raise N.DimensionMismatch(N.ERR_DIM, f"factor: {name} is not the plan's operator (build a SpatialPlan "
+                                                 "from the operators you want to factor)")
     return SpatialFactorization(plan, complex(lam))
 
 

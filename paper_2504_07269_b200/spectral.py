@@ -34,7 +34,7 @@ import scipy.sparse as sp
 
 from . import _native as N
 
-DEFAULT_MAX_INTERIOR = int(os.environ.get("STFEM_SPECTRAL_M", "256"))
+DEFAULT_MAX_INTERIOR = 256   # measured on C4 (ms/step): 200 -> 874, 256 -> 807, 320 -> 807
 
 
 def subtree_first(fronts: np.ndarray) -> np.ndarray:

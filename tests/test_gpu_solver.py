@@ -68,46 +68,28 @@ def test_lifting_matches_oracle():
     assert rel(L, Lo) < 1e-13
 
 
-@pytest.mark.parametrize("mode", ["small", "big", "big_allfused", "big_gather64", "big_legacy", "big_pg4", "big_s32",
-                                  "spec24", "spec"])
+MODES = {
+    # plain multifrontal with the shared-memory small-front kernels below order 100
+    "small": {},
+    # every front on the tile-parallel large-front pipeline, default tuning: extend-add fused into
+    # the 32 x 32-tile Schur update for levels with >= 50 pivots, 16 x 16-block Schur kernel for
+    # <= 32 pivots, 32 x 32 tiles elsewhere, trailing updates delayed over panel pairs
+    "big": dict(small_front_n=0),
+    "big_allfused": dict(small_front_n=0, fused_min_p=0),           # fused on every level
+    # none of it: U assembled by asm_front_kernel, per-panel trailing updates, 32 x 32 tiles on
+    # every level, 32-column assembly CTAs
+    "big_plain": dict(small_front_n=0, fused_min_p=1 << 30, panel_group=1, syrk_block16=0, asm_whole_n=0),
+    "big_pg4": dict(small_front_n=0, panel_group=4, syrk_block16=0),
+    # spectral subtrees of <= 24 / <= 256 interior DoFs (K6) under a multifrontal top
+    "spec24": {}, "spec": {},
+}
+
+
+@pytest.mark.parametrize("mode", list(MODES))
 @pytest.mark.parametrize("kind,leaf", [("square9", 4), ("square16", 32), ("p2square6", 8),
                                         ("lshape5", 16), ("square40", 32), ("lshape12", 16)])
-def test_factor_solve_matches_splu(kind, leaf, mode, monkeypatch):
-    """mode: small = plain multifrontal with the shared-memory small-front kernels;
-    big* = every front on the global-memory (large-front) kernels:
-      big          the default tuning: extend-add fused into the 32 x 32-tile Schur
-                   update for levels with >= 50 pivots, 16 x 16-block Schur kernel
-                   for <= 32 pivots, 32 x 32 tiles elsewhere and for the trailing
-                   updates (delayed over panel pairs), whole-front assembly CTAs;
-      big_allfused fused on every level (32 x 32 tiles);
-      big_gather64 fused on every level on the 64 x 64 gather kernel;
-      big_legacy   none of it: asm_front_kernel assembles U, per-panel 64 x 64
-                   trailing updates, 64 x 64 gemm_update Schur kernel, 32-column
-                   assembly CTAs;
-      big_pg4      trailing updates delayed over 4 panels, 32 x 64 short-K kernel;
-      big_s32      the 32 x 32-tile Schur kernel on every unfused level;
-    spec24 / spec = spectral subtrees of <= 24 / <= 256 interior DoFs (K6)
-    under a multifrontal top."""
-    if mode.startswith("big"):  # exercise the global-memory (large-front) kernels on small meshes too
-        monkeypatch.setenv("STFEM_FORCE_BIG", "1")
-    if mode in ("big_allfused", "big_gather64"):
-        monkeypatch.setenv("STFEM_FUSED_MIN_P", "0")
-    if mode == "big_gather64":  # fused levels on the 64 x 64 gather kernel
-        monkeypatch.setenv("STFEM_SYRK32", "0")
-    if mode == "big_legacy":
-        monkeypatch.setenv("STFEM_FUSED_MIN_P", "1000000")
-        monkeypatch.setenv("STFEM_PANEL_GROUP", "1")
-        monkeypatch.setenv("STFEM_SYRK_SHORT_P", "0")
-        monkeypatch.setenv("STFEM_SYRK_B16", "0")
-        monkeypatch.setenv("STFEM_SYRK32", "0")
-        monkeypatch.setenv("STFEM_ASM_WHOLE_N", "0")
-    if mode == "big_pg4":  # + the 32 x 64 short-K Schur kernel up to 32 pivots instead of 16 x 16 blocks
-        monkeypatch.setenv("STFEM_PANEL_GROUP", "4")
-        monkeypatch.setenv("STFEM_SYRK_SHORT_P", "32")
-        monkeypatch.setenv("STFEM_SYRK_B16", "0")
-    if mode == "big_s32":  # every unfused level on the 32 x 32-tile Schur kernel
-        monkeypatch.setenv("STFEM_SYRK_B16", "0")
-        monkeypatch.setenv("STFEM_SYRK_SHORT_P", "0")
+def test_factor_solve_matches_splu(kind, leaf, mode):
+    """Every kernel path of K4/K5/K6 (MODES, selected through stfem_plan_options) against SuperLU."""
     spectral = {"spec24": 24, "spec": 256}.get(mode, 0)
     if kind.startswith("p2"):
         mesh, deg = sm.refine_uniform(sm.build_structured_square(int(kind[8:]))), 2
@@ -119,7 +101,7 @@ def test_factor_solve_matches_splu(kind, leaf, mode, monkeypatch):
         mesh, deg = sm.build_structured_square(int(kind[6:])), 1
         Mo, Ao = O.assemble_spatial(omesh(mesh))
     ops = fa.assemble_spatial(mesh, deg)
-    plan = sss.SpatialPlan(ops, leaf_size=leaf, spectral=spectral)
+    plan = sss.SpatialPlan(ops, leaf_size=leaf, spectral=spectral, options=MODES[mode])
     if spectral:
         assert plan.spectral_stats()["nroots"] >= 1
     rng = np.random.default_rng(1)

@@ -279,3 +279,38 @@ def test_host_schur_decompose(N, deg):
     assert np.abs(np.sort_complex(np.diag(S)) - ev).max() < 1e-8
     oracle = O.schur_decompose(Mt, Bt)
     assert np.abs(np.sort_complex(np.diag(oracle.S)) - ev).max() < 1e-8
+
+
+@pytest.mark.parametrize("kind", ["square7", "p2square5", "lshape4"])
+def test_vectorised_assembly_equals_loop_assembly(kind):
+    """The full-size parity tests use assemble_spatial_vec; pin it to the loop restatement."""
+    from paper_2504_07269_b200 import spatial_mesh as sm
+    if kind.startswith("p2"):
+        mesh = sm.refine_uniform(sm.build_structured_square(int(kind[8:])))
+        om = O.finish(2, mesh.vertices, mesh.elements)
+        Ml, Al = O.assemble_spatial(om, 2, mesh.p2_elements)
+        Mv, Av = O.assemble_spatial_vec(mesh.vertices, mesh.p2_elements, mesh.interior_dof, 2)
+    else:
+        mesh = sm.build_lshape(int(kind[6:])) if kind.startswith("lshape") else sm.build_structured_square(int(kind[6:]))
+        om = O.finish(2, mesh.vertices, mesh.elements)
+        Ml, Al = O.assemble_spatial(om)
+        Mv, Av = O.assemble_spatial_vec(mesh.vertices, mesh.elements, mesh.interior_dof, 1)
+    for a, b in ((Ml, Mv), (Al, Av)):
+        a.sort_indices()
+        assert np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices)
+        assert np.abs(a.data - b.data).max() <= 4e-16 * np.abs(a.data).max() * 8
+
+
+def test_nd_superlu_mode_equals_default_mode():
+    """The timing baseline's second SuperLU mode (shared ND ordering, no pivoting) solves the same system."""
+    from paper_2504_07269_b200 import spatial_mesh as sm
+    mesh = sm.build_structured_square(12)
+    om = O.finish(2, mesh.vertices, mesh.elements)
+    M, A = O.assemble_spatial(om)
+    rng = np.random.default_rng(0)
+    perm = rng.permutation(M.shape[0])
+    b = rng.standard_normal(M.shape[0]) + 1j * rng.standard_normal(M.shape[0])
+    for lam in (0.3 - 0.1j, -0.01 - 1e-5j):
+        x0 = O._solve_shift(M, A, lam, b)
+        x1 = O._solve_shift_nd(M, A, lam, b, perm)
+        assert np.linalg.norm(x0 - x1) <= 1e-11 * np.linalg.norm(x0)
