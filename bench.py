@@ -201,8 +201,8 @@ def run_reference(args):
     op = OracleProblem(args.workload)
     threads = O.cpu_threads()
     # bounded sample: every step solves its own, disjoint set of shifts (a seeded permutation
-    # walked step by step), two waves of the host threads per step by default
-    k = min(args.sample_shifts or 2 * threads, op.nt)
+    # walked step by step), one wave of the host workers per step by default
+    k = min(args.sample_shifts or threads, op.nt)
     threads = min(threads, k)
     pool = O.ShiftPool(op.Mx, op.Ax, op.perm, threads)
     F = complex_gaussian(0, (op.n_rhs, op.nt, op.nx))
@@ -522,7 +522,7 @@ def run_ours(args):
         op = OracleProblem(args.workload)
         assert (op.nx, op.nt, op.n_rhs) == (prob.nx, prob.nt, prob.n_rhs)
         threads = O.cpu_threads()
-        k = min(args.sample_shifts or 2 * threads, prob.nt)
+        k = min(args.sample_shifts or threads, prob.nt)
         threads = min(threads, k)
         Fh = prob.F_host.numpy()
         shifts = np.linspace(0, prob.nt - 1, k).astype(int)

@@ -34,6 +34,7 @@ enum {
   STFEM_ERR_CUDA = 4,
   STFEM_ERR_NOMEM = 5,
   STFEM_ERR_INTERNAL = 6,
+  STFEM_ERR_NCCL = 7,
 };
 
 typedef struct stfem_plan stfem_plan;   /* symbolic analysis + device tables for one spatial pattern */
@@ -185,6 +186,9 @@ typedef struct {
   int32_t asm_whole_n;       /* fronts of order <= this are assembled by one CTA.  Default INT32_MAX */
   int32_t syrk_block16;      /* 1: short-K Schur updates (p <= 32, b <= 208) on 16 x 16 blocks.  Default 1 */
   int32_t level_timing;      /* 1: print per-launch CUDA-event times to stderr (diagnostics) */
+  int32_t syrk_stream;       /* tiles per CTA of the streamed Schur-update kernel (1..16); 0 = the per-tile
+                                kernel.  Default 8 */
+  int32_t reserved;
   double workspace_fraction; /* share of the free device memory the numeric workspace may take.  Default 0.70 */
   double pivot_tol;          /* relative pivot-collapse threshold (see stfem_plan_check).  Default 1e-10 */
 } stfem_plan_options;
@@ -285,6 +289,57 @@ int stfem_bs_update(const stfem_asm* a, const double* Avals, const void* w, int6
 int stfem_apply_global(const stfem_asm* a, const double* Mvals, const double* Avals,
                        const double* Mt_band, const double* Bt_band, int32_t bw, int32_t nt,
                        const void* v, void* out, void* work, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * The whole FD solve behind one call (kronecker_solver.solve, SPEC.md:374-382,
+ * steps 2-4; step 1 -- the temporal eigendecomposition -- is host work whose
+ * result arrives in stfem_fd_factors), single-GPU or sharded over NCCL
+ * (SURVEY.md §8b "fdm_solve(plan, comm, ...)" and "comm_init(unique_id[128],
+ * nranks, rank)", §8e partitioning).
+ *
+ * stfem_comm: one NCCL communicator per process / GPU.  Rank 0 calls
+ * stfem_comm_unique_id and hands the 128 bytes to every rank through the
+ * launcher's own channel (the torch.distributed store under torchrun); every
+ * rank then calls stfem_comm_init with the CUDA device it will use current.
+ * NCCL is bound at run time (dlopen libnccl.so.2); STFEM_ERR_NCCL if absent.
+ * stfem_comm_all_to_all: block q (count c128) of send -> rank q.
+ * ------------------------------------------------------------------------- */
+typedef struct stfem_comm stfem_comm;
+int stfem_comm_unique_id(uint8_t unique_id[128]);
+int stfem_comm_init(const uint8_t unique_id[128], int32_t nranks, int32_t rank, stfem_comm** out);
+int stfem_comm_destroy(stfem_comm* comm);
+int stfem_comm_info(const stfem_comm* comm, int32_t* nranks, int32_t* rank, int32_t* nccl_version);
+int stfem_comm_all_to_all(stfem_comm* comm, const void* send, void* recv, int64_t count, void* stream);
+
+/* Temporal factors of the FD solve in device memory (TemporalFactors).
+ * Either the K3p tables (stfem_transform_pair_fwd / _back arguments, built by
+ * paired_transform.py) or the dense X, Y of K3; lam always. */
+typedef struct {
+  int32_t nt;
+  const void* lam;          /* c128[nt], ordered as the rows of Y / columns of X */
+  const void* X;            /* c128 nt x nt row-major, or NULL with the paired tables */
+  const void* Y;
+  const double* A_fwd;      /* K3p forward: see stfem_transform_pair_fwd */
+  int32_t mrows_fwd;
+  const int32_t* rows_fwd;
+  const void* scale_fwd;
+  int32_t nsrc;
+  const double* A_back;     /* K3p back: see stfem_transform_pair_back */
+  const int32_t* mix_rows;
+  const void* mix_coef;
+  int32_t nmix;
+} stfem_fd_factors;
+
+/* Psi = A^{-1} F, A = i B_t (x) M_x + M_t (x) A_x.
+ * comm == NULL: F, Psi, work are (nrhs, n_t, n_x) c128 BlockVectors.
+ * comm with P ranks: they are this rank's (n_t, nrhs, c) shard, c = ceil(n_x / P)
+ *   spatial columns [rank c, (rank + 1) c) (zero padded), n_t divisible by P; the
+ *   rank factors shifts [rank n_t / P, (rank + 1) n_t / P) of tf->lam.
+ * F is read only; Psi and work are overwritten (work is scratch); the three must
+ * be distinct.  Stream-ordered; pivot collapse via stfem_plan_check(plan). */
+int stfem_fdm_solve(stfem_plan* plan, stfem_comm* comm, const double* Mvals, const double* Avals,
+                    const stfem_fd_factors* tf, const void* F, void* Psi, void* work, int32_t nrhs,
+                    void* stream);
 
 #ifdef __cplusplus
 }

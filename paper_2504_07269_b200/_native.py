@@ -14,7 +14,7 @@ import torch
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libstfem_b200.so")
 
-OK, ERR_ARG, ERR_DIM, ERR_SINGULAR, ERR_CUDA, ERR_NOMEM, ERR_INTERNAL = range(7)
+OK, ERR_ARG, ERR_DIM, ERR_SINGULAR, ERR_CUDA, ERR_NOMEM, ERR_INTERNAL, ERR_NCCL = range(8)
 
 
 class NativeUnavailable(RuntimeError):
@@ -52,7 +52,16 @@ class plan_options(C.Structure):
     """stfem_plan_options (include/stfem_b200.h): tuning knobs of one plan."""
     _fields_ = [("small_front_n", C.c_int32), ("fused_min_p", C.c_int32), ("panel_group", C.c_int32),
                 ("asm_whole_n", C.c_int32), ("syrk_block16", C.c_int32), ("level_timing", C.c_int32),
+                ("syrk_stream", C.c_int32), ("reserved", C.c_int32),
                 ("workspace_fraction", C.c_double), ("pivot_tol", C.c_double)]
+
+
+class fd_factors(C.Structure):
+    """stfem_fd_factors (include/stfem_b200.h): device pointers of the temporal factors."""
+    _fields_ = [("nt", C.c_int32), ("lam", C.c_void_p), ("X", C.c_void_p), ("Y", C.c_void_p),
+                ("A_fwd", C.c_void_p), ("mrows_fwd", C.c_int32), ("rows_fwd", C.c_void_p),
+                ("scale_fwd", C.c_void_p), ("nsrc", C.c_int32), ("A_back", C.c_void_p),
+                ("mix_rows", C.c_void_p), ("mix_coef", C.c_void_p), ("nmix", C.c_int32)]
 
 
 _lib = None
@@ -89,6 +98,12 @@ def _declare(lib):
                                                 C.POINTER(I64)]),
         "stfem_factor_solve": (C.c_int, [P, P, P, P, I32, I32, P, P, bv_layout, P]),
         "stfem_plan_check": (C.c_int, [P, P]),
+        "stfem_comm_unique_id": (C.c_int, [P]),
+        "stfem_comm_init": (C.c_int, [P, I32, I32, C.POINTER(P)]),
+        "stfem_comm_destroy": (C.c_int, [P]),
+        "stfem_comm_info": (C.c_int, [P, C.POINTER(I32), C.POINTER(I32), C.POINTER(I32)]),
+        "stfem_comm_all_to_all": (C.c_int, [P, P, P, I64, P]),
+        "stfem_fdm_solve": (C.c_int, [P, P, P, P, C.POINTER(fd_factors), P, P, P, I32, P]),
         "stfem_plan_set_shift_base": (C.c_int, [P, I32]),
         "stfem_plan_reserve": (C.c_int, [P, I32, I32]),
         "stfem_plan_get_options": (C.c_int, [P, C.POINTER(plan_options)]),

@@ -65,7 +65,7 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
         for c, l in zip(cmds, logs):
             if l.strip():
                 print(os.path.basename(c[-3]), l, file=sys.stderr)
-    link = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-lcudart"]
+    link = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-lcudart", "-ldl"]
     run(link)
     os.replace(LIB + ".tmp", LIB)
     for o in objs:

@@ -347,6 +347,242 @@ __global__ void __launch_bounds__(128, 4) syrk32_kernel(LevelArgs a, const int4*
   }
 }
 
+// ---------------------------------------------------------------------------
+// Streamed 32 x 32-tile update engine (Schur updates and trailing pivot-column
+// updates): C = Cinit - A A^T on lower tiles, DMMA.
+//
+// The per-tile kernels above pay, for every tile, a chain of dependent
+// descriptor loads, the pipeline fill and the drain/epilogue with nothing to
+// overlap them but other CTAs in the same phase (measured: 59-75% of the DMMA
+// peak for K = 63-255 against 94% for the long-K transform GEMM).  Here one CTA
+// walks a contiguous range of tiles as ONE stream of 16-deep K chunks: the
+// 3-stage cp.async pipeline keeps running across tile boundaries (the first
+// chunks of tile j+1 are in flight while tile j finishes), the tile
+// descriptors are decoded once per CTA into shared memory, and the tile's
+// starting values Cinit -- the assembled block, or (GATHER) the children's
+// extend-add through the inverse maps -- are fetched by cp.async into a shared
+// staging tile during the tile's K loop and only added in the epilogue, so no
+// global-load latency sits on the accumulators' critical path.  Tiles are
+// ordered instance-major (all tiles of one (front, shift) consecutively), so
+// the L21 rows a CTA re-reads across its tiles stay in L1/L2.
+// ---------------------------------------------------------------------------
+constexpr int ST_MAXT = 16;                 // tiles per CTA (upper bound)
+constexpr int ST_CS = 32 * S32_LD;          // one staged C tile: Cs[col * S32_LD + row] (complex)
+
+struct __align__(16) StreamTile {
+  const cplx* A;        // multiplier rows: element (r, kk) at A[r + kk * lda]
+  cplx* C;              // C[row + col * ldC]
+  const cplx* Uc[2];    // GATHER: the children's update blocks
+  int lda, ldC, K, M, N, i0, c0;
+  int bc[2];            // GATHER: children's boundary orders
+  int inv_off[2];       // GATHER: a.inv offset of boundary row 0 for child s (-1: no such child)
+  int pad;
+};
+
+template <bool GATHER>
+constexpr int stream_smem_bytes() {
+  return 3 * 2 * S32_STAGE * 16 + (GATHER ? 2 : 1) * ST_CS * 16 + ST_MAXT * (int)sizeof(StreamTile);
+}
+
+template <bool GATHER>
+__device__ __forceinline__ void stream_tiles(const StreamTile* __restrict__ desc, int nt, cplx* As, cplx* Bs,
+                                             cplx* Cs, const int32_t* __restrict__ inv) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3, wm = warp & 1, wn = warp >> 1;
+  auto nk_of = [&](int j) { return (desc[j].K + 15) >> 4; };
+  auto skip = [&](int& j, int& c) {
+    while (j < nt && c >= nk_of(j)) {
+      ++j;
+      c = 0;
+    }
+  };
+  int lj = 0, lc = 0;   // load cursor: next (tile, chunk) to request
+  skip(lj, lc);
+  if (lj >= nt) return;
+  auto load_item = [&](int stage) {
+    const StreamTile& D = desc[lj];
+    const cplx* A = D.A;
+    const int lda = D.lda, K = D.K, M = D.M, N = D.N, i0 = D.i0, c0 = D.c0;
+    cplx* as = As + stage * S32_STAGE;
+    cplx* bs = Bs + stage * S32_STAGE;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = tid + 128 * u, m = idx & 31, kk = lc * 16 + (idx >> 5);
+      const bool oka = kk < K && i0 + m < M, okb = kk < K && c0 + m < N;
+      cp_async16(as + (idx >> 5) * S32_LD + m, oka ? A + i0 + m + (int64_t)kk * lda : A, oka);
+      cp_async16(bs + (idx >> 5) * S32_LD + m, okb ? A + c0 + m + (int64_t)kk * lda : A, okb);
+    }
+    ++lc;
+    skip(lj, lc);
+  };
+  // starting values of tile j into the staging tile(s): lower entries only, zero elsewhere
+  auto load_c = [&](int j) {
+    const StreamTile& D = desc[j];
+    const int M = D.M, N = D.N, i0 = D.i0, c0 = D.c0;
+    const int r = tid & 31, row = i0 + r;
+    if constexpr (GATHER) {
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int off = D.inv_off[s];
+        if (off < 0) continue;                                   // uniform: no such child
+        const cplx* Uc = D.Uc[s];
+        const int bc = D.bc[s];
+        const int kr = row < M ? inv[off + row] : -1;
+        int kc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int col = c0 + (tid >> 5) + 4 * u;
+          kc[u] = (col < N && row >= col) ? inv[off + col] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = (tid >> 5) + 4 * u;
+          const bool ok = kr >= 0 && kc[u] >= 0;
+          cp_async16(Cs + s * ST_CS + c * S32_LD + r, ok ? Uc + (int64_t)kc[u] * bc + kr : Uc, ok);
+        }
+      }
+    } else {
+      const cplx* C = D.C;
+      const int ldC = D.ldC;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = (tid >> 5) + 4 * u, col = c0 + c;
+        const bool ok = row < M && col < N && row >= col;
+        cp_async16(Cs + c * S32_LD + r, ok ? C + row + (int64_t)col * ldC : C, ok);
+      }
+    }
+  };
+  int cj = lj, cc = 0;   // compute cursor
+  load_c(cj);
+#pragma unroll
+  for (int st = 0; st < 2; ++st) {
+    if (lj < nt) load_item(st);
+    cp_async_commit();
+  }
+  double cre[2][4], cim[2][4];
+#pragma unroll
+  for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) cre[ni][e] = cim[ni][e] = 0.0;
+  int it = 0, pending_c = -1;
+  bool first = true;
+  while (cj < nt) {
+    cp_async_wait<1>();
+    __syncthreads();   // chunk `it` landed for everyone; stage (it - 1) % 3 and (after an epilogue) Cs are free
+    if (lj < nt) load_item((it + 2) % 3);
+    if (pending_c >= 0) {
+      load_c(pending_c);
+      pending_c = -1;
+    }
+    cp_async_commit();
+    const StreamTile& D = desc[cj];
+    const int M = D.M, N = D.N, i0 = D.i0, c0 = D.c0;
+    // warps whose 16 x 16 block lies strictly above the diagonal (diagonal tiles) or outside
+    // the block skip their DMMAs (warp-uniform; their outputs are never stored)
+    const bool wact = (i0 + wm * 16 + 15 >= c0 + wn * 16) && (i0 + wm * 16 < M) && (c0 + wn * 16 < N);
+    if (wact) {
+      const cplx* as = As + (it % 3) * S32_STAGE + t * S32_LD + wm * 16 + g;
+      const cplx* bs = Bs + (it % 3) * S32_STAGE + t * S32_LD + wn * 16 + g;
+#pragma unroll
+      for (int kk = 0; kk < 16; kk += 4) {
+        const cplx a0 = as[kk * S32_LD], a1 = as[kk * S32_LD + 8];
+        const cplx b0 = bs[kk * S32_LD], b1 = bs[kk * S32_LD + 8];
+        // four independent accumulator chains between dependent DMMAs
+        dmma_16x8x4(cre[0], -a0.re, -a1.re, b0.re);
+        dmma_16x8x4(cim[0], -a0.re, -a1.re, b0.im);
+        dmma_16x8x4(cre[1], -a0.re, -a1.re, b1.re);
+        dmma_16x8x4(cim[1], -a0.re, -a1.re, b1.im);
+        dmma_16x8x4(cre[0], a0.im, a1.im, b0.im);
+        dmma_16x8x4(cim[0], -a0.im, -a1.im, b0.re);
+        dmma_16x8x4(cre[1], a0.im, a1.im, b1.im);
+        dmma_16x8x4(cim[1], -a0.im, -a1.im, b1.re);
+      }
+    }
+    ++it;
+    ++cc;
+    const int nk = (D.K + 15) >> 4;
+    if (cc == nk) {
+      // a tile shorter than the pipeline: its staged starting values may still be in flight
+      if (nk < 3 && !first) {
+        cp_async_wait<0>();
+        __syncthreads();
+      }
+      first = false;
+      cplx* C = D.C;
+      const int ldC = D.ldC;
+      const bool two = GATHER && D.inv_off[1] >= 0, one = !GATHER || D.inv_off[0] >= 0;
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int r = wm * 16 + g + 8 * h, c = wn * 16 + ni * 8 + 2 * t + v;
+            const int row = i0 + r, col = c0 + c;
+            if (row < M && col < N && row >= col) {
+              cplx o = cmk(0.0, 0.0);
+              if (one) o = cadd(o, Cs[c * S32_LD + r]);                 // same sum order as asm_front_kernel
+              if (two) o = cadd(o, Cs[ST_CS + c * S32_LD + r]);
+              stc(C + row + (int64_t)col * ldC, cmk(o.re + cre[ni][2 * h + v], o.im + cim[ni][2 * h + v]));
+            }
+            cre[ni][2 * h + v] = 0.0;
+            cim[ni][2 * h + v] = 0.0;
+          }
+      ++cj;
+      cc = 0;
+      skip(cj, cc);
+      pending_c = cj < nt ? cj : -1;   // requested after the next iteration's barrier (Cs is read above)
+    }
+  }
+  cp_async_wait<0>();
+}
+
+// Schur update U = (F22 | children's extend-add) - L21 L21^T of a level: tile q of the launch is
+// (shift q / n32, tile q % n32 of the level's tile list); CTA x takes tiles [x T, (x + 1) T).
+template <bool GATHER>
+__global__ void __launch_bounds__(128, GATHER ? 2 : 3)
+    syrk_stream_kernel(LevelArgs a, const int4* __restrict__ tiles, int n32, long long total, int T) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* As = reinterpret_cast<cplx*>(smem_raw);
+  cplx* Bs = As + 3 * S32_STAGE;
+  cplx* Cs = Bs + 3 * S32_STAGE;
+  StreamTile* desc = reinterpret_cast<StreamTile*>(Cs + (GATHER ? 2 : 1) * ST_CS);
+  const long long q0 = (long long)blockIdx.x * T;
+  const int nt = (int)min((long long)T, total - q0);
+  for (int j = threadIdx.x; j < nt; j += 128) {
+    const long long q = q0 + j;
+    const int k = (int)(q / n32);
+    const int4 tl = tiles[q - (long long)k * n32];
+    const FrontDev F = a.fronts[tl.x];
+    const int n = F.n, p = F.p, b = n - p;
+    StreamTile D;
+    D.A = a.factor + (int64_t)k * a.fstride + F.fofs + p;   // L21: row r, column kk at A[r + kk n]
+    D.C = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
+    D.lda = n;
+    D.ldC = b;
+    D.K = p;
+    D.M = D.N = b;
+    D.i0 = tl.y * 32;
+    D.c0 = tl.z * 32;
+    D.pad = 0;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      D.Uc[s] = nullptr;
+      D.bc[s] = 0;
+      D.inv_off[s] = -1;
+      if (GATHER && s < F.nchild) {
+        const FrontDev Cf = a.fronts[a.child_ids[F.child_beg + s]];
+        D.bc[s] = Cf.n - Cf.p;
+        D.Uc[s] = a.uchild + (int64_t)k * a.uchild_stride + Cf.uofs;
+        D.inv_off[s] = F.inv_beg + s * n + p;
+      }
+    }
+    desc[j] = D;
+  }
+  __syncthreads();
+  stream_tiles<GATHER>(desc, nt, As, Bs, Cs, a.inv);
+}
+
 // 32 x 32-tile trailing pivot-column update (see panel_update_kernel for the
 // delayed-update regions): the narrow (32-column) updates no longer fill half
 // of a 64-wide tile with waste.
@@ -601,6 +837,12 @@ int set_kernel_attributes(int dev) {
   STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk32_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, S32_SMEM));
   STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk32_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, S32_SMEM));
   STFEM_CUDA_TRY(cudaFuncSetAttribute(panel_update32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, S32_SMEM));
+  STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_stream_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      stream_smem_bytes<false>()));
+  STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_stream_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      stream_smem_bytes<true>()));
+  STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_stream_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_stream_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_block16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       b16_smem_bytes(B16_BMAX)));
   return STFEM_OK;
@@ -1048,7 +1290,14 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
           }
         }
         if (n32 > 0 && a.asm_pivots_only) {
-          syrk32_kernel<true><<<(unsigned)(n32 * nb), 128, S32_SMEM, st>>>(a, P.d_syrk32_tiles + P.syrk32_off[d]);
+          if (P.opt.syrk_stream) {
+            const long long total = (long long)n32 * nb;
+            const int T = std::max(1, std::min(ST_MAXT, P.opt.syrk_stream));
+            syrk_stream_kernel<true><<<(unsigned)((total + T - 1) / T), 128, stream_smem_bytes<true>(), st>>>(
+                a, P.d_syrk32_tiles + P.syrk32_off[d], (int)n32, total, T);
+          } else {
+            syrk32_kernel<true><<<(unsigned)(n32 * nb), 128, S32_SMEM, st>>>(a, P.d_syrk32_tiles + P.syrk32_off[d]);
+          }
           STFEM_LAUNCH_CHECK("syrk32_kernel<gather>");
           ++nlaunch;
           fam(FAM_SYRK);
@@ -1058,7 +1307,14 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
           ++nlaunch;
           fam(FAM_SYRK);
         } else if (n32 > 0) {
-          syrk32_kernel<false><<<(unsigned)(n32 * nb), 128, S32_SMEM, st>>>(a, P.d_syrk32_tiles + P.syrk32_off[d]);
+          if (P.opt.syrk_stream) {
+            const long long total = (long long)n32 * nb;
+            const int T = std::max(1, std::min(ST_MAXT, P.opt.syrk_stream));
+            syrk_stream_kernel<false><<<(unsigned)((total + T - 1) / T), 128, stream_smem_bytes<false>(), st>>>(
+                a, P.d_syrk32_tiles + P.syrk32_off[d], (int)n32, total, T);
+          } else {
+            syrk32_kernel<false><<<(unsigned)(n32 * nb), 128, S32_SMEM, st>>>(a, P.d_syrk32_tiles + P.syrk32_off[d]);
+          }
           STFEM_LAUNCH_CHECK("syrk32_kernel");
           ++nlaunch;
           fam(FAM_SYRK);

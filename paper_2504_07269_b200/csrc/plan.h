@@ -92,6 +92,7 @@ struct Plan {
     o.asm_whole_n = INT32_MAX;
     o.syrk_block16 = 1;
     o.level_timing = 0;
+    o.syrk_stream = 8;
     o.workspace_fraction = 0.70;
     o.pivot_tol = 1e-10;
     return o;

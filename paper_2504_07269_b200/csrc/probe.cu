@@ -41,10 +41,40 @@ __global__ void __launch_bounds__(256) dfma_probe_kernel(double* sink, int iters
   if (s == 12345.678) sink[threadIdx.x] = s;
 }
 
+// DMMA and DFMA interleaved in every warp, equal pipe time each if both run at 16 FMA / clk /
+// sub-partition (8 DMMAs = 256 issue cycles, 128 DFMAs = 256): do the two FP64 paths share one
+// datapath (time doubles, ~37 TFLOP/s total) or add up (~70 TFLOP/s)?
+__global__ void __launch_bounds__(256) mixed_probe_kernel(double* sink, int iters) {
+  double c[8][4], d[16];
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, b0 = 1.0 - a0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) c[i][v] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) d[i] = i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      dmma_16x8x4(c[i], a0, a1, b0);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) d[j] = fma(d[j], b0, a0);
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) s += c[i][v];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += d[i];
+  if (s == 12345.678) sink[threadIdx.x] = s;
+}
+
 }  // namespace
 }  // namespace stfem
 
-// kind 0 = DMMA (flops = 2*16*8*4 per mma per warp), 1 = DFMA.  Returns the
+// kind 0 = DMMA (flops = 2*16*8*4 per mma per warp), 1 = DFMA, 2 = both interleaved.  Returns the
 // real fp64 flop count executed in *flops; caller times it with events.
 extern "C" int stfem_probe_launch(int kind, int blocks, int iters, double* sink, double* flops,
                                   void* stream) {
@@ -53,6 +83,9 @@ extern "C" int stfem_probe_launch(int kind, int blocks, int iters, double* sink,
   if (kind == 0) {
     stfem::dmma_probe_kernel<<<blocks, 256, 0, s>>>(sink, iters);
     *flops = warps * iters * 8.0 * (2.0 * 16 * 8 * 4);
+  } else if (kind == 2) {
+    stfem::mixed_probe_kernel<<<blocks, 256, 0, s>>>(sink, iters);
+    *flops = warps * iters * 8.0 * (2.0 * 16 * 8 * 4) + blocks * 256.0 * iters * 128.0 * 2.0;
   } else {
     stfem::dfma_probe_kernel<<<blocks, 256, 0, s>>>(sink, iters);
     *flops = blocks * 256.0 * iters * 8.0 * 2.0;

@@ -124,14 +124,120 @@ class DistributedFDM:
         if F_p.shape != (nt, nr, c):
             raise N.DimensionMismatch(N.ERR_DIM, f"shard {tuple(F_p.shape)} != {(nt, nr, c)}")
         out = out if out is not None else torch.empty_like(F_p)
-        t = [time.perf_counter()]
         fwd = getattr(self.backend, "transform_fwd", self.backend.transform)
         back = getattr(self.backend, "transform_back", self.backend.transform)
+        cuda = F_p.is_cuda
+        marks = []
+
+        def mark():
+            if timings is None:
+                return
+            if cuda:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record()
+                marks.append(ev)
+            else:
+                marks.append(time.perf_counter())
+
+        mark()
         fwd(self.Y, F_p.view(nt, nr * c), self.G.view(nt, nr * c))                         # (2)
+        mark()
         self._a2a(self.R, self.G)                                                           # a2a #1
+        mark()
         self.backend.factor_solve(self.lam_local, self.R, self.W, self.layout, nr)         # (3)
+        mark()
         self._a2a(self.G, self.W)                                                           # a2a #2
+        mark()
         back(self.X, self.G.view(nt, nr * c), out.view(nt, nr * c))                        # (4)
+        mark()
+        if timings is not None:
+            if cuda:
+                marks[-1].synchronize()
+                dt = [marks[i].elapsed_time(marks[i + 1]) / 1e3 for i in range(5)]
+            else:
+                dt = [marks[i + 1] - marks[i] for i in range(5)]
+            for k, v in zip(("forward_transform_s", "a2a_fwd_s", "factor_solve_s", "a2a_back_s",
+                             "back_transform_s"), dt):
+                timings[k] = v
+            timings["a2a_bytes_each_way"] = 16 * nt * nr * c * (self.P - 1) // self.P
+        return out
+
+
+class NativeComm:
+    """stfem_comm: the library's own NCCL communicator (include/stfem_b200.h).  Rank 0 draws
+    the unique id, torch.distributed (any backend) carries its 128 bytes to the other ranks --
+    the "unique id broadcast through the torch store" of SURVEY.md §8b."""
+
+    def __init__(self, group=None):
+        import ctypes as C
+        N.require_cuda()
+        self.nranks = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if self.rank == 0:
+            buf = (C.c_uint8 * 128)()
+            N.check(N.lib().stfem_comm_unique_id(buf))
+            uid = torch.tensor(list(buf), dtype=torch.uint8)
+        if self.nranks > 1:
+            backend = dist.get_backend(group)
+            t = uid.cuda() if backend == "nccl" else uid
+            dist.broadcast(t, 0, group=group)
+            uid = t.cpu()
+        raw = (C.c_uint8 * 128)(*uid.tolist())
+        h = C.c_void_p()
+        N.check(N.lib().stfem_comm_init(raw, self.nranks, self.rank, C.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self) -> dict:
+        import ctypes as C
+        a, b, v = C.c_int32(), C.c_int32(), C.c_int32()
+        N.check(N.lib().stfem_comm_info(self._h, C.byref(a), C.byref(b), C.byref(v)))
+        return {"nranks": a.value, "rank": b.value, "nccl_version": v.value}
+
+    def all_to_all(self, send: torch.Tensor, recv: torch.Tensor, stream=None):
+        count = send.numel() // self.nranks
+        N.check(N.lib().stfem_comm_all_to_all(self._h, N.ptr(send), N.ptr(recv), count, N.stream_ptr(stream)))
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and N._lib is not None:
+            N._lib.stfem_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+class NativeShardedFDM:
+    """The sharded FD solve through ONE C-ABI call per solve (stfem_fdm_solve with a
+    stfem_comm): transforms, both exchanges and the local factor + solve are enqueued by the
+    library on the caller's stream.  Same shard layout as DistributedFDM: (n_t, n_rhs, c)."""
+
+    def __init__(self, fdm, nrhs: int, comm: NativeComm):
+        self.fdm, self.comm, self.nrhs = fdm, comm, nrhs
+        self.P, self.rank = comm.nranks, comm.rank
+        if fdm.nt % self.P:
+            raise N.DimensionMismatch(N.ERR_DIM, f"n_t={fdm.nt} must be divisible by the world size {self.P}")
+        self.c = shard_cols(fdm.ops.n, self.P)
+        self.work = torch.empty((fdm.nt, nrhs, self.c), dtype=C128, device=fdm.X.device)
+        fdm.plan.prepare()
+        fdm.plan.reserve(fdm.nt // self.P, nrhs)
+
+    def solve(self, F_p: torch.Tensor, out: torch.Tensor | None = None, stream=None, check: bool = True):
+        import ctypes as C
+        shape = (self.fdm.nt, self.nrhs, self.c)
+        if tuple(F_p.shape) != shape or not F_p.is_contiguous():
+            raise N.DimensionMismatch(N.ERR_DIM, f"shard {tuple(F_p.shape)} != {shape}")
+        out = out if out is not None else torch.empty_like(F_p)
+        fdm = self.fdm
+        N.check(N.lib().stfem_fdm_solve(fdm.plan.handle, self.comm.handle, N.ptr(fdm.ops.Mvals), N.ptr(fdm.ops.Avals),
+                                        C.byref(fdm.fd_factors()), N.ptr(F_p), N.ptr(out), N.ptr(self.work),
+                                        self.nrhs, N.stream_ptr(stream)))
+        if check:
+            fdm.plan.check(stream)
         return out
 
 
@@ -182,7 +288,8 @@ def bench_main(args):
     if pf is not None:
         Yt = torch.as_tensor(pf.Y, dtype=C128, device=dev)
     pairs = PT.DevicePairs(pf, dev) if pf is not None else None
-    plan = SpatialPlan(prob.ops)
+    # host setup of the spectral subtrees: this rank's share of the host cores, not all of them
+    plan = SpatialPlan(prob.ops, spectral_threads=max(1, len(os.sched_getaffinity(0)) // max(1, local_world_size())))
     t_setup = time.perf_counter() - t1
     solver = DistributedFDM(prob.nx, nt, prob.n_rhs, Xt, Yt, lt, CudaBackend(plan, pairs))
     # this rank's RHS shard: deterministic part on device + Gaussian columns from the shared streams
@@ -284,7 +391,14 @@ def _local_rhs(prob, rank, world, dev):
     Fp = torch.zeros((nt, prob.n_rhs, c), dtype=C128, device=dev)
     for i, part in enumerate(parts):
         Fp[:, i, :hi - lo] = part
-    if prob.cfg.n_gauss:
-        g = gaussian_rhs(prob.seed, prob.cfg.n_gauss, nt, nx)
-        Fp[:, len(parts):, :hi - lo] = torch.from_numpy(np.ascontiguousarray(g[:, :, lo:hi].transpose(1, 0, 2))).to(dev)
+    if prob.cfg.n_gauss and hi > lo:
+        # only this rank's columns are drawn (per-column-block streams): (n_gauss, n_t, hi - lo)
+        threads = max(1, len(os.sched_getaffinity(0)) // max(1, local_world_size()))
+        g = gaussian_rhs(prob.seed, prob.cfg.n_gauss, nt, nx, cols=(lo, hi), threads=threads)
+        Fp[:, len(parts):, :hi - lo] = torch.from_numpy(g).to(dev).permute(1, 0, 2)
     return Fp
+
+
+def local_world_size() -> int:
+    """Ranks sharing this host's cores (torchrun exports LOCAL_WORLD_SIZE)."""
+    return int(os.environ.get("LOCAL_WORLD_SIZE", os.environ.get("WORLD_SIZE", "1")))

@@ -136,10 +136,27 @@ class FDMSolver:
         self.lam = torch.as_tensor(lam, dtype=C128, device=dev)
         self.t_eig = time.perf_counter() - t2 + t1 - t0
         self.t_symbolic = t2 - t1
+        self._ffi = None
 
     @property
     def kappa2(self) -> float:
         return self.tf.kappa2
+
+    def fd_factors(self) -> N.fd_factors:
+        """stfem_fd_factors over this solver's device-resident temporal factors."""
+        if self._ffi is None:
+            f = N.fd_factors()
+            f.nt = self.nt
+            f.lam = self.lam.data_ptr()
+            f.X, f.Y = self.X.data_ptr(), self.Y.data_ptr()
+            if self.pairs is not None:
+                p = self.pairs
+                f.A_fwd, f.mrows_fwd = p.A_fwd.data_ptr(), p.mrows_fwd
+                f.rows_fwd, f.scale_fwd, f.nsrc = p.rows_fwd.data_ptr(), p.scale_fwd.data_ptr(), p.rows_fwd.shape[0]
+                f.A_back = p.A_back.data_ptr()
+                f.mix_rows, f.mix_coef, f.nmix = p.mix_rows.data_ptr(), p.mix_coef.data_ptr(), p.mix_rows.shape[0]
+            self._ffi = f
+        return self._ffi
 
     def forward_transform(self, F: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
         """G = (Y (x) I) F (step 2): K3p when the eigenvalues pair, else K3."""
@@ -171,6 +188,18 @@ class FDMSolver:
         if len({Fb.data_ptr(), G.data_ptr(), W.data_ptr()}) != 3:
             raise ValueError("solve: F, out and work must be three distinct buffers")
         s = stream if stream is not None else torch.cuda.current_stream()
+        if timings is None:
+            # the product path: steps 2-4 behind ONE C-ABI call (stfem_fdm_solve); the staged
+            # path below runs the same three entry points with CUDA events in between
+            self.plan.prepare()
+            N.check(N.lib().stfem_fdm_solve(self.plan.handle, None, N.ptr(self.ops.Mvals), N.ptr(self.ops.Avals),
+                                            C.byref(self.fd_factors()), N.ptr(Fb), N.ptr(G), N.ptr(W), nr,
+                                            N.stream_ptr(s)))
+            if check:
+                self.plan.check(s)
+            if out is not None:
+                return out
+            return G[0] if single else G
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timings is not None else None
         if ev:
             ev[0].record(s)

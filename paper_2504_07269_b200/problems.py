@@ -8,8 +8,9 @@ Conventions:
   C5  L-shape h=1/256, P1 x P1, T=1, N=1024, f=0, lifted wave packet psi0 + 8 Gaussian RHS
   paper0  square(32), T=5, N=64, the paper's manufactured solution
 s(x) = sin(pi x1) sin(pi x2).  Gaussian RHS = (N(0,1) + i N(0,1))/sqrt(2),
-drawn in chunks of 16 temporal rows from numpy default_rng((seed, rhs, chunk))
-(deterministic for any thread count).  The public benchmark suite of the
+drawn per block of 16 temporal rows x 8192 spatial columns from numpy
+default_rng((seed, rhs, row block, column block)) (deterministic for any thread
+count and any spatial sharding).  The public benchmark suite of the
 paper is not used: these are the seeded synthetic stand-ins BASELINE.json
 names.
 """
@@ -80,25 +81,38 @@ def psi0_interior(mesh: sm.SpatialMesh) -> np.ndarray:
     return wave_packet(v[:, 0], v[:, 1])
 
 
+COLS_PER_BLOCK = 8192
+
+
 def gaussian_rhs(seed: int, n_rhs: int, nt: int, nx: int, out: np.ndarray | None = None,
-                 threads: int | None = None) -> np.ndarray:
-    """(n_rhs, nt, nx) complex128 seeded Gaussian stack, chunked RNG streams."""
+                 threads: int | None = None, cols: tuple[int, int] | None = None) -> np.ndarray:
+    """(n_rhs, nt, hi - lo) complex128 seeded Gaussian stack for the spatial columns
+    cols = [lo, hi) (default: all n_x columns).  One RNG stream per (rhs, block of 16
+    temporal rows, block of 8192 columns): every entry depends only on the seed and its
+    own indices, so a spatial shard generates exactly its columns (no rank ever builds the
+    full stack) and the result is the same for any thread count or sharding."""
+    lo, hi = (0, nx) if cols is None else (max(0, cols[0]), min(nx, cols[1]))
+    w = max(0, hi - lo)
     if out is None:
-        out = np.empty((n_rhs, nt, nx), dtype=np.complex128)
-    view = out.view(np.float64).reshape(n_rhs, nt, nx, 2)
-    jobs = [(r, c) for r in range(n_rhs) for c in range(0, nt, ROWS_PER_CHUNK)]
+        out = np.empty((n_rhs, nt, w), dtype=np.complex128)
+    assert out.shape == (n_rhs, nt, w)
+    view = out.view(np.float64).reshape(n_rhs, nt, w, 2)
+    jobs = [(r, c, b) for r in range(n_rhs) for c in range(0, nt, ROWS_PER_CHUNK)
+            for b in range(lo // COLS_PER_BLOCK, -(-hi // COLS_PER_BLOCK) if w else 0)]
     scale = 1.0 / math.sqrt(2.0)
 
     def work(job):
-        r, c0 = job
+        r, c0, b = job
         c1 = min(nt, c0 + ROWS_PER_CHUNK)
-        rng = np.random.default_rng((seed, r, c0 // ROWS_PER_CHUNK))
-        re = rng.standard_normal((c1 - c0, nx))
-        im = rng.standard_normal((c1 - c0, nx))
-        view[r, c0:c1, :, 0] = re * scale
-        view[r, c0:c1, :, 1] = im * scale
+        b0, b1 = b * COLS_PER_BLOCK, min(nx, (b + 1) * COLS_PER_BLOCK)
+        rng = np.random.default_rng((seed, r, c0 // ROWS_PER_CHUNK, b))
+        re = rng.standard_normal((c1 - c0, b1 - b0))
+        im = rng.standard_normal((c1 - c0, b1 - b0))
+        s0, s1 = max(lo, b0), min(hi, b1)
+        view[r, c0:c1, s0 - lo:s1 - lo, 0] = re[:, s0 - b0:s1 - b0] * scale
+        view[r, c0:c1, s0 - lo:s1 - lo, 1] = im[:, s0 - b0:s1 - b0] * scale
 
-    nthr = threads or min(32, os.cpu_count() or 1)
+    nthr = threads or min(32, len(os.sched_getaffinity(0)))
     if nthr > 1 and len(jobs) > 1:
         with ThreadPoolExecutor(nthr) as ex:
             list(ex.map(work, jobs))

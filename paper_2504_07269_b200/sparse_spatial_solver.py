@@ -87,6 +87,14 @@ class SpatialPlan:
             self._attach_spectral()
         N.check(N.lib().stfem_plan_reserve(self._h, int(nshift), int(min(nrhs, self.max_rhs()))))
 
+    def prepare(self):
+        """Bring the value-dependent plan data up to date with the operators (spectral subtree
+        data are rebuilt when ops.assemble() produced new values) before a direct C-ABI call."""
+        if self.ops.Mvals is None:
+            raise RuntimeError("spatial operators are not assembled")
+        if self.spectral_m > 0 and self._spectral_key != self._ops_key():
+            self._attach_spectral()
+
     def max_rhs(self) -> int:
         mr = C.c_int32()
         N.check(N.lib().stfem_plan_max_rhs(self._h, C.byref(mr)))

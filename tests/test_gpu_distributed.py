@@ -59,3 +59,45 @@ def test_distributed_world1_matches_fdm():
     solver = D.DistributedFDM(ops.n, 16, 2, fdm.X, fdm.Y, fdm.lam, D.CudaBackend(fdm.plan))
     out = D.unshard(solver.solve(D.shard_rhs(F, 0, 1)), ops.n, 0, 1).cpu().numpy()
     assert np.linalg.norm(out - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
+def test_fdm_solve_c_abi_matches_staged_path():
+    """stfem_fdm_solve (one C call: the product path of FDMSolver.solve) = the three staged
+    entry points (transform, factor_solve, transform), bit for bit; paired and plain K3."""
+    mesh = sm.build_structured_square(24)
+    ops = fa.assemble_spatial(mesh)
+    Mt, Bt = fa.assemble_temporal(tm.uniform(1.0, 16))
+    rng = np.random.default_rng(2)
+    F = torch.from_numpy(rng.standard_normal((3, 16, ops.n)) + 1j * rng.standard_normal((3, 16, ops.n))).cuda()
+    for paired in (True, False):
+        fdm = ks.FDMSolver(ops, Mt, Bt, paired=paired)
+        assert (fdm.pairs is not None) == paired
+        one_call = fdm.solve(F)
+        staged = fdm.solve(F, timings={})
+        assert torch.equal(one_call, staged)
+
+
+def test_native_comm_sharded_solve_world1():
+    """stfem_comm_init (NCCL bound at run time, one rank) + the sharded branch of
+    stfem_fdm_solve: shard layout (n_t, n_rhs, c), both exchanges through ncclSend/ncclRecv,
+    factor + solve from the receive buffer's chunked layout."""
+    mesh = sm.build_structured_square(24)
+    ops = fa.assemble_spatial(mesh)
+    Mt, Bt = fa.assemble_temporal(tm.uniform(1.0, 16))
+    fdm = ks.FDMSolver(ops, Mt, Bt)
+    rng = np.random.default_rng(3)
+    F = torch.from_numpy(rng.standard_normal((2, 16, ops.n)) + 1j * rng.standard_normal((2, 16, ops.n))).cuda()
+    ref = fdm.solve(F)
+    comm = D.NativeComm()
+    info = comm.info()
+    assert info["nranks"] == 1 and info["rank"] == 0 and info["nccl_version"] >= 20000
+    # the exchange itself: one rank sends its only block to itself
+    a = torch.arange(10, dtype=torch.float64, device="cuda").to(torch.complex128)
+    b = torch.zeros_like(a)
+    comm.all_to_all(a, b)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    solver = D.NativeShardedFDM(fdm, 2, comm)
+    out = D.unshard(solver.solve(D.shard_rhs(F, 0, 1)), ops.n, 0, 1).contiguous()
+    assert torch.equal(out, ref)
+    comm.close()

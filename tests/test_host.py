@@ -80,6 +80,14 @@ def test_gaussian_rhs_deterministic_across_threads():
     assert abs(np.mean(np.abs(a) ** 2) - 1.0) < 0.1
 
 
+def test_gaussian_rhs_column_shards_match_full_stack():
+    """A spatial shard draws exactly its columns (multi-GPU ranks never build the full stack)."""
+    full = problems.gaussian_rhs(3, 2, 40, 20000)
+    for lo, hi in ((0, 2500), (5000, 17000), (17500, 20000), (8191, 8193)):
+        part = problems.gaussian_rhs(3, 2, 40, 20000, cols=(lo, hi), threads=2)
+        assert np.array_equal(full[:, :, lo:hi], part)
+
+
 def test_config_sizes():
     """BASELINE.json configs: n_x and n_t."""
     want = {"C1": (225, 16), "C2": (3969, 64), "C3": (65025, 256), "C4": (261121, 1024), "C5": (195585, 1024)}

@@ -34,11 +34,11 @@ def main():
     sm = torch.cuda.get_device_properties(0).multi_processor_count
     sink = torch.zeros(256, dtype=torch.float64, device="cuda")
     res = {"sm_count": sm}
-    for kind, name in ((0, "dmma"), (1, "dfma")):
+    for kind, name in ((0, "dmma"), (1, "dfma"), (2, "dmma_dfma_mixed")):
         best = 0
         for cps in (1, 2, 4):
             fl = C.c_double()
-            iters = 20000 if kind == 0 else 100000
+            iters = 100000 if kind == 1 else (5000 if kind == 2 else 20000)
 
             def run():
                 N.check(lib.stfem_probe_launch(kind, sm * cps, iters, C.c_void_p(sink.data_ptr()), C.byref(fl),
