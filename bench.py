@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sample-shifts", type=int, default=0)
+    ap.add_argument("--proxy-ranks", type=int, default=0,
+                    help="one-GPU proxy of a P-rank run: time ONE rank's share (transforms on n_x/P columns, "
+                         "n_t/P shifts, the exchange volume) and print the predicted P-GPU time")
     ap.add_argument("--variant", default="fd", choices=["fd", "bs"],
                     help="fd: fast diagonalization (the headline path); bs: Bartels-Stewart sweep (SPEC.md:377)")
     return ap.parse_args()
@@ -373,9 +376,86 @@ def run_ours_bs(args):
     print(json.dumps(line), flush=True)
 
 
+def run_proxy(args):
+    """One-GPU proxy of a P-rank sharded FD solve (no multi-GPU box in this run).
+    One rank's work is timed for real on this GPU: K3p forward + back on its c = ceil(n_x / P)
+    spatial columns, factor + solve of its n_t / P shifts (all columns), and two device-to-device
+    copies of its exchange volume as a stand-in for the NCCL all-to-alls, whose NVLink time is
+    also modelled (bytes / 900 GB/s per direction x 0.7 efficiency).  Every rank does the same
+    amount of work, so predicted P-GPU step = the sum; predicted speed-up = measured 1-GPU step /
+    that.  A prediction, labelled as such: not a multi-GPU measurement."""
+    import torch
+    from paper_2504_07269_b200 import kronecker_solver as ks
+    from paper_2504_07269_b200.problems import Problem
+    from paper_2504_07269_b200.sparse_spatial_solver import blockvector_layout
+    torch.cuda.set_device(0)
+    prob = Problem(args.workload, device="cuda", rhs_host=False)
+    fdm = ks.FDMSolver(prob.ops, prob.M_t, prob.B_t)
+    F = prob.F
+    nr, nt, nx = F.shape
+    G, W = torch.empty_like(F), torch.empty_like(F)
+    stream = torch.cuda.current_stream()
+
+    def timed(fn, reps):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / 1e3 / reps
+
+    fdm.plan.reserve(nt, nr)
+    t1 = timed(lambda: fdm.solve(F, out=W, work=G, stream=stream, check=False), max(2, args.steps))
+    fdm.plan.check(stream)
+    rows = []
+    for P in [p for p in (2, 4, 8) if p <= args.proxy_ranks and nt % p == 0]:
+        c, ntl = -(-nx // P), nt // P
+        Fc, Gc, Wc = F[..., :c], G[..., :c], W[..., :c]
+        t_fwd = timed(lambda: fdm.forward_transform(Fc, Gc, stream), 5)
+        t_back = timed(lambda: fdm.back_transform(Wc, Gc, stream), 5)
+        lam = fdm.lam[:ntl].contiguous()
+        Gl, Wl = G[:, :ntl].contiguous(), W[:, :ntl].contiguous()
+        lay = blockvector_layout(ntl, nx)
+        t_fs = timed(lambda: fdm.plan.factor_solve(lam, Gl, Wl, lay, nr, stream=stream, check=False),
+                     max(2, args.steps))
+        fdm.plan.check(stream)
+        a2a_bytes = 16 * nt * nr * c * (P - 1) // P           # leaves (and enters) each rank, each way
+        src = torch.empty(a2a_bytes, dtype=torch.uint8, device="cuda")
+        dst = torch.empty_like(src)
+        t_copy = timed(lambda: dst.copy_(src), 5)
+        t_nvl = a2a_bytes / (900e9 * 0.7)
+        tP = t_fwd + t_fs + t_back + 2 * t_nvl
+        rows.append({"ranks": P, "cols_per_rank": c, "shifts_per_rank": ntl, "forward_s": t_fwd, "back_s": t_back,
+                     "factor_solve_s": t_fs, "a2a_bytes_each_way": a2a_bytes, "a2a_device_copy_s": t_copy,
+                     "a2a_nvlink_model_s": t_nvl, "predicted_step_s": tP, "predicted_speedup": t1 / tP,
+                     "predicted_efficiency": t1 / tP / P,
+                     "factor_solve_vs_ideal": fdm_fs_share(t1, t_fs, P)})
+        del src, dst
+    dofs = nx * nt * nr
+    line = {"metric": "space-time DoF/s (complex fp64) of the FDM direct solve", "impl": "proxy",
+            "note": "one-GPU PROXY of the sharded multi-GPU path: per-rank work measured on one B200, exchange "
+                    "modelled at NVLink rates; not a multi-GPU measurement",
+            "config": config_dict(args.workload, nx, nt, nr), "n_gpus": 1, "one_gpu_step_s": t1,
+            "one_gpu_value": dofs / t1, "proxy": rows,
+            "host_setup_s": {"eig": fdm.t_eig, "spatial": fdm.t_symbolic, "wall": fdm.t_setup,
+                             "note": "replicated on every rank (eig could be broadcast from rank 0)"}}
+    print(json.dumps(line), flush=True)
+
+
+def fdm_fs_share(t1, t_fs, P):
+    """How far the per-rank factor+solve is from 1/P of a full solve (1.0 = perfect)."""
+    return (t1 / P) / t_fs if t_fs > 0 else None
+
+
 def run_ours(args):
     import torch
     rank, world, local = dist_env()
+    if args.proxy_ranks:
+        return run_proxy(args)
     if args.variant == "bs":
         return run_ours_bs(args)
     if world > 1 or os.environ.get("STFEM_DIST_BENCH"):   # the env var runs the sharded path at world 1 (tests)

@@ -186,9 +186,9 @@ typedef struct {
   int32_t asm_whole_n;       /* fronts of order <= this are assembled by one CTA.  Default INT32_MAX */
   int32_t syrk_block16;      /* 1: short-K Schur updates (p <= 32, b <= 208) on 16 x 16 blocks.  Default 1 */
   int32_t level_timing;      /* 1: print per-launch CUDA-event times to stderr (diagnostics) */
-  int32_t syrk_stream;       /* tiles per CTA of the streamed Schur-update kernel (1..16); 0 = the per-tile
-                                kernel.  Default 8 */
-  int32_t reserved;
+  int32_t syrk_stream;       /* Schur-update kernel: -T = warp-specialised, TMA-fed, T tiles per CTA (1..16);
+                                +T = cp.async stream over T tiles; 0 = one tile per CTA */
+  int32_t ws_stages;         /* ring depth of the warp-specialised kernel (2, 3 or 4).  Default 2 */
   double workspace_fraction; /* share of the free device memory the numeric workspace may take.  Default 0.70 */
   double pivot_tol;          /* relative pivot-collapse threshold (see stfem_plan_check).  Default 1e-10 */
 } stfem_plan_options;

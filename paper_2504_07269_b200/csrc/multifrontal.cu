@@ -583,6 +583,293 @@ __global__ void __launch_bounds__(128, GATHER ? 2 : 3)
   stream_tiles<GATHER>(desc, nt, As, Bs, Cs, a.inv);
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised, TMA-fed update engine: C = Cinit - A A^T on lower 32 x 32
+// tiles (Schur updates; DMMA).  One producer warp feeds a 4-stage ring of
+// 16-deep K chunks with 1-D bulk copies (cp.async.bulk, the TMA engine: one
+// 512-byte column segment per lane, completion counted in bytes on the
+// stage's "full" mbarrier); four consumer warps (2 x 2 of 16 x 16) do nothing
+// but wait on "full", LDS, DMMA and release the stage on its "empty" mbarrier
+// -- no address arithmetic, no cp.async issue, no CTA-wide barrier in the
+// DMMA warps, and every consumer warp runs on its own (a delayed warp stalls
+// nobody else).  The ring runs across tile boundaries (a CTA walks up to 16
+// tiles), so pipeline fill / drain and descriptor latency are paid once per
+// CTA.  The tile's starting values -- the assembled block (bulk copies), or
+// with GATHER the children's extend-add (16-byte cp.async through the inverse
+// maps, completion forwarded to the "cfull" mbarrier) -- are staged in shared
+// memory by the producer during the tile's K loop and added in the epilogue.
+// A DMMA needs no second warp to hide its latency (measured: one warp per SM
+// sub-partition with a single dependent accumulator chain reaches 36.8 of
+// 37.1 TFLOP/s, tools/probe_dmma.py), so 2 CTAs x 4 consumer warps per SM are
+// enough to keep the pipe busy through the other CTA's epilogues.
+// ---------------------------------------------------------------------------
+// warps 0-3: DMMA consumers (2 x 2 of 16 x 16); warp 4: bulk copies of the A rows of every chunk;
+// warp 5: the B rows; warp 6: the tile's starting values.  (Measured on C4, 384 shifts, depths 1-6,
+// ms per batch: one bulk-copy warp for A and B 91.0 -- its 32 UBLKCPs per chunk issue one by one,
+// their operands being uniform registers -- two warps 79.4, four 81.3; a cp.async producer 86.9;
+// staging the starting values from the A warp instead of a third warp cost another 8 ms.)
+constexpr int WS_THREADS = 224;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.b32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// a wait that cannot hang the GPU: a protocol bug traps (kernel error) instead of spinning forever
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  for (uint32_t spin = 0; !mbar_try_wait(b, parity); ++spin)
+    if (spin > (1u << 28)) __trap();
+}
+// 1-D bulk copy global -> shared (TMA engine), bytes a multiple of 16, both addresses 16-byte aligned
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(b))
+               : "memory");
+}
+// arrive on b once every cp.async this thread issued so far has landed (counts as one expected arrival)
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+
+template <bool GATHER, int WS_STAGES>
+constexpr int ws_smem_bytes() {
+  return WS_STAGES * 2 * S32_STAGE * 16 + (GATHER ? 2 : 1) * ST_CS * 16 + ST_MAXT * (int)sizeof(StreamTile) +
+         (2 * WS_STAGES + 2) * 8;
+}
+
+template <bool GATHER, int WS_STAGES>
+__device__ __forceinline__ void ws_tiles(const StreamTile* __restrict__ desc, int nt, cplx* As, cplx* Bs, cplx* Cs,
+                                         uint64_t* full, uint64_t* empty, uint64_t* cfull, uint64_t* cempty,
+                                         const int32_t* __restrict__ inv) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (warp == 6) {
+    // ---------------- starting values: one staging tile (two with GATHER) per tile ----------------
+    uint32_t cphase = 0;
+    for (int j = 0; j < nt; ++j) {
+      const StreamTile& D = desc[j];
+      if (D.K <= 0) continue;
+      const int M = D.M, N = D.N, i0 = D.i0, c0 = D.c0;
+      mbar_wait(cempty, cphase ^ 1);   // the consumers have read the previous tile's values
+      cphase ^= 1;
+      if constexpr (GATHER) {
+        // the children's extend-add through the inverse maps: lane = tile row; the column map is
+        // loaded once (lane = column) and broadcast
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const int off = D.inv_off[s];
+          if (off < 0) continue;
+          const cplx* Uc = D.Uc[s];
+          const int bc = D.bc[s];
+          const int kr = (i0 + lane < M) ? inv[off + i0 + lane] : -1;
+          const int kcl = (c0 + lane < N) ? inv[off + c0 + lane] : -1;
+          cplx* dst = Cs + s * ST_CS + lane;
+#pragma unroll 8
+          for (int cc = 0; cc < 32; ++cc) {
+            const int kc = __shfl_sync(0xffffffffu, kcl, cc);
+            const bool ok = kr >= 0 && kc >= 0 && i0 + lane >= c0 + cc;
+            cp_async16(dst + cc * S32_LD, ok ? Uc + (int64_t)kc * bc + kr : Uc, ok);
+          }
+        }
+        cp_async_mbar_arrive(cfull);   // 32 expected arrivals: one per lane, when its copies have landed
+      } else {
+        const int ncol = min(32, N - c0), rows = min(32, M - i0);
+        if (lane == 0) mbar_arrive_expect_tx(cfull, (uint32_t)ncol * (uint32_t)rows * 16u);
+        __syncwarp();
+        if (lane < ncol)
+          bulk_g2s(Cs + lane * S32_LD, D.C + i0 + (int64_t)(c0 + lane) * D.ldC, (uint32_t)rows * 16u, cfull);
+      }
+    }
+    return;
+  }
+  if (warp >= 4) {
+    // ---------------- K chunks: warp 4 copies the A rows, warp 5 the B rows (lane = column) ----------------
+    const int isB = warp - 4;
+    cplx* ring = isB ? Bs : As;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int j = 0; j < nt; ++j) {
+      const StreamTile& D = desc[j];
+      const int K = D.K, nk = (K + 15) >> 4;
+      if (nk == 0) continue;
+      const int lda = D.lda;
+      const int r0 = isB ? D.c0 : D.i0, rows = min(32, (isB ? D.N : D.M) - r0);
+      const cplx* src0 = D.A + r0 + (int64_t)lane * lda;
+      const uint32_t myb = (uint32_t)rows * 16u;
+      for (int c = 0; c < nk; ++c) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        const int kv = min(16, K - c * 16);   // columns >= kv are not copied: the consumers mask them
+        if (lane == 0) mbar_arrive_expect_tx(&full[stage], (uint32_t)kv * myb);
+        __syncwarp();
+        if (lane < kv) bulk_g2s(ring + stage * S32_STAGE + lane * S32_LD, src0 + (int64_t)(c * 16) * lda, myb, &full[stage]);
+        if (++stage == WS_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    return;
+  }
+  // ---------------- consumers ----------------
+  const int g = lane >> 2, t = lane & 3, wm = warp & 1, wn = warp >> 1;
+  int stage = 0;
+  uint32_t phase = 0, cphase = 0;
+  for (int j = 0; j < nt; ++j) {
+    const StreamTile& D = desc[j];
+    const int K = D.K, nk = (K + 15) >> 4;
+    if (nk == 0) continue;
+    const int M = D.M, N = D.N, i0 = D.i0, c0 = D.c0;
+    // warps whose 16 x 16 block lies strictly above the diagonal (diagonal tiles) or outside
+    // the block skip their DMMAs (warp-uniform; their outputs are never stored)
+    const bool wact = (i0 + wm * 16 + 15 >= c0 + wn * 16) && (i0 + wm * 16 < M) && (c0 + wn * 16 < N);
+    double cre[2][4], cim[2][4];
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) cre[ni][e] = cim[ni][e] = 0.0;
+    for (int c = 0; c < nk; ++c) {
+      mbar_wait(&full[stage], phase);
+      if (wact) {
+        const cplx* as = As + stage * S32_STAGE + t * S32_LD + wm * 16 + g;
+        const cplx* bs = Bs + stage * S32_STAGE + t * S32_LD + wn * 16 + g;
+        const int kv = K - c * 16;   // valid k columns of this chunk (>= 16: all)
+        if (kv >= 16) {
+#pragma unroll
+          for (int kk = 0; kk < 16; kk += 4) {
+            const cplx a0 = as[kk * S32_LD], a1 = as[kk * S32_LD + 8];
+            const cplx b0 = bs[kk * S32_LD], b1 = bs[kk * S32_LD + 8];
+            dmma_16x8x4(cre[0], -a0.re, -a1.re, b0.re);
+            dmma_16x8x4(cim[0], -a0.re, -a1.re, b0.im);
+            dmma_16x8x4(cre[1], -a0.re, -a1.re, b1.re);
+            dmma_16x8x4(cim[1], -a0.re, -a1.re, b1.im);
+            dmma_16x8x4(cre[0], a0.im, a1.im, b0.im);
+            dmma_16x8x4(cim[0], -a0.im, -a1.im, b0.re);
+            dmma_16x8x4(cre[1], a0.im, a1.im, b1.im);
+            dmma_16x8x4(cim[1], -a0.im, -a1.im, b1.re);
+          }
+        } else {
+          // K tail: columns >= kv of the stage were not copied (stale data): masked out
+          for (int kk = 0; kk < kv; kk += 4) {
+            const bool ok = kk + t < kv;
+            const cplx z = cmk(0.0, 0.0);
+            const cplx a0 = ok ? as[kk * S32_LD] : z, a1 = ok ? as[kk * S32_LD + 8] : z;
+            const cplx b0 = ok ? bs[kk * S32_LD] : z, b1 = ok ? bs[kk * S32_LD + 8] : z;
+            dmma_16x8x4(cre[0], -a0.re, -a1.re, b0.re);
+            dmma_16x8x4(cim[0], -a0.re, -a1.re, b0.im);
+            dmma_16x8x4(cre[1], -a0.re, -a1.re, b1.re);
+            dmma_16x8x4(cim[1], -a0.re, -a1.re, b1.im);
+            dmma_16x8x4(cre[0], a0.im, a1.im, b0.im);
+            dmma_16x8x4(cim[0], -a0.im, -a1.im, b0.re);
+            dmma_16x8x4(cre[1], a0.im, a1.im, b1.im);
+            dmma_16x8x4(cim[1], -a0.im, -a1.im, b1.re);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == WS_STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    // epilogue: C = Cinit + acc
+    mbar_wait(cfull, cphase);
+    cphase ^= 1;
+    cplx* C = D.C;
+    const int ldC = D.ldC;
+    const bool two = GATHER && D.inv_off[1] >= 0, one = !GATHER || D.inv_off[0] >= 0;
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int r = wm * 16 + g + 8 * h, cc = wn * 16 + ni * 8 + 2 * t + v;
+          const int row = i0 + r, col = c0 + cc;
+          if (row < M && col < N && row >= col) {
+            cplx o = cmk(0.0, 0.0);
+            if (one) o = cadd(o, Cs[cc * S32_LD + r]);              // same sum order as asm_front_kernel
+            if (two) o = cadd(o, Cs[ST_CS + cc * S32_LD + r]);
+            stc(C + row + (int64_t)col * ldC, cmk(o.re + cre[ni][2 * h + v], o.im + cim[ni][2 * h + v]));
+          }
+        }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(cempty);
+  }
+}
+
+// Schur update of a level through the warp-specialised engine: tile q of the launch is
+// (shift q / n32, tile q % n32 of the level's tile list); CTA x takes tiles [x T, (x + 1) T).
+template <bool GATHER, int WS_STAGES>
+__global__ void __launch_bounds__(WS_THREADS, WS_STAGES <= (GATHER ? 2 : 3) ? 3 : 2)
+    syrk_ws_kernel(LevelArgs a, const int4* __restrict__ tiles, int n32, long long total, int T) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* As = reinterpret_cast<cplx*>(smem_raw);
+  cplx* Bs = As + WS_STAGES * S32_STAGE;
+  cplx* Cs = Bs + WS_STAGES * S32_STAGE;
+  StreamTile* desc = reinterpret_cast<StreamTile*>(Cs + (GATHER ? 2 : 1) * ST_CS);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(desc + ST_MAXT);
+  uint64_t *full = bars, *empty = bars + WS_STAGES, *cfull = bars + 2 * WS_STAGES, *cempty = cfull + 1;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < WS_STAGES; ++s) {
+      mbar_init(&full[s], 2);     // the A and the B warp's arrive.expect_tx (+ their copies' bytes)
+      mbar_init(&empty[s], 4);    // one arrival per consumer warp
+    }
+    mbar_init(cfull, GATHER ? 32 : 1);
+    mbar_init(cempty, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  const long long q0 = (long long)blockIdx.x * T;
+  const int nt = (int)min((long long)T, total - q0);
+  for (int j = threadIdx.x; j < nt; j += WS_THREADS) {
+    const long long q = q0 + j;
+    const int k = (int)(q / n32);
+    const int4 tl = tiles[q - (long long)k * n32];
+    const FrontDev F = a.fronts[tl.x];
+    const int n = F.n, p = F.p, b = n - p;
+    StreamTile D;
+    D.A = a.factor + (int64_t)k * a.fstride + F.fofs + p;   // L21: row r, column kk at A[r + kk n]
+    D.C = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
+    D.lda = n;
+    D.ldC = b;
+    D.K = p;
+    D.M = D.N = b;
+    D.i0 = tl.y * 32;
+    D.c0 = tl.z * 32;
+    D.pad = 0;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      D.Uc[s] = nullptr;
+      D.bc[s] = 0;
+      D.inv_off[s] = -1;
+      if (GATHER && s < F.nchild) {
+        const FrontDev Cf = a.fronts[a.child_ids[F.child_beg + s]];
+        D.bc[s] = Cf.n - Cf.p;
+        D.Uc[s] = a.uchild + (int64_t)k * a.uchild_stride + Cf.uofs;
+        D.inv_off[s] = F.inv_beg + s * n + p;
+      }
+    }
+    desc[j] = D;
+  }
+  __syncthreads();
+  ws_tiles<GATHER, WS_STAGES>(desc, nt, As, Bs, Cs, full, empty, cfull, cempty, a.inv);
+}
+
 // 32 x 32-tile trailing pivot-column update (see panel_update_kernel for the
 // delayed-update regions): the narrow (32-column) updates no longer fill half
 // of a 64-wide tile with waste.
@@ -841,6 +1128,13 @@ int set_kernel_attributes(int dev) {
                                       stream_smem_bytes<false>()));
   STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_stream_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       stream_smem_bytes<true>()));
+#define STFEM_WS_ATTR(G, S)                                                                                     \
+  STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_ws_kernel<G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                                      ws_smem_bytes<G, S>()));                                                  \
+  STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_ws_kernel<G, S>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  STFEM_WS_ATTR(false, 4) STFEM_WS_ATTR(false, 3) STFEM_WS_ATTR(false, 2)
+  STFEM_WS_ATTR(true, 4) STFEM_WS_ATTR(true, 3) STFEM_WS_ATTR(true, 2)
+#undef STFEM_WS_ATTR
   STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_stream_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_stream_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_block16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1290,7 +1584,19 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
           }
         }
         if (n32 > 0 && a.asm_pivots_only) {
-          if (P.opt.syrk_stream) {
+          if (P.opt.syrk_stream < 0) {
+            const long long total = (long long)n32 * nb;
+            const int T = std::max(1, std::min(ST_MAXT, -P.opt.syrk_stream));
+            const unsigned gr = (unsigned)((total + T - 1) / T);
+            const int4* tl = P.d_syrk32_tiles + P.syrk32_off[d];
+            const int ws_stages = P.opt.ws_stages;
+            if (ws_stages == 2)
+              syrk_ws_kernel<true, 2><<<gr, WS_THREADS, ws_smem_bytes<true, 2>(), st>>>(a, tl, (int)n32, total, T);
+            else if (ws_stages == 3)
+              syrk_ws_kernel<true, 3><<<gr, WS_THREADS, ws_smem_bytes<true, 3>(), st>>>(a, tl, (int)n32, total, T);
+            else
+              syrk_ws_kernel<true, 4><<<gr, WS_THREADS, ws_smem_bytes<true, 4>(), st>>>(a, tl, (int)n32, total, T);
+          } else if (P.opt.syrk_stream) {
             const long long total = (long long)n32 * nb;
             const int T = std::max(1, std::min(ST_MAXT, P.opt.syrk_stream));
             syrk_stream_kernel<true><<<(unsigned)((total + T - 1) / T), 128, stream_smem_bytes<true>(), st>>>(
@@ -1307,7 +1613,19 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
           ++nlaunch;
           fam(FAM_SYRK);
         } else if (n32 > 0) {
-          if (P.opt.syrk_stream) {
+          if (P.opt.syrk_stream < 0) {
+            const long long total = (long long)n32 * nb;
+            const int T = std::max(1, std::min(ST_MAXT, -P.opt.syrk_stream));
+            const unsigned gr = (unsigned)((total + T - 1) / T);
+            const int4* tl = P.d_syrk32_tiles + P.syrk32_off[d];
+            const int ws_stages = P.opt.ws_stages;
+            if (ws_stages == 2)
+              syrk_ws_kernel<false, 2><<<gr, WS_THREADS, ws_smem_bytes<false, 2>(), st>>>(a, tl, (int)n32, total, T);
+            else if (ws_stages == 3)
+              syrk_ws_kernel<false, 3><<<gr, WS_THREADS, ws_smem_bytes<false, 3>(), st>>>(a, tl, (int)n32, total, T);
+            else
+              syrk_ws_kernel<false, 4><<<gr, WS_THREADS, ws_smem_bytes<false, 4>(), st>>>(a, tl, (int)n32, total, T);
+          } else if (P.opt.syrk_stream) {
             const long long total = (long long)n32 * nb;
             const int T = std::max(1, std::min(ST_MAXT, P.opt.syrk_stream));
             syrk_stream_kernel<false><<<(unsigned)((total + T - 1) / T), 128, stream_smem_bytes<false>(), st>>>(

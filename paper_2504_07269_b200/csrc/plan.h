@@ -87,12 +87,13 @@ struct Plan {
   static stfem_plan_options default_options() {
     stfem_plan_options o{};
     o.small_front_n = 100;
-    o.fused_min_p = 50;
+    o.fused_min_p = 0;
     o.panel_group = 2;
     o.asm_whole_n = INT32_MAX;
     o.syrk_block16 = 1;
     o.level_timing = 0;
-    o.syrk_stream = 8;
+    o.syrk_stream = -16;
+    o.ws_stages = 2;
     o.workspace_fraction = 0.70;
     o.pivot_tol = 1e-10;
     return o;

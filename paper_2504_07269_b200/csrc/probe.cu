@@ -71,8 +71,49 @@ __global__ void __launch_bounds__(256) mixed_probe_kernel(double* sink, int iter
   if (s == 12345.678) sink[threadIdx.x] = s;
 }
 
+// DMMA issue / latency characterisation: CHAINS independent accumulator chains per warp,
+// blockDim.x / 32 warps per CTA.  How many DMMAs must be in flight per SM sub-partition to
+// reach the pipe's peak decides the warp tile and occupancy of the update kernels.
+template <int CHAINS>
+__global__ void dmma_chain_probe_kernel(double* sink, int iters) {
+  double c[CHAINS][4];
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, b0 = 1.0 - a0;
+#pragma unroll
+  for (int i = 0; i < CHAINS; ++i)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) c[i][v] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 8 / CHAINS; ++r)
+#pragma unroll
+      for (int i = 0; i < CHAINS; ++i) dmma_16x8x4(c[i], a0, a1, b0);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < CHAINS; ++i)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) s += c[i][v];
+  if (s == 12345.678) sink[threadIdx.x] = s;
+}
+
 }  // namespace
 }  // namespace stfem
+
+// 8 DMMAs per iteration per warp on `chains` (1, 2, 4 or 8) independent accumulators
+extern "C" int stfem_probe_dmma_chains(int chains, int warps_per_cta, int blocks, int iters, double* sink,
+                                       double* flops, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  const int th = 32 * warps_per_cta;
+  switch (chains) {
+    case 1: stfem::dmma_chain_probe_kernel<1><<<blocks, th, 0, s>>>(sink, iters); break;
+    case 2: stfem::dmma_chain_probe_kernel<2><<<blocks, th, 0, s>>>(sink, iters); break;
+    case 4: stfem::dmma_chain_probe_kernel<4><<<blocks, th, 0, s>>>(sink, iters); break;
+    default: stfem::dmma_chain_probe_kernel<8><<<blocks, th, 0, s>>>(sink, iters); break;
+  }
+  *flops = (double)blocks * warps_per_cta * iters * 8.0 * (2.0 * 16 * 8 * 4);
+  STFEM_LAUNCH_CHECK("probe");
+  return STFEM_OK;
+}
 
 // kind 0 = DMMA (flops = 2*16*8*4 per mma per warp), 1 = DFMA, 2 = both interleaved.  Returns the
 // real fp64 flop count executed in *flops; caller times it with events.

@@ -80,6 +80,15 @@ MODES = {
     # every level, 32-column assembly CTAs
     "big_plain": dict(small_front_n=0, fused_min_p=1 << 30, panel_group=1, syrk_block16=0, asm_whole_n=0),
     "big_pg4": dict(small_front_n=0, panel_group=4, syrk_block16=0),
+    # the per-tile Schur kernel (syrk_stream=0) and the warp-specialised TMA-fed one (< 0), with the
+    # extend-add fused on every level and on none
+    "big_tile_fused": dict(small_front_n=0, fused_min_p=0, syrk_stream=0),
+    "big_stream_fused": dict(small_front_n=0, fused_min_p=0, syrk_stream=8),
+    "big_ws_fused": dict(small_front_n=0, fused_min_p=0, syrk_stream=-8),
+    "big_ws_plain": dict(small_front_n=0, fused_min_p=1 << 30, syrk_block16=0, syrk_stream=-3),
+    "big_ws_s4_fused": dict(small_front_n=0, fused_min_p=0, syrk_stream=-5, ws_stages=4),
+    "big_ws_s2_fused": dict(small_front_n=0, fused_min_p=0, syrk_stream=-16, ws_stages=2),
+    "big_ws_s3_plain": dict(small_front_n=0, fused_min_p=1 << 30, syrk_block16=0, syrk_stream=-7, ws_stages=3),
     # spectral subtrees of <= 24 / <= 256 interior DoFs (K6) under a multifrontal top
     "spec24": {}, "spec": {},
 }
