@@ -180,15 +180,13 @@ typedef struct {
                                 small-front kernel (unit-L LDL^T); 0 = every front on the tile-parallel
                                 large-front pipeline.  Default 100 */
   int32_t fused_min_p;       /* levels with >= this many pivots fuse the children's extend-add into the
-                                Schur-update tiles (U never assembled).  Default 50 */
+                                Schur-update tiles (U never assembled).  Default 0: every level */
   int32_t panel_group;       /* trailing pivot-column updates are delayed over this many 32-wide panels.
                                 Default 2 */
   int32_t asm_whole_n;       /* fronts of order <= this are assembled by one CTA.  Default INT32_MAX */
-  int32_t syrk_block16;      /* 1: short-K Schur updates (p <= 32, b <= 208) on 16 x 16 blocks.  Default 1 */
   int32_t level_timing;      /* 1: print per-launch CUDA-event times to stderr (diagnostics) */
-  int32_t syrk_stream;       /* Schur-update kernel: -T = warp-specialised, TMA-fed, T tiles per CTA (1..16);
-                                +T = cp.async stream over T tiles; 0 = one tile per CTA */
-  int32_t ws_stages;         /* ring depth of the warp-specialised kernel (2, 3 or 4).  Default 2 */
+  int32_t tiles_per_cta;     /* tiles a CTA of the update engine walks (1..16).  Default 16 */
+  int32_t ws_stages;         /* ring depth of the update engine (2, 3 or 4).  Default 2 */
   double workspace_fraction; /* share of the free device memory the numeric workspace may take.  Default 0.70 */
   double pivot_tol;          /* relative pivot-collapse threshold (see stfem_plan_check).  Default 1e-10 */
 } stfem_plan_options;

@@ -85,287 +85,12 @@ __device__ __forceinline__ int64_t bv_off(const stfem_bv_layout& L, int r, int64
          j % L.chunk_cols;
 }
 
-// Tile initialiser of the DMMA update kernels: the accumulators start from
-// cinit(row, col) -- C itself here, or the children's extend-add (Gather32) so a
-// caller can assemble C on the fly.
-struct CLoad {
-  const cplx* C;
-  int ldC;
-  __device__ __forceinline__ cplx operator()(int row, int col) const {
-    return ldc(C + (int64_t)row + (int64_t)col * ldC);
-  }
-};
-
 #include "multifrontal_large.cuh"
 
-// Short-K Schur update at 16 x 16 granularity (levels with p <= 32 pivots and
-// b <= 208 boundary rows: C4 depths 7-9).  There the 64 x 64 tiles are mostly
-// waste -- b ~ 100 computes 2.4x the lower triangle, and the DMMA pipe is the
-// bottleneck (ncu: 65-72% active) -- so one CTA per (front, shift) instance
-// stages its L21 panel (b x p) in shared memory with cp.async and its 8 warps
-// walk the lower 16 x 16 blocks of U (1.2-1.4x the triangle): per block the
-// F22 entries are loaded into the accumulators (the next block's are
-// prefetched into registers while this one multiplies), K/4 DMMA steps on two
-// 16 x 8 fragments, lower entries stored.
-constexpr int B16_KMAX = 32, B16_BMAX = 208;
-__host__ __device__ inline int b16_ld(int b) { return b + ((10 - b % 8) % 8); }   // = 2 (mod 8)
-__host__ __device__ inline int b16_smem_bytes(int bmax) { return b16_ld(bmax) * B16_KMAX * 16; }
+// Geometry of the 32 x 32-tile DMMA update engine: shared K chunks [16][32 + 2] complex (the
+// 2-element pad keeps the fragment loads of the 32 lanes on 8 distinct 16-byte bank groups)
+constexpr int S32_LD = 32 + 2, S32_STAGE = 16 * S32_LD;
 
-__global__ void __launch_bounds__(NT, 2) syrk_block16_kernel(LevelArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  cplx* Ls = reinterpret_cast<cplx*>(smem_raw);   // Ls[k * ld + r] = L21[r][k]
-  const int inst = blockIdx.x;
-  const int k = inst % a.nbatch;
-  const FrontDev F = a.fronts[a.list[inst / a.nbatch]];
-  const int n = F.n, p = F.p, b = n - p;
-  if (b <= 0) return;
-  const int ld = b16_ld(b);
-  const cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
-  cplx* U = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
-  const int tid = threadIdx.x;
-  const int kpad = (p + 3) & ~3;
-  for (int idx = tid; idx < b * kpad; idx += NT) {
-    const int r = idx % b, kk = idx / b;
-    const bool ok = kk < p;
-    cp_async16(Ls + kk * ld + r, ok ? P + p + r + (int64_t)kk * n : P, ok);
-  }
-  cp_async_commit();
-  const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
-  const int nbk = (b + 15) >> 4, nblk = nbk * (nbk + 1) / 2;
-  // block q -> (bi, bj), bj <= bi, row-major over the lower triangle
-  auto coords = [](int q, int& bi, int& bj) {
-    bi = (int)((sqrtf(8.0f * q + 1.0f) - 1.0f) * 0.5f);
-    while ((bi + 1) * (bi + 2) / 2 <= q) ++bi;
-    while (bi * (bi + 1) / 2 > q) --bi;
-    bj = q - bi * (bi + 1) / 2;
-  };
-  auto load_c = [&](int bi, int bj, cplx (&c)[2][4]) {
-#pragma unroll
-    for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          const int row = bi * 16 + g + 8 * h, col = bj * 16 + ni * 8 + 2 * t + v;
-          c[ni][2 * h + v] = (row < b && col < b && row >= col) ? ldc(U + row + (int64_t)col * b) : cmk(0.0, 0.0);
-        }
-  };
-  int q = warp, bi = 0, bj = 0;
-  cplx cn[2][4];
-  if (q < nblk) {
-    coords(q, bi, bj);
-    load_c(bi, bj, cn);
-  }
-  cp_async_wait<0>();
-  __syncthreads();
-  for (; q < nblk; q += NT / 32) {
-    double cre[2][4], cim[2][4];
-#pragma unroll
-    for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        cre[ni][e] = cn[ni][e].re;
-        cim[ni][e] = cn[ni][e].im;
-      }
-    const int ci = bi, cj = bj;
-    if (q + NT / 32 < nblk) {   // prefetch the next block's F22 entries
-      coords(q + NT / 32, bi, bj);
-      load_c(bi, bj, cn);
-    }
-    const int ra = min(ci * 16 + g, b - 1), ra8 = min(ci * 16 + g + 8, b - 1);
-    const int rb0 = min(cj * 16 + g, b - 1), rb1 = min(cj * 16 + 8 + g, b - 1);
-    for (int kk = 0; kk < kpad; kk += 4) {
-      const cplx* col = Ls + (kk + t) * ld;
-      const cplx a0 = col[ra], a1 = col[ra8], b0 = col[rb0], b1 = col[rb1];
-      dmma_16x8x4(cre[0], -a0.re, -a1.re, b0.re);
-      dmma_16x8x4(cre[0], a0.im, a1.im, b0.im);
-      dmma_16x8x4(cim[0], -a0.re, -a1.re, b0.im);
-      dmma_16x8x4(cim[0], -a0.im, -a1.im, b0.re);
-      dmma_16x8x4(cre[1], -a0.re, -a1.re, b1.re);
-      dmma_16x8x4(cre[1], a0.im, a1.im, b1.im);
-      dmma_16x8x4(cim[1], -a0.re, -a1.re, b1.im);
-      dmma_16x8x4(cim[1], -a0.im, -a1.im, b1.re);
-    }
-#pragma unroll
-    for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          const int row = ci * 16 + g + 8 * h, col = cj * 16 + ni * 8 + 2 * t + v;
-          if (row < b && col < b && row >= col) stc(U + row + (int64_t)col * b, cmk(cre[ni][2 * h + v], cim[ni][2 * h + v]));
-        }
-  }
-}
-
-// Schur update on 32 x 32 lower tiles (levels below the fused threshold that
-// the 16 x 16 kernel does not take: p > 32 or b > 208; C4 depths 5-6).  The
-// 64 x 64 tiles of gemm_update compute ~2x the lower triangle of b ~ 200-380
-// blocks with the DMMA pipe already the bottleneck; 32 x 32 tiles cut that
-// to ~1.3x.  128 threads = 2 x 2 warps of 16 x 16, 3-stage cp.async K pipeline
-// (52 KB), F22 into the accumulators, 4 CTAs per SM.
-constexpr int S32_LD = 32 + 2, S32_STAGE = 16 * S32_LD;   // [k][m] complex
-constexpr int S32_SMEM = 3 * 2 * S32_STAGE * 16 + 128 * 4;
-
-// GATHER: the tile starts from the children's extend-add (fused levels, U never
-// assembled; the tile's 32 row / 32 column inverse maps staged in shared memory)
-// instead of the assembled F22.
-// One 32 x 32 lower tile of C -= A A^T (C: M x N lower trapezoid, ld ldC; A: M
-// rows x K, ld lda; row c of A pairs with column c of C).  cinit(row, col) gives
-// the tile's starting values.  128 threads = 2 x 2 warps of 16 x 16, 3-stage
-// cp.async K pipeline.
-template <class CInit>
-__device__ __forceinline__ void sym_tile32(cplx* __restrict__ C, int ldC, int M, int N, const cplx* __restrict__ A,
-                                           int lda, int K, int i0, int c0, cplx* As, cplx* Bs, const CInit& cinit) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3, wm = warp & 1, wn = warp >> 1;
-  const int nk = (K + 15) / 16;
-  auto load = [&](int stage, int kc) {
-    cplx* as = As + stage * S32_STAGE;
-    cplx* bs = Bs + stage * S32_STAGE;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int idx = tid + 128 * u, m = idx & 31, kk = kc * 16 + (idx >> 5);
-      const bool oka = kk < K && i0 + m < M, okb = kk < K && c0 + m < N;
-      cp_async16(as + (idx >> 5) * S32_LD + m, oka ? A + i0 + m + (int64_t)kk * lda : A, oka);
-      cp_async16(bs + (idx >> 5) * S32_LD + m, okb ? A + c0 + m + (int64_t)kk * lda : A, okb);
-    }
-  };
-#pragma unroll
-  for (int st = 0; st < 2; ++st) {
-    if (st < nk) load(st, st);
-    cp_async_commit();
-  }
-  double cre[2][4], cim[2][4];
-#pragma unroll
-  for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const int row = i0 + wm * 16 + g + 8 * h, col = c0 + wn * 16 + ni * 8 + 2 * t + v;
-        const cplx o = (row < M && col < N && row >= col) ? cinit(row, col) : cmk(0.0, 0.0);
-        cre[ni][2 * h + v] = o.re;
-        cim[ni][2 * h + v] = o.im;
-      }
-  // warps whose 16 x 16 block lies strictly above the diagonal (diagonal tiles) or below
-  // the last row skip their DMMAs (warp-uniform; their outputs are never stored)
-  const bool wact = (i0 + wm * 16 + 15 >= c0 + wn * 16) && (i0 + wm * 16 < M) && (c0 + wn * 16 < N);
-  for (int kc = 0; kc < nk; ++kc) {
-    cp_async_wait<1>();
-    __syncthreads();
-    if (kc + 2 < nk) load((kc + 2) % 3, kc + 2);
-    cp_async_commit();
-    if (!wact) continue;
-    const cplx* as = As + (kc % 3) * S32_STAGE + t * S32_LD + wm * 16 + g;
-    const cplx* bs = Bs + (kc % 3) * S32_STAGE + t * S32_LD + wn * 16 + g;
-#pragma unroll
-    for (int kk = 0; kk < 16; kk += 4) {
-      const cplx a0 = as[kk * S32_LD], a1 = as[kk * S32_LD + 8];
-      const cplx b0 = bs[kk * S32_LD], b1 = bs[kk * S32_LD + 8];
-      dmma_16x8x4(cre[0], -a0.re, -a1.re, b0.re);
-      dmma_16x8x4(cre[0], a0.im, a1.im, b0.im);
-      dmma_16x8x4(cim[0], -a0.re, -a1.re, b0.im);
-      dmma_16x8x4(cim[0], -a0.im, -a1.im, b0.re);
-      dmma_16x8x4(cre[1], -a0.re, -a1.re, b1.re);
-      dmma_16x8x4(cre[1], a0.im, a1.im, b1.im);
-      dmma_16x8x4(cim[1], -a0.re, -a1.re, b1.im);
-      dmma_16x8x4(cim[1], -a0.im, -a1.im, b1.re);
-    }
-  }
-  cp_async_wait<0>();
-#pragma unroll
-  for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const int row = i0 + wm * 16 + g + 8 * h, col = c0 + wn * 16 + ni * 8 + 2 * t + v;
-        if (row < M && col < N && row >= col)
-          stc(C + row + (int64_t)col * ldC, cmk(cre[ni][2 * h + v], cim[ni][2 * h + v]));
-      }
-}
-
-// extend-add of the (at most two) children's update blocks for one 32 x 32 tile
-struct Gather32 {
-  const int* inv_s;   // [2 children][rows 32 | cols 32]
-  const cplx* Uc[2];
-  int bc[2], nc, i0, c0;
-  __device__ __forceinline__ cplx operator()(int row, int col) const {
-    cplx o = cmk(0.0, 0.0);
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {   // same sum order as asm_front_kernel: 0 + c0 + c1
-      const int kr = s < nc ? inv_s[s * 64 + row - i0] : -1;
-      const int kc = s < nc ? inv_s[s * 64 + 32 + col - c0] : -1;
-      if (kr >= 0 && kc >= 0) o = cadd(o, ldc(Uc[s] + (int64_t)kc * bc[s] + kr));
-    }
-    return o;
-  }
-};
-
-// GATHER: the tile starts from the children's extend-add (fused levels, U never
-// assembled; the tile's 32 row / 32 column inverse maps staged in shared memory)
-// instead of the assembled F22.
-template <bool GATHER>
-__global__ void __launch_bounds__(128, 4) syrk32_kernel(LevelArgs a, const int4* __restrict__ tiles) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  cplx* As = reinterpret_cast<cplx*>(smem_raw);
-  cplx* Bs = As + 3 * S32_STAGE;
-  int* inv_s = reinterpret_cast<int*>(Bs + 3 * S32_STAGE);
-  const int k = blockIdx.x % a.nbatch;
-  const int4 tl = tiles[blockIdx.x / a.nbatch];
-  const FrontDev F = a.fronts[tl.x];
-  const int n = F.n, p = F.p, b = n - p;
-  const int i0 = tl.y * 32, c0 = tl.z * 32;
-  const cplx* L = a.factor + (int64_t)k * a.fstride + F.fofs + p;   // L21: row r, column kk at L[r + kk n]
-  cplx* U = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
-  if constexpr (GATHER) {
-    Gather32 gi;
-    gi.inv_s = inv_s;
-    gi.nc = min(F.nchild, 2);
-    gi.i0 = i0;
-    gi.c0 = c0;
-    for (int q = threadIdx.x; q < 128; q += 128) {
-      const int s = q >> 6, r = q & 31, isc = (q >> 5) & 1;
-      const int fr = (isc ? c0 : i0) + r;
-      inv_s[q] = (s < gi.nc && fr < b) ? a.inv[F.inv_beg + s * n + p + fr] : -1;
-    }
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      gi.Uc[s] = nullptr;
-      gi.bc[s] = 0;
-      if (s < gi.nc) {
-        const FrontDev Cf = a.fronts[a.child_ids[F.child_beg + s]];
-        gi.bc[s] = Cf.n - Cf.p;
-        gi.Uc[s] = a.uchild + (int64_t)k * a.uchild_stride + Cf.uofs;
-      }
-    }
-    __syncthreads();
-    sym_tile32(U, b, b, b, L, n, p, i0, c0, As, Bs, gi);
-  } else {
-    sym_tile32(U, b, b, b, L, n, p, i0, c0, As, Bs, CLoad{U, b});
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Streamed 32 x 32-tile update engine (Schur updates and trailing pivot-column
-// updates): C = Cinit - A A^T on lower tiles, DMMA.
-//
-// The per-tile kernels above pay, for every tile, a chain of dependent
-// descriptor loads, the pipeline fill and the drain/epilogue with nothing to
-// overlap them but other CTAs in the same phase (measured: 59-75% of the DMMA
-// peak for K = 63-255 against 94% for the long-K transform GEMM).  Here one CTA
-// walks a contiguous range of tiles as ONE stream of 16-deep K chunks: the
-// 3-stage cp.async pipeline keeps running across tile boundaries (the first
-// chunks of tile j+1 are in flight while tile j finishes), the tile
-// descriptors are decoded once per CTA into shared memory, and the tile's
-// starting values Cinit -- the assembled block, or (GATHER) the children's
-// extend-add through the inverse maps -- are fetched by cp.async into a shared
-// staging tile during the tile's K loop and only added in the epilogue, so no
-// global-load latency sits on the accumulators' critical path.  Tiles are
-// ordered instance-major (all tiles of one (front, shift) consecutively), so
-// the L21 rows a CTA re-reads across its tiles stay in L1/L2.
-// ---------------------------------------------------------------------------
 constexpr int ST_MAXT = 16;                 // tiles per CTA (upper bound)
 constexpr int ST_CS = 32 * S32_LD;          // one staged C tile: Cs[col * S32_LD + row] (complex)
 
@@ -378,210 +103,6 @@ struct __align__(16) StreamTile {
   int inv_off[2];       // GATHER: a.inv offset of boundary row 0 for child s (-1: no such child)
   int pad;
 };
-
-template <bool GATHER>
-constexpr int stream_smem_bytes() {
-  return 3 * 2 * S32_STAGE * 16 + (GATHER ? 2 : 1) * ST_CS * 16 + ST_MAXT * (int)sizeof(StreamTile);
-}
-
-template <bool GATHER>
-__device__ __forceinline__ void stream_tiles(const StreamTile* __restrict__ desc, int nt, cplx* As, cplx* Bs,
-                                             cplx* Cs, const int32_t* __restrict__ inv) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3, wm = warp & 1, wn = warp >> 1;
-  auto nk_of = [&](int j) { return (desc[j].K + 15) >> 4; };
-  auto skip = [&](int& j, int& c) {
-    while (j < nt && c >= nk_of(j)) {
-      ++j;
-      c = 0;
-    }
-  };
-  int lj = 0, lc = 0;   // load cursor: next (tile, chunk) to request
-  skip(lj, lc);
-  if (lj >= nt) return;
-  auto load_item = [&](int stage) {
-    const StreamTile& D = desc[lj];
-    const cplx* A = D.A;
-    const int lda = D.lda, K = D.K, M = D.M, N = D.N, i0 = D.i0, c0 = D.c0;
-    cplx* as = As + stage * S32_STAGE;
-    cplx* bs = Bs + stage * S32_STAGE;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int idx = tid + 128 * u, m = idx & 31, kk = lc * 16 + (idx >> 5);
-      const bool oka = kk < K && i0 + m < M, okb = kk < K && c0 + m < N;
-      cp_async16(as + (idx >> 5) * S32_LD + m, oka ? A + i0 + m + (int64_t)kk * lda : A, oka);
-      cp_async16(bs + (idx >> 5) * S32_LD + m, okb ? A + c0 + m + (int64_t)kk * lda : A, okb);
-    }
-    ++lc;
-    skip(lj, lc);
-  };
-  // starting values of tile j into the staging tile(s): lower entries only, zero elsewhere
-  auto load_c = [&](int j) {
-    const StreamTile& D = desc[j];
-    const int M = D.M, N = D.N, i0 = D.i0, c0 = D.c0;
-    const int r = tid & 31, row = i0 + r;
-    if constexpr (GATHER) {
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const int off = D.inv_off[s];
-        if (off < 0) continue;                                   // uniform: no such child
-        const cplx* Uc = D.Uc[s];
-        const int bc = D.bc[s];
-        const int kr = row < M ? inv[off + row] : -1;
-        int kc[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int col = c0 + (tid >> 5) + 4 * u;
-          kc[u] = (col < N && row >= col) ? inv[off + col] : -1;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int c = (tid >> 5) + 4 * u;
-          const bool ok = kr >= 0 && kc[u] >= 0;
-          cp_async16(Cs + s * ST_CS + c * S32_LD + r, ok ? Uc + (int64_t)kc[u] * bc + kr : Uc, ok);
-        }
-      }
-    } else {
-      const cplx* C = D.C;
-      const int ldC = D.ldC;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int c = (tid >> 5) + 4 * u, col = c0 + c;
-        const bool ok = row < M && col < N && row >= col;
-        cp_async16(Cs + c * S32_LD + r, ok ? C + row + (int64_t)col * ldC : C, ok);
-      }
-    }
-  };
-  int cj = lj, cc = 0;   // compute cursor
-  load_c(cj);
-#pragma unroll
-  for (int st = 0; st < 2; ++st) {
-    if (lj < nt) load_item(st);
-    cp_async_commit();
-  }
-  double cre[2][4], cim[2][4];
-#pragma unroll
-  for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) cre[ni][e] = cim[ni][e] = 0.0;
-  int it = 0, pending_c = -1;
-  bool first = true;
-  while (cj < nt) {
-    cp_async_wait<1>();
-    __syncthreads();   // chunk `it` landed for everyone; stage (it - 1) % 3 and (after an epilogue) Cs are free
-    if (lj < nt) load_item((it + 2) % 3);
-    if (pending_c >= 0) {
-      load_c(pending_c);
-      pending_c = -1;
-    }
-    cp_async_commit();
-    const StreamTile& D = desc[cj];
-    const int M = D.M, N = D.N, i0 = D.i0, c0 = D.c0;
-    // warps whose 16 x 16 block lies strictly above the diagonal (diagonal tiles) or outside
-    // the block skip their DMMAs (warp-uniform; their outputs are never stored)
-    const bool wact = (i0 + wm * 16 + 15 >= c0 + wn * 16) && (i0 + wm * 16 < M) && (c0 + wn * 16 < N);
-    if (wact) {
-      const cplx* as = As + (it % 3) * S32_STAGE + t * S32_LD + wm * 16 + g;
-      const cplx* bs = Bs + (it % 3) * S32_STAGE + t * S32_LD + wn * 16 + g;
-#pragma unroll
-      for (int kk = 0; kk < 16; kk += 4) {
-        const cplx a0 = as[kk * S32_LD], a1 = as[kk * S32_LD + 8];
-        const cplx b0 = bs[kk * S32_LD], b1 = bs[kk * S32_LD + 8];
-        // four independent accumulator chains between dependent DMMAs
-        dmma_16x8x4(cre[0], -a0.re, -a1.re, b0.re);
-        dmma_16x8x4(cim[0], -a0.re, -a1.re, b0.im);
-        dmma_16x8x4(cre[1], -a0.re, -a1.re, b1.re);
-        dmma_16x8x4(cim[1], -a0.re, -a1.re, b1.im);
-        dmma_16x8x4(cre[0], a0.im, a1.im, b0.im);
-        dmma_16x8x4(cim[0], -a0.im, -a1.im, b0.re);
-        dmma_16x8x4(cre[1], a0.im, a1.im, b1.im);
-        dmma_16x8x4(cim[1], -a0.im, -a1.im, b1.re);
-      }
-    }
-    ++it;
-    ++cc;
-    const int nk = (D.K + 15) >> 4;
-    if (cc == nk) {
-      // a tile shorter than the pipeline: its staged starting values may still be in flight
-      if (nk < 3 && !first) {
-        cp_async_wait<0>();
-        __syncthreads();
-      }
-      first = false;
-      cplx* C = D.C;
-      const int ldC = D.ldC;
-      const bool two = GATHER && D.inv_off[1] >= 0, one = !GATHER || D.inv_off[0] >= 0;
-#pragma unroll
-      for (int ni = 0; ni < 2; ++ni)
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int v = 0; v < 2; ++v) {
-            const int r = wm * 16 + g + 8 * h, c = wn * 16 + ni * 8 + 2 * t + v;
-            const int row = i0 + r, col = c0 + c;
-            if (row < M && col < N && row >= col) {
-              cplx o = cmk(0.0, 0.0);
-              if (one) o = cadd(o, Cs[c * S32_LD + r]);                 // same sum order as asm_front_kernel
-              if (two) o = cadd(o, Cs[ST_CS + c * S32_LD + r]);
-              stc(C + row + (int64_t)col * ldC, cmk(o.re + cre[ni][2 * h + v], o.im + cim[ni][2 * h + v]));
-            }
-            cre[ni][2 * h + v] = 0.0;
-            cim[ni][2 * h + v] = 0.0;
-          }
-      ++cj;
-      cc = 0;
-      skip(cj, cc);
-      pending_c = cj < nt ? cj : -1;   // requested after the next iteration's barrier (Cs is read above)
-    }
-  }
-  cp_async_wait<0>();
-}
-
-// Schur update U = (F22 | children's extend-add) - L21 L21^T of a level: tile q of the launch is
-// (shift q / n32, tile q % n32 of the level's tile list); CTA x takes tiles [x T, (x + 1) T).
-template <bool GATHER>
-__global__ void __launch_bounds__(128, GATHER ? 2 : 3)
-    syrk_stream_kernel(LevelArgs a, const int4* __restrict__ tiles, int n32, long long total, int T) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  cplx* As = reinterpret_cast<cplx*>(smem_raw);
-  cplx* Bs = As + 3 * S32_STAGE;
-  cplx* Cs = Bs + 3 * S32_STAGE;
-  StreamTile* desc = reinterpret_cast<StreamTile*>(Cs + (GATHER ? 2 : 1) * ST_CS);
-  const long long q0 = (long long)blockIdx.x * T;
-  const int nt = (int)min((long long)T, total - q0);
-  for (int j = threadIdx.x; j < nt; j += 128) {
-    const long long q = q0 + j;
-    const int k = (int)(q / n32);
-    const int4 tl = tiles[q - (long long)k * n32];
-    const FrontDev F = a.fronts[tl.x];
-    const int n = F.n, p = F.p, b = n - p;
-    StreamTile D;
-    D.A = a.factor + (int64_t)k * a.fstride + F.fofs + p;   // L21: row r, column kk at A[r + kk n]
-    D.C = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
-    D.lda = n;
-    D.ldC = b;
-    D.K = p;
-    D.M = D.N = b;
-    D.i0 = tl.y * 32;
-    D.c0 = tl.z * 32;
-    D.pad = 0;
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      D.Uc[s] = nullptr;
-      D.bc[s] = 0;
-      D.inv_off[s] = -1;
-      if (GATHER && s < F.nchild) {
-        const FrontDev Cf = a.fronts[a.child_ids[F.child_beg + s]];
-        D.bc[s] = Cf.n - Cf.p;
-        D.Uc[s] = a.uchild + (int64_t)k * a.uchild_stride + Cf.uofs;
-        D.inv_off[s] = F.inv_beg + s * n + p;
-      }
-    }
-    desc[j] = D;
-  }
-  __syncthreads();
-  stream_tiles<GATHER>(desc, nt, As, Bs, Cs, a.inv);
-}
 
 // ---------------------------------------------------------------------------
 // Warp-specialised, TMA-fed update engine: C = Cinit - A A^T on lower 32 x 32
@@ -813,6 +334,17 @@ __device__ __forceinline__ void ws_tiles(const StreamTile* __restrict__ desc, in
   }
 }
 
+template <bool GATHER, int WS_STAGES>
+__device__ __forceinline__ void ws_init_barriers(uint64_t* full, uint64_t* empty, uint64_t* cfull, uint64_t* cempty) {
+  for (int s = 0; s < WS_STAGES; ++s) {
+    mbar_init(&full[s], 2);     // the A and the B warp's arrive.expect_tx (+ their copies' bytes)
+    mbar_init(&empty[s], 4);    // one arrival per consumer warp
+  }
+  mbar_init(cfull, GATHER ? 32 : 1);
+  mbar_init(cempty, 4);
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+
 // Schur update of a level through the warp-specialised engine: tile q of the launch is
 // (shift q / n32, tile q % n32 of the level's tile list); CTA x takes tiles [x T, (x + 1) T).
 template <bool GATHER, int WS_STAGES>
@@ -825,15 +357,7 @@ __global__ void __launch_bounds__(WS_THREADS, WS_STAGES <= (GATHER ? 2 : 3) ? 3 
   StreamTile* desc = reinterpret_cast<StreamTile*>(Cs + (GATHER ? 2 : 1) * ST_CS);
   uint64_t* bars = reinterpret_cast<uint64_t*>(desc + ST_MAXT);
   uint64_t *full = bars, *empty = bars + WS_STAGES, *cfull = bars + 2 * WS_STAGES, *cempty = cfull + 1;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < WS_STAGES; ++s) {
-      mbar_init(&full[s], 2);     // the A and the B warp's arrive.expect_tx (+ their copies' bytes)
-      mbar_init(&empty[s], 4);    // one arrival per consumer warp
-    }
-    mbar_init(cfull, GATHER ? 32 : 1);
-    mbar_init(cempty, 4);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
+  if (threadIdx.x == 0) ws_init_barriers<GATHER, WS_STAGES>(full, empty, cfull, cempty);
   const long long q0 = (long long)blockIdx.x * T;
   const int nt = (int)min((long long)T, total - q0);
   for (int j = threadIdx.x; j < nt; j += WS_THREADS) {
@@ -870,9 +394,10 @@ __global__ void __launch_bounds__(WS_THREADS, WS_STAGES <= (GATHER ? 2 : 3) ? 3 
   ws_tiles<GATHER, WS_STAGES>(desc, nt, As, Bs, Cs, full, empty, cfull, cempty, a.inv);
 }
 
-// 32 x 32-tile trailing pivot-column update (see panel_update_kernel for the
-// delayed-update regions): the narrow (32-column) updates no longer fill half
-// of a 64-wide tile with waste.
+// Trailing pivot-column updates, delayed over groups of panels (multifrontal_large.cuh), through
+// the same engine: F[cb:, cb:cb+cols] -= X X^T with X = F[cb:, k0:k0+K) (the TRSM'd panel rows),
+// lower trapezoid of 32 x 32 tiles.  Tile q of the launch = (shift, front of the level, tile t of
+// the front's trapezoid); fronts with fewer tiles than the level maximum get empty (K = 0) tiles.
 __host__ __device__ inline int panel_update_tiles32(int n, int p, int cb, int narrow) {
   const int cols = cb >= p ? 0 : (narrow ? min(NB, p - cb) : p - cb);
   if (cols <= 0) return 0;
@@ -880,30 +405,61 @@ __host__ __device__ inline int panel_update_tiles32(int n, int p, int cb, int na
   return tn * tm - tn * (tn - 1) / 2;
 }
 
-__global__ void __launch_bounds__(128, 4) panel_update32_kernel(LevelArgs a, int cb, int k0, int K, int narrow) {
+template <int WS_STAGES>
+__global__ void __launch_bounds__(WS_THREADS, WS_STAGES <= 3 ? 3 : 2)
+    panel_ws_kernel(LevelArgs a, int cb, int k0, int K, int narrow, int tiles_max, long long total, int T) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* As = reinterpret_cast<cplx*>(smem_raw);
-  cplx* Bs = As + 3 * S32_STAGE;
-  const int inst = blockIdx.x;
-  const int k = inst % a.nbatch;
-  const FrontDev F = a.fronts[a.list[inst / a.nbatch]];
-  const int n = F.n, p = F.p;
-  const int cols = cb >= p ? 0 : (narrow ? min(NB, p - cb) : p - cb);
-  if (cols <= 0) return;
-  const int kk = min(K, p - k0);
-  const int tm = (n - cb + 31) / 32, tn = (cols + 31) / 32;
-  int t = blockIdx.y, ti = -1, tj = 0;
-  for (; tj < tn; ++tj) {
-    if (t < tm - tj) {
-      ti = tj + t;
-      break;
+  cplx* Bs = As + WS_STAGES * S32_STAGE;
+  cplx* Cs = Bs + WS_STAGES * S32_STAGE;
+  StreamTile* desc = reinterpret_cast<StreamTile*>(Cs + ST_CS);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(desc + ST_MAXT);
+  uint64_t *full = bars, *empty = bars + WS_STAGES, *cfull = bars + 2 * WS_STAGES, *cempty = cfull + 1;
+  if (threadIdx.x == 0) ws_init_barriers<false, WS_STAGES>(full, empty, cfull, cempty);
+  const long long q0 = (long long)blockIdx.x * T;
+  const int nt = (int)min((long long)T, total - q0);
+  for (int j = threadIdx.x; j < nt; j += WS_THREADS) {
+    const long long q = q0 + j;
+    const int t = (int)(q % tiles_max);
+    const long long inst = q / tiles_max;
+    const int fi = (int)(inst % a.nlist), k = (int)(inst / a.nlist);
+    const FrontDev F = a.fronts[a.list[fi]];
+    const int n = F.n, p = F.p;
+    const int cols = cb >= p ? 0 : (narrow ? min(NB, p - cb) : p - cb);
+    StreamTile D;
+    D.K = 0;
+    D.M = D.N = D.i0 = D.c0 = D.lda = D.ldC = D.pad = 0;
+    D.A = nullptr;
+    D.C = nullptr;
+    D.Uc[0] = D.Uc[1] = nullptr;
+    D.bc[0] = D.bc[1] = 0;
+    D.inv_off[0] = D.inv_off[1] = -1;
+    if (cols > 0) {
+      const int tm = (n - cb + 31) / 32, tn = (cols + 31) / 32;
+      int r = t, ti = -1, tj = 0;
+      for (; tj < tn; ++tj) {
+        if (r < tm - tj) {
+          ti = tj + r;
+          break;
+        }
+        r -= tm - tj;
+      }
+      if (ti >= 0) {
+        cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
+        D.A = P + cb + (int64_t)k0 * n;
+        D.C = P + cb + (int64_t)cb * n;
+        D.lda = D.ldC = n;
+        D.K = min(K, p - k0);
+        D.M = n - cb;
+        D.N = cols;
+        D.i0 = ti * 32;
+        D.c0 = tj * 32;
+      }
     }
-    t -= tm - tj;
+    desc[j] = D;
   }
-  if (ti < 0) return;
-  cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
-  cplx* C = P + cb + (int64_t)cb * n;
-  sym_tile32(C, n, n - cb, cols, P + cb + (int64_t)k0 * n, n, kk, ti * 32, tj * 32, As, Bs, CLoad{C, n});
+  __syncthreads();
+  ws_tiles<false, WS_STAGES>(desc, nt, As, Bs, Cs, full, empty, cfull, cempty, a.inv);
 }
 
 // Backward substitution of one level, one CTA per (front, shift) instance:
@@ -1121,13 +677,6 @@ int set_kernel_attributes(int dev) {
   static DeviceOnce once;
   (void)dev;
   if (!once.first()) return STFEM_OK;
-  STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk32_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, S32_SMEM));
-  STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk32_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, S32_SMEM));
-  STFEM_CUDA_TRY(cudaFuncSetAttribute(panel_update32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, S32_SMEM));
-  STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_stream_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      stream_smem_bytes<false>()));
-  STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_stream_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      stream_smem_bytes<true>()));
 #define STFEM_WS_ATTR(G, S)                                                                                     \
   STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_ws_kernel<G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
                                       ws_smem_bytes<G, S>()));                                                  \
@@ -1135,10 +684,12 @@ int set_kernel_attributes(int dev) {
   STFEM_WS_ATTR(false, 4) STFEM_WS_ATTR(false, 3) STFEM_WS_ATTR(false, 2)
   STFEM_WS_ATTR(true, 4) STFEM_WS_ATTR(true, 3) STFEM_WS_ATTR(true, 2)
 #undef STFEM_WS_ATTR
-  STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_stream_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_stream_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_block16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      b16_smem_bytes(B16_BMAX)));
+#define STFEM_PW_ATTR(S)                                                                                        \
+  STFEM_CUDA_TRY(cudaFuncSetAttribute(panel_ws_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
+                                      ws_smem_bytes<false, S>()));                                              \
+  STFEM_CUDA_TRY(cudaFuncSetAttribute(panel_ws_kernel<S>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  STFEM_PW_ATTR(4) STFEM_PW_ATTR(3) STFEM_PW_ATTR(2)
+#undef STFEM_PW_ATTR
   return STFEM_OK;
 }
 
@@ -1542,8 +1093,10 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
       } else {
         // large fronts: tile-parallel pipeline over all (front, shift) instances of the level
         const int ninst = a.nlist * nb, pmax = P.level_pmax[d];
+        const int T = std::max(1, std::min(ST_MAXT, P.opt.tiles_per_cta));   // tiles per CTA of the update engine
+        const int ws_stages = P.opt.ws_stages;
         const int64_t n32 = P.syrk32_off[d + 1] - P.syrk32_off[d];
-        // fused levels: the boundary block U is gathered by syrk32_kernel<true>, not assembled here
+        // fused levels: the boundary block U is gathered by syrk_ws_kernel<true>, not assembled here
         a.asm_pivots_only = (n32 > 0 && pmax >= P.opt.fused_min_p) ? 1 : 0;
         const int asm_cols = a.asm_pivots_only ? pmax : nmax;
         // deep levels (fronts of order <= asm_whole_n): one CTA per instance for all columns
@@ -1577,63 +1130,36 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
           for (int32_t f : P.levels[d])
             tiles = std::max(tiles, panel_update_tiles32(P.fronts[f].n, P.fronts[f].p, cb, narrow));
           if (tiles > 0) {
-            panel_update32_kernel<<<dim3(ninst, tiles), 128, S32_SMEM, st>>>(a, cb, k0, K, narrow);
-            STFEM_LAUNCH_CHECK("panel_update32_kernel");
+            const long long total = (long long)ninst * tiles;
+            const unsigned gr = (unsigned)((total + T - 1) / T);
+            if (ws_stages == 2)
+              panel_ws_kernel<2><<<gr, WS_THREADS, ws_smem_bytes<false, 2>(), st>>>(a, cb, k0, K, narrow, tiles, total, T);
+            else if (ws_stages == 4)
+              panel_ws_kernel<4><<<gr, WS_THREADS, ws_smem_bytes<false, 4>(), st>>>(a, cb, k0, K, narrow, tiles, total, T);
+            else
+              panel_ws_kernel<3><<<gr, WS_THREADS, ws_smem_bytes<false, 3>(), st>>>(a, cb, k0, K, narrow, tiles, total, T);
+            STFEM_LAUNCH_CHECK("panel_ws_kernel");
             ++nlaunch;
             fam(FAM_PANEL);
           }
         }
-        if (n32 > 0 && a.asm_pivots_only) {
-          if (P.opt.syrk_stream < 0) {
-            const long long total = (long long)n32 * nb;
-            const int T = std::max(1, std::min(ST_MAXT, -P.opt.syrk_stream));
-            const unsigned gr = (unsigned)((total + T - 1) / T);
-            const int4* tl = P.d_syrk32_tiles + P.syrk32_off[d];
-            const int ws_stages = P.opt.ws_stages;
-            if (ws_stages == 2)
-              syrk_ws_kernel<true, 2><<<gr, WS_THREADS, ws_smem_bytes<true, 2>(), st>>>(a, tl, (int)n32, total, T);
-            else if (ws_stages == 3)
-              syrk_ws_kernel<true, 3><<<gr, WS_THREADS, ws_smem_bytes<true, 3>(), st>>>(a, tl, (int)n32, total, T);
-            else
-              syrk_ws_kernel<true, 4><<<gr, WS_THREADS, ws_smem_bytes<true, 4>(), st>>>(a, tl, (int)n32, total, T);
-          } else if (P.opt.syrk_stream) {
-            const long long total = (long long)n32 * nb;
-            const int T = std::max(1, std::min(ST_MAXT, P.opt.syrk_stream));
-            syrk_stream_kernel<true><<<(unsigned)((total + T - 1) / T), 128, stream_smem_bytes<true>(), st>>>(
-                a, P.d_syrk32_tiles + P.syrk32_off[d], (int)n32, total, T);
+        if (n32 > 0) {
+          const long long total = (long long)n32 * nb;
+          const unsigned gr = (unsigned)((total + T - 1) / T);
+          const int4* tl = P.d_syrk32_tiles + P.syrk32_off[d];
+#define STFEM_SYRK_LAUNCH(G, S) \
+  syrk_ws_kernel<G, S><<<gr, WS_THREADS, ws_smem_bytes<G, S>(), st>>>(a, tl, (int)n32, total, T)
+          if (a.asm_pivots_only) {
+            if (ws_stages == 2) STFEM_SYRK_LAUNCH(true, 2);
+            else if (ws_stages == 3) STFEM_SYRK_LAUNCH(true, 3);
+            else STFEM_SYRK_LAUNCH(true, 4);
           } else {
-            syrk32_kernel<true><<<(unsigned)(n32 * nb), 128, S32_SMEM, st>>>(a, P.d_syrk32_tiles + P.syrk32_off[d]);
+            if (ws_stages == 2) STFEM_SYRK_LAUNCH(false, 2);
+            else if (ws_stages == 4) STFEM_SYRK_LAUNCH(false, 4);
+            else STFEM_SYRK_LAUNCH(false, 3);
           }
-          STFEM_LAUNCH_CHECK("syrk32_kernel<gather>");
-          ++nlaunch;
-          fam(FAM_SYRK);
-        } else if (n32 > 0 && pmax <= B16_KMAX && P.opt.syrk_block16 && level_bmax(P, d) <= B16_BMAX) {
-          syrk_block16_kernel<<<ninst, NT, b16_smem_bytes(level_bmax(P, d)), st>>>(a);
-          STFEM_LAUNCH_CHECK("syrk_block16_kernel");
-          ++nlaunch;
-          fam(FAM_SYRK);
-        } else if (n32 > 0) {
-          if (P.opt.syrk_stream < 0) {
-            const long long total = (long long)n32 * nb;
-            const int T = std::max(1, std::min(ST_MAXT, -P.opt.syrk_stream));
-            const unsigned gr = (unsigned)((total + T - 1) / T);
-            const int4* tl = P.d_syrk32_tiles + P.syrk32_off[d];
-            const int ws_stages = P.opt.ws_stages;
-            if (ws_stages == 2)
-              syrk_ws_kernel<false, 2><<<gr, WS_THREADS, ws_smem_bytes<false, 2>(), st>>>(a, tl, (int)n32, total, T);
-            else if (ws_stages == 3)
-              syrk_ws_kernel<false, 3><<<gr, WS_THREADS, ws_smem_bytes<false, 3>(), st>>>(a, tl, (int)n32, total, T);
-            else
-              syrk_ws_kernel<false, 4><<<gr, WS_THREADS, ws_smem_bytes<false, 4>(), st>>>(a, tl, (int)n32, total, T);
-          } else if (P.opt.syrk_stream) {
-            const long long total = (long long)n32 * nb;
-            const int T = std::max(1, std::min(ST_MAXT, P.opt.syrk_stream));
-            syrk_stream_kernel<false><<<(unsigned)((total + T - 1) / T), 128, stream_smem_bytes<false>(), st>>>(
-                a, P.d_syrk32_tiles + P.syrk32_off[d], (int)n32, total, T);
-          } else {
-            syrk32_kernel<false><<<(unsigned)(n32 * nb), 128, S32_SMEM, st>>>(a, P.d_syrk32_tiles + P.syrk32_off[d]);
-          }
-          STFEM_LAUNCH_CHECK("syrk32_kernel");
+#undef STFEM_SYRK_LAUNCH
+          STFEM_LAUNCH_CHECK("syrk_ws_kernel");
           ++nlaunch;
           fam(FAM_SYRK);
         }

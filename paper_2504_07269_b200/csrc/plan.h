@@ -90,9 +90,8 @@ struct Plan {
     o.fused_min_p = 0;
     o.panel_group = 2;
     o.asm_whole_n = INT32_MAX;
-    o.syrk_block16 = 1;
     o.level_timing = 0;
-    o.syrk_stream = -16;
+    o.tiles_per_cta = 16;
     o.ws_stages = 2;
     o.workspace_fraction = 0.70;
     o.pivot_tol = 1e-10;

@@ -138,9 +138,10 @@ class FDMSolver:
             # the paired eigenbasis (partners rebuilt from their leads) drives every stage
             lam, X, Y = pf.lam, pf.X, pf.Y
             self.pairs = PT.DevicePairs(pf, dev)
-        self.X = torch.as_tensor(X, dtype=C128, device=dev)
-        self.Y = torch.as_tensor(Y, dtype=C128, device=dev)
-        self.lam = torch.as_tensor(lam, dtype=C128, device=dev)
+        # row-major on the device: the C-ABI takes raw pointers (LAPACK hands back Fortran order)
+        self.X = torch.as_tensor(np.ascontiguousarray(X), dtype=C128, device=dev).contiguous()
+        self.Y = torch.as_tensor(np.ascontiguousarray(Y), dtype=C128, device=dev).contiguous()
+        self.lam = torch.as_tensor(np.ascontiguousarray(lam), dtype=C128, device=dev).contiguous()
         self.t_eig = box["t"]
         self.t_symbolic = t2 - t1
         self.t_setup = time.perf_counter() - t0

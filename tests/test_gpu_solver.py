@@ -71,24 +71,16 @@ def test_lifting_matches_oracle():
 MODES = {
     # plain multifrontal with the shared-memory small-front kernels below order 100
     "small": {},
-    # every front on the tile-parallel large-front pipeline, default tuning: extend-add fused into
-    # the 32 x 32-tile Schur update for levels with >= 50 pivots, 16 x 16-block Schur kernel for
-    # <= 32 pivots, 32 x 32 tiles elsewhere, trailing updates delayed over panel pairs
+    # every front on the tile-parallel large-front pipeline, default tuning: the children's
+    # extend-add fused into the Schur-update tiles on every level, trailing updates delayed over
+    # panel pairs, update engine with a 2-deep ring walking 16 tiles per CTA
     "big": dict(small_front_n=0),
-    "big_allfused": dict(small_front_n=0, fused_min_p=0),           # fused on every level
-    # none of it: U assembled by asm_front_kernel, per-panel trailing updates, 32 x 32 tiles on
-    # every level, 32-column assembly CTAs
-    "big_plain": dict(small_front_n=0, fused_min_p=1 << 30, panel_group=1, syrk_block16=0, asm_whole_n=0),
-    "big_pg4": dict(small_front_n=0, panel_group=4, syrk_block16=0),
-    # the per-tile Schur kernel (syrk_stream=0) and the warp-specialised TMA-fed one (< 0), with the
-    # extend-add fused on every level and on none
-    "big_tile_fused": dict(small_front_n=0, fused_min_p=0, syrk_stream=0),
-    "big_stream_fused": dict(small_front_n=0, fused_min_p=0, syrk_stream=8),
-    "big_ws_fused": dict(small_front_n=0, fused_min_p=0, syrk_stream=-8),
-    "big_ws_plain": dict(small_front_n=0, fused_min_p=1 << 30, syrk_block16=0, syrk_stream=-3),
-    "big_ws_s4_fused": dict(small_front_n=0, fused_min_p=0, syrk_stream=-5, ws_stages=4),
-    "big_ws_s2_fused": dict(small_front_n=0, fused_min_p=0, syrk_stream=-16, ws_stages=2),
-    "big_ws_s3_plain": dict(small_front_n=0, fused_min_p=1 << 30, syrk_block16=0, syrk_stream=-7, ws_stages=3),
+    # U assembled by asm_front_kernel (no fusion), per-panel trailing updates, 32-column assembly CTAs
+    "big_plain": dict(small_front_n=0, fused_min_p=1 << 30, panel_group=1, asm_whole_n=0),
+    "big_pg4": dict(small_front_n=0, panel_group=4, tiles_per_cta=5),
+    "big_fuse40": dict(small_front_n=0, fused_min_p=40, ws_stages=3, tiles_per_cta=1),
+    "big_s4": dict(small_front_n=0, ws_stages=4, tiles_per_cta=7),
+    "big_s4_plain": dict(small_front_n=0, fused_min_p=1 << 30, ws_stages=4),
     # spectral subtrees of <= 24 / <= 256 interior DoFs (K6) under a multifrontal top
     "spec24": {}, "spec": {},
 }
