@@ -26,6 +26,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <array>
 #include <string>
 
 #include "plan.h"
@@ -785,7 +786,7 @@ int upload(Plan& P) {
         for (int32_t t : roots) {
           const SubDev& S = P.subs[t];
           if (j == 0) {
-            const int nbk = (S.g + 7) / 8;
+            const int nbk = P.sub_rep[t] ? (S.g + 7) / 8 : 0;   // the class's update block: once
             for (int bj = 0; bj < nbk; ++bj)
               for (int bi = bj; bi < nbk; ++bi) items.push_back(make_int4(OP_U, t, bi, bj));
             for (int q = 0; q < (S.m + SP_BM - 1) / SP_BM; ++q) items.push_back(make_int4(OP_F1, t, q, 0));
@@ -1367,15 +1368,42 @@ extern "C" int stfem_plan_set_spectral(stfem_plan* plan, int32_t nroots, const i
       if (!skip[f]) P.levels[d].push_back(f);
   for (int32_t t = 0; t < nroots; ++t) P.sub_levels[P.fronts[root_front[t]].depth].push_back(t);
   stfem::assign_factor_offsets(P, skip);
+  // Congruent subtrees (spectral.py hands them the SAME data offsets) have the same update block
+  // U(lam) = -(R diag(w) R^T + C0 + lam C1) for every shift: it is computed once per class (by the
+  // class's first subtree of each pool parity) and the other roots' update blocks alias it -- the
+  // parents gather through their own inverse maps, so nothing else changes.  C4: 1024 subtrees,
+  // 20 classes: 98% of the update-block GEMMs of the spectral level disappear.
+  for (int32_t f = 0; f < nf; ++f) P.fronts[f].uofs = P.uofs0[f];
+  P.sub_rep.assign(nroots, 1);
+  {
+    std::vector<std::pair<std::array<int64_t, 5>, int32_t>> seen;
+    for (int32_t t = 0; t < nroots; ++t) {
+      const stfem::SubDev& S = subs[t];
+      const std::array<int64_t, 5> key{S.vofs, S.tofs, S.rqofs, S.cofs, (int64_t)(P.fronts[S.front].depth & 1)};
+      int32_t rep = -1;
+      for (const auto& e : seen)
+        if (e.first == key) {
+          rep = e.second;
+          break;
+        }
+      if (rep < 0) {
+        seen.push_back({key, t});
+      } else {
+        P.sub_rep[t] = 0;
+        P.fronts[S.front].uofs = P.fronts[subs[rep].front].uofs;
+      }
+    }
+  }
   P.h_V.assign(V, V + (nroots ? nV : 0));
   P.h_th.assign(theta, theta + (nroots ? ntheta : 0));
   P.h_RQ.assign(RQ, RQ + (nroots ? nRQ : 0));
   P.h_C01.assign(C01, C01 + (nroots ? nC01 : 0));
   P.spectral_flops_u = 0;
   P.spectral_flops_rhs = 0;
-  for (const auto& S : subs) {
+  for (int32_t t = 0; t < nroots; ++t) {
+    const stfem::SubDev& S = subs[t];
     const int64_t E = (int64_t)S.g * (S.g + 1) / 2;
-    P.spectral_flops_u += 4 * E * S.m;
+    if (P.sub_rep[t]) P.spectral_flops_u += 4 * E * S.m;   // executed: one update block per class
     P.spectral_flops_rhs += 4LL * S.m * S.m * 2 + 4LL * S.g * 2 * S.m * 2;
   }
   return STFEM_OK;

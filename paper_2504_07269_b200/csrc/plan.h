@@ -62,6 +62,8 @@ struct Plan {
   // ---- spectral subtrees (optional, stfem_plan_set_spectral) ----
   std::vector<std::vector<int32_t>> levels_all;   // every front per depth (levels = multifrontal ones)
   std::vector<SubDev> subs;
+  std::vector<char> sub_rep;                      // subtree t computes its class's update block (others alias it)
+  std::vector<int64_t> uofs0;                     // update-block offsets of the symbolic analysis (before aliasing)
   std::vector<std::vector<int32_t>> sub_levels;   // per depth: indices into subs
   std::vector<double> h_V, h_th, h_RQ, h_C01;
   int64_t spectral_flops_u = 0;                   // DMMA flops per shift of OP_U (4 E m)

@@ -366,6 +366,8 @@ int build_symbolic(Plan& P, int32_t n, const int64_t* rowptr, const int32_t* col
     P.upool_stride[d & 1] = std::max(P.upool_stride[d & 1], u);
     P.rpool_stride[d & 1] = std::max(P.rpool_stride[d & 1], r);
   }
+  P.uofs0.resize(nf);
+  for (int32_t f = 0; f < nf; ++f) P.uofs0[f] = P.fronts[f].uofs;
   return STFEM_OK;
 }
 
