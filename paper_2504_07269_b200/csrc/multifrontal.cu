@@ -126,11 +126,14 @@ struct __align__(16) StreamTile {
 // enough to keep the pipe busy through the other CTA's epilogues.
 // ---------------------------------------------------------------------------
 // warps 0-3: DMMA consumers (2 x 2 of 16 x 16); warp 4: bulk copies of the A rows of every chunk;
-// warp 5: the B rows; warp 6: the tile's starting values.  (Measured on C4, 384 shifts, depths 1-6,
-// ms per batch: one bulk-copy warp for A and B 91.0 -- its 32 UBLKCPs per chunk issue one by one,
-// their operands being uniform registers -- two warps 79.4, four 81.3; a cp.async producer 86.9;
-// staging the starting values from the A warp instead of a third warp cost another 8 ms.)
-constexpr int WS_THREADS = 224;
+// warp 5: the B rows; warps 6, 7: the tile's starting values (GATHER: one warp per child -- a
+// single staging warp was issue bound at the short-K levels, ncu had the consumers waiting on
+// "cfull" in 22% of all samples: C4 Schur updates 278 -> 271 ms with two; otherwise warp 6 alone).
+// (Measured on C4, 384 shifts, depths 1-6, ms per batch: one bulk-copy warp for A and B 91.0 --
+// its 32 UBLKCPs per chunk issue one by one, their operands being uniform registers -- two warps
+// 79.4, four 81.3; a cp.async producer 86.9; staging the starting values from the A warp instead
+// of a third warp cost another 8 ms.)
+constexpr int WS_THREADS = 256;
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
@@ -180,26 +183,36 @@ __device__ __forceinline__ void ws_tiles(const StreamTile* __restrict__ desc, in
                                          uint64_t* full, uint64_t* empty, uint64_t* cfull, uint64_t* cempty,
                                          const int32_t* __restrict__ inv) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (warp == 6) {
-    // ---------------- starting values: one staging tile (two with GATHER) per tile ----------------
+  if (warp >= 6) {
+    // ---------------- starting values: one staging tile per child (GATHER) or one in all ----------------
+    const int s = warp - 6;   // GATHER: this warp's child
+    if (!GATHER && s == 1) return;
     uint32_t cphase = 0;
-    for (int j = 0; j < nt; ++j) {
-      const StreamTile& D = desc[j];
-      if (D.K <= 0) continue;
-      const int M = D.M, N = D.N, i0 = D.i0, c0 = D.c0;
-      mbar_wait(cempty, cphase ^ 1);   // the consumers have read the previous tile's values
-      cphase ^= 1;
-      if constexpr (GATHER) {
-        // the children's extend-add through the inverse maps: lane = tile row; the column map is
-        // loaded once (lane = column) and broadcast
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          const int off = D.inv_off[s];
-          if (off < 0) continue;
+    if constexpr (GATHER) {
+      // the child's extend-add through the inverse maps: lane = tile row; the column map is
+      // loaded once (lane = column) and broadcast.  The maps of the next tile are fetched before
+      // this tile's copies are issued, so their latency never sits between two tiles.
+      int jn = 0;
+      while (jn < nt && desc[jn].K <= 0) ++jn;
+      int kr_n = -1, kc_n = -1;
+      auto fetch = [&](int j) {
+        const StreamTile& D = desc[j];
+        const int off = D.inv_off[s];
+        kr_n = (off >= 0 && D.i0 + lane < D.M) ? inv[off + D.i0 + lane] : -1;
+        kc_n = (off >= 0 && D.c0 + lane < D.N) ? inv[off + D.c0 + lane] : -1;
+      };
+      if (jn < nt) fetch(jn);
+      while (jn < nt) {
+        const int j = jn;
+        const int kr = kr_n, kcl = kc_n;
+        do ++jn; while (jn < nt && desc[jn].K <= 0);
+        if (jn < nt) fetch(jn);
+        const StreamTile& D = desc[j];
+        mbar_wait(cempty, cphase ^ 1);   // the consumers have read the previous tile's values
+        cphase ^= 1;
+        if (D.inv_off[s] >= 0) {
           const cplx* Uc = D.Uc[s];
-          const int bc = D.bc[s];
-          const int kr = (i0 + lane < M) ? inv[off + i0 + lane] : -1;
-          const int kcl = (c0 + lane < N) ? inv[off + c0 + lane] : -1;
+          const int bc = D.bc[s], i0 = D.i0, c0 = D.c0;
           cplx* dst = Cs + s * ST_CS + lane;
 #pragma unroll 8
           for (int cc = 0; cc < 32; ++cc) {
@@ -208,8 +221,15 @@ __device__ __forceinline__ void ws_tiles(const StreamTile* __restrict__ desc, in
             cp_async16(dst + cc * S32_LD, ok ? Uc + (int64_t)kc * bc + kr : Uc, ok);
           }
         }
-        cp_async_mbar_arrive(cfull);   // 32 expected arrivals: one per lane, when its copies have landed
-      } else {
+        cp_async_mbar_arrive(cfull);   // 64 expected arrivals: one per lane of both warps, when its copies have landed
+      }
+    } else {
+      for (int j = 0; j < nt; ++j) {
+        const StreamTile& D = desc[j];
+        if (D.K <= 0) continue;
+        const int M = D.M, N = D.N, i0 = D.i0, c0 = D.c0;
+        mbar_wait(cempty, cphase ^ 1);
+        cphase ^= 1;
         const int ncol = min(32, N - c0), rows = min(32, M - i0);
         if (lane == 0) mbar_arrive_expect_tx(cfull, (uint32_t)ncol * (uint32_t)rows * 16u);
         __syncwarp();
@@ -341,7 +361,7 @@ __device__ __forceinline__ void ws_init_barriers(uint64_t* full, uint64_t* empty
     mbar_init(&full[s], 2);     // the A and the B warp's arrive.expect_tx (+ their copies' bytes)
     mbar_init(&empty[s], 4);    // one arrival per consumer warp
   }
-  mbar_init(cfull, GATHER ? 32 : 1);
+  mbar_init(cfull, GATHER ? 64 : 1);
   mbar_init(cempty, 4);
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 }
@@ -1256,6 +1276,8 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
       P.family_ms[fe.second] += ms;
       P.family_launches[fe.second] += 1;
       dfm[(size_t)(fev_depth[i] + 1) * NFAM + fe.second] += ms;
+      if (level_print && fe.second == FAM_SPECTRAL)
+        fprintf(stderr, "[stfem spectral launch] depth %d: %.3f ms\n", fev_depth[i], ms);
       prev = fe.first;
     }
     if (level_print) {
