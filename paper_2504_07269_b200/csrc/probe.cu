@@ -96,8 +96,33 @@ __global__ void dmma_chain_probe_kernel(double* sink, int iters) {
   if (s == 12345.678) sink[threadIdx.x] = s;
 }
 
+// Workspace-layout probe: CTA (front f, shift k) -- shifts fastest, as in every level kernel --
+// reads (or writes) one contiguous chunk at buf + k * kstride + f * fstride (complex elements).
+// "shift-major" (kstride = whole per-shift workspace) against "front-major" (kstride = chunk).
+__global__ void __launch_bounds__(128) layout_probe_kernel(cplx* buf, long long kstride, long long fstride,
+                                                           int chunk, int nshift, int write, double* sink) {
+  const long long inst = blockIdx.x;
+  const long long k = inst % nshift, f = inst / nshift;
+  cplx* p = buf + k * kstride + f * fstride;
+  double acc = 0.0;
+  if (write) {
+    for (int i = threadIdx.x; i < chunk; i += 128) stc(p + i, cmk(1.0, 2.0));
+  } else {
+    for (int i = threadIdx.x; i < chunk; i += 128) acc += ldc(p + i).re;
+  }
+  if (acc == 12345.678) sink[0] = acc;
+}
+
 }  // namespace
 }  // namespace stfem
+
+extern "C" int stfem_probe_layout(void* buf, long long kstride, long long fstride, int chunk, int nshift,
+                                  int nfront, int write, double* sink, void* stream) {
+  stfem::layout_probe_kernel<<<(unsigned)((long long)nshift * nfront), 128, 0, (cudaStream_t)stream>>>(
+      (stfem::cplx*)buf, kstride, fstride, chunk, nshift, write, sink);
+  STFEM_LAUNCH_CHECK("layout probe");
+  return STFEM_OK;
+}
 
 // 8 DMMAs per iteration per warp on `chains` (1, 2, 4 or 8) independent accumulators
 extern "C" int stfem_probe_dmma_chains(int chains, int warps_per_cta, int blocks, int iters, double* sink,
