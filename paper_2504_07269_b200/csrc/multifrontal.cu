@@ -82,8 +82,13 @@ struct LevelArgs {
 };
 
 __device__ __forceinline__ int64_t bv_off(const stfem_bv_layout& L, int r, int64_t shift, int64_t j) {
-  return r * L.rhs_stride + shift * L.shift_stride + (j / L.chunk_cols) * L.chunk_stride +
-         j % L.chunk_cols;
+  // un-chunked BlockVectors (chunk_cols >= n_x: every single-GPU call) skip the 64-bit division
+  int64_t q = 0;
+  if (j >= L.chunk_cols) {
+    q = j / L.chunk_cols;
+    j -= q * L.chunk_cols;
+  }
+  return r * L.rhs_stride + shift * L.shift_stride + q * L.chunk_stride + j;
 }
 
 #include "multifrontal_large.cuh"
@@ -631,6 +636,188 @@ int launch_backward_level(const LevelArgs& a, int grid, int nmax, int unit, cuda
   }
   backward_level_kernel<NR><<<grid, NT, (size_t)nmax * a.nrhs * 16, s>>>(a, unit);
   STFEM_LAUNCH_CHECK("backward_level_kernel");
+  return STFEM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Multi-RHS backward substitution of one level on the FP64 tensor pipe.
+// backward_level_kernel turns every pivot column into nrhs warp-wide dot
+// products: with 9 right-hand sides (C5) it ran at 15% of the HBM roofline, the
+// top levels at one CTA of 8 warps per SM walking a 996 x 255 front column by
+// column.  Here the same two products are GEMMs over the right-hand sides,
+//   T = Z_p - L21^T X_B                     (M = p columns, N = nrhs, K = b rows)
+//   T[0:kb] -= L[kb:kb+w, 0:kb]^T X[kb:kb+w] after panel kb is solved (right-looking, K = w),
+// on m16n8k4 DMMAs: A = L^T read from global memory straight in fragment layout (8 columns x 4
+// consecutive rows = eight 64-byte segments per load), B = x from shared memory, 4 real
+// DMMAs per complex 16 x 8 x 4 block.  Warps own 16-column tiles; fronts with fewer tiles than
+// warps split K over the spare warps and reduce through shared memory in a fixed order
+// (deterministic).  Only the 32 x 32 triangle of each panel stays a warp-per-RHS substitution.
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int bwd_nrp(int nrhs) { return nrhs <= 10 ? 10 : 18; }   // xs row pitch: = 2 mod 8, >= nrhs
+template <int NW>
+__host__ __device__ constexpr int bwd_mrhs_smem(int nmax, int nrhs) { return (nmax * bwd_nrp(nrhs) + NW * 256) * 16; }
+
+// acc(16 columns x 8 NT8 rhs) = sum over k steps ks = ks0, ks0 + kstep, ... < KS of
+// L[row0 + 4 ks + t][j0 + g (+8)] * xs[row0 + 4 ks + t][rhs]; K = valid rows from row0
+template <int NT8>
+__device__ __forceinline__ void bwd_gemm_tile(const cplx* __restrict__ P, int n, int j0, int jlim, int row0, int K,
+                                              int ks0, int kstep, const cplx* xs, int NRP, int nrhs,
+                                              double (&cr)[2][4], double (&ci)[2][4]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const cplx zero = cmk(0.0, 0.0);
+  const cplx* c0 = P + (int64_t)min(j0 + g, jlim - 1) * n + row0 + t;
+  const cplx* c1 = P + (int64_t)min(j0 + g + 8, jlim - 1) * n + row0 + t;
+  const cplx* xb = xs + (int64_t)(row0 + t) * NRP + g;
+  const int KS = (K + 3) >> 2;
+  constexpr int UN = 4;   // k steps in flight
+  for (int ks = ks0; ks < KS; ks += UN * kstep) {
+    cplx a0[UN], a1[UN];
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int kq = ks + u * kstep;
+      const bool ok = kq < KS && 4 * kq + t < K;
+      a0[u] = ok ? ldc(c0 + 4 * kq) : zero;
+      a1[u] = ok ? ldc(c1 + 4 * kq) : zero;
+    }
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int kq = ks + u * kstep;
+      if (kq >= KS) break;
+      const int rr = min(4 * kq + t, K - 1) - t;   // clamped: a zero A fragment must not meet a NaN
+#pragma unroll
+      for (int ni = 0; ni < NT8; ++ni) {
+        const cplx bx = ni * 8 + g < nrhs ? xb[(int64_t)rr * NRP + ni * 8] : zero;
+        dmma_16x8x4(cr[ni], a0[u].re, a1[u].re, bx.re);
+        dmma_16x8x4(cr[ni], -a0[u].im, -a1[u].im, bx.im);
+        dmma_16x8x4(ci[ni], a0[u].re, a1[u].re, bx.im);
+        dmma_16x8x4(ci[ni], a0[u].im, a1[u].im, bx.re);
+      }
+    }
+  }
+}
+
+template <int NW, int NT8>
+__global__ void __launch_bounds__(32 * NW) backward_mrhs_kernel(LevelArgs a, int unit) {
+  __shared__ cplx l11[NB * LDD];   // l11[c * LDD + i] = L[kb+i][kb+c], i > c; diagonal: 1/L[c][c] (or 1)
+  extern __shared__ __align__(16) unsigned char bwd_smem[];
+  constexpr int NTH = 32 * NW;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int inst = blockIdx.x;
+  const int k = inst % a.nbatch;
+  const FrontDev F = a.fronts[a.list[inst / a.nbatch]];
+  const int n = F.n, p = F.p, b = n - p;
+  const int nrhs = a.nrhs, nx = a.nx, NRP = bwd_nrp(nrhs);
+  const cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
+  cplx* Zk = a.Z + (int64_t)k * nx * nrhs;
+  const int32_t* bidx = a.bidx + F.bidx_beg;
+  const int64_t shift = a.shift0 + k;
+  const cplx zero = cmk(0.0, 0.0);
+  cplx* xs = reinterpret_cast<cplx*>(bwd_smem);   // [n][NRP]: x (boundary rows), t then x (pivot rows); rhs >= nrhs: 0
+  cplx* slots = xs + (int64_t)n * NRP;            // [NW][16 columns][16 rhs] partial tiles of a split K
+  // rows fastest (coalesced along the pivot rows)
+  for (int q = tid; q < n * nrhs; q += NTH) {
+    const int r = q / n, i = q - r * n;
+    xs[i * NRP + r] = ldc(Zk + (i < p ? F.pbeg + i : bidx[i - p]) + (int64_t)r * nx);
+  }
+  __syncthreads();
+  auto apply = [&](int j0, int jlim, double (&cr)[2][4], double (&ci)[2][4]) {
+#pragma unroll
+    for (int ni = 0; ni < NT8; ++ni)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int j = j0 + g + 8 * h;
+          if (j < jlim && ni * 8 + 2 * t + v < nrhs) {
+            cplx* d = xs + j * NRP + ni * 8 + 2 * t + v;
+            *d = cmk(d->re - cr[ni][2 * h + v], d->im - ci[ni][2 * h + v]);
+          }
+        }
+  };
+  // 2. boundary contributions of all pivot columns
+  if (b > 0) {
+    const int MT = (p + 15) >> 4;
+    if (MT >= NW) {
+      for (int mt = warp; mt < MT; mt += NW) {
+        double cr[2][4] = {}, ci[2][4] = {};
+        bwd_gemm_tile<NT8>(P, n, mt * 16, p, p, b, 0, 1, xs, NRP, nrhs, cr, ci);
+        apply(mt * 16, p, cr, ci);
+      }
+    } else {
+      // fewer column tiles than warps: S warps share a tile, interleaved over the k steps
+      const int MTc = MT <= 1 ? 1 : MT <= 2 ? 2 : MT <= 4 ? 4 : 8, S = NW / MTc;
+      const int mt = warp % MTc, sl = warp / MTc;
+      {
+        double cr[2][4] = {}, ci[2][4] = {};
+        if (mt < MT && sl < S) bwd_gemm_tile<NT8>(P, n, mt * 16, p, p, b, sl, S, xs, NRP, nrhs, cr, ci);
+        cplx* my = slots + warp * 256;
+#pragma unroll
+        for (int ni = 0; ni < NT8; ++ni)
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            my[(g + 8 * (e >> 1)) * 16 + ni * 8 + 2 * t + (e & 1)] = cmk(cr[ni][e], ci[ni][e]);
+      }
+      __syncthreads();
+      for (int q = tid; q < MT * 16 * 8 * NT8; q += NTH) {
+        const int r = q % (8 * NT8), j = q / (8 * NT8), m2 = j >> 4;
+        if (j >= p || r >= nrhs) continue;
+        cplx sum = zero;
+        for (int s2 = 0; s2 < S; ++s2) sum = cadd(sum, slots[(s2 * MTc + m2) * 256 + (j & 15) * 16 + r]);
+        cplx* d = xs + j * NRP + r;
+        *d = csub(*d, sum);
+      }
+    }
+    __syncthreads();
+  }
+  // 3. pivot triangle, panels from the last; each solved panel updates all earlier columns
+  for (int kb = ((p - 1) / NB) * NB; kb >= 0; kb -= NB) {
+    const int w = min(NB, p - kb);
+    for (int idx = tid; idx < NB * NB; idx += NTH) {
+      const int i = idx % NB, c = idx / NB;
+      if (i < w && c < w && i >= c) {
+        const cplx v = ldc(P + (kb + i) + (int64_t)(kb + c) * n);
+        l11[c * LDD + i] = i > c ? v : (unit ? cmk(1.0, 0.0) : crecip(v));
+      }
+    }
+    __syncthreads();
+    // x_j = (t_j - sum_{c>j} L[c][j] x_c) * dinv_j in column (axpy) form, one warp per RHS
+    for (int r = warp; r < nrhs; r += NW) {
+      cplx xl = lane < w ? xs[(kb + lane) * NRP + r] : zero;
+      for (int c = w - 1; c >= 0; --c) {
+        if (lane == c) xl = cmul(xl, l11[c * LDD + c]);
+        const cplx xc = cmk(__shfl_sync(0xffffffffu, xl.re, c), __shfl_sync(0xffffffffu, xl.im, c));
+        if (lane < c) xl = cfms(xl, l11[lane * LDD + c], xc);
+      }
+      if (lane < w) {
+        stc(Zk + F.pbeg + kb + lane + (int64_t)r * nx, xl);
+        stc(a.W + bv_off(a.lay, r, shift, a.perm[F.pbeg + kb + lane]), xl);
+        xs[(kb + lane) * NRP + r] = xl;
+      }
+    }
+    __syncthreads();
+    if (kb > 0) {
+      const int MT = (kb + 15) >> 4;
+      for (int mt = warp; mt < MT; mt += NW) {
+        double cr[2][4] = {}, ci[2][4] = {};
+        bwd_gemm_tile<NT8>(P, n, mt * 16, kb, kb, w, 0, 1, xs, NRP, nrhs, cr, ci);
+        apply(mt * 16, kb, cr, ci);
+      }
+      __syncthreads();
+    }
+  }
+}
+
+template <int NW, int NT8>
+int launch_backward_mrhs(const LevelArgs& a, int grid, int nmax, int unit, cudaStream_t s) {
+  static DeviceOnce attr_once;
+  if (attr_once.first()) {
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_mrhs_kernel<NW, NT8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        200 * 1024));
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_mrhs_kernel<NW, NT8>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        100));
+  }
+  backward_mrhs_kernel<NW, NT8><<<grid, 32 * NW, bwd_mrhs_smem<NW>(nmax, a.nrhs), s>>>(a, unit);
+  STFEM_LAUNCH_CHECK("backward_mrhs_kernel");
   return STFEM_OK;
 }
 
@@ -1214,9 +1401,13 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
         b.list = a.list + off;
         b.nlist = cnt;
         const int bsm = small_bwd_smem_bytes(nmax, pmax, small_nr(nrhs));
-        if (nmax <= SMALL_N && bsm <= 200 * 1024 && P.opt.small_front_n > 0)
+        if (nmax <= SMALL_N && bsm <= 200 * 1024 && P.opt.small_front_n > 0 && (ldlt || nrhs < 2 || pmax <= P.opt.bwd_dmma_min_p))
           return launch_small_backward_any(b, cnt * nb, nmax, pmax, st);
         const int u = ldlt ? 1 : 0, gsz = cnt * nb;
+        if (nrhs >= 2 && pmax > P.opt.bwd_dmma_min_p && bwd_mrhs_smem<8>(nmax, nrhs) <= 200 * 1024) {
+          // multi-RHS, multi-panel fronts: GEMMs over the right-hand sides on DMMA
+          return nrhs <= 8 ? launch_backward_mrhs<8, 1>(b, gsz, nmax, u, st) : launch_backward_mrhs<8, 2>(b, gsz, nmax, u, st);
+        }
         switch (small_nr(nrhs)) {
           case 1: return launch_backward_level<1>(b, gsz, nmax, u, st);
           case 2: return launch_backward_level<2>(b, gsz, nmax, u, st);

@@ -95,6 +95,7 @@ struct Plan {
     o.level_timing = 0;
     o.tiles_per_cta = 16;
     o.ws_stages = 2;
+    o.bwd_dmma_min_p = 32;
     o.workspace_fraction = 0.70;
     o.pivot_tol = 1e-10;
     return o;

@@ -39,7 +39,8 @@ constexpr int SP_LDA = SP_BM + 4;   // As[k][row] doubles: (t*68 + g) mod 16 hit
 constexpr int SP_LDB = SP_BN + 2;   // Bs[k][col] complex: (t*66 + g) mod 8 hits each 16-B bank group 4x
 constexpr int SP_A_STAGE = SP_BK * SP_LDA;   // doubles
 constexpr int SP_B_STAGE = SP_BK * SP_LDB;   // complex
-constexpr int SP_SMEM = 2 * (SP_A_STAGE * 8 + SP_B_STAGE * 16);
+constexpr int SP_STAGES = 3;   // cp.async ring of the plain-copy ops (F1, B1); U, F2 and B2 use two
+constexpr int SP_SMEM = SP_STAGES * (SP_A_STAGE * 8 + SP_B_STAGE * 16);
 // + OP_U staging: the tile's 16 R rows over the subtree's m
 __host__ __device__ constexpr int spectral_smem_bytes(int mmax) { return SP_SMEM + 16 * (mmax | 1) * 8; }
 enum { OP_U = 0, OP_F1 = 1, OP_F2 = 2, OP_B1 = 3, OP_B2 = 4 };
@@ -108,7 +109,7 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
 
   // OP_U operands are generated from shared memory: the 16 R rows of the
   // tile's (i, j) block over all k, theta, and the tile's 64 shifts
-  double* Rs = reinterpret_cast<double*>(Bs + 2 * SP_B_STAGE);   // [16][ms], ms = m | 1 (odd: no bank conflicts)
+  double* Rs = reinterpret_cast<double*>(Bs + SP_STAGES * SP_B_STAGE);   // [16][ms], ms = m | 1 (odd: no bank conflicts)
   const int ms = m | 1;
   const cplx* __restrict__ wsub = a.wbuf + (int64_t)S.tofs * a.wstride;   // w[k * wstride + s]
   if constexpr (OP == OP_U) {
@@ -118,6 +119,16 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
       const int row = rr < 8 ? it.z * 8 + rr : it.w * 8 + rr - 8;
       Rs[rr * ms + k] = row < g ? Rm[row + (int64_t)k * g] : 0.0;
     }
+    __syncthreads();
+  }
+  // OP_F1 / OP_B1 gather their B operand through an index table (the permutation of the subtree's
+  // interior DoFs / the root's boundary rows).  Staged once per tile: the per-chunk fetch is then
+  // one global load deep instead of two dependent ones (ncu: the index loads were 23% of all
+  // stall samples of the F1 launch, long scoreboard)
+  int* idx_s = reinterpret_cast<int*>(Rs);
+  if constexpr (OP == OP_F1 || OP == OP_B1) {
+    const int cnt = OP == OP_F1 ? m : g;
+    for (int q = tid; q < cnt; q += 256) idx_s[q] = OP == OP_F1 ? a.perm[S.first + q] : bidx[q];
     __syncthreads();
   }
 
@@ -148,10 +159,10 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
     if (OP == OP_U) return ldc(wsub + (int64_t)k * a.wstride + cg);
     const int s = cg / nrhs, r = cg - s * nrhs;
     const cplx* Zs = a.Z + (int64_t)s * nx * nrhs + (int64_t)r * nx;
-    if (OP == OP_F1) return ldc(a.G + bv_off(a.lay, r, a.shift0 + s, a.perm[S.first + k]));
+    if (OP == OP_F1) return ldc(a.G + bv_off(a.lay, r, a.shift0 + s, idx_s[k]));
     if (OP == OP_F2)
       return k < m ? cmul(ldc(wsub + (int64_t)k * a.wstride + s), ldc(Zs + S.first + k)) : ldc(Zs + S.first + k - m);
-    if (OP == OP_B1) return ldc(Zs + bidx[k]);
+    if (OP == OP_B1) return ldc(Zs + idx_s[k]);
     return ldc(Zs + S.first + k);
   };
 
@@ -199,19 +210,12 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
       for (int v = 0; v < 4; ++v) acc[mi][ni][0][v] = acc[mi][ni][1][v] = 0.0;
 
   const int nk = (K + SP_BK - 1) / SP_BK;
-  if (nk > 0) {
-    fetch(0);
-    store(0);
-  }
-  if constexpr (OP == OP_U) cp_async_wait<0>();
-  __syncthreads();
   // the last column tile of a batch is partial (e.g. 342 shifts = 5 x 64 + 22): warps whose
   // 16 (or upper 8) columns are all past ncols skip their DMMAs (warp-uniform)
   const bool wact = n0 + wn * 16 < ncols, wact1 = n0 + wn * 16 + 8 < ncols;
-  for (int kc = 0; kc < nk; ++kc) {
-    if (kc + 1 < nk) fetch(kc + 1);
-    const double* as = As + (kc & 1) * SP_A_STAGE + tq * SP_LDA + wm * 32 + gq;
-    const cplx* bs = Bs + (kc & 1) * SP_B_STAGE + tq * SP_LDB + wn * 16 + gq;
+  auto compute = [&](int st) {
+    const double* as = As + st * SP_A_STAGE + tq * SP_LDA + wm * 32 + gq;
+    const cplx* bs = Bs + st * SP_B_STAGE + tq * SP_LDB + wn * 16 + gq;
 #pragma unroll
     for (int kk = 0; kk < SP_BK; kk += 4) {
       if (!wact) break;
@@ -233,9 +237,80 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
           dmma_16x8x4(acc[mi][ni][1], af[mi][0], af[mi][1], bf[ni].im);
         }
     }
-    if (kc + 1 < nk) store((kc + 1) & 1);
+  };
+  if constexpr (OP == OP_F1 || OP == OP_B1) {
+    // Plain-copy operands (matrix tiles of V / R / Q, vectors gathered through the staged index
+    // table): a 3-stage cp.async ring, one barrier per K chunk, nothing staged through
+    // registers.  The thread's B column is the same for every chunk: its base pointer (and
+    // the shift / RHS split of the column) is formed once.  (Measured per batch, register
+    // path -> ring: C4 F1 5.45 -> 5.61, B1 3.58 -> 3.69, B2 4.43 -> 5.43 ms; C5 (9 RHS) F1 11.4 ->
+    // 10.0, B1 10.1 -> 8.9, B2 10.2 -> 10.0: B2 stays on the register path.)
+    const int bc = tid & 63, bcg = n0 + bc;
+    const bool bcol_ok = bcg < ncols;
+    const int bs_ = bcol_ok ? bcg / nrhs : 0, br = bcol_ok ? bcg - bs_ * nrhs : 0;
+    const cplx* bbase = OP == OP_F1 ? a.G + bv_off(a.lay, br, a.shift0 + bs_, 0)
+                                    : a.Z + (int64_t)bs_ * nx * nrhs + (int64_t)br * nx + (OP == OP_B2 ? S.first : 0);
+    const bool unchunked = a.lay.chunk_cols >= nx;
+    auto issue = [&](int st, int kc) {
+      const int k0 = kc * SP_BK;
+      double* as = As + st * SP_A_STAGE;
+      cplx* bs = Bs + st * SP_B_STAGE;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = tid + 256 * u;
+        if constexpr (OP == OP_F1) {
+          const int r = idx >> 4, k = k0 + (idx & 15), ko = it.z * SP_BM + r;
+          const bool ok = ko < m && k < K;
+          cp_async8(as + (idx & 15) * SP_LDA + r, ok ? V + k + (int64_t)ko * m : V, ok);
+        } else if constexpr (OP == OP_B1) {
+          const int r = idx & 63, k = k0 + (idx >> 6), kk = it.z * 32 + (r >> 4) * 8 + (r & 7);
+          const bool ok = kk < m && k < K;
+          cp_async8(as + (idx >> 6) * SP_LDA + r, ok ? ((r >> 3) & 1 ? Qm : Rm) + k + (int64_t)kk * g : Rm, ok);
+        } else {
+          const int r = idx & 63, k = k0 + (idx >> 6), i = it.z * SP_BM + r;
+          const bool ok = i < m && k < K;
+          cp_async8(as + (idx >> 6) * SP_LDA + r, ok ? V + i + (int64_t)k * m : V, ok);
+        }
+        const int k = k0 + (idx >> 6);
+        const bool ok = bcol_ok && k < K;
+        const cplx* src = bbase;
+        if (ok) {
+          if constexpr (OP == OP_F1)
+            src = unchunked ? bbase + idx_s[k] : a.G + bv_off(a.lay, br, a.shift0 + bs_, idx_s[k]);
+          else if constexpr (OP == OP_B1) src = bbase + idx_s[k];
+          else src = bbase + k;
+        }
+        cp_async16(bs + (idx >> 6) * SP_LDB + bc, src, ok);
+      }
+    };
+#pragma unroll
+    for (int st = 0; st < SP_STAGES - 1; ++st) {
+      if (st < nk) issue(st, st);
+      cp_async_commit();
+    }
+    for (int kc = 0; kc < nk; ++kc) {
+      cp_async_wait<SP_STAGES - 2>();
+      __syncthreads();
+      const int nxt = kc + SP_STAGES - 1;
+      if (nxt < nk) issue(nxt % SP_STAGES, nxt);
+      cp_async_commit();
+      compute(kc % SP_STAGES);
+    }
+    cp_async_wait<0>();
+  } else {
+    if (nk > 0) {
+      fetch(0);
+      store(0);
+    }
     if constexpr (OP == OP_U) cp_async_wait<0>();
     __syncthreads();
+    for (int kc = 0; kc < nk; ++kc) {
+      if (kc + 1 < nk) fetch(kc + 1);
+      compute(kc & 1);
+      if (kc + 1 < nk) store((kc + 1) & 1);
+      if constexpr (OP == OP_U) cp_async_wait<0>();
+      __syncthreads();
+    }
   }
 
   // ---- epilogues ----
@@ -298,7 +373,7 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
 __global__ void __launch_bounds__(256, 2) spectral_kernel(SpecArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* As = reinterpret_cast<double*>(smem_raw);
-  cplx* Bs = reinterpret_cast<cplx*>(As + 2 * SP_A_STAGE);
+  cplx* Bs = reinterpret_cast<cplx*>(As + SP_STAGES * SP_A_STAGE);
   const int4 it = a.items[blockIdx.x];
   switch (it.x) {
     case OP_U: spectral_tile<OP_U>(a, it, As, Bs); break;

@@ -118,9 +118,11 @@ class FDMSolver:
         self.M_t = np.asarray(M_t, float)
         self.B_t = np.asarray(B_t, float)
         self.nt = self.M_t.shape[0]
-        # (Running the temporal eigendecomposition beside the spatial setup was measured and
-        # dropped: the spectral build pins BLAS to one thread per worker process-wide, which
-        # starves zgeev -- eig 1.7 -> 3.5 s, setup 3.7 -> 4.3 s on the 16-core host.)
+        # (Running the temporal eigendecomposition on a worker thread beside the spatial setup was
+        # measured twice and dropped: round 1, eig 1.7 -> 3.5 s because the spectral build pinned
+        # BLAS to one thread process-wide; round 2, with that build serial and unpinned, zgeev
+        # still slowed from 1.57 to 4.85 s (C4) and 10.6 s (C5) beside the symbolic analysis on
+        # the 16-core host.)
         box = {}
         t = time.perf_counter()
         tf = factors if factors is not None else temporal_factors(self.M_t, self.B_t)

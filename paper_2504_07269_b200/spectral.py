@@ -179,9 +179,15 @@ def build(fronts: np.ndarray, front_rows, perm: np.ndarray, M_x: sp.spmatrix, A_
         step = max(1, min(64, (len(cs) + 7) // 8))
         chunks += [cs[i:i + step] for i in range(0, len(cs), step)]
     nth = threads or len(os.sched_getaffinity(0))
-    from threadpoolctl import threadpool_limits
-    with threadpool_limits(limits=1), ThreadPoolExecutor(max(1, nth)) as ex:
-        list(ex.map(work, chunks))
+    if int((mc ** 3).sum()) < 2 * 10 ** 9 or nth <= 1:
+        # a few classes of congruent subtrees (C4: 20 x 225^3): serial, no BLAS pinning -- a
+        # process-wide thread limit here would starve a concurrent temporal eigendecomposition
+        for cs in chunks:
+            work(cs)
+    else:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=1), ThreadPoolExecutor(max(1, nth)) as ex:
+            list(ex.map(work, chunks))
     offs = coffs[cls] if nr else np.zeros((0, 4), dtype=np.int64)      # every subtree points at its class data
     data = SpectralData(roots, first, np.ascontiguousarray(offs).ravel().copy(), V, theta, RQ, C01, m, g)
     data.classes, data.cls = nc, cls
