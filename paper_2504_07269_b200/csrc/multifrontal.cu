@@ -607,17 +607,34 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int uni
       // holds t_j; once x_c is final it is broadcast and every lane j < c subtracts
       // L[c][j] x_c -- one broadcast per step instead of a 5-level warp reduction.
       // The right-hand sides are spread over the warps.
-      for (int r = warp; r < nrhs; r += NT / 32) {
-        cplx xl = lane < w ? xs[(kb + lane) * nrhs + r] : zero;
+      // two right-hand sides per warp and pass (independent chains interleave)
+      for (int r0 = 2 * warp; r0 < nrhs; r0 += 2 * (NT / 32)) {
+        const bool two = r0 + 1 < nrhs;
+        cplx x0 = lane < w ? xs[(kb + lane) * nrhs + r0] : zero;
+        cplx x1 = (lane < w && two) ? xs[(kb + lane) * nrhs + r0 + 1] : zero;
         for (int c = w - 1; c >= 0; --c) {
-          if (lane == c) xl = cmul(xl, l11[c * LDD + c]);
-          const cplx xc = cmk(__shfl_sync(0xffffffffu, xl.re, c), __shfl_sync(0xffffffffu, xl.im, c));
-          if (lane < c) xl = cfms(xl, l11[lane * LDD + c], xc);
+          const cplx dc = l11[c * LDD + c], lc = lane < c ? l11[lane * LDD + c] : zero;
+          if (lane == c) {
+            x0 = cmul(x0, dc);
+            x1 = cmul(x1, dc);
+          }
+          const cplx c0 = cmk(__shfl_sync(0xffffffffu, x0.re, c), __shfl_sync(0xffffffffu, x0.im, c));
+          const cplx c1 = cmk(__shfl_sync(0xffffffffu, x1.re, c), __shfl_sync(0xffffffffu, x1.im, c));
+          if (lane < c) {
+            x0 = cfms(x0, lc, c0);
+            x1 = cfms(x1, lc, c1);
+          }
         }
         if (lane < w) {
-          stc(Zk + F.pbeg + kb + lane + (int64_t)r * nx, xl);
-          stc(a.W + bv_off(a.lay, r, shift, a.perm[F.pbeg + kb + lane]), xl);
-          xs[(kb + lane) * nrhs + r] = xl;
+          const int prow = a.perm[F.pbeg + kb + lane];
+          stc(Zk + F.pbeg + kb + lane + (int64_t)r0 * nx, x0);
+          stc(a.W + bv_off(a.lay, r0, shift, prow), x0);
+          xs[(kb + lane) * nrhs + r0] = x0;
+          if (two) {
+            stc(Zk + F.pbeg + kb + lane + (int64_t)(r0 + 1) * nx, x1);
+            stc(a.W + bv_off(a.lay, r0 + 1, shift, prow), x1);
+            xs[(kb + lane) * nrhs + r0 + 1] = x1;
+          }
         }
       }
     }
@@ -781,17 +798,33 @@ __global__ void __launch_bounds__(32 * NW) backward_mrhs_kernel(LevelArgs a, int
     }
     __syncthreads();
     // x_j = (t_j - sum_{c>j} L[c][j] x_c) * dinv_j in column (axpy) form, one warp per RHS
-    for (int r = warp; r < nrhs; r += NW) {
-      cplx xl = lane < w ? xs[(kb + lane) * NRP + r] : zero;
+    for (int r0 = 2 * warp; r0 < nrhs; r0 += 2 * NW) {   // two right-hand sides per warp and pass
+      const bool two = r0 + 1 < nrhs;
+      cplx x0 = lane < w ? xs[(kb + lane) * NRP + r0] : zero;
+      cplx x1 = (lane < w && two) ? xs[(kb + lane) * NRP + r0 + 1] : zero;
       for (int c = w - 1; c >= 0; --c) {
-        if (lane == c) xl = cmul(xl, l11[c * LDD + c]);
-        const cplx xc = cmk(__shfl_sync(0xffffffffu, xl.re, c), __shfl_sync(0xffffffffu, xl.im, c));
-        if (lane < c) xl = cfms(xl, l11[lane * LDD + c], xc);
+        const cplx dc = l11[c * LDD + c], lc = lane < c ? l11[lane * LDD + c] : zero;
+        if (lane == c) {
+          x0 = cmul(x0, dc);
+          x1 = cmul(x1, dc);
+        }
+        const cplx c0 = cmk(__shfl_sync(0xffffffffu, x0.re, c), __shfl_sync(0xffffffffu, x0.im, c));
+        const cplx c1 = cmk(__shfl_sync(0xffffffffu, x1.re, c), __shfl_sync(0xffffffffu, x1.im, c));
+        if (lane < c) {
+          x0 = cfms(x0, lc, c0);
+          x1 = cfms(x1, lc, c1);
+        }
       }
       if (lane < w) {
-        stc(Zk + F.pbeg + kb + lane + (int64_t)r * nx, xl);
-        stc(a.W + bv_off(a.lay, r, shift, a.perm[F.pbeg + kb + lane]), xl);
-        xs[(kb + lane) * NRP + r] = xl;
+        const int prow = a.perm[F.pbeg + kb + lane];
+        stc(Zk + F.pbeg + kb + lane + (int64_t)r0 * nx, x0);
+        stc(a.W + bv_off(a.lay, r0, shift, prow), x0);
+        xs[(kb + lane) * NRP + r0] = x0;
+        if (two) {
+          stc(Zk + F.pbeg + kb + lane + (int64_t)(r0 + 1) * nx, x1);
+          stc(a.W + bv_off(a.lay, r0 + 1, shift, prow), x1);
+          xs[(kb + lane) * NRP + r0 + 1] = x1;
+        }
       }
     }
     __syncthreads();
@@ -1319,7 +1352,7 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
           if (nrhs == 1)
             diag_kernel<true><<<ninst, 32, 0, st>>>(a, kb);
           else
-            diag_kernel<false><<<ninst, 32 * std::min(8, nrhs), 0, st>>>(a, kb);
+            diag_kernel<false><<<ninst, 32 * std::min(8, (nrhs + DIAG_RPW - 1) / DIAG_RPW), 0, st>>>(a, kb);
           STFEM_LAUNCH_CHECK("diag_kernel");
           fam(FAM_DIAG);
           const dim3 tg(ninst, (unsigned)std::max(1, (nmax - kb + TR_ROWS - 1) / TR_ROWS));

@@ -158,6 +158,7 @@ __global__ void __launch_bounds__(NT, 4) asm_front_kernel(LevelArgs a) {
 // packed lower triangle of the w x w block (column-major): element (row r, column c), r >= c
 __device__ __forceinline__ int lp(int c, int r) { return c * (2 * NB - c + 1) / 2 + r - c; }
 constexpr int LP_SIZE = NB * (NB + 1) / 2;
+constexpr int DIAG_RPW = 3;   // right-hand sides per warp in the panel forward solve
 
 // PACK (one-warp CTAs, nrhs == 1): packed triangle, 8.4 KB instead of 17 KB of shared memory
 // per instance -- those CTAs are shared-memory limited, so twice as many resident instances
@@ -242,15 +243,27 @@ __global__ void __launch_bounds__(256) diag_kernel(LevelArgs a, int kb) {
   __syncthreads();
   // y = C11^{-1} r in column (axpy) form: lane i holds r_i; once y_j is final it
   // is broadcast and every lane i > j subtracts C[i][j] y_j (RHS over warps)
-  for (int r = warp; r < nrhs; r += nwarp) {
-    cplx* z = Zk + F.pbeg + kb + (int64_t)r * nx;
-    cplx yl = lane < w ? ldc(z + lane) : zero;
+  // A warp carries RPW (3; single-RHS instances 1) right-hand sides through the 32-step chain at once (independent
+  // chains interleave in the pipeline): 9 RHS need 3 warps, not 8 -- and a multi-RHS CTA of 96
+  // instead of 256 threads leaves room for three times as many resident instances.
+  constexpr int RPW = PACK ? 1 : DIAG_RPW;
+  for (int r0 = warp * RPW; r0 < nrhs; r0 += nwarp * RPW) {
+    cplx* z = Zk + F.pbeg + kb + (int64_t)r0 * nx;
+    cplx yl[RPW];
+#pragma unroll
+    for (int q = 0; q < RPW; ++q) yl[q] = (lane < w && r0 + q < nrhs) ? ldc(z + (int64_t)q * nx + lane) : zero;
     for (int j = 0; j < w; ++j) {
-      if (lane == j) yl = cmul(yl, dinv_s[j]);
-      const cplx yj = cmk(__shfl_sync(0xffffffffu, yl.re, j), __shfl_sync(0xffffffffu, yl.im, j));
-      if (lane > j && lane < w) yl = cfms(yl, Ld[dix<PACK>(j, lane)], yj);
+      const cplx dj = dinv_s[j], lj = (lane > j && lane < w) ? Ld[dix<PACK>(j, lane)] : zero;
+#pragma unroll
+      for (int q = 0; q < RPW; ++q) {
+        if (lane == j) yl[q] = cmul(yl[q], dj);
+        const cplx yj = cmk(__shfl_sync(0xffffffffu, yl[q].re, j), __shfl_sync(0xffffffffu, yl[q].im, j));
+        if (lane > j) yl[q] = cfms(yl[q], lj, yj);
+      }
     }
-    if (lane < w) stc(z + lane, yl);
+#pragma unroll
+    for (int q = 0; q < RPW; ++q)
+      if (lane < w && r0 + q < nrhs) stc(z + (int64_t)q * nx + lane, yl[q]);
   }
 }
 

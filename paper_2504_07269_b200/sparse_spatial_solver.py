@@ -37,8 +37,9 @@ class SpatialPlan:
     when `ops.assemble()` produces new value tensors.
 
     options: stfem_plan_options fields to override (small_front_n, fused_min_p,
-    panel_group, asm_whole_n, syrk_block16, level_timing, workspace_fraction,
-    pivot_tol) -- the plan's only tuning interface (no environment variables)."""
+    panel_group, asm_whole_n, level_timing, tiles_per_cta, ws_stages, bwd_dmma_min_p,
+    workspace_fraction, pivot_tol) -- the plan's only tuning interface (no environment
+    variables)."""
 
     def __init__(self, ops: SpatialOperators, leaf_size: int = 16, spectral: int | None = None,
                  options: dict | None = None, spectral_threads: int | None = None):

@@ -7,6 +7,7 @@ mkdir -p gpurun_out
 rep=/tmp/ncu_$tag
 timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:$regex" --launch-skip "$skip" -c "$count" -o "$rep" -f "$@" > "gpurun_out/ncu_$tag.log" 2>&1
 ncu -i "$rep.ncu-rep" --page raw --csv > "gpurun_out/ncu_${tag}_raw.csv" 2>/dev/null
-ncu -i "$rep.ncu-rep" --page source --csv > "gpurun_out/ncu_${tag}_src.csv" 2>/dev/null
+# the source page (per-instruction stall samples) is large: gzip it, and only when asked for
+if [ -n "$NCU_SRC" ]; then ncu -i "$rep.ncu-rep" --page source --csv 2>/dev/null | gzip -9 > "gpurun_out/ncu_${tag}_src.csv.gz"; fi
 rm -f "$rep.ncu-rep"
-ls -la gpurun_out/ncu_${tag}_*.csv
+ls -la gpurun_out/ncu_${tag}_*
