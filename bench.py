@@ -277,9 +277,9 @@ FAMILY_NAMES = {"spectral": "spectral_kernel (K6 spectral subtrees, DMMA)",
                 "assembly": "asm_front_kernel (front assembly, HBM)",
                 "diag": "diag_kernel (diagonal blocks, FP64)",
                 "trsm": "trsm_kernel (panel TRSM, FP64)",
-                "panel_update": "panel_update32_kernel (trailing pivot columns, DMMA)",
-                "syrk": "Schur-update kernels (syrk32_kernel<gather> p >= 50 / syrk32_kernel / syrk_block16_kernel "
-                        "p <= 32: U = F22 - L21 L21^T, DMMA)",
+                "panel_update": "panel_ws_kernel (trailing pivot columns, warp-specialised TMA-fed update engine, DMMA)",
+                "syrk": "syrk_ws_kernel (Schur updates U = sum children - L21 L21^T on the warp-specialised TMA-fed "
+                        "update engine, DMMA)",
                 "backward": "backward kernels (HBM)",
                 "small_factor": "factor_small_kernel (shared-memory fronts)"}
 
@@ -309,6 +309,9 @@ def family_roofline(plan, nshift, nrhs, peak, workload, t_tr=None, flops_tr=None
             ent = json.load(f).get(f"{workload}:{top}")
         if ent:
             traffic = ent["dram_bytes_per_launch"]
+            if ent.get("shifts_per_launch"):
+                # captured at a smaller batch: a level launch's traffic is proportional to its shifts
+                traffic *= nshift / max(1, plan.last_num_batches()) / ent["shifts_per_launch"]
     if top == "transform":
         roof = {"bound": "tensor", "kernel": "time transforms (K3/K3p, DMMA)", "achieved": fam[top]["tflops"],
                 "peak": peak, "unit": "TFLOP/s", "frac": fam[top]["tflops"] / peak, "traffic": traffic,
