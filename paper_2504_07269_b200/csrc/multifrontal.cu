@@ -127,8 +127,17 @@ struct __align__(16) StreamTile {
 // memory by the producer during the tile's K loop and added in the epilogue.
 // A DMMA needs no second warp to hide its latency (measured: one warp per SM
 // sub-partition with a single dependent accumulator chain reaches 36.8 of
-// 37.1 TFLOP/s, tools/probe_dmma.py), so 2 CTAs x 4 consumer warps per SM are
-// enough to keep the pipe busy through the other CTA's epilogues.
+// 37.1 TFLOP/s, tools/probe_dmma.py), so 3 CTAs x 4 consumer warps per SM
+// keep the pipe busy through the other CTAs' epilogues.
+// The complex product is formed from three real DMMAs instead of four ("3M":
+// P1 = ar br, P2 = ai bi, P3 = (ar + ai)(br + bi); re = P1 - P2, im = P3 - P1 -
+// P2), accumulated separately over K and combined in the epilogue: 6 DMMAs and 4
+// DADDs per k step of a 16 x 16 block instead of 8 DMMAs.  The third
+// accumulator set needs 104 registers in the DMMA warps; setmaxnreg moves them
+// over from the copy warps (56), so the CTA keeps its 80-register launch
+// footprint and 3 CTAs per SM.  Measured on C4: Schur updates 271 -> 246 ms,
+// trailing updates 66 -> 58 ms per step (the DMMA-bound levels gain 12%, the
+// short-K levels 2-5%); without the re-balancing (2 CTAs per SM) only 8% / -10%.
 // ---------------------------------------------------------------------------
 // warps 0-3: DMMA consumers (2 x 2 of 16 x 16); warp 4: bulk copies of the A rows of every chunk;
 // warp 5: the B rows; warps 6, 7: the tile's starting values (GATHER: one warp per child -- a
@@ -183,11 +192,22 @@ constexpr int ws_smem_bytes() {
          (2 * WS_STAGES + 2) * 8;
 }
 
+// resident CTAs per SM (shared memory: 71 KB with a 2-stage ring); the 2-CTA variants run at 128 registers
+template <bool GATHER, int WS_STAGES>
+constexpr int ws_ctas_per_sm() { return WS_STAGES <= (GATHER ? 2 : 3) ? 3 : 2; }
+
 template <bool GATHER, int WS_STAGES>
 __device__ __forceinline__ void ws_tiles(const StreamTile* __restrict__ desc, int nt, cplx* As, cplx* Bs, cplx* Cs,
                                          uint64_t* full, uint64_t* empty, uint64_t* cfull, uint64_t* cempty,
                                          const int32_t* __restrict__ inv) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // register re-balancing between the two warpgroups (80 per thread at launch, 3 CTAs per SM):
+  // the copy warps give up registers, the DMMA warps take them for the third accumulator set
+  // (ptxas allocates each role's code against its own limit)
+  if constexpr (ws_ctas_per_sm<GATHER, WS_STAGES>() == 3) {
+    if (warp >= 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
+    else asm volatile("setmaxnreg.inc.sync.aligned.u32 104;\n");
+  }
   if (warp >= 6) {
     // ---------------- starting values: one staging tile per child (GATHER) or one in all ----------------
     const int s = warp - 6;   // GATHER: this warp's child
@@ -285,10 +305,14 @@ __device__ __forceinline__ void ws_tiles(const StreamTile* __restrict__ desc, in
     // the block skip their DMMAs (warp-uniform; their outputs are never stored)
     const bool wact = (i0 + wm * 16 + 15 >= c0 + wn * 16) && (i0 + wm * 16 < M) && (c0 + wn * 16 < N);
     double cre[2][4], cim[2][4];
+    double c3[2][4];
 #pragma unroll
     for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) cre[ni][e] = cim[ni][e] = 0.0;
+      for (int e = 0; e < 4; ++e) {
+        cre[ni][e] = cim[ni][e] = 0.0;
+        c3[ni][e] = 0.0;
+      }
     for (int c = 0; c < nk; ++c) {
       mbar_wait(&full[stage], phase);
       if (wact) {
@@ -300,14 +324,16 @@ __device__ __forceinline__ void ws_tiles(const StreamTile* __restrict__ desc, in
           for (int kk = 0; kk < 16; kk += 4) {
             const cplx a0 = as[kk * S32_LD], a1 = as[kk * S32_LD + 8];
             const cplx b0 = bs[kk * S32_LD], b1 = bs[kk * S32_LD + 8];
-            dmma_16x8x4(cre[0], -a0.re, -a1.re, b0.re);
-            dmma_16x8x4(cim[0], -a0.re, -a1.re, b0.im);
-            dmma_16x8x4(cre[1], -a0.re, -a1.re, b1.re);
-            dmma_16x8x4(cim[1], -a0.re, -a1.re, b1.im);
-            dmma_16x8x4(cre[0], a0.im, a1.im, b0.im);
-            dmma_16x8x4(cim[0], -a0.im, -a1.im, b0.re);
-            dmma_16x8x4(cre[1], a0.im, a1.im, b1.im);
-            dmma_16x8x4(cim[1], -a0.im, -a1.im, b1.re);
+            // 3M complex product: P1 += ar br, P2 += ai bi, P3 += (ar + ai)(br + bi)
+            {
+              const double s0 = a0.re + a0.im, s1 = a1.re + a1.im;
+              dmma_16x8x4(cre[0], a0.re, a1.re, b0.re);
+              dmma_16x8x4(cim[0], a0.im, a1.im, b0.im);
+              dmma_16x8x4(c3[0], s0, s1, b0.re + b0.im);
+              dmma_16x8x4(cre[1], a0.re, a1.re, b1.re);
+              dmma_16x8x4(cim[1], a0.im, a1.im, b1.im);
+              dmma_16x8x4(c3[1], s0, s1, b1.re + b1.im);
+            }
           }
         } else {
           // K tail: columns >= kv of the stage were not copied (stale data): masked out
@@ -316,14 +342,16 @@ __device__ __forceinline__ void ws_tiles(const StreamTile* __restrict__ desc, in
             const cplx z = cmk(0.0, 0.0);
             const cplx a0 = ok ? as[kk * S32_LD] : z, a1 = ok ? as[kk * S32_LD + 8] : z;
             const cplx b0 = ok ? bs[kk * S32_LD] : z, b1 = ok ? bs[kk * S32_LD + 8] : z;
-            dmma_16x8x4(cre[0], -a0.re, -a1.re, b0.re);
-            dmma_16x8x4(cim[0], -a0.re, -a1.re, b0.im);
-            dmma_16x8x4(cre[1], -a0.re, -a1.re, b1.re);
-            dmma_16x8x4(cim[1], -a0.re, -a1.re, b1.im);
-            dmma_16x8x4(cre[0], a0.im, a1.im, b0.im);
-            dmma_16x8x4(cim[0], -a0.im, -a1.im, b0.re);
-            dmma_16x8x4(cre[1], a0.im, a1.im, b1.im);
-            dmma_16x8x4(cim[1], -a0.im, -a1.im, b1.re);
+            // 3M complex product: P1 += ar br, P2 += ai bi, P3 += (ar + ai)(br + bi)
+            {
+              const double s0 = a0.re + a0.im, s1 = a1.re + a1.im;
+              dmma_16x8x4(cre[0], a0.re, a1.re, b0.re);
+              dmma_16x8x4(cim[0], a0.im, a1.im, b0.im);
+              dmma_16x8x4(c3[0], s0, s1, b0.re + b0.im);
+              dmma_16x8x4(cre[1], a0.re, a1.re, b1.re);
+              dmma_16x8x4(cim[1], a0.im, a1.im, b1.im);
+              dmma_16x8x4(c3[1], s0, s1, b1.re + b1.im);
+            }
           }
         }
       }
@@ -352,7 +380,8 @@ __device__ __forceinline__ void ws_tiles(const StreamTile* __restrict__ desc, in
             cplx o = cmk(0.0, 0.0);
             if (one) o = cadd(o, Cs[cc * S32_LD + r]);              // same sum order as asm_front_kernel
             if (two) o = cadd(o, Cs[ST_CS + cc * S32_LD + r]);
-            stc(C + row + (int64_t)col * ldC, cmk(o.re + cre[ni][2 * h + v], o.im + cim[ni][2 * h + v]));
+            const double p1 = cre[ni][2 * h + v], p2 = cim[ni][2 * h + v], p3 = c3[ni][2 * h + v];
+            stc(C + row + (int64_t)col * ldC, cmk(o.re - (p1 - p2), o.im - (p3 - p1 - p2)));
           }
         }
     __syncwarp();
@@ -374,7 +403,7 @@ __device__ __forceinline__ void ws_init_barriers(uint64_t* full, uint64_t* empty
 // Schur update of a level through the warp-specialised engine: tile q of the launch is
 // (shift q / n32, tile q % n32 of the level's tile list); CTA x takes tiles [x T, (x + 1) T).
 template <bool GATHER, int WS_STAGES>
-__global__ void __launch_bounds__(WS_THREADS, WS_STAGES <= (GATHER ? 2 : 3) ? 3 : 2)
+__global__ void __launch_bounds__(WS_THREADS, ws_ctas_per_sm<GATHER, WS_STAGES>())
     syrk_ws_kernel(LevelArgs a, const int4* __restrict__ tiles, int n32, long long total, int T) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* As = reinterpret_cast<cplx*>(smem_raw);
@@ -432,7 +461,7 @@ __host__ __device__ inline int panel_update_tiles32(int n, int p, int cb, int na
 }
 
 template <int WS_STAGES>
-__global__ void __launch_bounds__(WS_THREADS, WS_STAGES <= 3 ? 3 : 2)
+__global__ void __launch_bounds__(WS_THREADS, ws_ctas_per_sm<false, WS_STAGES>())
     panel_ws_kernel(LevelArgs a, int cb, int k0, int K, int narrow, int tiles_max, long long total, int T) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* As = reinterpret_cast<cplx*>(smem_raw);
