@@ -216,6 +216,21 @@ int stfem_plan_last_batches(const stfem_plan* plan, int32_t* batches);
 int stfem_plan_last_launches(const stfem_plan* plan, int64_t* launches);
 
 /* ---------------------------------------------------------------------------
+ * GPU uniform refinement of a conforming triangulation (spatial_mesh.refine_uniform,
+ * /root/reference/pkg/src/stfem/spatial_mesh.py:121-156, with the boundary flags and
+ * interior-DoF numbering of _finish :51-70): midpoints appended in first-encounter
+ * order of the edges, four children per triangle, the P2 node table
+ * (v0, v1, v2, m01, m12, m20) per parent.  All arrays are device memory;
+ * outputs sized for the worst case nv + 3 ne vertices: verts_out double[2 (nv + 3 ne)],
+ * elems_out int64[12 ne], p2_out int64[6 ne], boundary_out uint8[nv + 3 ne],
+ * interior_dof_out int64[nv + 3 ne].  *nv_out / *ndof_out (host) receive the
+ * refined vertex and interior-DoF counts.  Waits for the stream.
+ * ------------------------------------------------------------------------- */
+int stfem_mesh_refine2d(int32_t nv, const double* verts, int32_t ne, const int64_t* elems,
+                        double* verts_out, int64_t* elems_out, int64_t* p2_out, uint8_t* boundary_out,
+                        int64_t* interior_dof_out, int32_t* nv_out, int32_t* ndof_out, void* stream);
+
+/* ---------------------------------------------------------------------------
  * K6  spectral subtree elimination (optional; replaces the bottom of the
  * elimination tree for every shift at once, csrc/spectral.cuh).  Call once
  * after assembly with host data computed from M_x / A_x (paper_2504_07269_b200

@@ -110,6 +110,7 @@ def _declare(lib):
         "stfem_plan_set_options": (C.c_int, [P, C.POINTER(plan_options)]),
         "stfem_asm_create": (C.c_int, [I32, I32, P, I32, P, P, C.POINTER(P)]),
         "stfem_asm_destroy": (C.c_int, [P]),
+        "stfem_mesh_refine2d": (C.c_int, [I32, P, I32, P, P, P, P, P, P, C.POINTER(I32), C.POINTER(I32), P]),
         "stfem_asm_pattern": (C.c_int, [P, C.POINTER(I32), C.POINTER(I64), P, P]),
         "stfem_asm_spatial": (C.c_int, [P, P, P, P]),
         "stfem_asm_rhs": (C.c_int, [P, I32, P, I32, P, I64, P]),
