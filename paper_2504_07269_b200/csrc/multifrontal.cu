@@ -552,6 +552,43 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int uni
   // sides in register chunks of RB (the column is re-read from L1 per chunk) so many-RHS
   // solves keep the register count -- and the occupancy -- of the few-RHS ones
   if (n > p) {
+    if (NR > 1 && n - p <= 128) {
+      // multi-RHS, short columns (the single-panel fronts of the deep levels): the lane's (at most
+      // four) column entries are loaded once, together, and reused for every chunk of right-hand
+      // sides -- one exposed load latency per column instead of one per row block and chunk
+      for (int j = warp; j < p; j += NT / 32) {
+        const cplx* col = P + (int64_t)j * n;
+        cplx lv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = p + lane + 32 * q;
+          lv[q] = i < n ? ldc(col + i) : zero;
+        }
+        for (int r0 = 0; r0 < nrhs; r0 += RB) {
+          cplx acc[RB];
+#pragma unroll
+          for (int r = 0; r < RB; ++r) acc[r] = zero;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int i = min(p + lane + 32 * q, n - 1);   // lv is zero past the column
+#pragma unroll
+            for (int r = 0; r < RB; ++r)
+              if (r0 + r < nrhs) acc[r] = cfma(lv[q], xs[i * nrhs + r0 + r], acc[r]);
+          }
+#pragma unroll
+          for (int r = 0; r < RB; ++r) {
+            if (r0 + r >= nrhs) break;
+            double re = acc[r].re, im = acc[r].im;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              re += __shfl_xor_sync(0xffffffffu, re, o);
+              im += __shfl_xor_sync(0xffffffffu, im, o);
+            }
+            if (lane == 0) xs[j * nrhs + r0 + r] = cmk(xs[j * nrhs + r0 + r].re - re, xs[j * nrhs + r0 + r].im - im);
+          }
+        }
+      }
+    } else {
     for (int j = warp; j < p; j += NT / 32) {
       const cplx* col = P + (int64_t)j * n;
       for (int r0 = 0; r0 < nrhs; r0 += RB) {
@@ -576,6 +613,7 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int uni
           if (lane == 0) xs[j * nrhs + r0 + r] = cmk(xs[j * nrhs + r0 + r].re - re, xs[j * nrhs + r0 + r].im - im);
         }
       }
+    }
     }
     __syncthreads();
   }
