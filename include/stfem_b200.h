@@ -173,6 +173,11 @@ int stfem_plan_set_shift_base(stfem_plan* plan, int32_t base);
  * (and any call that needs more than is reserved) allocates, which
  * synchronises the device once. */
 int stfem_plan_reserve(stfem_plan* plan, int32_t nshift, int32_t nrhs);
+/* Concurrency: a plan owns ONE numeric workspace (factor storage, update pools, the latched
+ * error flag).  Calls on the same plan must be issued from one host thread at a time and are
+ * ordered on the device only through the stream they are given: enqueue them on one stream
+ * (or order the streams yourself).  Independent concurrent solves need one plan each; the
+ * symbolic analysis is cheap to repeat (C4: 0.2 s). */
 /* Tuning knobs of one plan (no environment variables).  get -> modify -> set;
  * set rebuilds the device tables on the next call. */
 typedef struct {

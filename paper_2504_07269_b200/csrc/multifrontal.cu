@@ -1116,7 +1116,7 @@ int upload(Plan& P) {
       if ((rc = up(&P.d_C01, P.h_C01))) return rc;
       if ((rc = up(&P.d_spec_items, items))) return rc;
       int mmax = 0;
-      for (const auto& S : P.subs) mmax = std::max(mmax, S.m);
+      for (const auto& S : P.subs) mmax = std::max(mmax, std::max(S.m, S.g));
       P.spec_smem = spectral_smem_bytes(mmax);
       if (P.spec_smem > 227 * 1024)
         return fail(STFEM_ERR_DIM, "spectral subtrees: interior too large for the shared-memory staging");

@@ -42,7 +42,7 @@ constexpr int SP_B_STAGE = SP_BK * SP_LDB;   // complex
 constexpr int SP_STAGES = 3;   // cp.async ring of the plain-copy ops (F1, B1); U, F2 and B2 use two
 constexpr int SP_SMEM = SP_STAGES * (SP_A_STAGE * 8 + SP_B_STAGE * 16);
 // + OP_U staging: the tile's 16 R rows over the subtree's m
-__host__ __device__ constexpr int spectral_smem_bytes(int mmax) { return SP_SMEM + 16 * (mmax | 1) * 8; }
+__host__ __device__ constexpr int spectral_smem_bytes(int mmax) { return SP_SMEM + 4 * ((mmax + 3) & ~3); }   // + the staged index table
 enum { OP_U = 0, OP_F1 = 1, OP_F2 = 2, OP_B1 = 3, OP_B2 = 4 };
 
 __device__ __forceinline__ cplx spec_w(double th, cplx l) { return crecip_fast(cmk(th + l.re, l.im)); }
@@ -107,25 +107,15 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
   const int gq = lane >> 2, tq = lane & 3, wm = warp & 1, wn = warp >> 1;
   const cplx zero = cmk(0.0, 0.0);
 
-  // OP_U operands are generated from shared memory: the 16 R rows of the
-  // tile's (i, j) block over all k, theta, and the tile's 64 shifts
-  double* Rs = reinterpret_cast<double*>(Bs + SP_STAGES * SP_B_STAGE);   // [16][ms], ms = m | 1 (odd: no bank conflicts)
-  const int ms = m | 1;
+  // OP_U operands R_ik R_jk are formed from the class's R (column-major, L2-resident: one copy
+  // per class of congruent subtrees) -- two loads per A element; nothing of size m is staged, so
+  // the subtree size does not limit the CTAs per SM
   const cplx* __restrict__ wsub = a.wbuf + (int64_t)S.tofs * a.wstride;   // w[k * wstride + s]
-  if constexpr (OP == OP_U) {
-    // rows fastest: each k reads two runs of 8 consecutive doubles of column-major R
-    for (int q = tid; q < 16 * m; q += 256) {
-      const int k = q >> 4, rr = q & 15;
-      const int row = rr < 8 ? it.z * 8 + rr : it.w * 8 + rr - 8;
-      Rs[rr * ms + k] = row < g ? Rm[row + (int64_t)k * g] : 0.0;
-    }
-    __syncthreads();
-  }
   // OP_F1 / OP_B1 gather their B operand through an index table (the permutation of the subtree's
   // interior DoFs / the root's boundary rows).  Staged once per tile: the per-chunk fetch is then
   // one global load deep instead of two dependent ones (ncu: the index loads were 23% of all
   // stall samples of the F1 launch, long scoreboard)
-  int* idx_s = reinterpret_cast<int*>(Rs);
+  int* idx_s = reinterpret_cast<int*>(Bs + SP_STAGES * SP_B_STAGE);
   if constexpr (OP == OP_F1 || OP == OP_B1) {
     const int cnt = OP == OP_F1 ? m : g;
     for (int q = tid; q < cnt; q += 256) idx_s[q] = OP == OP_F1 ? a.perm[S.first + q] : bidx[q];
@@ -136,7 +126,8 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
   auto a_val = [&](int r, int k) -> double {
     if (k >= K) return 0.0;
     if (OP == OP_U) {
-      return Rs[(r >> 3) * ms + k] * Rs[(8 + (r & 7)) * ms + k];
+      const int i = it.z * 8 + (r >> 3), j = it.w * 8 + (r & 7);
+      return (i < g && j < g) ? Rm[i + (int64_t)k * g] * Rm[j + (int64_t)k * g] : 0.0;
     } else if (OP == OP_F1) {
       const int ko = it.z * SP_BM + r;
       return ko < m ? V[k + (int64_t)ko * m] : 0.0;

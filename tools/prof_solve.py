@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--level-timing", action="store_true")
     ap.add_argument("--full-solve", action="store_true")
     ap.add_argument("--opt", action="append", default=[], help="plan option name=value (repeatable)")
+    ap.add_argument("--spectral", type=int, default=None, help="max interior DoFs of the spectral subtrees")
     a = ap.parse_args()
     opts = {}
     for kv in a.opt:
@@ -37,14 +38,14 @@ def main():
         opts[k] = float(v) if "." in v or "e" in v else int(v)
     prob = Problem(a.workload, device="cuda")
     if a.full_solve:
-        fdm = ks.FDMSolver(prob.ops, prob.M_t, prob.B_t, plan=SpatialPlan(prob.ops, a.leaf, options=opts))
+        fdm = ks.FDMSolver(prob.ops, prob.M_t, prob.B_t, plan=SpatialPlan(prob.ops, a.leaf, spectral=a.spectral, options=opts))
         for _ in range(a.reps):
             psi = fdm.solve(prob.F)
         torch.cuda.synchronize()
         print("ok full solve, residual", ks.relative_residual(prob.ops, prob.M_t, prob.B_t, psi, prob.F))
         return
     tf = temporal_factors(prob.M_t, prob.B_t)
-    plan = SpatialPlan(prob.ops, a.leaf, options=opts)
+    plan = SpatialPlan(prob.ops, a.leaf, spectral=a.spectral, options=opts)
     ns = prob.nt if a.shifts <= 0 else min(a.shifts, prob.nt)
     # the hardest shifts first (smallest |Im lam|), so a short run still sees them
     import numpy as np
