@@ -279,7 +279,8 @@ FAMILY_NAMES = {"spectral": "spectral_kernel (K6 spectral subtrees, DMMA)",
                 "trsm": "trsm_kernel (panel TRSM, FP64)",
                 "panel_update": "panel_ws_kernel (trailing pivot columns, warp-specialised TMA-fed update engine, DMMA)",
                 "syrk": "syrk_ws_kernel (Schur updates U = sum children - L21 L21^T on the warp-specialised TMA-fed "
-                        "update engine, DMMA)",
+                        "update engine; single-panel levels: syrk_front_kernel, L21 resident in shared memory; DMMA, "
+                        "3M complex product)",
                 "backward": "backward kernels (HBM)",
                 "small_factor": "factor_small_kernel (shared-memory fronts)"}
 

@@ -192,6 +192,8 @@ typedef struct {
   int32_t level_timing;      /* 1: print per-launch CUDA-event times to stderr (diagnostics) */
   int32_t tiles_per_cta;     /* tiles a CTA of the update engine walks (1..16).  Default 16 */
   int32_t ws_stages;         /* ring depth of the update engine (2, 3 or 4).  Default 2 */
+  int32_t front_syrk_max_p;  /* Schur updates of levels with at most this many pivots (one panel) run one CTA per
+                                instance with L21 resident in shared memory (syrk_front_kernel).  Default 32; 0: never */
   int32_t bwd_dmma_min_p;    /* multi-RHS backward substitution of levels with more than this many pivots runs as
                                 GEMMs over the right-hand sides on the FP64 tensor pipe (default 32: every
                                 multi-panel level; INT32_MAX: column dot products everywhere) */

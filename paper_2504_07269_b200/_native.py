@@ -52,7 +52,7 @@ class plan_options(C.Structure):
     """stfem_plan_options (include/stfem_b200.h): tuning knobs of one plan."""
     _fields_ = [("small_front_n", C.c_int32), ("fused_min_p", C.c_int32), ("panel_group", C.c_int32),
                 ("asm_whole_n", C.c_int32), ("level_timing", C.c_int32), ("tiles_per_cta", C.c_int32),
-                ("ws_stages", C.c_int32), ("bwd_dmma_min_p", C.c_int32),
+                ("ws_stages", C.c_int32), ("front_syrk_max_p", C.c_int32), ("bwd_dmma_min_p", C.c_int32),
                 ("workspace_fraction", C.c_double), ("pivot_tol", C.c_double)]
 
 

@@ -107,7 +107,7 @@ struct __align__(16) StreamTile {
   int lda, ldC, K, M, N, i0, c0;
   int bc[2];            // GATHER: children's boundary orders
   int inv_off[2];       // GATHER: a.inv offset of boundary row 0 for child s (-1: no such child)
-  int pad;
+  int pad;              // rows of C that may be stored (>= M: the update block's leading dimension; panel updates: M)
 };
 
 // ---------------------------------------------------------------------------
@@ -362,28 +362,40 @@ __device__ __forceinline__ void ws_tiles(const StreamTile* __restrict__ desc, in
         phase ^= 1;
       }
     }
-    // epilogue: C = Cinit + acc
+    // epilogue: C = Cinit + acc.  The DMMA accumulator layout would store 128-byte pieces at
+    // 16-byte alignment (8 rows x 4 columns per instruction): measured 3.7 TB/s against 6 TB/s for
+    // aligned 256-byte pieces (tools/probe_store.py).  So the warp writes its finished 16 x 16
+    // block over its own corner of the first staging tile and stores it from there, two columns
+    // of 16 rows per instruction.  Diagonal blocks are stored whole (their upper entries are the
+    // mirror values and are never read); rows up to the block's leading dimension are written,
+    // so that every touched line of an update block is written completely.
     mbar_wait(cfull, cphase);
     cphase ^= 1;
     cplx* C = D.C;
-    const int ldC = D.ldC;
+    const int ldC = D.ldC, rowlim = D.pad;
     const bool two = GATHER && D.inv_off[1] >= 0, one = !GATHER || D.inv_off[0] >= 0;
+    if (wact) {
 #pragma unroll
-    for (int ni = 0; ni < 2; ++ni)
+      for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          const int r = wm * 16 + g + 8 * h, cc = wn * 16 + ni * 8 + 2 * t + v;
-          const int row = i0 + r, col = c0 + cc;
-          if (row < M && col < N && row >= col) {
+          for (int v = 0; v < 2; ++v) {
+            const int r = wm * 16 + g + 8 * h, cc = wn * 16 + ni * 8 + 2 * t + v;
             cplx o = cmk(0.0, 0.0);
             if (one) o = cadd(o, Cs[cc * S32_LD + r]);              // same sum order as asm_front_kernel
             if (two) o = cadd(o, Cs[ST_CS + cc * S32_LD + r]);
             const double p1 = cre[ni][2 * h + v], p2 = cim[ni][2 * h + v], p3 = c3[ni][2 * h + v];
-            stc(C + row + (int64_t)col * ldC, cmk(o.re - (p1 - p2), o.im - (p3 - p1 - p2)));
+            Cs[cc * S32_LD + r] = cmk(o.re - (p1 - p2), o.im - (p3 - p1 - p2));
           }
-        }
+      __syncwarp();
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int r = wm * 16 + (lane & 15), cc = wn * 16 + 2 * it + (lane >> 4);
+        const int row = i0 + r, col = c0 + cc;
+        if (row < rowlim && col < N) stc(C + row + (int64_t)col * ldC, Cs[cc * S32_LD + r]);
+      }
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(cempty);
   }
@@ -425,12 +437,12 @@ __global__ void __launch_bounds__(WS_THREADS, ws_ctas_per_sm<GATHER, WS_STAGES>(
     D.A = a.factor + (int64_t)k * a.fstride + F.fofs + p;   // L21: row r, column kk at A[r + kk n]
     D.C = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
     D.lda = n;
-    D.ldC = b;
+    D.ldC = ldu(b);
     D.K = p;
     D.M = D.N = b;
     D.i0 = tl.y * 32;
     D.c0 = tl.z * 32;
-    D.pad = 0;
+    D.pad = ldu(b);   // rows stored: up to the leading dimension
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       D.Uc[s] = nullptr;
@@ -438,7 +450,7 @@ __global__ void __launch_bounds__(WS_THREADS, ws_ctas_per_sm<GATHER, WS_STAGES>(
       D.inv_off[s] = -1;
       if (GATHER && s < F.nchild) {
         const FrontDev Cf = a.fronts[a.child_ids[F.child_beg + s]];
-        D.bc[s] = Cf.n - Cf.p;
+        D.bc[s] = ldu(Cf.n - Cf.p);   // the child's update-block leading dimension
         D.Uc[s] = a.uchild + (int64_t)k * a.uchild_stride + Cf.uofs;
         D.inv_off[s] = F.inv_beg + s * n + p;
       }
@@ -447,6 +459,144 @@ __global__ void __launch_bounds__(WS_THREADS, ws_ctas_per_sm<GATHER, WS_STAGES>(
   }
   __syncthreads();
   ws_tiles<GATHER, WS_STAGES>(desc, nt, As, Bs, Cs, full, empty, cfull, cempty, a.inv);
+}
+
+// ---------------------------------------------------------------------------
+// Schur update of the short-K levels (one pivot panel, K = p <= 32), one CTA per
+// (front, shift) instance with the whole L21 (b x K) resident in shared memory.
+// On these levels a 32 x 32 tile of the update engine above is one or two K chunks:
+// its ring and staging handshakes (~1800 clocks per tile) and the serial gather of the
+// starting values cost more than the DMMAs (C4 depths 7-9: DMMA pipe 31-50% active, DRAM
+// 30-39%).  Here L21 arrives once per instance by K bulk copies (one mbarrier wait), after
+// which every warp is on its own: it takes 16 x 16 blocks of the lower triangle from a shared
+// counter, loads the children's entries of its block straight into registers through
+// inverse maps staged in shared memory, runs the K loop from shared memory (3M product,
+// as in the engine -- the results are bit-identical to the engine's) and stores the block.
+// No per-tile protocol; the other warps of the SM cover a warp's load latency.
+// ---------------------------------------------------------------------------
+constexpr int SF_KMAX = 32;
+__host__ __device__ constexpr int sf_ld(int b) { return ((b + 15) & ~15) + 2; }   // row pitch: = 2 mod 8, covers whole blocks
+constexpr int SF_TS = 16 * 18;   // per-warp staging of a finished 16 x 16 block (pitch 18: = 2 mod 8)
+__host__ __device__ constexpr int sf_smem_bytes(int bmax, int pmax, int nwarp) {
+  return (pmax * sf_ld(bmax) + nwarp * SF_TS) * 16 + 2 * ((bmax + 15) & ~15) * 2 + 32;
+}
+
+template <int NTH>
+__global__ void __launch_bounds__(NTH, NTH >= 256 ? 2 : 4) syrk_front_kernel(LevelArgs a) {
+  extern __shared__ __align__(16) unsigned char sf_smem[];
+  const int tid = threadIdx.x, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int inst = blockIdx.x;
+  const int k = inst % a.nbatch;
+  const FrontDev F = a.fronts[a.list[inst / a.nbatch]];
+  const int n = F.n, K = F.p, b = n - K;
+  if (b <= 0) return;
+  const int LD = sf_ld(b), bp = (b + 15) & ~15;
+  cplx* Ls = reinterpret_cast<cplx*>(sf_smem);                           // Ls[kk * LD + row] = L21[row][kk]
+  cplx* Ts = Ls + (int64_t)K * LD + (tid >> 5) * SF_TS;                  // this warp's output staging
+  int16_t* maps = reinterpret_cast<int16_t*>(Ls + (int64_t)K * LD + (NTH / 32) * SF_TS);   // maps[s * bp + row]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(maps + 2 * bp + (((2 * bp) & 3) ? 4 - ((2 * bp) & 3) : 0));
+  int* next = reinterpret_cast<int*>(bar + 1);
+  const cplx* L21 = a.factor + (int64_t)k * a.fstride + F.fofs + K;      // row r, column kk at L21[r + kk n]
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    *next = 0;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)K * (uint32_t)b * 16u);
+    __syncwarp();
+    if (lane < K) bulk_g2s(Ls + lane * LD, L21 + (int64_t)lane * n, (uint32_t)b * 16u, bar);
+  }
+  const cplx* Uc[2] = {nullptr, nullptr};
+  int bc[2] = {0, 0};
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+    if (s < F.nchild) {
+      const FrontDev Cf = a.fronts[a.child_ids[F.child_beg + s]];
+      bc[s] = ldu(Cf.n - Cf.p);   // leading dimension
+      Uc[s] = a.uchild + (int64_t)k * a.uchild_stride + Cf.uofs;
+    }
+  for (int q = tid; q < 2 * bp; q += NTH) {
+    const int s = q / bp, r = q - s * bp;
+    maps[q] = (s < F.nchild && r < b) ? (int16_t)a.inv[F.inv_beg + s * n + K + r] : (int16_t)-1;
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  cplx* U = a.ucur + (int64_t)k * a.ucur_stride + F.uofs;
+  const int nblk = bp >> 4, nwork = nblk * (nblk + 1) / 2;
+  const cplx zero = cmk(0.0, 0.0);
+  for (;;) {
+    int wb = 0;
+    if (lane == 0) wb = atomicAdd(next, 1);
+    wb = __shfl_sync(0xffffffffu, wb, 0);
+    if (wb >= nwork) break;
+    int bi = (int)((sqrtf(8.0f * (float)wb + 1.0f) - 1.0f) * 0.5f);
+    while (bi * (bi + 1) / 2 > wb) --bi;
+    while ((bi + 1) * (bi + 2) / 2 <= wb) ++bi;
+    const int bj = wb - bi * (bi + 1) / 2;
+    const int rb = bi * 16, cb = bj * 16;
+    double p1[2][4] = {}, p2[2][4] = {}, p3[2][4] = {};
+    const cplx* as = Ls + t * LD + rb + g;
+    const cplx* bs = Ls + t * LD + cb + g;
+    for (int kk = 0; kk < K; kk += 4) {
+      const bool ok = kk + t < K;
+      const cplx a0 = ok ? as[kk * LD] : zero, a1 = ok ? as[kk * LD + 8] : zero;
+      const cplx b0 = ok ? bs[kk * LD] : zero, b1 = ok ? bs[kk * LD + 8] : zero;
+      const double s0 = a0.re + a0.im, s1 = a1.re + a1.im;
+      dmma_16x8x4(p1[0], a0.re, a1.re, b0.re);
+      dmma_16x8x4(p2[0], a0.im, a1.im, b0.im);
+      dmma_16x8x4(p3[0], s0, s1, b0.re + b0.im);
+      dmma_16x8x4(p1[1], a0.re, a1.re, b1.re);
+      dmma_16x8x4(p2[1], a0.im, a1.im, b1.im);
+      dmma_16x8x4(p3[1], s0, s1, b1.re + b1.im);
+    }
+    // the children's entries of the block (lower triangle only) through the staged inverse maps:
+    // one half block (8 columns) at a time, its loads issued together, then combined and stored
+    int kr0[2], kr1[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      kr0[h] = maps[rb + g + 8 * h];
+      kr1[h] = maps[bp + rb + g + 8 * h];
+    }
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) {
+      cplx v0[4], v1[4];
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int col = cb + ni * 8 + 2 * t + v;
+        const int kc0 = maps[col], kc1 = maps[bp + col];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const bool low = rb + g + 8 * h >= col;
+          const bool ok0 = low && kr0[h] >= 0 && kc0 >= 0, ok1 = low && kr1[h] >= 0 && kc1 >= 0;
+          v0[2 * h + v] = ok0 ? ldc(Uc[0] + (int64_t)kc0 * bc[0] + kr0[h]) : zero;
+          v1[2 * h + v] = ok1 ? ldc(Uc[1] + (int64_t)kc1 * bc[1] + kr1[h]) : zero;
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int e = 2 * h + v;
+          const cplx o = cadd(cadd(zero, v0[e]), v1[e]);   // same sum order as asm_front_kernel
+          Ts[(ni * 8 + 2 * t + v) * 18 + g + 8 * h] =
+              cmk(o.re - (p1[ni][e] - p2[ni][e]), o.im - (p3[ni][e] - p1[ni][e] - p2[ni][e]));
+        }
+    }
+    __syncwarp();
+    // whole lines: two columns of 16 rows per instruction, rows up to the leading dimension
+    // (diagonal blocks are stored whole: their upper entries are never read)
+    {
+      const int ldU = ldu(b);
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int r = lane & 15, cc = 2 * it + (lane >> 4);
+        if (rb + r < ldU && cb + cc < b) stc(U + rb + r + (int64_t)(cb + cc) * ldU, Ts[cc * 18 + r]);
+      }
+    }
+    __syncwarp();
+  }
 }
 
 // Trailing pivot-column updates, delayed over groups of panels (multifrontal_large.cuh), through
@@ -506,6 +656,7 @@ __global__ void __launch_bounds__(WS_THREADS, ws_ctas_per_sm<false, WS_STAGES>()
         D.lda = D.ldC = n;
         D.K = min(K, p - k0);
         D.M = n - cb;
+        D.pad = D.M;
         D.N = cols;
         D.i0 = ti * 32;
         D.c0 = tj * 32;
@@ -1451,7 +1602,22 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
             fam(FAM_PANEL);
           }
         }
-        if (n32 > 0) {
+        const int bmax = level_bmax(P, d);
+        if (n32 > 0 && a.asm_pivots_only && pmax <= P.opt.front_syrk_max_p && pmax <= SF_KMAX &&
+            sf_smem_bytes(bmax, pmax, bmax <= 112 ? 4 : 8) <= 100 * 1024) {
+          // one pivot panel: the whole L21 of an instance fits in shared memory
+          static DeviceOnce sf_once;
+          if (sf_once.first()) {
+            STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_front_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+            STFEM_CUDA_TRY(cudaFuncSetAttribute(syrk_front_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+          }
+          const int sm_b = sf_smem_bytes(bmax, pmax, bmax <= 112 ? 4 : 8);
+          if (bmax <= 112) syrk_front_kernel<128><<<ninst, 128, sm_b, st>>>(a);
+          else syrk_front_kernel<256><<<ninst, 256, sm_b, st>>>(a);
+          STFEM_LAUNCH_CHECK("syrk_front_kernel");
+          ++nlaunch;
+          fam(FAM_SYRK);
+        } else if (n32 > 0) {
           const long long total = (long long)n32 * nb;
           const unsigned gr = (unsigned)((total + T - 1) / T);
           const int4* tl = P.d_syrk32_tiles + P.syrk32_off[d];

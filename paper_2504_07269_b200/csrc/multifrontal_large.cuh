@@ -52,10 +52,11 @@ __global__ void __launch_bounds__(NT, 4) asm_front_kernel(LevelArgs a) {
   for (int q = tid; q < nc * n; q += NT) inv_s[q] = a.inv[F.inv_beg + q];
   const cplx* Ucs[2] = {nullptr, nullptr};
   const cplx* Rcs[2] = {nullptr, nullptr};
-  int bcs[2] = {0, 0};
+  int bcs[2] = {0, 0}, lcs[2] = {0, 0};   // children's boundary orders / update-block leading dimensions
   for (int s = 0; s < nc; ++s) {
     const FrontDev Cf = a.fronts[a.child_ids[F.child_beg + s]];
     bcs[s] = Cf.n - Cf.p;
+    lcs[s] = ldu(bcs[s]);
     Ucs[s] = a.uchild + (int64_t)k * a.uchild_stride + Cf.uofs;
     Rcs[s] = a.rchild + ((int64_t)k * a.rchild_stride + Cf.rofs) * nrhs;
   }
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(NT, 4) asm_front_kernel(LevelArgs a) {
       const int c2 = min(c0 + warp + u * NW, cend - 1);
 #pragma unroll
       for (int s = 0; s < 2; ++s) k2[s][u] = s < nc ? inv_s[s * n + c2] : -1;
-      dst[u] = (c2 < p) ? P + (int64_t)c2 * n : U + (int64_t)(c2 - p) * b - p;
+      dst[u] = (c2 < p) ? P + (int64_t)c2 * n : U + (int64_t)(c2 - p) * ldu(b) - p;
     }
     // two row blocks per iteration: 16 independent child loads in flight per thread
     for (int rb = c0 + warp + lane; rb < n; rb += 64) {
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(NT, 4) asm_front_kernel(LevelArgs a) {
 #pragma unroll
           for (int s = 0; s < 2; ++s)
             if (k1[s] >= 0 && k2[s][u] >= 0)
-              v[h][u] = cadd(v[h][u], ldc(Ucs[s] + (int64_t)k2[s][u] * bcs[s] + k1[s]));
+              v[h][u] = cadd(v[h][u], ldc(Ucs[s] + (int64_t)k2[s][u] * lcs[s] + k1[s]));
         }
       }
 #pragma unroll

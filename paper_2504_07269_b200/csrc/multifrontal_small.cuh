@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
 #pragma unroll
         for (int u = 0; u < CU; ++u) {
           const int k2 = k2b + u * nwarp;
-          v[u] = (k2 < bc && k1 >= k2) ? ldc(Uc + (int64_t)k2 * bc + k1) : zero;
+          v[u] = (k2 < bc && k1 >= k2) ? ldc(Uc + (int64_t)k2 * ldu(bc) + k1) : zero;
         }
 #pragma unroll
         for (int u = 0; u < CU; ++u) {
@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
     if (i >= p) {
       q = pk(i, p, n);
       for (int c = p; c <= i; ++c) {
-        stc(Ug + (i - p) + (int64_t)(c - p) * b, F[q]);
+        stc(Ug + (i - p) + (int64_t)(c - p) * ldu(b), F[q]);
         q += n - c - 1;
       }
 #pragma unroll

@@ -95,6 +95,7 @@ struct Plan {
     o.level_timing = 0;
     o.tiles_per_cta = 16;
     o.ws_stages = 2;
+    o.front_syrk_max_p = 32;
     o.bwd_dmma_min_p = 32;
     o.workspace_fraction = 0.70;
     o.pivot_tol = 1e-10;
@@ -137,6 +138,12 @@ struct Plan {
   void free_device();
   void free_workspace();
 };
+
+// Leading dimension of a front's b x b update block: b rounded up to 8 complex (128 bytes), so
+// every column starts on a cache line and the Schur-update epilogues can store whole lines (the
+// DMMA accumulator layout -- 128-byte pieces at 16-byte alignment -- writes at 3.7 TB/s, aligned
+// 256-byte pieces at 6 TB/s: tools/probe_store.py)
+__host__ __device__ constexpr int ldu(int b) { return (b + 7) & ~7; }
 
 // factor-block offsets (fofs) and factor_stride over the multifrontal fronts only
 void assign_factor_offsets(Plan& P, const std::vector<char>& skip);

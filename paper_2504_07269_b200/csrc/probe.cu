@@ -113,8 +113,70 @@ __global__ void __launch_bounds__(128) layout_probe_kernel(cplx* buf, long long 
   if (acc == 12345.678) sink[0] = acc;
 }
 
+// Store-pattern probe: one CTA per b x b column-major block (lower triangle), 8 warps.
+// mode 0: DMMA-epilogue pattern -- a warp stores 16 x 16 sub-blocks, each instruction 8 rows x
+// 4 columns (128 contiguous bytes per column); mode 1: the same bytes column by column, a warp
+// per column segment (contiguous runs of up to 512 B per instruction).
+__global__ void __launch_bounds__(256) store_probe_kernel(cplx* buf, int b, long long bstride, int mode) {
+  cplx* U = buf + (long long)blockIdx.x * bstride;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  const cplx v = cmk(1.0, 2.0);
+  if (mode == 0 || mode == 2) {
+    const int nblk = (b + 15) >> 4, nwork = nblk * (nblk + 1) / 2;
+    for (int wb = warp; wb < nwork; wb += 8) {
+      int bi = 0;
+      while ((bi + 1) * (bi + 2) / 2 <= wb) ++bi;
+      const int bj = wb - bi * (bi + 1) / 2, rb = bi * 16, cb = bj * 16;
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int row = rb + g + 8 * h, col = cb + ni * 8 + 2 * t + q;
+            // mode 2: packed lower triangle, column c starts at c (2 b - c - 1) / 2
+            if (row < b && col < b && row >= col)
+              stc(U + row + (mode == 2 ? (long long)col * (2 * b - col - 1) / 2 : (long long)col * b), v);
+          }
+    }
+  } else if (mode == 1) {
+    for (int col = warp; col < b; col += 8)
+      for (int row = col + lane; row < b; row += 32) stc(U + row + (long long)col * b, v);
+  } else if (mode == 3) {
+    // packed, column by column
+    for (int col = warp; col < b; col += 8)
+      for (int row = col + lane; row < b; row += 32) stc(U + row + (long long)col * (2 * b - col - 1) / 2, v);
+  } else if (mode == 4) {
+    // ld padded to a multiple of 8 (128-byte columns), lower part rounded down to an 8-row boundary
+    const int ld = (b + 7) & ~7;
+    for (int col = warp; col < b; col += 8)
+      for (int row = (col & ~7) + lane; row < ld; row += 32) stc(U + row + (long long)col * ld, v);
+  } else {
+    // mode 5: ld padded to 8; 16 x 16 blocks stored as 256-byte column pieces (lanes 0-15 one column,
+    // 16-31 the next): the transposed epilogue.  Diagonal blocks are written whole.
+    const int ld = (b + 7) & ~7;
+    const int nblk = (b + 15) >> 4, nwork = nblk * (nblk + 1) / 2;
+    for (int wb = warp; wb < nwork; wb += 8) {
+      int bi = 0;
+      while ((bi + 1) * (bi + 2) / 2 <= wb) ++bi;
+      const int bj = wb - bi * (bi + 1) / 2, rb = bi * 16, cb = bj * 16;
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int row = rb + (lane & 15), col = cb + 2 * it + (lane >> 4);
+        if (row < ld && col < b) stc(U + row + (long long)col * ld, v);
+      }
+    }
+  }
+}
+
 }  // namespace
 }  // namespace stfem
+
+extern "C" int stfem_probe_store(void* buf, int b, long long bstride, int nblocks, int mode, void* stream) {
+  stfem::store_probe_kernel<<<nblocks, 256, 0, (cudaStream_t)stream>>>((stfem::cplx*)buf, b, bstride, mode);
+  STFEM_LAUNCH_CHECK("store probe");
+  return STFEM_OK;
+}
 
 extern "C" int stfem_probe_layout(void* buf, long long kstride, long long fstride, int chunk, int nshift,
                                   int nfront, int write, double* sink, void* stream) {

@@ -337,7 +337,7 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
             const int64_t e = i + (int64_t)j * g;
             const cplx l = a.lam[cg];
             cplx* U = a.ucur + (int64_t)cg * a.ucur_stride + F.uofs;
-            stc(U + e, cmk(-(v.re + C0[e] + l.re * C1[e]), -(v.im + l.im * C1[e])));
+            stc(U + i + (int64_t)j * ldu(g), cmk(-(v.re + C0[e] + l.re * C1[e]), -(v.im + l.im * C1[e])));
           } else if (OP == OP_F1) {
             const int ko = it.z * SP_BM + row;
             if (ko >= m) continue;

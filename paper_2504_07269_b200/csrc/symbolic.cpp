@@ -360,7 +360,7 @@ int build_symbolic(Plan& P, int32_t n, const int64_t* rowptr, const int32_t* col
       int64_t b = F.n - F.p;
       F.uofs = u;
       F.rofs = r;
-      u += b * b;
+      u += (int64_t)ldu((int)b) * b;
       r += b;
     }
     P.upool_stride[d & 1] = std::max(P.upool_stride[d & 1], u);

@@ -78,6 +78,8 @@ MODES = {
     # U assembled by asm_front_kernel (no fusion), per-panel trailing updates, 32-column assembly CTAs
     "big_plain": dict(small_front_n=0, fused_min_p=1 << 30, panel_group=1, asm_whole_n=0),
     "big_pg4": dict(small_front_n=0, panel_group=4, tiles_per_cta=5),
+    # single-panel levels through the update engine instead of the L21-resident kernel
+    "big_no_front_syrk": dict(small_front_n=0, front_syrk_max_p=0),
     "big_fuse40": dict(small_front_n=0, fused_min_p=40, ws_stages=3, tiles_per_cta=1),
     "big_s4": dict(small_front_n=0, ws_stages=4, tiles_per_cta=7),
     "big_s4_plain": dict(small_front_n=0, fused_min_p=1 << 30, ws_stages=4),
