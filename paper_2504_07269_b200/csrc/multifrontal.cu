@@ -894,7 +894,7 @@ __host__ __device__ constexpr int bwd_mrhs_smem(int nmax, int nrhs) { return (nm
 
 // acc(16 columns x 8 NT8 rhs) = sum over k steps ks = ks0, ks0 + kstep, ... < KS of
 // L[row0 + 4 ks + t][j0 + g (+8)] * xs[row0 + 4 ks + t][rhs]; K = valid rows from row0
-template <int NT8>
+template <int NT8, int UN>
 __device__ __forceinline__ void bwd_gemm_tile(const cplx* __restrict__ P, int n, int j0, int jlim, int row0, int K,
                                               int ks0, int kstep, const cplx* xs, int NRP, int nrhs,
                                               double (&cr)[2][4], double (&ci)[2][4]) {
@@ -904,7 +904,6 @@ __device__ __forceinline__ void bwd_gemm_tile(const cplx* __restrict__ P, int n,
   const cplx* c1 = P + (int64_t)min(j0 + g + 8, jlim - 1) * n + row0 + t;
   const cplx* xb = xs + (int64_t)(row0 + t) * NRP + g;
   const int KS = (K + 3) >> 2;
-  constexpr int UN = 4;   // k steps in flight
   for (int ks = ks0; ks < KS; ks += UN * kstep) {
     cplx a0[UN], a1[UN];
 #pragma unroll
@@ -931,7 +930,11 @@ __device__ __forceinline__ void bwd_gemm_tile(const cplx* __restrict__ P, int n,
   }
 }
 
-template <int NW, int NT8>
+// NW warps per CTA, UN k steps of A fragments in flight per warp: (8, 4) for the ordinary levels;
+// (16, 8) for the launches of fronts above n = 256, whose staged x leaves room for one CTA per SM
+// only -- registers and thread slots are free there, and more loads in flight is what hides the
+// memory latency
+template <int NW, int NT8, int UN>
 __global__ void __launch_bounds__(32 * NW) backward_mrhs_kernel(LevelArgs a, int unit) {
   __shared__ cplx l11[NB * LDD];   // l11[c * LDD + i] = L[kb+i][kb+c], i > c; diagonal: 1/L[c][c] (or 1)
   extern __shared__ __align__(16) unsigned char bwd_smem[];
@@ -975,16 +978,18 @@ __global__ void __launch_bounds__(32 * NW) backward_mrhs_kernel(LevelArgs a, int
     if (MT >= NW) {
       for (int mt = warp; mt < MT; mt += NW) {
         double cr[2][4] = {}, ci[2][4] = {};
-        bwd_gemm_tile<NT8>(P, n, mt * 16, p, p, b, 0, 1, xs, NRP, nrhs, cr, ci);
+        bwd_gemm_tile<NT8, UN>(P, n, mt * 16, p, p, b, 0, 1, xs, NRP, nrhs, cr, ci);
         apply(mt * 16, p, cr, ci);
       }
     } else {
       // fewer column tiles than warps: S warps share a tile, interleaved over the k steps
-      const int MTc = MT <= 1 ? 1 : MT <= 2 ? 2 : MT <= 4 ? 4 : 8, S = NW / MTc;
+      int MTc = 1;
+      while (MTc < MT) MTc <<= 1;   // power of two >= MT (<= NW here)
+      const int S = NW / MTc;
       const int mt = warp % MTc, sl = warp / MTc;
       {
         double cr[2][4] = {}, ci[2][4] = {};
-        if (mt < MT && sl < S) bwd_gemm_tile<NT8>(P, n, mt * 16, p, p, b, sl, S, xs, NRP, nrhs, cr, ci);
+        if (mt < MT && sl < S) bwd_gemm_tile<NT8, UN>(P, n, mt * 16, p, p, b, sl, S, xs, NRP, nrhs, cr, ci);
         cplx* my = slots + warp * 256;
 #pragma unroll
         for (int ni = 0; ni < NT8; ++ni)
@@ -1050,7 +1055,7 @@ __global__ void __launch_bounds__(32 * NW) backward_mrhs_kernel(LevelArgs a, int
       const int MT = (kb + 15) >> 4;
       for (int mt = warp; mt < MT; mt += NW) {
         double cr[2][4] = {}, ci[2][4] = {};
-        bwd_gemm_tile<NT8>(P, n, mt * 16, kb, kb, w, 0, 1, xs, NRP, nrhs, cr, ci);
+        bwd_gemm_tile<NT8, UN>(P, n, mt * 16, kb, kb, w, 0, 1, xs, NRP, nrhs, cr, ci);
         apply(mt * 16, kb, cr, ci);
       }
       __syncthreads();
@@ -1058,16 +1063,16 @@ __global__ void __launch_bounds__(32 * NW) backward_mrhs_kernel(LevelArgs a, int
   }
 }
 
-template <int NW, int NT8>
+template <int NW, int NT8, int UN>
 int launch_backward_mrhs(const LevelArgs& a, int grid, int nmax, int unit, cudaStream_t s) {
   static DeviceOnce attr_once;
   if (attr_once.first()) {
-    STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_mrhs_kernel<NW, NT8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_mrhs_kernel<NW, NT8, UN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         200 * 1024));
-    STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_mrhs_kernel<NW, NT8>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(backward_mrhs_kernel<NW, NT8, UN>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                         100));
   }
-  backward_mrhs_kernel<NW, NT8><<<grid, 32 * NW, bwd_mrhs_smem<NW>(nmax, a.nrhs), s>>>(a, unit);
+  backward_mrhs_kernel<NW, NT8, UN><<<grid, 32 * NW, bwd_mrhs_smem<NW>(nmax, a.nrhs), s>>>(a, unit);
   STFEM_LAUNCH_CHECK("backward_mrhs_kernel");
   return STFEM_OK;
 }
@@ -1672,7 +1677,14 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
         const int u = ldlt ? 1 : 0, gsz = cnt * nb;
         if (nrhs >= 2 && pmax > P.opt.bwd_dmma_min_p && bwd_mrhs_smem<8>(nmax, nrhs) <= 200 * 1024) {
           // multi-RHS, multi-panel fronts: GEMMs over the right-hand sides on DMMA
-          return nrhs <= 8 ? launch_backward_mrhs<8, 1>(b, gsz, nmax, u, st) : launch_backward_mrhs<8, 2>(b, gsz, nmax, u, st);
+          if (nmax > BWD_SPLIT_N && bwd_mrhs_smem<16>(nmax, nrhs) <= 200 * 1024)
+            return nrhs <= 8 ? launch_backward_mrhs<16, 1, 8>(b, gsz, nmax, u, st)
+                             : launch_backward_mrhs<16, 2, 8>(b, gsz, nmax, u, st);
+          if (nmax > BWD_SPLIT_N)   // the largest fronts: 8 warps (their staged x leaves no room for 16 reduction slots)
+            return nrhs <= 8 ? launch_backward_mrhs<8, 1, 8>(b, gsz, nmax, u, st)
+                             : launch_backward_mrhs<8, 2, 8>(b, gsz, nmax, u, st);
+          return nrhs <= 8 ? launch_backward_mrhs<8, 1, 4>(b, gsz, nmax, u, st)
+                           : launch_backward_mrhs<8, 2, 4>(b, gsz, nmax, u, st);
         }
         switch (small_nr(nrhs)) {
           case 1: return launch_backward_level<1>(b, gsz, nmax, u, st);
