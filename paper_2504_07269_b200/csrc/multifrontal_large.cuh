@@ -272,10 +272,12 @@ __global__ void __launch_bounds__(256) diag_kernel(LevelArgs a, int kb) {
 // forward RHS r -= x y.  The W-wide panel is solved in register blocks of 16
 // columns (right-looking inside a block, independent update chains); a later
 // block first subtracts the finished blocks, re-read from global (L1-hot).
-// Register blocks of 16 keep the kernel near 100 registers (4+ CTAs per SM).
+// Measured on C4 (ms per step): blocks of 8 at 64 registers / 8 CTAs per SM 72.9,
+// blocks of 16 at 96 registers / 5 CTAs 69.0 (48 instead of 80 loads per row),
+// at 128 registers / 4 CTAs 76.8, at 80 registers / 6 CTAs it spills.
 template <int W>
-__global__ void __launch_bounds__(TR_ROWS, 8) trsm_kernel(LevelArgs a, int kb) {
-  constexpr int WB = 8;
+__global__ void __launch_bounds__(TR_ROWS, 5) trsm_kernel(LevelArgs a, int kb) {
+  constexpr int WB = 16;
   constexpr int LW = W + 1;           // padded pitch: the column-wise staging below is conflict-free
   __shared__ cplx Ls[W * LW];         // Ls[c * LW + c'] = C[kb+c][kb+c'] (c' < c); Ls[c*LW+c] = 1 / c_cc
   __shared__ cplx ys[W * MAXR];
