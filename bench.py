@@ -536,7 +536,10 @@ def run_ours(args):
     if not args.no_e2e:
         Fh = prob.F_host
         Ph = torch.empty_like(Fh, pin_memory=True)
-        bufs = (F, G, Psi)   # the step re-uploads its input into the resident buffers (no extra HBM)
+        bufs = (F, G, Psi)   # the step re-uploads its input into the resident buffers
+        if 4 * Fh.numel() * 16 <= 0.2 * torch.cuda.get_device_properties(0).total_memory:
+            # a fourth stack decouples the drain of Psi_k from step k + 1 (FDMSolver.solve_host_stream)
+            bufs = bufs + (torch.empty_like(F),)
 
         # public API: pinned host F in, pinned host Psi out, every step.  solve_host_stream runs
         # the steps as a stream of solves: step k+1's H2D overlaps step k's spatial solves and

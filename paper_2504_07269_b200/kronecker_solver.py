@@ -255,7 +255,7 @@ class FDMSolver:
         dev = self.X.device
         if dev_buffers is None:
             dev_buffers = tuple(torch.empty(Fh.shape, dtype=C128, device=dev) for _ in range(3))
-        Fd, G, W = dev_buffers
+        Fd, G, W = dev_buffers[:3]
         s = stream if stream is not None else torch.cuda.current_stream()
         if getattr(self, "_copy_stream", None) is None:
             self._copy_stream = torch.cuda.Stream(device=dev)
@@ -313,8 +313,14 @@ class FDMSolver:
         nr, nt, nx = shape
         dev = self.X.device
         if dev_buffers is None:
-            dev_buffers = tuple(torch.empty(shape, dtype=C128, device=dev) for _ in range(3))
+            # a fourth buffer (when four stacks are a small part of the device memory) lets Psi_k
+            # drain to the host during the whole of step k + 1 instead of having to be gone before
+            # factor_solve(k + 1) overwrites it
+            nbytes = 16 * nr * nt * nx
+            total = torch.cuda.get_device_properties(dev).total_memory
+            dev_buffers = tuple(torch.empty(shape, dtype=C128, device=dev) for _ in range(4 if 4 * nbytes <= 0.2 * total else 3))
         A = dev_buffers[0]
+        four = len(dev_buffers) >= 4
         s = stream if stream is not None else torch.cuda.current_stream()
         if getattr(self, "_h2d_stream", None) is None:
             self._h2d_stream = torch.cuda.Stream(device=dev)
@@ -334,8 +340,12 @@ class FDMSolver:
         hs.wait_event(start)
         ds.wait_event(start)
         d2h_done = None
+        d2h_events = []
         for k in range(n):
-            G, W = (dev_buffers[1], dev_buffers[2]) if k % 2 == 0 else (dev_buffers[2], dev_buffers[1])
+            if four:   # W fixed; G (which also receives Psi_k) alternates: Psi_k drains while step k + 1 runs
+                G, W = dev_buffers[2 + (k % 2)], dev_buffers[1]
+            else:
+                G, W = (dev_buffers[1], dev_buffers[2]) if k % 2 == 0 else (dev_buffers[2], dev_buffers[1])
             if k == 0:                                   # prologue: H2D(0) block-pipelined with the transform
                 for c0, c1 in blocks:
                     h2d(0, c0, c1)
@@ -345,7 +355,9 @@ class FDMSolver:
                     self.forward_transform(A[..., c0:c1], G[..., c0:c1], s)
             else:
                 s.wait_event(h2d_done)
-                self.forward_transform(A, G, s)          # G_k = W_{k-1}: dead since back(k-1)
+                if four and k >= 2:                      # G_k = G_{k-2} held Psi_{k-2}: drained a step ago
+                    s.wait_event(d2h_events[k - 2])
+                self.forward_transform(A, G, s)          # three buffers: G_k = W_{k-1}, dead since back(k-1)
             if k + 1 < n:                                # H2D(k+1) during factor_solve(k)
                 fwd_done = torch.cuda.Event()
                 fwd_done.record(s)
@@ -354,7 +366,7 @@ class FDMSolver:
                     h2d(k + 1, c0, c1)
                 h2d_done = torch.cuda.Event()
                 h2d_done.record(hs)
-            if d2h_done is not None:                     # W_k = G_{k-1} holds Psi_{k-1} until drained
+            if not four and d2h_done is not None:        # W_k = G_{k-1} holds Psi_{k-1} until drained
                 s.wait_event(d2h_done)
             self.plan.factor_solve(self.lam, G, W, layout, nr, stream=s, check=False)
             for c0, c1 in blocks:                        # back transform W -> G, D2H block-pipelined
@@ -366,6 +378,7 @@ class FDMSolver:
                                             c1 - c0, nr * nt, 1, N.stream_ptr(ds)))
             d2h_done = torch.cuda.Event()
             d2h_done.record(ds)
+            d2h_events.append(d2h_done)
         s.wait_event(d2h_done)
         self.plan.check(s)        # one wait for the whole sequence
         return out_hosts

@@ -290,9 +290,12 @@ def test_solve_host_stream_matches_device_solves():
           for _ in range(4)]
     refs = [fdm.solve(F.cuda()).cpu().numpy() for F in Fs]
     Fh = [F.pin_memory() for F in Fs]
-    for chunks in (1, 5):
+    for chunks, nbuf in ((1, None), (5, None), (3, 3), (2, 4)):
+        # nbuf None: the solver allocates (four stacks when they are a small part of the memory);
+        # 3 / 4: caller-owned buffers, the three-buffer rotation and the four-buffer one
+        bufs = None if nbuf is None else tuple(torch.empty_like(Fs[0], device="cuda") for _ in range(nbuf))
         Ph = [torch.zeros_like(F).pin_memory() for F in Fs]
-        fdm.solve_host_stream(Fh, Ph, chunks=chunks)
+        fdm.solve_host_stream(Fh, Ph, chunks=chunks, dev_buffers=bufs)
         torch.cuda.synchronize()
         for P, ref in zip(Ph, refs):
             assert np.array_equal(P.numpy(), ref)
