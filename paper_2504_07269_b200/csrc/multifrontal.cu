@@ -1333,7 +1333,12 @@ int auto_batch(Plan& P, int nshift, int nrhs) {
   // keep whatever workspace we already own in the budget; the default 70% of what is free
   // leaves room for the caller's temporaries (residual checks)
   size_t owned = P.d_factor ? (size_t)bytes_per_shift(P, P.ws_nrhs) * P.ws_batch : 0;
-  double budget = P.opt.workspace_fraction * (double)(fr + owned);
+  // workspace_fraction of what is free, or more when that still leaves two BlockVector stacks of
+  // this solve (the caller's output / residual temporaries) and 15% free: C4 then runs 2 batches
+  // of 512 shifts instead of 384 + 384 + 256 (-5 ms per step); C5, whose stacks are 29 GB, stays
+  // at the fraction
+  const double avail = (double)(fr + owned), bv = 16.0 * (double)P.n * nshift * nrhs;
+  double budget = std::max(P.opt.workspace_fraction * avail, std::min(0.85 * avail, avail - 2.0 * bv));
   int64_t per = bytes_per_shift(P, nrhs);
   int64_t bmax = std::min<int64_t>(std::max<int64_t>(1, (int64_t)(budget / (double)per)), 4096);
   return even_batch(nshift, bmax);
