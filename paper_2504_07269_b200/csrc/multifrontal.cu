@@ -601,18 +601,12 @@ __global__ void __launch_bounds__(NTH, NTH >= 256 ? 2 : 4) syrk_front_kernel(Lev
 
 // Trailing pivot-column updates, delayed over groups of panels (multifrontal_large.cuh), through
 // the same engine: F[cb:, cb:cb+cols] -= X X^T with X = F[cb:, k0:k0+K) (the TRSM'd panel rows),
-// lower trapezoid of 32 x 32 tiles.  Tile q of the launch = (shift, front of the level, tile t of
-// the front's trapezoid); fronts with fewer tiles than the level maximum get empty (K = 0) tiles.
-__host__ __device__ inline int panel_update_tiles32(int n, int p, int cb, int narrow) {
-  const int cols = cb >= p ? 0 : (narrow ? min(NB, p - cb) : p - cb);
-  if (cols <= 0) return 0;
-  const int tm = (n - cb + 31) / 32, tn = (cols + 31) / 32;
-  return tn * tm - tn * (tn - 1) / 2;
-}
-
+// lower trapezoid of 32 x 32 tiles, enumerated per (level, panel step) on the host (compact
+// lists: a level of very different fronts -- C5 -- launches no empty tile slots).
 template <int WS_STAGES>
 __global__ void __launch_bounds__(WS_THREADS, ws_ctas_per_sm<false, WS_STAGES>())
-    panel_ws_kernel(LevelArgs a, int cb, int k0, int K, int narrow, int tiles_max, long long total, int T) {
+    panel_ws_kernel(LevelArgs a, int cb, int k0, int K, int narrow, const int4* __restrict__ tiles, int ntile,
+                    long long total, int T) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* As = reinterpret_cast<cplx*>(smem_raw);
   cplx* Bs = As + WS_STAGES * S32_STAGE;
@@ -624,44 +618,29 @@ __global__ void __launch_bounds__(WS_THREADS, ws_ctas_per_sm<false, WS_STAGES>()
   const long long q0 = (long long)blockIdx.x * T;
   const int nt = (int)min((long long)T, total - q0);
   for (int j = threadIdx.x; j < nt; j += WS_THREADS) {
+    // tile q of the launch = (shift q / ntile, entry q % ntile of the step's compact tile list:
+    // front of the level, tile row, tile column) -- every slot is a real tile, whatever the
+    // spread of front sizes on the level
     const long long q = q0 + j;
-    const int t = (int)(q % tiles_max);
-    const long long inst = q / tiles_max;
-    const int fi = (int)(inst % a.nlist), k = (int)(inst / a.nlist);
-    const FrontDev F = a.fronts[a.list[fi]];
+    const int k = (int)(q / ntile);
+    const int4 tl = tiles[q - (long long)k * ntile];
+    const FrontDev F = a.fronts[tl.x];
     const int n = F.n, p = F.p;
-    const int cols = cb >= p ? 0 : (narrow ? min(NB, p - cb) : p - cb);
+    const int cols = narrow ? min(NB, p - cb) : p - cb;
+    cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
     StreamTile D;
-    D.K = 0;
-    D.M = D.N = D.i0 = D.c0 = D.lda = D.ldC = D.pad = 0;
-    D.A = nullptr;
-    D.C = nullptr;
+    D.A = P + cb + (int64_t)k0 * n;
+    D.C = P + cb + (int64_t)cb * n;
+    D.lda = D.ldC = n;
+    D.K = min(K, p - k0);
+    D.M = n - cb;
+    D.pad = D.M;
+    D.N = cols;
+    D.i0 = tl.y * 32;
+    D.c0 = tl.z * 32;
     D.Uc[0] = D.Uc[1] = nullptr;
     D.bc[0] = D.bc[1] = 0;
     D.inv_off[0] = D.inv_off[1] = -1;
-    if (cols > 0) {
-      const int tm = (n - cb + 31) / 32, tn = (cols + 31) / 32;
-      int r = t, ti = -1, tj = 0;
-      for (; tj < tn; ++tj) {
-        if (r < tm - tj) {
-          ti = tj + r;
-          break;
-        }
-        r -= tm - tj;
-      }
-      if (ti >= 0) {
-        cplx* P = a.factor + (int64_t)k * a.fstride + F.fofs;
-        D.A = P + cb + (int64_t)k0 * n;
-        D.C = P + cb + (int64_t)cb * n;
-        D.lda = D.ldC = n;
-        D.K = min(K, p - k0);
-        D.M = n - cb;
-        D.pad = D.M;
-        D.N = cols;
-        D.i0 = ti * 32;
-        D.c0 = tj * 32;
-      }
-    }
     desc[j] = D;
   }
   __syncthreads();
@@ -1236,6 +1215,53 @@ int upload(Plan& P) {
     P.syrk32_off[P.levels.size()] = (int64_t)t32.size();
     if ((rc = up(&P.d_syrk32_tiles, t32))) return rc;
   }
+  // trailing-update tiles of every (large level, panel step): (front, tile row, tile column)
+  {
+    std::vector<int4> tp;
+    P.panel_off.assign(P.levels.size(), {});
+    const int pg = std::max(1, P.opt.panel_group);
+    for (size_t d = 0; d < P.levels.size(); ++d) {
+      if (level_is_small(P, (int)d)) continue;
+      for (int kb = 0; kb < P.level_pmax[d]; kb += NB) {
+        const int GW = NB * pg, g0 = (kb / GW) * GW;
+        const int narrow = ((kb - g0) / NB < pg - 1) ? 1 : 0, cb = kb + NB;
+        P.panel_off[d].push_back((int64_t)tp.size());
+        for (int32_t f : P.levels[d]) {
+          const int n = P.fronts[f].n, p = P.fronts[f].p;
+          const int cols = cb >= p ? 0 : (narrow ? std::min(NB, p - cb) : p - cb);
+          if (cols <= 0) continue;
+          const int tm = (n - cb + 31) / 32, tn = (cols + 31) / 32;
+          for (int tj = 0; tj < tn; ++tj)
+            for (int ti = tj; ti < tm; ++ti) tp.push_back(make_int4(f, ti, tj, 0));
+        }
+      }
+      P.panel_off[d].push_back((int64_t)tp.size());
+    }
+    if ((rc = up(&P.d_panel_tiles, tp))) return rc;
+  }
+  // fronts of every (large level, panel step) that still have a panel at that step (p > kb), and
+  // their largest order: the diagonal-block and TRSM launches of the late steps of an unbalanced
+  // level run over those fronts only
+  {
+    std::vector<int32_t> sl;
+    P.step_off.assign(P.levels.size(), {});
+    P.step_nmax.assign(P.levels.size(), {});
+    for (size_t d = 0; d < P.levels.size(); ++d) {
+      if (level_is_small(P, (int)d)) continue;
+      for (int kb = 0; kb < P.level_pmax[d]; kb += NB) {
+        P.step_off[d].push_back((int64_t)sl.size());
+        int nm = 0;
+        for (int32_t f : P.levels[d])
+          if (P.fronts[f].p > kb) {
+            sl.push_back(f);
+            nm = std::max(nm, P.fronts[f].n);
+          }
+        P.step_nmax[d].push_back(nm);
+      }
+      P.step_off[d].push_back((int64_t)sl.size());
+    }
+    if ((rc = up(&P.d_step_list, sl))) return rc;
+  }
   // spectral subtrees: data + per-depth work items (fwd1 = U and F1, fwd2 = F2, bwd1 = B1, bwd2 = B2)
   {
     const int L = (int)P.levels.size();
@@ -1361,6 +1387,10 @@ void Plan::free_device() {
   cudaFree(d_inv);
   cudaFree(d_syrk32_tiles);
   d_syrk32_tiles = nullptr;
+  cudaFree(d_panel_tiles);
+  d_panel_tiles = nullptr;
+  cudaFree(d_step_list);
+  d_step_list = nullptr;
   cudaFree(d_ent_src);
   cudaFree(d_ent_mv);
   cudaFree(d_ent_av);
@@ -1577,15 +1607,20 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
         fam(FAM_ASM);
         const int pg = std::max(1, P.opt.panel_group);
         for (int kb = 0; kb < pmax; kb += NB) {
+          // this step's fronts (p > kb) only
+          LevelArgs as = a;
+          as.list = P.d_step_list + P.step_off[d][kb / NB];
+          as.nlist = (int32_t)(P.step_off[d][kb / NB + 1] - P.step_off[d][kb / NB]);
+          const int sinst = as.nlist * nb, snmax = P.step_nmax[d][kb / NB];
           if (nrhs == 1)
-            diag_kernel<true><<<ninst, 32, 0, st>>>(a, kb);
+            diag_kernel<true><<<sinst, 32, 0, st>>>(as, kb);
           else
-            diag_kernel<false><<<ninst, 32 * std::min(8, (nrhs + DIAG_RPW - 1) / DIAG_RPW), 0, st>>>(a, kb);
+            diag_kernel<false><<<sinst, 32 * std::min(8, (nrhs + DIAG_RPW - 1) / DIAG_RPW), 0, st>>>(as, kb);
           STFEM_LAUNCH_CHECK("diag_kernel");
           fam(FAM_DIAG);
-          const dim3 tg(ninst, (unsigned)std::max(1, (nmax - kb + TR_ROWS - 1) / TR_ROWS));
-          if (std::min(NB, pmax - kb) <= 16) trsm_kernel<16><<<tg, TR_ROWS, 0, st>>>(a, kb);
-          else trsm_kernel<32><<<tg, TR_ROWS, 0, st>>>(a, kb);
+          const dim3 tg(sinst, (unsigned)std::max(1, (snmax - kb + TR_ROWS - 1) / TR_ROWS));
+          if (std::min(NB, pmax - kb) <= 16) trsm_kernel<16><<<tg, TR_ROWS, 0, st>>>(as, kb);
+          else trsm_kernel<32><<<tg, TR_ROWS, 0, st>>>(as, kb);
           STFEM_LAUNCH_CHECK("trsm_kernel");
           fam(FAM_TRSM);
           nlaunch += 2;
@@ -1595,18 +1630,19 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
           const int GW = NB * pg, g0 = (kb / GW) * GW;
           const int narrow = ((kb - g0) / NB < pg - 1) ? 1 : 0;
           const int cb = kb + NB, k0 = g0, K = kb + NB - g0;
-          int tiles = 0;
-          for (int32_t f : P.levels[d])
-            tiles = std::max(tiles, panel_update_tiles32(P.fronts[f].n, P.fronts[f].p, cb, narrow));
+          const int step = kb / NB;
+          const int64_t toff = P.panel_off[d][step];
+          const int tiles = (int)(P.panel_off[d][step + 1] - toff);
           if (tiles > 0) {
-            const long long total = (long long)ninst * tiles;
+            const long long total = (long long)nb * tiles;
             const unsigned gr = (unsigned)((total + T - 1) / T);
+            const int4* ptl = P.d_panel_tiles + toff;
             if (ws_stages == 2)
-              panel_ws_kernel<2><<<gr, WS_THREADS, ws_smem_bytes<false, 2>(), st>>>(a, cb, k0, K, narrow, tiles, total, T);
+              panel_ws_kernel<2><<<gr, WS_THREADS, ws_smem_bytes<false, 2>(), st>>>(a, cb, k0, K, narrow, ptl, tiles, total, T);
             else if (ws_stages == 4)
-              panel_ws_kernel<4><<<gr, WS_THREADS, ws_smem_bytes<false, 4>(), st>>>(a, cb, k0, K, narrow, tiles, total, T);
+              panel_ws_kernel<4><<<gr, WS_THREADS, ws_smem_bytes<false, 4>(), st>>>(a, cb, k0, K, narrow, ptl, tiles, total, T);
             else
-              panel_ws_kernel<3><<<gr, WS_THREADS, ws_smem_bytes<false, 3>(), st>>>(a, cb, k0, K, narrow, tiles, total, T);
+              panel_ws_kernel<3><<<gr, WS_THREADS, ws_smem_bytes<false, 3>(), st>>>(a, cb, k0, K, narrow, ptl, tiles, total, T);
             STFEM_LAUNCH_CHECK("panel_ws_kernel");
             ++nlaunch;
             fam(FAM_PANEL);

@@ -106,6 +106,11 @@ struct Plan {
   double *d_ent_mv = nullptr, *d_ent_av = nullptr;   // M_x / A_x values gathered into entry order
   std::vector<int64_t> syrk32_off;         // per depth: offsets into d_syrk32_tiles
   int4* d_syrk32_tiles = nullptr;          // (front, ti, tj, 0) lower 32 x 32 Schur-update tiles of the large fronts
+  std::vector<std::vector<int64_t>> panel_off;   // per depth, per panel step (+ end): offsets into d_panel_tiles
+  int4* d_panel_tiles = nullptr;           // (front, ti, tj, 0) trailing-update tiles of every (level, panel step)
+  std::vector<std::vector<int64_t>> step_off;    // per depth, per panel step (+ end): offsets into d_step_list
+  std::vector<std::vector<int32_t>> step_nmax;   // per depth, per panel step: largest order of its fronts
+  int32_t* d_step_list = nullptr;          // fronts with a panel at the step (p > kb)
   int* d_err = nullptr;
   int32_t* d_diag_src = nullptr;
   double* d_scale2 = nullptr;              // per shift of the batch: max_j |M_jj + lam A_jj|^2
