@@ -37,6 +37,7 @@ namespace {
 int upload(Plan& P);
 int ensure_workspace(Plan& P, int batch, int nrhs);
 int auto_batch(Plan& P, int nshift, int nrhs);
+int ensure_workspace_backoff(Plan& P, int* batch, int nrhs);
 
 constexpr int NT = 256;
 constexpr int NB = 32;            // panel width
@@ -1349,6 +1350,19 @@ int even_batch(int nshift, int64_t bmax) {
   return (int)((r64 <= bmax && (nshift + r64 - 1) / r64 == nb) ? r64 : even);
 }
 
+// Workspace for `batch` shifts; when the device cannot give it (fragmentation, a caller that took
+// memory since cudaMemGetInfo) the batch is halved until it fits: slower, never an error a smaller
+// batch would have avoided.  Returns the batch actually allocated in *batch.
+int ensure_workspace_backoff(Plan& P, int* batch, int nrhs) {
+  for (;;) {
+    const int rc = ensure_workspace(P, *batch, nrhs);
+    if (rc != STFEM_ERR_NOMEM || *batch <= 1) return rc;
+    (void)cudaGetLastError();
+    P.free_workspace();
+    *batch = (*batch + 1) / 2;
+  }
+}
+
 int auto_batch(Plan& P, int nshift, int nrhs) {
   if (P.batch > 0) return std::min(P.batch, nshift);
   // an existing workspace fixes the split (stfem_plan_reserve, or the first call): no
@@ -1447,8 +1461,8 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
   if (nshift == 0) return STFEM_OK;
   int rc;
   if ((rc = upload(P))) return rc;
-  const int batch = auto_batch(P, nshift, nrhs);
-  if ((rc = ensure_workspace(P, batch, nrhs))) return rc;
+  int batch = auto_batch(P, nshift, nrhs);
+  if ((rc = ensure_workspace_backoff(P, &batch, nrhs))) return rc;
 
   LevelArgs a{};
   a.fronts = P.d_fronts;
@@ -1810,7 +1824,8 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
 int plan_reserve(Plan& P, int nshift, int nrhs) {
   int rc;
   if ((rc = upload(P))) return rc;
-  return ensure_workspace(P, auto_batch(P, nshift, nrhs), nrhs);
+  int batch = auto_batch(P, nshift, nrhs);
+  return ensure_workspace_backoff(P, &batch, nrhs);
 }
 
 // wait for the work issued so far on `stream`, read and clear the latched pivot-collapse flag

@@ -136,6 +136,32 @@ def test_multi_rhs_backward(nr, opts):
         assert rel(W[:, l, :], ref) < 1e-11, (l, rel(W[:, l, :], ref))
 
 
+def test_workspace_backoff_when_memory_is_short():
+    """A batch the device cannot hold is halved until it fits (no error a smaller batch would
+    have avoided); the results do not depend on the batch."""
+    mesh = sm.build_structured_square(48)
+    ops = fa.assemble_spatial(mesh)
+    rng = np.random.default_rng(7)
+    nt = 256
+    lam = rng.standard_normal(nt) - 1j * (0.05 + rng.random(nt))
+    G = torch.from_numpy(rng.standard_normal((1, nt, ops.n)) + 0j).cuda()
+    plan = sss.SpatialPlan(ops, spectral=0)
+    plan.set_batch(16)
+    ref = sss.factor_solve_batch(plan, lam, G).cpu().numpy()
+    del plan
+    plan = sss.SpatialPlan(ops, spectral=0)
+    bps = plan.set_batch(nt)                      # bytes per shift of the numeric workspace
+    free, _ = torch.cuda.mem_get_info()
+    keep = bps * nt // 3                          # leave room for a third of the requested batch
+    hog = torch.empty(max(0, free - keep), dtype=torch.uint8, device="cuda")
+    try:
+        W = sss.factor_solve_batch(plan, lam, G).cpu().numpy()
+        assert 1 < plan.last_num_batches()        # the full batch did not fit
+    finally:
+        del hog
+    assert np.array_equal(W, ref)
+
+
 @pytest.mark.parametrize("spectral", [0, 64])
 def test_batching_invariance(spectral):
     """Results identical whatever the shift batch size."""
