@@ -97,6 +97,23 @@ int stfem_transform_pair_back(const double* A, int nt, const int32_t* mix_rows, 
                               int nmix, void* in, int64_t ld_in, void* out, int64_t ld_out,
                               int64_t ncols, int batch, int64_t bstride_in, int64_t bstride_out,
                               void* stream);
+/* The same two transforms with the spatial permutation of the shifted solves fused in (FD steps
+ * 2 and 4 around stfem_factor_solve with stfem_plan_set_io_permuted(plan, 1)):
+ *   _fwd_map : result column j is written at column out_cols[j] of `out` (out_cols = iperm, old -> new);
+ *   _back_map: result column j reads operand column in_cols[j] of `in` (in_cols = iperm); with a
+ *              map the pre-pass must have run over ALL columns of `in` first (stfem_pair_mix) and
+ *              nmix is 0.  A NULL map is the identity.  A mapped side is addressed from its base
+ *              pointer with absolute columns, so column blocks of the other side can be processed
+ *              one at a time (pipelined host copies). */
+int stfem_transform_pair_fwd_map(const double* A, int mrows, int nt, const int32_t* rows, const void* scale,
+                                 int nsrc, const void* in, int64_t ld_in, void* out, int64_t ld_out, int64_t ncols,
+                                 int batch, int64_t bstride_in, int64_t bstride_out, const int32_t* out_cols,
+                                 void* stream);
+int stfem_pair_mix(const int32_t* mix_rows, const void* mix_coef, int nmix, void* W, int64_t ld, int64_t ncols,
+                   int batch, int64_t bstride, void* stream);
+int stfem_transform_pair_back_map(const double* A, int nt, const int32_t* mix_rows, const void* mix_coef, int nmix,
+                                  void* in, int64_t ld_in, void* out, int64_t ld_out, int64_t ncols, int batch,
+                                  int64_t bstride_in, int64_t bstride_out, const int32_t* in_cols, void* stream);
 
 /* Column block [0, ncols) of `rows` rows between host and device
  * (cudaMemcpy2DAsync; leading dimensions in complex128 elements; kind 0 =
@@ -166,6 +183,13 @@ int stfem_factor_solve(stfem_plan* plan, const double* Mvals, const double* Aval
  * sweep reports its sweep index l this way). */
 int stfem_plan_check(stfem_plan* plan, void* stream);
 int stfem_plan_set_shift_base(stfem_plan* plan, int32_t base);
+/* G and W of the following stfem_factor_solve calls are indexed in the plan's own numbering
+ * (column new = iperm[old]) instead of the operators': pivot rows are then contiguous, and the
+ * permutation is applied by the transforms around the solves (the _map variants above).
+ * stfem_plan_device_iperm: the device copy of iperm (int32[n]); valid until the next
+ * stfem_plan_set_spectral / stfem_plan_set_options. */
+int stfem_plan_set_io_permuted(stfem_plan* plan, int32_t on);
+int stfem_plan_device_iperm(stfem_plan* plan, const int32_t** iperm);
 /* Allocate the numeric workspace for calls of up to `nshift` shifts and `nrhs`
  * right-hand sides now (the batch size is fixed here: equal batches from
  * workspace_fraction of the free memory, or stfem_plan_set_batch), so that

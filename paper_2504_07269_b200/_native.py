@@ -76,6 +76,13 @@ def _declare(lib):
         "stfem_time_transform": (C.c_int, [P, C.c_int, P, I64, P, I64, I64, C.c_int, I64, I64, P]),
         "stfem_transform_pair_fwd": (C.c_int, [P, C.c_int, C.c_int, P, P, C.c_int, P, I64, P, I64, I64, C.c_int,
                                                I64, I64, P]),
+        "stfem_transform_pair_fwd_map": (C.c_int, [P, C.c_int, C.c_int, P, P, C.c_int, P, I64, P, I64, I64, C.c_int,
+                                                  I64, I64, P, P]),
+        "stfem_pair_mix": (C.c_int, [P, P, C.c_int, P, I64, I64, C.c_int, I64, P]),
+        "stfem_transform_pair_back_map": (C.c_int, [P, C.c_int, P, P, C.c_int, P, I64, P, I64, I64, C.c_int, I64, I64,
+                                                   P, P]),
+        "stfem_plan_set_io_permuted": (C.c_int, [P, I32]),
+        "stfem_plan_device_iperm": (C.c_int, [P, C.POINTER(P)]),
         "stfem_transform_pair_back": (C.c_int, [P, C.c_int, P, P, C.c_int, P, I64, P, I64, I64, C.c_int, I64, I64,
                                                 P]),
         "stfem_copy_cols": (C.c_int, [P, I64, P, I64, I64, I64, I32, P]),

@@ -824,7 +824,7 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int uni
           }
         }
         if (lane < w) {
-          const int prow = a.perm[F.pbeg + kb + lane];
+          const int prow = a.perm ? a.perm[F.pbeg + kb + lane] : F.pbeg + kb + lane;
           stc(Zk + F.pbeg + kb + lane + (int64_t)r0 * nx, x0);
           stc(a.W + bv_off(a.lay, r0, shift, prow), x0);
           xs[(kb + lane) * nrhs + r0] = x0;
@@ -1019,7 +1019,7 @@ __global__ void __launch_bounds__(32 * NW) backward_mrhs_kernel(LevelArgs a, int
         }
       }
       if (lane < w) {
-        const int prow = a.perm[F.pbeg + kb + lane];
+        const int prow = a.perm ? a.perm[F.pbeg + kb + lane] : F.pbeg + kb + lane;
         stc(Zk + F.pbeg + kb + lane + (int64_t)r0 * nx, x0);
         stc(a.W + bv_off(a.lay, r0, shift, prow), x0);
         xs[(kb + lane) * NRP + r0] = x0;
@@ -1188,6 +1188,7 @@ int upload(Plan& P) {
   if ((rc = up(&P.d_ent_dst, P.ent_dst))) return rc;
   if ((rc = up(&P.d_ent_colptr, P.ent_colptr))) return rc;
   if ((rc = up(&P.d_perm, P.perm))) return rc;
+  if ((rc = up(&P.d_iperm, P.iperm))) return rc;
   if ((rc = up(&P.d_diag_src, P.diag_src))) return rc;
   STFEM_CUDA_TRY(cudaMalloc(&P.d_err, sizeof(int)));
   STFEM_CUDA_TRY(cudaMemset(P.d_err, 0, sizeof(int)));
@@ -1413,6 +1414,8 @@ void Plan::free_device() {
   cudaFree(d_ent_colptr);
   d_ent_colptr = nullptr;
   cudaFree(d_perm);
+  cudaFree(d_iperm);
+  d_iperm = nullptr;
   cudaFree(d_diag_src);
   d_diag_src = nullptr;
   cudaFree(d_err);
@@ -1473,7 +1476,7 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
   a.ent_src = P.d_ent_src;
   a.ent_dst = P.d_ent_dst;
   a.ent_colptr = P.d_ent_colptr;
-  a.perm = P.d_perm;
+  a.perm = P.io_permuted ? nullptr : P.d_perm;   // nullptr: G and W are indexed in the plan's numbering
   {
     const int64_t ne = (int64_t)P.ent_src.size();
     if (ne > 0) {
@@ -1543,7 +1546,7 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
     sa.C01 = P.d_C01;
     sa.fronts = P.d_fronts;
     sa.bidx = P.d_bidx;
-    sa.perm = P.d_perm;
+    sa.perm = P.io_permuted ? nullptr : P.d_perm;
     sa.lam = lam + s0;
     sa.nb = nb;
     sa.nrhs = nrhs;
@@ -1820,6 +1823,8 @@ int factor_solve(Plan& P, const double* Mv, const double* Av, const cplx* lam, i
   }
   return STFEM_OK;
 }
+
+int upload_tables(Plan& P) { return upload(P); }
 
 int plan_reserve(Plan& P, int nshift, int nrhs) {
   int rc;
@@ -2113,6 +2118,24 @@ extern "C" int stfem_plan_last_launches(const stfem_plan* plan, int64_t* launche
 extern "C" int stfem_plan_check(stfem_plan* plan, void* stream) {
   if (!plan) return stfem::fail(STFEM_ERR_ARG, "plan_check: null plan");
   return stfem::plan_check(*reinterpret_cast<Plan*>(plan), (cudaStream_t)stream);
+}
+
+// G and W of the following factor_solve calls are indexed in the plan's numbering (new = iperm[old])
+// instead of the operators' -- the FD solver lets the time transforms apply the permutation
+// (stfem_transform_pair_fwd_map / _back_map with the map from stfem_plan_device_iperm)
+extern "C" int stfem_plan_set_io_permuted(stfem_plan* plan, int32_t on) {
+  if (!plan) return stfem::fail(STFEM_ERR_ARG, "plan_set_io_permuted: null plan");
+  reinterpret_cast<Plan*>(plan)->io_permuted = on != 0;
+  return STFEM_OK;
+}
+
+extern "C" int stfem_plan_device_iperm(stfem_plan* plan, const int32_t** iperm) {
+  if (!plan || !iperm) return stfem::fail(STFEM_ERR_ARG, "plan_device_iperm: null pointer");
+  Plan& P = *reinterpret_cast<Plan*>(plan);
+  int rc = stfem::upload_tables(P);
+  if (rc) return rc;
+  *iperm = P.d_iperm;
+  return STFEM_OK;
 }
 
 extern "C" int stfem_plan_set_shift_base(stfem_plan* plan, int32_t base) {

@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(NT, 4) asm_front_kernel(LevelArgs a) {
     for (int q = tid; q < n * nrhs; q += NT) {
       const int r1 = q % n, r = q / n;
       cplx v = zero;
-      if (r1 < p) v = ldc(a.G + bv_off(a.lay, r, shift, a.perm[F.pbeg + r1]));
+      if (r1 < p) v = ldc(a.G + bv_off(a.lay, r, shift, a.perm ? a.perm[F.pbeg + r1] : F.pbeg + r1));
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         const int kk = s < nc ? inv_s[s * n + r1] : -1;

@@ -120,11 +120,11 @@ __global__ void __launch_bounds__(SMALL_N) factor_small_kernel(LevelArgs a, int 
       eval[u] = cmk(fma(lam.re, av, mv), lam.im * av);
     }
   }
-  const int64_t jrow = (i < p) ? a.perm[Fr.pbeg + i] : 0;
+  const int64_t jrow = (i < p) ? (a.perm ? a.perm[Fr.pbeg + i] : Fr.pbeg + i) : 0;
   const int tri = (n * (n + 1)) / 2;
   for (int q = i; q < tri; q += nt) F[q] = zero;
   for (int row = i; row < n; row += nt) {
-    int64_t j = row < p ? (row == i ? jrow : a.perm[Fr.pbeg + row]) : 0;
+    int64_t j = row < p ? (row == i ? jrow : (a.perm ? a.perm[Fr.pbeg + row] : Fr.pbeg + row)) : 0;
 #pragma unroll
     for (int r = 0; r < NR; ++r)
       Rsm[row * NR + r] = (row < p && r < nrhs) ? a.G[bv_off(a.lay, r, shift, j)] : zero;
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(SMALL_N) backward_small_kernel(LevelArgs a, in
         Tsm[jj * NR + lane] = x;
         const int col = Fr.pbeg + kb + jj;
         stc(Zk + col + (int64_t)lane * nx, x);
-        a.W[bv_off(a.lay, lane, shift, a.perm[col])] = x;
+        a.W[bv_off(a.lay, lane, shift, a.perm ? a.perm[col] : col)] = x;
       }
     }
     __syncthreads();

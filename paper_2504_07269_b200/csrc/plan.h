@@ -136,6 +136,8 @@ struct Plan {
   cplx* d_rpool[2] = {nullptr, nullptr};
   cplx* d_Z = nullptr;
   cplx* d_wbuf = nullptr;                   // spectral w = 1 / (theta + lam), sum(m) x batch
+  bool io_permuted = false;                 // G / W of factor_solve are in the plan's (permuted) numbering
+  int32_t* d_iperm = nullptr;               // iperm[old] = new, on the device (column maps of the transforms)
   int32_t shift_base = 0;                   // added to the shift index reported by stfem_plan_check
   int* h_err = nullptr;                     // pinned: the latched error flag read back by stfem_plan_check
 

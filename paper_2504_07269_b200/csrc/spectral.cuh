@@ -118,7 +118,7 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
   int* idx_s = reinterpret_cast<int*>(Bs + SP_STAGES * SP_B_STAGE);
   if constexpr (OP == OP_F1 || OP == OP_B1) {
     const int cnt = OP == OP_F1 ? m : g;
-    for (int q = tid; q < cnt; q += 256) idx_s[q] = OP == OP_F1 ? a.perm[S.first + q] : bidx[q];
+    for (int q = tid; q < cnt; q += 256) idx_s[q] = OP == OP_F1 ? (a.perm ? a.perm[S.first + q] : S.first + q) : bidx[q];
     __syncthreads();
   }
 
@@ -353,7 +353,7 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
             const int i = it.z * SP_BM + row;
             if (i >= m) continue;
             const int s = cg / nrhs, r = cg - s * nrhs;
-            stc(a.W + bv_off(a.lay, r, a.shift0 + s, a.perm[S.first + i]), v);
+            stc(a.W + bv_off(a.lay, r, a.shift0 + s, a.perm ? a.perm[S.first + i] : S.first + i), v);
           }
         }
         }

@@ -160,7 +160,8 @@ template <int EPI>
 __global__ void __launch_bounds__(256, 2)
 transform_rc_kernel(const double* __restrict__ A, int M, int K, const cplx* __restrict__ in, int64_t ld_in,
                     cplx* __restrict__ out, int64_t ld_out, int64_t ncols, int64_t bs_in, int64_t bs_out,
-                    const int2* __restrict__ rows, const cplx* __restrict__ scale, int nsrc) {
+                    const int2* __restrict__ rows, const cplx* __restrict__ scale, int nsrc,
+                    const int32_t* __restrict__ in_cols, const int32_t* __restrict__ out_cols) {
   // M: output rows (EPI_PLAIN) / A rows; A holds ceil(M / 16) packed 16-row blocks
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* As = reinterpret_cast<double*>(smem_raw);
@@ -174,6 +175,14 @@ transform_rc_kernel(const double* __restrict__ A, int M, int K, const cplx* __re
   in += (int64_t)blockIdx.z * bs_in;
   out += (int64_t)blockIdx.z * bs_out;
   const int nk = (K + RC_BK - 1) / RC_BK;
+  // Column maps (both optional): operand column j of this launch is read at column in_cols[j] of
+  // `in`, result column j is written at column out_cols[j] of `out`.  The FD solve passes the
+  // inverse nested-dissection permutation, so the spatial solves in between see G and W in
+  // their own numbering (contiguous pivot rows) at no extra pass: the operand copies are 16-byte
+  // cp.async per element either way, and the kernel is DMMA bound.  A thread's operand column
+  // is the same for every k tile (tid & 63).
+  const int64_t bcol = j0 + (tid & 63);
+  const int64_t bsrc = (in_cols && bcol < ncols) ? (int64_t)in_cols[bcol] : bcol;
 
   auto load_stage = [&](int stage, int kt) {
     const int k0 = kt * RC_BK;
@@ -193,7 +202,7 @@ transform_rc_kernel(const double* __restrict__ A, int M, int K, const cplx* __re
       const int idx = tid + 256 * r;
       const int k = idx >> 6, n = idx & 63;
       const bool ok = (k0 + k < K) && (j0 + n < ncols);
-      cp_async16(bs + k * LDB + n, ok ? in + (int64_t)(k0 + k) * ld_in + (j0 + n) : in, ok);
+      cp_async16(bs + k * LDB + n, ok ? in + (int64_t)(k0 + k) * ld_in + bsrc : in, ok);
     }
   };
 
@@ -256,19 +265,21 @@ transform_rc_kernel(const double* __restrict__ A, int M, int K, const cplx* __re
 #pragma unroll
         for (int cv = 0; cv < 2; ++cv) {
           if (col + cv >= ncols) continue;
+          const int64_t oc = out_cols ? (int64_t)out_cols[col + cv] : col + cv;
           const cplx u = cmk(cre[mi][ni][cv], cim[mi][ni][cv]);        // c F
           const cplx v = cmk(cre[mi][ni][2 + cv], cim[mi][ni][2 + cv]);  // d F
-          stc(out + (int64_t)lp.x * ld_out + col + cv, cmk(u.re - v.im, u.im + v.re));
-          if (lp.y >= 0) stc(out + (int64_t)lp.y * ld_out + col + cv, cmul(sc, cmk(u.re + v.im, u.im - v.re)));
+          stc(out + (int64_t)lp.x * ld_out + oc, cmk(u.re - v.im, u.im + v.re));
+          if (lp.y >= 0) stc(out + (int64_t)lp.y * ld_out + oc, cmul(sc, cmk(u.re + v.im, u.im - v.re)));
         }
       } else {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int row = m0 + wm * 32 + mi * 16 + g + 8 * h;
           if (row >= M) continue;
-          cplx* dst = out + (int64_t)row * ld_out + col;
-          if (col < ncols) stc(dst, cmk(cre[mi][ni][2 * h], cim[mi][ni][2 * h]));
-          if (col + 1 < ncols) stc(dst + 1, cmk(cre[mi][ni][2 * h + 1], cim[mi][ni][2 * h + 1]));
+          cplx* dst = out + (int64_t)row * ld_out;
+          if (col < ncols) stc(dst + (out_cols ? (int64_t)out_cols[col] : col), cmk(cre[mi][ni][2 * h], cim[mi][ni][2 * h]));
+          if (col + 1 < ncols)
+            stc(dst + (out_cols ? (int64_t)out_cols[col + 1] : col + 1), cmk(cre[mi][ni][2 * h + 1], cim[mi][ni][2 * h + 1]));
         }
       }
     }
@@ -299,7 +310,7 @@ __global__ void pair_mix_kernel(cplx* __restrict__ W, int64_t ld, int64_t ncols,
 template <int EPI>
 int launch_rc(const double* A, int M, int K, const cplx* in, int64_t ld_in, cplx* out, int64_t ld_out,
               int64_t ncols, int batch, int64_t bs_in, int64_t bs_out, const int2* rows, const cplx* scale,
-              int nsrc, cudaStream_t stream) {
+              int nsrc, const int32_t* in_cols, const int32_t* out_cols, cudaStream_t stream) {
   static DeviceOnce attr_once;
   if (attr_once.first()) {
     STFEM_CUDA_TRY(cudaFuncSetAttribute(transform_rc_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -308,8 +319,11 @@ int launch_rc(const double* A, int M, int K, const cplx* in, int64_t ld_in, cplx
   for (int64_t c0 = 0; c0 < ncols; c0 += 65535LL * BN) {
     const int64_t cn = ncols - c0 < 65535LL * BN ? ncols - c0 : 65535LL * BN;
     dim3 grid((M + BM - 1) / BM, (unsigned)((cn + BN - 1) / BN), batch);
-    transform_rc_kernel<EPI><<<grid, 256, RC_SMEM, stream>>>(A, M, K, in + c0, ld_in, out + c0, ld_out, cn, bs_in,
-                                                             bs_out, rows, scale, nsrc);
+    // a mapped side keeps its base pointer: the map holds absolute columns
+    transform_rc_kernel<EPI><<<grid, 256, RC_SMEM, stream>>>(A, M, K, in_cols ? in : in + c0, ld_in,
+                                                             out_cols ? out : out + c0, ld_out, cn, bs_in, bs_out, rows,
+                                                             scale, nsrc, in_cols ? in_cols + c0 : nullptr,
+                                                             out_cols ? out_cols + c0 : nullptr);
     STFEM_LAUNCH_CHECK("transform_rc_kernel");
   }
   return STFEM_OK;
@@ -358,39 +372,78 @@ extern "C" int stfem_time_transform(const void* T, int nt, const void* in, int64
                                bstride_out, (cudaStream_t)stream);
 }
 
-extern "C" int stfem_transform_pair_fwd(const double* A, int mrows, int nt, const int32_t* rows,
-                                        const void* scale, int nsrc, const void* in, int64_t ld_in, void* out,
-                                        int64_t ld_out, int64_t ncols, int batch, int64_t bstride_in,
-                                        int64_t bstride_out, void* stream) {
+extern "C" int stfem_transform_pair_fwd_map(const double* A, int mrows, int nt, const int32_t* rows,
+                                            const void* scale, int nsrc, const void* in, int64_t ld_in, void* out,
+                                            int64_t ld_out, int64_t ncols, int batch, int64_t bstride_in,
+                                            int64_t bstride_out, const int32_t* out_cols, void* stream) {
   using namespace stfem;
   if (nt <= 0 || (nt & 1) || mrows <= 0 || (mrows & 15) || nsrc <= 0 || 2 * nsrc > mrows + 16 || ncols < 0 ||
-      batch < 0 || ld_in < ncols || ld_out < ncols)
+      batch < 0 || ld_in < ncols || (!out_cols && ld_out < ncols))
     return fail(STFEM_ERR_DIM, "transform_pair_fwd: bad dimensions");
   if (!A || !rows || !scale || !in || !out) return fail(STFEM_ERR_ARG, "transform_pair_fwd: null pointer");
   if (((uintptr_t)A | (uintptr_t)in | (uintptr_t)out) & 15)
     return fail(STFEM_ERR_ARG, "transform_pair_fwd: buffers must be 16-byte aligned");
   if (ncols == 0 || batch == 0) return STFEM_OK;
   return launch_rc<EPI_PAIR>(A, mrows, nt, (const cplx*)in, ld_in, (cplx*)out, ld_out, ncols, batch, bstride_in,
-                             bstride_out, (const int2*)rows, (const cplx*)scale, nsrc, (cudaStream_t)stream);
+                             bstride_out, (const int2*)rows, (const cplx*)scale, nsrc, nullptr, out_cols,
+                             (cudaStream_t)stream);
+}
+
+extern "C" int stfem_transform_pair_fwd(const double* A, int mrows, int nt, const int32_t* rows,
+                                        const void* scale, int nsrc, const void* in, int64_t ld_in, void* out,
+                                        int64_t ld_out, int64_t ncols, int batch, int64_t bstride_in,
+                                        int64_t bstride_out, void* stream) {
+  return stfem_transform_pair_fwd_map(A, mrows, nt, rows, scale, nsrc, in, ld_in, out, ld_out, ncols, batch,
+                                      bstride_in, bstride_out, nullptr, stream);
+}
+
+// in-place pre-pass of the paired back transform over `ncols` columns of W (all of them, before any
+// column block is transformed, when the transform gathers its operand columns through a map)
+extern "C" int stfem_pair_mix(const int32_t* mix_rows, const void* mix_coef, int nmix, void* W, int64_t ld,
+                              int64_t ncols, int batch, int64_t bstride, void* stream) {
+  using namespace stfem;
+  if (nmix <= 0 || ncols < 0 || batch < 0 || ld < ncols) return fail(STFEM_ERR_DIM, "pair_mix: bad dimensions");
+  if (!mix_rows || !mix_coef || !W) return fail(STFEM_ERR_ARG, "pair_mix: null pointer");
+  if (ncols == 0 || batch == 0) return STFEM_OK;
+  const int64_t gx = std::min<int64_t>((ncols + 255) / 256, 1024);
+  pair_mix_kernel<<<dim3((unsigned)gx, nmix, batch), 256, 0, (cudaStream_t)stream>>>(
+      (cplx*)W, ld, ncols, bstride, (const int2*)mix_rows, (const cplx*)mix_coef);
+  STFEM_LAUNCH_CHECK("pair_mix_kernel");
+  return STFEM_OK;
+}
+
+// nmix = 0: the pre-pass has been run already (stfem_pair_mix); in_cols (optional): result column j
+// reads operand column in_cols[j] of `in`
+extern "C" int stfem_transform_pair_back_map(const double* A, int nt, const int32_t* mix_rows, const void* mix_coef,
+                                             int nmix, void* in, int64_t ld_in, void* out, int64_t ld_out,
+                                             int64_t ncols, int batch, int64_t bstride_in, int64_t bstride_out,
+                                             const int32_t* in_cols, void* stream) {
+  using namespace stfem;
+  if (nt <= 0 || (nt & 1) || nmix < 0 || nmix > nt || ncols < 0 || batch < 0 || (!in_cols && ld_in < ncols) ||
+      ld_out < ncols)
+    return fail(STFEM_ERR_DIM, "transform_pair_back: bad dimensions");
+  if (!A || !in || !out || (nmix > 0 && (!mix_rows || !mix_coef)))
+    return fail(STFEM_ERR_ARG, "transform_pair_back: null pointer");
+  if (nmix > 0 && in_cols)
+    return fail(STFEM_ERR_ARG, "transform_pair_back: with a column map run stfem_pair_mix over all of W first");
+  if (((uintptr_t)A | (uintptr_t)in | (uintptr_t)out) & 15)
+    return fail(STFEM_ERR_ARG, "transform_pair_back: buffers must be 16-byte aligned");
+  if (in == out) return fail(STFEM_ERR_ARG, "transform_pair_back: in and out must not alias");
+  if (ncols == 0 || batch == 0) return STFEM_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (nmix > 0) {
+    int rc = stfem_pair_mix(mix_rows, mix_coef, nmix, in, ld_in, ncols, batch, bstride_in, stream);
+    if (rc) return rc;
+  }
+  return launch_rc<EPI_PLAIN>(A, nt, nt, (const cplx*)in, ld_in, (cplx*)out, ld_out, ncols, batch, bstride_in,
+                              bstride_out, nullptr, nullptr, 0, in_cols, nullptr, st);
 }
 
 extern "C" int stfem_transform_pair_back(const double* A, int nt, const int32_t* mix_rows, const void* mix_coef,
                                          int nmix, void* in, int64_t ld_in, void* out, int64_t ld_out,
                                          int64_t ncols, int batch, int64_t bstride_in, int64_t bstride_out,
                                          void* stream) {
-  using namespace stfem;
-  if (nt <= 0 || (nt & 1) || nmix <= 0 || nmix > nt || ncols < 0 || batch < 0 || ld_in < ncols || ld_out < ncols)
-    return fail(STFEM_ERR_DIM, "transform_pair_back: bad dimensions");
-  if (!A || !mix_rows || !mix_coef || !in || !out) return fail(STFEM_ERR_ARG, "transform_pair_back: null pointer");
-  if (((uintptr_t)A | (uintptr_t)in | (uintptr_t)out) & 15)
-    return fail(STFEM_ERR_ARG, "transform_pair_back: buffers must be 16-byte aligned");
-  if (in == out) return fail(STFEM_ERR_ARG, "transform_pair_back: in and out must not alias");
-  if (ncols == 0 || batch == 0) return STFEM_OK;
-  cudaStream_t st = (cudaStream_t)stream;
-  const int64_t gx = std::min<int64_t>((ncols + 255) / 256, 1024);
-  pair_mix_kernel<<<dim3((unsigned)gx, nmix, batch), 256, 0, st>>>((cplx*)in, ld_in, ncols, bstride_in,
-                                                                    (const int2*)mix_rows, (const cplx*)mix_coef);
-  STFEM_LAUNCH_CHECK("pair_mix_kernel");
-  return launch_rc<EPI_PLAIN>(A, nt, nt, (const cplx*)in, ld_in, (cplx*)out, ld_out, ncols, batch, bstride_in,
-                              bstride_out, nullptr, nullptr, 0, st);
+  if (nmix <= 0) return stfem::fail(STFEM_ERR_DIM, "transform_pair_back: bad dimensions");
+  return stfem_transform_pair_back_map(A, nt, mix_rows, mix_coef, nmix, in, ld_in, out, ld_out, ncols, batch,
+                                       bstride_in, bstride_out, nullptr, stream);
 }

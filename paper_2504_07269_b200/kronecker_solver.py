@@ -181,6 +181,44 @@ class FDMSolver:
             return K.transform_pair_back(self.pairs, W, out=out, stream=stream)
         return K.time_transform(self.X, W, out=out, stream=stream)
 
+    # ---- the spatial permutation fused into the transforms (paired transforms only) ----
+    # The forward transform scatters its result columns to the plan's numbering (column
+    # iperm[x]) and the back transform gathers its operand columns from there, so the spatial
+    # solves in between read G and write W with contiguous pivot rows (stfem_plan_set_io_permuted)
+    # and no separate permutation pass exists.  Both transforms move their operands as 16-byte
+    # cp.async copies anyway and are DMMA bound.
+    @property
+    def fused_perm(self) -> bool:
+        return self.pairs is not None
+
+    def _iperm(self) -> torch.Tensor:
+        if getattr(self, "_iperm_d", None) is None:
+            perm = self.plan.perm()
+            ip = np.empty_like(perm)
+            ip[perm] = np.arange(len(perm), dtype=perm.dtype)
+            self._iperm_d = torch.as_tensor(ip.astype(np.int32), device=self.X.device)
+        return self._iperm_d
+
+    def _fwd_block(self, Fblk: torch.Tensor, G: torch.Tensor, c0: int, c1: int, stream=None):
+        """Forward transform of spatial columns [c0, c1) (Fblk) into the whole stack G."""
+        if self.fused_perm:
+            return K.transform_pair_fwd(self.pairs, Fblk, out=G, stream=stream, out_cols=self._iperm()[c0:c1])
+        return self.forward_transform(Fblk, G[..., c0:c1], stream)
+
+    def _back_block(self, W: torch.Tensor, out_blk: torch.Tensor, c0: int, c1: int, stream=None):
+        """Back transform into spatial columns [c0, c1) (out_blk) from the whole stack W (fused:
+        `K.pair_mix` must have run over W)."""
+        if self.fused_perm:
+            return K.transform_pair_back(self.pairs, W, out=out_blk, stream=stream, in_cols=self._iperm()[c0:c1],
+                                         mixed=True)
+        return self.back_transform(W[..., c0:c1], out_blk, stream)
+
+    def _spatial_solves(self, G, W, nr, stream):
+        self.plan.factor_solve(self.lam, G, W, blockvector_layout(self.nt, self.ops.n), nr, stream=stream,
+                               check=False, permuted=self.fused_perm)
+        if self.fused_perm:
+            K.pair_mix(self.pairs, W, stream=stream)
+
     def solve(self, F: torch.Tensor, out: torch.Tensor | None = None, work: torch.Tensor | None = None,
               stream=None, timings: dict | None = None, check: bool = True) -> torch.Tensor:
         """Psi for F of shape (n_t, n_x) or (n_rhs, n_t, n_x), complex128 on the GPU.
@@ -214,14 +252,14 @@ class FDMSolver:
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timings is not None else None
         if ev:
             ev[0].record(s)
-        self.forward_transform(Fb, G, s)                               # (2)
+        nx = self.ops.n
+        self._fwd_block(Fb, G, 0, nx, s)                               # (2)
         if ev:
             ev[1].record(s)
-        self.plan.factor_solve(self.lam, G, W, blockvector_layout(self.nt, self.ops.n), nr, stream=s,
-                               check=False)                            # (3)
+        self._spatial_solves(G, W, nr, s)                              # (3) (+ the pair pre-pass of step 4)
         if ev:
             ev[2].record(s)
-        self.back_transform(W, G, s)                                   # (4) (W is scratch)
+        self._back_block(W, G, 0, nx, s)                               # (4) (W is scratch)
         if check:
             self.plan.check(s)       # SingularPivot names the shift; waits for the stream
         if ev:
@@ -272,10 +310,10 @@ class FDMSolver:
             ev = torch.cuda.Event()
             ev.record(cs)
             s.wait_event(ev)
-            self.forward_transform(Fd[..., c0:c1], G[..., c0:c1], s)
-        self.plan.factor_solve(self.lam, G, W, blockvector_layout(nt, nx), nr, stream=s, check=False)   # (3)
+            self._fwd_block(Fd[..., c0:c1], G, c0, c1, s)
+        self._spatial_solves(G, W, nr, s)                                 # (3)
         for c0, c1 in blocks:                                             # (4) pipelined with D2H
-            self.back_transform(W[..., c0:c1], G[..., c0:c1], s)
+            self._back_block(W, G[..., c0:c1], c0, c1, s)
             ev = torch.cuda.Event()
             ev.record(s)
             cs.wait_event(ev)
@@ -352,12 +390,12 @@ class FDMSolver:
                     ev = torch.cuda.Event()
                     ev.record(hs)
                     s.wait_event(ev)
-                    self.forward_transform(A[..., c0:c1], G[..., c0:c1], s)
+                    self._fwd_block(A[..., c0:c1], G, c0, c1, s)
             else:
                 s.wait_event(h2d_done)
                 if four and k >= 2:                      # G_k = G_{k-2} held Psi_{k-2}: drained a step ago
                     s.wait_event(d2h_events[k - 2])
-                self.forward_transform(A, G, s)          # three buffers: G_k = W_{k-1}, dead since back(k-1)
+                self._fwd_block(A, G, 0, nx, s)          # three buffers: G_k = W_{k-1}, dead since back(k-1)
             if k + 1 < n:                                # H2D(k+1) during factor_solve(k)
                 fwd_done = torch.cuda.Event()
                 fwd_done.record(s)
@@ -368,9 +406,9 @@ class FDMSolver:
                 h2d_done.record(hs)
             if not four and d2h_done is not None:        # W_k = G_{k-1} holds Psi_{k-1} until drained
                 s.wait_event(d2h_done)
-            self.plan.factor_solve(self.lam, G, W, layout, nr, stream=s, check=False)
+            self._spatial_solves(G, W, nr, s)
             for c0, c1 in blocks:                        # back transform W -> G, D2H block-pipelined
-                self.back_transform(W[..., c0:c1], G[..., c0:c1], s)
+                self._back_block(W, G[..., c0:c1], c0, c1, s)
                 ev = torch.cuda.Event()
                 ev.record(s)
                 ds.wait_event(ev)

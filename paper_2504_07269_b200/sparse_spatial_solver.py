@@ -189,7 +189,7 @@ class SpatialPlan:
         return bps.value
 
     def factor_solve(self, lam: torch.Tensor, G: torch.Tensor, W: torch.Tensor, layout: N.bv_layout,
-                     nrhs: int, stream=None, check: bool = True):
+                     nrhs: int, stream=None, check: bool = True, permuted: bool = False):
         """(M_x + lam[s] A_x) W[r, s] = G[r, s] for every shift s (device c128).
 
         The C call only enqueues work.  check=True (default) then waits for it and raises
@@ -202,6 +202,9 @@ class SpatialPlan:
         if self.spectral_m > 0 and self._spectral_key != self._ops_key():
             self._attach_spectral()     # first use, or ops.assemble() produced new values
         lam = lam.to(device=G.device, dtype=torch.complex128).contiguous()
+        # permuted: G and W are indexed in the plan's numbering (the FD solver's transforms apply
+        # the permutation, kronecker_solver.FDMSolver._fwd_block / _back_block)
+        N.check(N.lib().stfem_plan_set_io_permuted(self._h, 1 if permuted else 0))
         step = self.max_rhs()
         for r0 in range(0, nrhs, step):
             nr = min(step, nrhs - r0)
