@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--proxy-ranks", type=int, default=0,
                     help="one-GPU proxy of a P-rank run: time ONE rank's share (transforms on n_x/P columns, "
                          "n_t/P shifts, the exchange volume) and print the predicted P-GPU time")
+    ap.add_argument("--plan-opt", action="append", default=[],
+                    help="stfem_plan_options field name=value (repeatable; A/B runs of a tuning knob)")
     ap.add_argument("--variant", default="fd", choices=["fd", "bs"],
                     help="fd: fast diagonalization (the headline path); bs: Bartels-Stewart sweep (SPEC.md:377)")
     return ap.parse_args()
@@ -476,6 +478,9 @@ def run_ours(args):
     t1 = time.perf_counter()
     fdm = ks.FDMSolver(prob.ops, prob.M_t, prob.B_t)
     t_setup = time.perf_counter() - t1
+    if args.plan_opt:
+        fdm.plan.set_options(**{k: (float(v) if "." in v or "e" in v else int(v))
+                                for k, v in (kv.split("=") for kv in args.plan_opt)})
     F = prob.F
     G = torch.empty_like(F)
     Psi = torch.empty_like(F)
