@@ -149,44 +149,6 @@ struct __align__(16) StreamTile {
 // 79.4, four 81.3; a cp.async producer 86.9; staging the starting values from the A warp instead
 // of a third warp cost another 8 ms.)
 constexpr int WS_THREADS = 256;
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint64_t* b, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n.reg .pred p;\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      "selp.b32 %0, 1, 0, p;\n}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(b)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-// a wait that cannot hang the GPU: a protocol bug traps (kernel error) instead of spinning forever
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  for (uint32_t spin = 0; !mbar_try_wait(b, parity); ++spin)
-    if (spin > (1u << 28)) __trap();
-}
-// 1-D bulk copy global -> shared (TMA engine), bytes a multiple of 16, both addresses 16-byte aligned
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(b))
-               : "memory");
-}
-// arrive on b once every cp.async this thread issued so far has landed (counts as one expected arrival)
-__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* b) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(b)) : "memory");
-}
-
 template <bool GATHER, int WS_STAGES>
 constexpr int ws_smem_bytes() {
   return WS_STAGES * 2 * S32_STAGE * 16 + (GATHER ? 2 : 1) * ST_CS * 16 + ST_MAXT * (int)sizeof(StreamTile) +

@@ -26,6 +26,9 @@ constexpr int A_STAGE = BM * LDA;
 constexpr int B_STAGE = BK * LDB;
 constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * 16;
 
+// (Operand tiles by 1-D bulk copies, as in transform_rc_kernel<EPI, true> below, were measured on
+// this kernel too: C4 64.0 ms against 62.4 ms with cp.async -- four DMMAs per fragment pair leave
+// the mbarrier wait of every k tile less slack.  Not kept here.)
 __global__ void __launch_bounds__(256, 2)
 time_transform_kernel(const cplx* __restrict__ T, int nt, const cplx* __restrict__ in,
                       int64_t ld_in, cplx* __restrict__ out, int64_t ld_out, int64_t ncols,
@@ -156,7 +159,14 @@ constexpr int RC_B_STAGE = RC_BK * LDB;
 constexpr int RC_SMEM = RC_STAGES * (RC_A_STAGE * 8 + RC_B_STAGE * 16);
 enum { EPI_PLAIN = 0, EPI_PAIR = 1 };
 
-template <int EPI>
+// TMA: the operand tile's 16 rows of 64 contiguous complex columns arrive as 1-D bulk copies
+// (cp.async.bulk, the TMA engine: one 1 KB row per lane of warp 0, completion counted in bytes on
+// the stage's mbarrier) instead of 1024 16-byte cp.async issued by all 256 threads; used when the
+// operand columns are not gathered through a map and K is a multiple of the k tile.  The packed A
+// tile (its shared-memory rows are padded) stays on cp.async.  Measured neutral against the
+// cp.async operand path (tools/prof_transform.py: C4 32.9 vs 32.7 ms, C5 221.7 vs 220.1 ms): the
+// kernel is bound by DMMA issue (87-89% active), not by the copy instructions.
+template <int EPI, bool TMA>
 __global__ void __launch_bounds__(256, 2)
 transform_rc_kernel(const double* __restrict__ A, int M, int K, const cplx* __restrict__ in, int64_t ld_in,
                     cplx* __restrict__ out, int64_t ld_out, int64_t ncols, int64_t bs_in, int64_t bs_out,
@@ -166,6 +176,7 @@ transform_rc_kernel(const double* __restrict__ A, int M, int K, const cplx* __re
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* As = reinterpret_cast<double*>(smem_raw);
   cplx* Bs = reinterpret_cast<cplx*>(As + RC_STAGES * RC_A_STAGE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + RC_STAGES * RC_B_STAGE);   // TMA: one mbarrier per stage
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -175,6 +186,16 @@ transform_rc_kernel(const double* __restrict__ A, int M, int K, const cplx* __re
   in += (int64_t)blockIdx.z * bs_in;
   out += (int64_t)blockIdx.z * bs_out;
   const int nk = (K + RC_BK - 1) / RC_BK;
+  if constexpr (TMA) {
+    if (tid == 0) {
+      for (int s = 0; s < RC_STAGES; ++s) mbar_init(full + s, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+  }
+  // TMA: bytes of one operand row of this column tile (the last tile of a launch may be partial:
+  // its missing columns keep stale shared memory, and feed only accumulators that are never stored)
+  const uint32_t row_bytes = (uint32_t)(16 * (ncols - j0 < BN ? ncols - j0 : (int64_t)BN));
   // Column maps (both optional): operand column j of this launch is read at column in_cols[j] of
   // `in`, result column j is written at column out_cols[j] of `out`.  The FD solve passes the
   // inverse nested-dissection permutation, so the spatial solves in between see G and W in
@@ -197,12 +218,20 @@ transform_rc_kernel(const double* __restrict__ A, int M, int K, const cplx* __re
       const bool ok = (gmb < mblks) && (k0 + k < K);
       cp_async16(as + (mb * RC_BK + k) * RC_KS + 2 * gg, ok ? A + ((int64_t)gmb * K + (k0 + k)) * 16 + 2 * gg : A, ok);
     }
+    if constexpr (TMA) {
+      if (warp == 0) {
+        if (lane == 0) mbar_arrive_expect_tx(full + stage, RC_BK * row_bytes);
+        __syncwarp();
+        if (lane < RC_BK) bulk_g2s(bs + lane * LDB, in + (int64_t)(k0 + lane) * ld_in + j0, row_bytes, full + stage);
+      }
+    } else {
 #pragma unroll
-    for (int r = 0; r < RC_BK / 4; ++r) {
-      const int idx = tid + 256 * r;
-      const int k = idx >> 6, n = idx & 63;
-      const bool ok = (k0 + k < K) && (j0 + n < ncols);
-      cp_async16(bs + k * LDB + n, ok ? in + (int64_t)(k0 + k) * ld_in + bsrc : in, ok);
+      for (int r = 0; r < RC_BK / 4; ++r) {
+        const int idx = tid + 256 * r;
+        const int k = idx >> 6, n = idx & 63;
+        const bool ok = (k0 + k < K) && (j0 + n < ncols);
+        cp_async16(bs + k * LDB + n, ok ? in + (int64_t)(k0 + k) * ld_in + bsrc : in, ok);
+      }
     }
   };
 
@@ -221,6 +250,7 @@ transform_rc_kernel(const double* __restrict__ A, int M, int K, const cplx* __re
   }
   for (int kt = 0; kt < nk; ++kt) {
     cp_async_wait<RC_STAGES - 2>();
+    if constexpr (TMA) mbar_wait(full + kt % RC_STAGES, (kt / RC_STAGES) & 1);
     __syncthreads();
     {
       const int nxt = kt + RC_STAGES - 1;
@@ -313,17 +343,24 @@ int launch_rc(const double* A, int M, int K, const cplx* in, int64_t ld_in, cplx
               int nsrc, const int32_t* in_cols, const int32_t* out_cols, cudaStream_t stream) {
   static DeviceOnce attr_once;
   if (attr_once.first()) {
-    STFEM_CUDA_TRY(cudaFuncSetAttribute(transform_rc_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(transform_rc_kernel<EPI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        RC_SMEM + RC_STAGES * 8));
+    STFEM_CUDA_TRY(cudaFuncSetAttribute(transform_rc_kernel<EPI, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         RC_SMEM));
   }
   for (int64_t c0 = 0; c0 < ncols; c0 += 65535LL * BN) {
     const int64_t cn = ncols - c0 < 65535LL * BN ? ncols - c0 : 65535LL * BN;
     dim3 grid((M + BM - 1) / BM, (unsigned)((cn + BN - 1) / BN), batch);
     // a mapped side keeps its base pointer: the map holds absolute columns
-    transform_rc_kernel<EPI><<<grid, 256, RC_SMEM, stream>>>(A, M, K, in_cols ? in : in + c0, ld_in,
-                                                             out_cols ? out : out + c0, ld_out, cn, bs_in, bs_out, rows,
-                                                             scale, nsrc, in_cols ? in_cols + c0 : nullptr,
-                                                             out_cols ? out_cols + c0 : nullptr);
+    if (!in_cols && K % RC_BK == 0)
+      transform_rc_kernel<EPI, true><<<grid, 256, RC_SMEM + RC_STAGES * 8, stream>>>(
+          A, M, K, in + c0, ld_in, out_cols ? out : out + c0, ld_out, cn, bs_in, bs_out, rows, scale, nsrc, nullptr,
+          out_cols ? out_cols + c0 : nullptr);
+    else
+      transform_rc_kernel<EPI, false><<<grid, 256, RC_SMEM, stream>>>(A, M, K, in_cols ? in : in + c0, ld_in,
+                                                                      out_cols ? out : out + c0, ld_out, cn, bs_in, bs_out,
+                                                                      rows, scale, nsrc, in_cols ? in_cols + c0 : nullptr,
+                                                                      out_cols ? out_cols + c0 : nullptr);
     STFEM_LAUNCH_CHECK("transform_rc_kernel");
   }
   return STFEM_OK;

@@ -130,3 +130,30 @@ def test_paired_transform_self_pairs():
     assert np.linalg.norm(G - Y @ F) / np.linalg.norm(Y @ F) < 1e-13
     P = K.transform_pair_back(dp, torch.from_numpy(F).cuda()).cpu().numpy()
     assert np.linalg.norm(P - X @ F) / np.linalg.norm(X @ F) < 1e-13
+
+
+@pytest.mark.parametrize("N,deg,ncols", [(64, 1, 450), (256, 1, 4097), (40, 2, 65)])
+def test_paired_transforms_column_maps(N, deg, ncols):
+    """stfem_transform_pair_fwd_map scatters its result columns (out_cols), stfem_pair_mix +
+    stfem_transform_pair_back_map gathers its operand columns (in_cols): with a permutation and
+    its use as both maps the pair reproduces the unmapped transforms column for column
+    (bit-identical: the same arithmetic per column), also on column blocks of a wider stack."""
+    pf, dp = _pairs(N, deg)
+    nt = pf.X.shape[0]
+    rng = np.random.default_rng(N + ncols)
+    F = torch.from_numpy(crand(rng, nt, ncols)).cuda()
+    iperm = torch.from_numpy(rng.permutation(ncols).astype(np.int32)).cuda()
+    G_ref = K.transform_pair_fwd(dp, F)
+    G = torch.full_like(F, float("nan"))
+    c_mid = ncols // 3
+    for c0, c1 in ((0, c_mid), (c_mid, ncols)):          # column blocks of F into the whole of G
+        K.transform_pair_fwd(dp, F[:, c0:c1], out=G, out_cols=iperm[c0:c1])
+    assert torch.equal(G[:, iperm.long()], G_ref)
+    P_ref = K.transform_pair_back(dp, G_ref.clone())
+    K.pair_mix(dp, G)
+    P = torch.empty_like(F)
+    for c0, c1 in ((0, c_mid), (c_mid, ncols)):
+        K.transform_pair_back(dp, G, out=P[:, c0:c1], in_cols=iperm[c0:c1], mixed=True)
+    assert torch.equal(P, P_ref)
+    with pytest.raises(Exception):
+        K.transform_pair_back(dp, G, out=P, in_cols=iperm)            # a map needs the pre-pass first

@@ -38,7 +38,20 @@ def main():
         ev[2].record()
         K.time_transform(Y, F, out=G)
         ev[3].record()
+    # the back GEMM alone, operand tile by bulk copies (no column map) against 16-byte cp.async
+    # through an identity column map
+    ident = torch.arange(prob.nx, dtype=torch.int32, device="cuda")
+    ev2 = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    K.pair_mix(dp, G)
+    for _ in range(2):
+        ev2[0].record()
+        K.transform_pair_back(dp, G, out=F, mixed=True)
+        ev2[1].record()
+        K.transform_pair_back(dp, G, out=F, mixed=True, in_cols=ident)
+        ev2[2].record()
     torch.cuda.synchronize()
+    print(f"{a.workload}: back GEMM, bulk-copy operand tiles {ev2[0].elapsed_time(ev2[1]):.2f} ms, "
+          f"cp.async through a column map {ev2[1].elapsed_time(ev2[2]):.2f} ms")
     print(f"{a.workload}: paired fwd {ev[0].elapsed_time(ev[1]):.2f} ms, paired back {ev[1].elapsed_time(ev[2]):.2f} ms,"
           f" complex K3 {ev[2].elapsed_time(ev[3]):.2f} ms")
 
