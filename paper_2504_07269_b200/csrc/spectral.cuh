@@ -175,7 +175,9 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
         cp_async16(Bs + (kc & 1) * SP_B_STAGE + (idx >> 6) * SP_LDB + (idx & 63),
                    ok ? wsub + (int64_t)k * a.wstride + cg : wsub, ok);
       } else {
-        rb[u] = b_val(k0 + (idx >> 6), idx & 63);
+        // 16 consecutive lanes walk down k of one column (Z and, in the plan's numbering, G are
+        // contiguous in k: 256-byte runs instead of 32 separate 16-byte pieces per warp)
+        rb[u] = b_val(k0 + (idx & 15), idx >> 4);
       }
     }
     if constexpr (OP == OP_U) cp_async_commit();
@@ -188,7 +190,7 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
       const int idx = tid + 256 * u;
       if constexpr (OP == OP_F1) as[(idx & 15) * SP_LDA + (idx >> 4)] = ra[u];
       else as[(idx >> 6) * SP_LDA + (idx & 63)] = ra[u];
-      if constexpr (OP != OP_U) stc(bs + (idx >> 6) * SP_LDB + (idx & 63), rb[u]);
+      if constexpr (OP != OP_U) stc(bs + (idx & 15) * SP_LDB + (idx >> 4), rb[u]);
     }
   };
 
@@ -236,11 +238,21 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
     // the shift / RHS split of the column) is formed once.  (Measured per batch, register
     // path -> ring: C4 F1 5.45 -> 5.61, B1 3.58 -> 3.69, B2 4.43 -> 5.43 ms; C5 (9 RHS) F1 11.4 ->
     // 10.0, B1 10.1 -> 8.9, B2 10.2 -> 10.0: B2 stays on the register path.)
-    const int bc = tid & 63, bcg = n0 + bc;
-    const bool bcol_ok = bcg < ncols;
-    const int bs_ = bcol_ok ? bcg / nrhs : 0, br = bcol_ok ? bcg - bs_ * nrhs : 0;
-    const cplx* bbase = OP == OP_F1 ? a.G + bv_off(a.lay, br, a.shift0 + bs_, 0)
-                                    : a.Z + (int64_t)bs_ * nx * nrhs + (int64_t)br * nx + (OP == OP_B2 ? S.first : 0);
+    // B operand: 16 consecutive lanes walk down k of one column (contiguous in the plan's
+    // numbering: 256-byte runs), a thread's four copies of a chunk are columns bq + 16 u
+    const int kq = tid & 15, bq = tid >> 4;
+    bool bcol_ok[4];
+    int bs_[4], br[4];
+    const cplx* bbase[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int bcg = n0 + bq + 16 * u;
+      bcol_ok[u] = bcg < ncols;
+      bs_[u] = bcol_ok[u] ? bcg / nrhs : 0;
+      br[u] = bcol_ok[u] ? bcg - bs_[u] * nrhs : 0;
+      bbase[u] = OP == OP_F1 ? a.G + bv_off(a.lay, br[u], a.shift0 + bs_[u], 0)
+                             : a.Z + (int64_t)bs_[u] * nx * nrhs + (int64_t)br[u] * nx + (OP == OP_B2 ? S.first : 0);
+    }
     const bool unchunked = a.lay.chunk_cols >= nx;
     auto issue = [&](int st, int kc) {
       const int k0 = kc * SP_BK;
@@ -262,16 +274,16 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
           const bool ok = i < m && k < K;
           cp_async8(as + (idx >> 6) * SP_LDA + r, ok ? V + i + (int64_t)k * m : V, ok);
         }
-        const int k = k0 + (idx >> 6);
-        const bool ok = bcol_ok && k < K;
-        const cplx* src = bbase;
+        const int k = k0 + kq;
+        const bool ok = bcol_ok[u] && k < K;
+        const cplx* src = bbase[u];
         if (ok) {
           if constexpr (OP == OP_F1)
-            src = unchunked ? bbase + idx_s[k] : a.G + bv_off(a.lay, br, a.shift0 + bs_, idx_s[k]);
-          else if constexpr (OP == OP_B1) src = bbase + idx_s[k];
-          else src = bbase + k;
+            src = unchunked ? bbase[u] + idx_s[k] : a.G + bv_off(a.lay, br[u], a.shift0 + bs_[u], idx_s[k]);
+          else if constexpr (OP == OP_B1) src = bbase[u] + idx_s[k];
+          else src = bbase[u] + k;
         }
-        cp_async16(bs + (idx >> 6) * SP_LDB + bc, src, ok);
+        cp_async16(bs + kq * SP_LDB + bq + 16 * u, src, ok);
       }
     };
 #pragma unroll
