@@ -266,9 +266,10 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
           const bool ok = ko < m && k < K;
           cp_async8(as + (idx & 15) * SP_LDA + r, ok ? V + k + (int64_t)ko * m : V, ok);
         } else if constexpr (OP == OP_B1) {
-          const int r = idx & 63, k = k0 + (idx >> 6), kk = it.z * 32 + (r >> 4) * 8 + (r & 7);
+          // rows of R^T / Q^T = columns of R / Q, contiguous in k: k fastest (128-byte runs)
+          const int r = idx >> 4, k = k0 + (idx & 15), kk = it.z * 32 + (r >> 4) * 8 + (r & 7);
           const bool ok = kk < m && k < K;
-          cp_async8(as + (idx >> 6) * SP_LDA + r, ok ? ((r >> 3) & 1 ? Qm : Rm) + k + (int64_t)kk * g : Rm, ok);
+          cp_async8(as + (idx & 15) * SP_LDA + r, ok ? ((r >> 3) & 1 ? Qm : Rm) + k + (int64_t)kk * g : Rm, ok);
         } else {
           const int r = idx & 63, k = k0 + (idx >> 6), i = it.z * SP_BM + r;
           const bool ok = i < m && k < K;
