@@ -157,6 +157,23 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
     return ldc(Zs + S.first + k);
   };
 
+  // F2 / B2 (register path): a thread's four B elements of a chunk are row k0 + kq of the columns
+  // bq + 16 u -- the same columns for every chunk, so their Z (and w) column pointers, with the
+  // shift / RHS split of the column index, are formed once per tile
+  const int kq = tid & 15;
+  const cplx* zc[4] = {nullptr, nullptr, nullptr, nullptr};
+  const cplx* wc[4] = {nullptr, nullptr, nullptr, nullptr};
+  if constexpr (OP == OP_F2 || OP == OP_B2) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int cg = n0 + (tid >> 4) + 16 * u;
+      if (cg < ncols) {
+        const int s = cg / nrhs, r = cg - s * nrhs;
+        zc[u] = a.Z + (int64_t)s * nx * nrhs + (int64_t)r * nx + S.first;
+        wc[u] = wsub + s;
+      }
+    }
+  }
   double ra[4];
   cplx rb[4];
   auto fetch = [&](int kc) {
@@ -174,9 +191,14 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
         const bool ok = k < K && cg < ncols;
         cp_async16(Bs + (kc & 1) * SP_B_STAGE + (idx >> 6) * SP_LDB + (idx & 63),
                    ok ? wsub + (int64_t)k * a.wstride + cg : wsub, ok);
+      } else if constexpr (OP == OP_F2 || OP == OP_B2) {
+        // 16 consecutive lanes walk down k of one column (Z is contiguous in k: 256-byte runs
+        // instead of 32 separate 16-byte pieces per warp)
+        const int k = k0 + kq;
+        if (zc[u] == nullptr || k >= K) rb[u] = zero;
+        else if constexpr (OP == OP_B2) rb[u] = ldc(zc[u] + k);
+        else rb[u] = k < m ? cmul(ldc(wc[u] + (int64_t)k * a.wstride), ldc(zc[u] + k)) : ldc(zc[u] + k - m);
       } else {
-        // 16 consecutive lanes walk down k of one column (Z and, in the plan's numbering, G are
-        // contiguous in k: 256-byte runs instead of 32 separate 16-byte pieces per warp)
         rb[u] = b_val(k0 + (idx & 15), idx >> 4);
       }
     }
