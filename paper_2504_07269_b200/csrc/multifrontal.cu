@@ -1246,7 +1246,10 @@ int upload(Plan& P) {
           } else if (j == 1) {
             for (int q = 0; q < (S.g + SP_BM - 1) / SP_BM; ++q) items.push_back(make_int4(OP_F2, t, q, 0));
           } else if (j == 2) {
-            for (int q = 0; q < (S.m + 31) / 32; ++q) items.push_back(make_int4(OP_B1, t, q, 0));
+            // x_Gam resident, all row tiles (a root without boundary rows has no K loop: per-tile path)
+            if (S.g >= 1 && S.g <= SP_B1R_K) items.push_back(make_int4(OP_B1R, t, 0, 0));
+            else
+              for (int q = 0; q < (S.m + 31) / 32; ++q) items.push_back(make_int4(OP_B1, t, q, 0));
           } else {
             for (int q = 0; q < (S.m + SP_BM - 1) / SP_BM; ++q) items.push_back(make_int4(OP_B2, t, q, 0));
           }
@@ -1263,7 +1266,7 @@ int upload(Plan& P) {
       if ((rc = up(&P.d_spec_items, items))) return rc;
       int mmax = 0;
       for (const auto& S : P.subs) mmax = std::max(mmax, std::max(S.m, S.g));
-      P.spec_smem = spectral_smem_bytes(mmax);
+      P.spec_smem = std::max(spectral_smem_bytes(mmax), SP_B1R_SMEM);
       if (P.spec_smem > 227 * 1024)
         return fail(STFEM_ERR_DIM, "spectral subtrees: interior too large for the shared-memory staging");
       STFEM_CUDA_TRY(cudaFuncSetAttribute(spectral_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, P.spec_smem));

@@ -43,7 +43,14 @@ constexpr int SP_STAGES = 3;   // cp.async ring of the plain-copy ops (F1, B1); 
 constexpr int SP_SMEM = SP_STAGES * (SP_A_STAGE * 8 + SP_B_STAGE * 16);
 // + OP_U staging: the tile's 16 R rows over the subtree's m
 __host__ __device__ constexpr int spectral_smem_bytes(int mmax) { return SP_SMEM + 4 * ((mmax + 3) & ~3); }   // + the staged index table
-enum { OP_U = 0, OP_F1 = 1, OP_F2 = 2, OP_B1 = 3, OP_B2 = 4 };
+enum { OP_U = 0, OP_F1 = 1, OP_F2 = 2, OP_B1 = 3, OP_B2 = 4, OP_B1R = 5 };
+// OP_B1R: B1 of a whole subtree whose root has at most SP_B1R_K boundary rows, one CTA per column
+// tile: x_Gam of the tile (K = gam rows x 64 columns, gathered through the boundary index table)
+// is staged ONCE and stays resident while the CTA walks the subtree's row tiles, streaming only
+// the R^T / Q^T tiles.  The per-tile B1 re-gathers x_Gam for each of its m / 32 row tiles and pays
+// the index-table / gather / fill latency chain for 4 k chunks of work.
+constexpr int SP_B1R_K = 64;
+constexpr int SP_B1R_SMEM = SP_STAGES * SP_A_STAGE * 8 + (SP_B1R_K / SP_BK) * SP_B_STAGE * 16 + 4 * SP_B1R_K;
 
 __device__ __forceinline__ cplx spec_w(double th, cplx l) { return crecip_fast(cmk(th + l.re, l.im)); }
 
@@ -396,6 +403,121 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
     }
 }
 
+__device__ __forceinline__ void spectral_b1_resident(const SpecArgs& a, const int4 it, double* As, cplx* Bs) {
+  const SubDev S = a.subs[it.y];
+  const FrontDev F = a.fronts[S.front];
+  const int m = S.m, g = S.g, nrhs = a.nrhs, nx = a.nx;
+  const int ncols = a.nb * nrhs;
+  const int n0 = blockIdx.y * SP_BN;
+  if (n0 >= ncols) return;
+  const int K = g, nk = (K + SP_BK - 1) / SP_BK;   // <= SP_B1R_K / SP_BK resident chunks
+  const double* __restrict__ Rm = a.RQ + S.rqofs;
+  const double* __restrict__ Qm = Rm + (int64_t)g * m;
+  const int32_t* __restrict__ bidx = a.bidx + F.bidx_beg;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3, wm = warp & 1, wn = warp >> 1;
+  const cplx* __restrict__ wsub = a.wbuf + (int64_t)S.tofs * a.wstride;
+  int* idx_s = reinterpret_cast<int*>(Bs + (SP_B1R_K / SP_BK) * SP_B_STAGE);
+  for (int q = tid; q < g; q += 256) idx_s[q] = bidx[q];
+  __syncthreads();
+  // x_Gam of this column tile: every chunk at once (16 consecutive lanes walk down k of a column)
+  const int kq = tid & 15, bq = tid >> 4;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int bcg = n0 + bq + 16 * u;
+    const bool cok = bcg < ncols;
+    const int s = cok ? bcg / nrhs : 0, r = cok ? bcg - s * nrhs : 0;
+    const cplx* bbase = a.Z + (int64_t)s * nx * nrhs + (int64_t)r * nx;
+    for (int kc = 0; kc < nk; ++kc) {
+      const int k = kc * SP_BK + kq;
+      const bool ok = cok && k < K;
+      cp_async16(Bs + kc * SP_B_STAGE + kq * SP_LDB + bq + 16 * u, ok ? bbase + idx_s[k] : bbase, ok);
+    }
+  }
+  cp_async_commit();
+  const int ntile = (m + 31) / 32, total = ntile * nk;
+  auto issue_a = [&](int c) {   // chunk c = (row tile c / nk, k chunk c % nk) into A stage c % SP_STAGES
+    const int tile = c / nk, k0 = (c - tile * nk) * SP_BK;
+    double* as = As + (c % SP_STAGES) * SP_A_STAGE;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = tid + 256 * u;
+      const int r = idx >> 4, k = k0 + (idx & 15), kk = tile * 32 + (r >> 4) * 8 + (r & 7);
+      const bool ok = kk < m && k < K;
+      cp_async8(as + (idx & 15) * SP_LDA + r, ok ? ((r >> 3) & 1 ? Qm : Rm) + k + (int64_t)kk * g : Rm, ok);
+    }
+  };
+#pragma unroll
+  for (int c = 0; c < SP_STAGES - 1; ++c) {
+    if (c < total) issue_a(c);
+    cp_async_commit();
+  }
+  double acc[2][2][2][4];
+  const bool wact = n0 + wn * 16 < ncols, wact1 = n0 + wn * 16 + 8 < ncols;
+  for (int c = 0; c < total; ++c) {
+    const int tile = c / nk, kc = c - tile * nk;
+    if (kc == 0) {
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[mi][ni][0][v] = acc[mi][ni][1][v] = 0.0;
+    }
+    cp_async_wait<SP_STAGES - 2>();
+    __syncthreads();
+    if (c + SP_STAGES - 1 < total) issue_a(c + SP_STAGES - 1);
+    cp_async_commit();
+    if (wact) {
+      const double* as = As + (c % SP_STAGES) * SP_A_STAGE + tq * SP_LDA + wm * 32 + gq;
+      const cplx* bs = Bs + kc * SP_B_STAGE + tq * SP_LDB + wn * 16 + gq;
+#pragma unroll
+      for (int kk = 0; kk < SP_BK; kk += 4) {
+        double af[2][2];
+        cplx bf[2];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+          af[mi][0] = as[kk * SP_LDA + mi * 16];
+          af[mi][1] = as[kk * SP_LDA + mi * 16 + 8];
+        }
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) bf[ni] = ldc(bs + kk * SP_LDB + ni * 8);
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni) {
+            if (ni == 1 && !wact1) continue;
+            dmma_16x8x4(acc[mi][ni][0], af[mi][0], af[mi][1], bf[ni].re);
+            dmma_16x8x4(acc[mi][ni][1], af[mi][0], af[mi][1], bf[ni].im);
+          }
+      }
+    }
+    if (kc == nk - 1) {
+      // y = w o (c - R^T x_Gam) - Q^T x_Gam: rows rbase (R^T x) and rbase + 8 (Q^T x) belong to the
+      // same interior index
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) {
+          const int rbase = wm * 32 + mi * 16 + gq;
+          const int kk = tile * 32 + (rbase >> 4) * 8 + (rbase & 7);
+#pragma unroll
+          for (int cv = 0; cv < 2; ++cv) {
+            const int cg = n0 + wn * 16 + ni * 8 + 2 * tq + cv;
+            if (cg >= ncols || kk >= m) continue;
+            const int s = cg / nrhs, r = cg - s * nrhs;
+            cplx* zp = a.Z + (int64_t)s * nx * nrhs + (int64_t)r * nx + S.first + kk;
+            const cplx t1 = cmk(acc[mi][ni][0][cv], acc[mi][ni][1][cv]);
+            const cplx t2 = cmk(acc[mi][ni][0][2 + cv], acc[mi][ni][1][2 + cv]);
+            const cplx w = ldc(wsub + (int64_t)kk * a.wstride + s);
+            stc(zp, csub(cmul(w, csub(ldc(zp), t1)), t2));
+          }
+        }
+    }
+  }
+  cp_async_wait<0>();
+}
+
 __global__ void __launch_bounds__(256, 2) spectral_kernel(SpecArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* As = reinterpret_cast<double*>(smem_raw);
@@ -406,6 +528,7 @@ __global__ void __launch_bounds__(256, 2) spectral_kernel(SpecArgs a) {
     case OP_F1: spectral_tile<OP_F1>(a, it, As, Bs); break;
     case OP_F2: spectral_tile<OP_F2>(a, it, As, Bs); break;
     case OP_B1: spectral_tile<OP_B1>(a, it, As, Bs); break;
+    case OP_B1R: spectral_b1_resident(a, it, As, Bs); break;
     default: spectral_tile<OP_B2>(a, it, As, Bs); break;
   }
 }
