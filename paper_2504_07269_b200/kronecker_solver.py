@@ -181,15 +181,15 @@ class FDMSolver:
             return K.transform_pair_back(self.pairs, W, out=out, stream=stream)
         return K.time_transform(self.X, W, out=out, stream=stream)
 
-    # ---- the spatial permutation fused into the transforms (paired transforms only) ----
-    # The forward transform scatters its result columns to the plan's numbering (column
-    # iperm[x]) and the back transform gathers its operand columns from there, so the spatial
-    # solves in between read G and write W with contiguous pivot rows (stfem_plan_set_io_permuted)
-    # and no separate permutation pass exists.  Both transforms move their operands as 16-byte
-    # cp.async copies anyway and are DMMA bound.
-    @property
-    def fused_perm(self) -> bool:
-        return self.pairs is not None
+    # ---- the spatial permutation fused into the transforms (paired transforms only; opt-in) ----
+    # With fused_perm the forward transform scatters its result columns to the plan's numbering
+    # (column iperm[x]) and the back transform gathers its operand columns from there, so the
+    # spatial solves in between read G and write W with contiguous pivot rows
+    # (stfem_plan_set_io_permuted) and no kernel gathers through the permutation.  Measured A/B
+    # (tools/ab_fused.py, ms per solve, fused / not): C4 576.6 / 575.0, C5 1299.4 / 1293.3 -- the
+    # solves gain 1-2 ms, the gathering back transform (16-byte cp.async per element instead of
+    # bulk-copied tiles) loses 3: off by default.
+    fused_perm = False
 
     def _iperm(self) -> torch.Tensor:
         if getattr(self, "_iperm_d", None) is None:

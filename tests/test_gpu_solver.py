@@ -228,6 +228,29 @@ def test_fdm_solve_matches_oracle(m, T, N, source):
             assert abs(a - b) / b < 5e-4
 
 
+@pytest.mark.parametrize("m,N", [(64, 64), (40, 48)])
+def test_fdm_fused_permutation_matches_default(m, N):
+    """FDMSolver.fused_perm (the nested-dissection permutation applied by the transforms'
+    column maps, stfem_plan_set_io_permuted in between) gives the default path's Psi: staged
+    solve, pipelined host solve and the host stream."""
+    mesh, tmesh, ops, Mt, Bt, F = fd_case(m, 1.0, N, "sinpit")
+    fdm = ks.FDMSolver(ops, Mt, Bt)
+    ref = fdm.solve(F, timings={}).clone()
+    fdm.fused_perm = True
+    psi = fdm.solve(F, timings={})
+    assert rel(psi.cpu().numpy(), ref.cpu().numpy()) < 1e-13
+    Fh = F.cpu().pin_memory()
+    Ph = torch.empty_like(Fh).pin_memory()
+    fdm.solve_host(Fh, Ph)
+    assert rel(Ph.numpy(), ref.cpu().numpy()) < 1e-13
+    Ph2 = [torch.empty_like(Fh).pin_memory() for _ in range(3)]
+    fdm.solve_host_stream([Fh] * 3, Ph2)
+    for P in Ph2:
+        assert rel(P.numpy(), ref.cpu().numpy()) < 1e-13
+    fdm.fused_perm = False
+    assert rel(fdm.solve(F).cpu().numpy(), ref.cpu().numpy()) < 1e-13
+
+
 def test_spec_1x1_global():
     """SPEC.md:380: n_x = n_t = 1 global system, psi = 1/(4/3 + i/16)."""
     ops = fa.assemble_spatial(sm.build_structured_square(2))
