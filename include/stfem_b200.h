@@ -186,6 +186,8 @@ int stfem_plan_set_shift_base(stfem_plan* plan, int32_t base);
 /* G and W of the following stfem_factor_solve calls are indexed in the plan's own numbering
  * (column new = iperm[old]) instead of the operators': pivot rows are then contiguous, and the
  * permutation is applied by the transforms around the solves (the _map variants above).
+ * The setting stays in the plan until it is changed; stfem_fdm_solve, whose transforms carry no
+ * maps, clears it.
  * stfem_plan_device_iperm: the device copy of iperm (int32[n]); valid until the next
  * stfem_plan_set_spectral / stfem_plan_set_options. */
 int stfem_plan_set_io_permuted(stfem_plan* plan, int32_t on);

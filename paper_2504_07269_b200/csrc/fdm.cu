@@ -200,6 +200,9 @@ extern "C" int stfem_fdm_solve(stfem_plan* plan, stfem_comm* comm, const double*
   };
   const stfem::cplx* lam = (const stfem::cplx*)tf->lam + (size_t)rank * ntl;
   int rc;
+  // the transforms of this entry point carry no column maps: G and W are in the operators' numbering,
+  // whatever an earlier stfem_plan_set_io_permuted call left in the plan
+  P.io_permuted = false;
   // at most 16 right-hand sides per factor_solve call (and fewer for very large fronts)
   int32_t step = 16;
   if ((rc = stfem_plan_max_rhs(plan, &step))) return rc;

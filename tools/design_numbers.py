@@ -21,7 +21,7 @@ def main():
         print(f"roofline: {r.get('kernel', '')[:60]} achieved {r.get('achieved', 0):.2f} / {r.get('peak', 0):.2f} "
               f"{r.get('unit')} frac {r.get('frac', 0):.3f} traffic {r.get('traffic')}")
         for k in ("roofline_multifrontal", "roofline_transform", "roofline_solve"):
-            if k in d:
+            if d.get(k):
                 print(f"  {k}: achieved {d[k]['achieved']:.2f} frac {d[k]['frac']:.3f}")
         for fam, v in d.get("kernel_families", {}).items():
             print(f"  {fam:14s} {v['ms']:8.1f} ms  {v['launches']:5d} launches  {v['tflops']:6.2f} TF  "
