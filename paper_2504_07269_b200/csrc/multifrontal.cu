@@ -636,9 +636,18 @@ __global__ void __launch_bounds__(NT) backward_level_kernel(LevelArgs a, int uni
   const cplx zero = cmk(0.0, 0.0);
   extern __shared__ __align__(16) unsigned char bwd_smem[];
   cplx* xs = reinterpret_cast<cplx*>(bwd_smem);   // n x nrhs: x (boundary rows), t then x (pivot rows)
-  for (int q = tid; q < n * nrhs; q += NT) {
-    const int i = q / nrhs, r = q - i * nrhs;
-    xs[q] = ldc(Zk + (i < p ? F.pbeg + i : bidx[i - p]) + (int64_t)r * nx);
+  if (nrhs & 1) {
+    // rows fastest: consecutive lanes read consecutive rows of one right-hand side (the right-hand
+    // sides are n_x apart in Z); the shared-memory stride of nrhs complex is conflict free for odd nrhs
+    for (int q = tid; q < n * nrhs; q += NT) {
+      const int r = q / n, i = q - r * n;
+      xs[i * nrhs + r] = ldc(Zk + (i < p ? F.pbeg + i : bidx[i - p]) + (int64_t)r * nx);
+    }
+  } else {
+    for (int q = tid; q < n * nrhs; q += NT) {
+      const int i = q / nrhs, r = q - i * nrhs;
+      xs[q] = ldc(Zk + (i < p ? F.pbeg + i : bidx[i - p]) + (int64_t)r * nx);
+    }
   }
   __syncthreads();
   // 2. boundary contributions of all pivot columns (parallel over columns); the right-hand
