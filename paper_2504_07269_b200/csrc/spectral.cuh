@@ -463,6 +463,24 @@ __device__ __forceinline__ void spectral_b1_resident(const SpecArgs& a, const in
         for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
           for (int v = 0; v < 4; ++v) acc[mi][ni][0][v] = acc[mi][ni][1][v] = 0.0;
+      // the tile's epilogue reads c (in Z, last touched by the forward sweep) and w: pull their
+      // lines into L2 now, a whole K loop ahead (no registers held, unlike an early load)
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) {
+          const int rbase = wm * 32 + mi * 16 + gq;
+          const int kk = tile * 32 + (rbase >> 4) * 8 + (rbase & 7);
+#pragma unroll
+          for (int cv = 0; cv < 2; ++cv) {
+            const int cg = n0 + wn * 16 + ni * 8 + 2 * tq + cv;
+            if (cg < ncols && kk < m) {
+              const int s = cg / nrhs, r = cg - s * nrhs;
+              asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a.Z + (int64_t)s * nx * nrhs + (int64_t)r * nx + S.first + kk));
+              if (cv == 0) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(wsub + (int64_t)kk * a.wstride + s));
+            }
+          }
+        }
     }
     cp_async_wait<SP_STAGES - 2>();
     __syncthreads();
