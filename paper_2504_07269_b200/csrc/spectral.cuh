@@ -39,6 +39,7 @@ constexpr int SP_LDA = SP_BM + 4;   // As[k][row] doubles: (t*68 + g) mod 16 hit
 constexpr int SP_LDB = SP_BN + 2;   // Bs[k][col] complex: (t*66 + g) mod 8 hits each 16-B bank group 4x
 constexpr int SP_A_STAGE = SP_BK * SP_LDA;   // doubles
 constexpr int SP_B_STAGE = SP_BK * SP_LDB;   // complex
+constexpr int SP_PF = 2;       // chunks ahead of the register prefetch that F2 / B2 pull their Z lines into L2
 constexpr int SP_STAGES = 3;   // cp.async ring of the plain-copy ops (F1, B1); U, F2 and B2 use two
 constexpr int SP_SMEM = SP_STAGES * (SP_A_STAGE * 8 + SP_B_STAGE * 16);
 // + OP_U staging: the tile's 16 R rows over the subtree's m
@@ -202,6 +203,14 @@ __device__ __forceinline__ void spectral_tile(const SpecArgs& a, const int4 it, 
         // 16 consecutive lanes walk down k of one column (Z is contiguous in k: 256-byte runs
         // instead of 32 separate 16-byte pieces per warp)
         const int k = k0 + kq;
+        // the register double buffer looks one chunk ahead; an L2 prefetch of the Z lines of the
+        // chunk SP_PF further on covers the rest of the HBM latency (F2's second half re-reads
+        // the lines of its first: no prefetch there)
+        {
+          const int kp = k + SP_PF * SP_BK;
+          if (zc[u] != nullptr && kp < (OP == OP_B2 ? K : m) && (kq & 7) == 0)
+            asm volatile("prefetch.global.L2 [%0];\n" ::"l"(zc[u] + kp));
+        }
         if (zc[u] == nullptr || k >= K) rb[u] = zero;
         else if constexpr (OP == OP_B2) rb[u] = ldc(zc[u] + k);
         else rb[u] = k < m ? cmul(ldc(wc[u] + (int64_t)k * a.wstride), ldc(zc[u] + k)) : ldc(zc[u] + k - m);
