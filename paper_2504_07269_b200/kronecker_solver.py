@@ -191,6 +191,10 @@ class FDMSolver:
     # bulk-copied tiles) loses 3: off by default.
     fused_perm = False
 
+    @property
+    def _fused(self) -> bool:
+        return bool(self.fused_perm) and self.pairs is not None   # the column maps exist on K3p only
+
     def _iperm(self) -> torch.Tensor:
         if getattr(self, "_iperm_d", None) is None:
             perm = self.plan.perm()
@@ -201,22 +205,22 @@ class FDMSolver:
 
     def _fwd_block(self, Fblk: torch.Tensor, G: torch.Tensor, c0: int, c1: int, stream=None):
         """Forward transform of spatial columns [c0, c1) (Fblk) into the whole stack G."""
-        if self.fused_perm:
+        if self._fused:
             return K.transform_pair_fwd(self.pairs, Fblk, out=G, stream=stream, out_cols=self._iperm()[c0:c1])
         return self.forward_transform(Fblk, G[..., c0:c1], stream)
 
     def _back_block(self, W: torch.Tensor, out_blk: torch.Tensor, c0: int, c1: int, stream=None):
         """Back transform into spatial columns [c0, c1) (out_blk) from the whole stack W (fused:
         `K.pair_mix` must have run over W)."""
-        if self.fused_perm:
+        if self._fused:
             return K.transform_pair_back(self.pairs, W, out=out_blk, stream=stream, in_cols=self._iperm()[c0:c1],
                                          mixed=True)
         return self.back_transform(W[..., c0:c1], out_blk, stream)
 
     def _spatial_solves(self, G, W, nr, stream):
         self.plan.factor_solve(self.lam, G, W, blockvector_layout(self.nt, self.ops.n), nr, stream=stream,
-                               check=False, permuted=self.fused_perm)
-        if self.fused_perm:
+                               check=False, permuted=self._fused)
+        if self._fused:
             K.pair_mix(self.pairs, W, stream=stream)
 
     def solve(self, F: torch.Tensor, out: torch.Tensor | None = None, work: torch.Tensor | None = None,
